@@ -1,0 +1,187 @@
+/*
+ * fgt_cuda.h -- C ABI of libfgtcuda.so, the sm_100a (B200) hot path of the
+ * plane-wave fast Gauss transform (Greengard, Jiang, Rachh, Wang; arXiv 2305.07165).
+ *
+ * Two layers:
+ *
+ *  1. Kernel-level drop-ins for the reference's compiled-backend slot
+ *     `fgt._kernels_cy` (declared at /root/reference/pkg/setup.py:12-18, bound by
+ *     /root/reference/pkg/src/fgt/backend.py:22-27).  Their contract is the numpy
+ *     fallback /root/reference/pkg/src/fgt/_kernels_py.py:14-100.  All pointers are
+ *     HOST pointers, caller-owned, C-contiguous float64 / complex128 (interleaved
+ *     re,im).  Outputs are accumulated in place exactly as the numpy versions do.
+ *
+ *  2. Phase/pipeline entry points for the discrete transform (Alg 2,
+ *     /root/reference/PAPER.md:840-872; contract SPEC.md:361-444): the GPU tree
+ *     (Alg 1, reference tree.py:442-527), the P/D lists, and
+ *     fgt_points.  `*_dev` variants take DEVICE pointers and a
+ *     cudaStream_t (passed as void*), so a caller holding inputs already resident
+ *     in HBM avoids the host round trip.
+ *
+ * Every function returns 0 on success.  Non-zero codes:
+ *   FGT_EINVAL  (1)  bad argument        -> Python shim raises ValueError
+ *   FGT_ECUDA   (2)  CUDA runtime error  -> RuntimeError (message via fgt_last_error)
+ *   FGT_ERANGE  (3)  outside supported range (e.g. tree deeper than 19 levels in 3-D)
+ *   FGT_ENOMEM  (4)  device allocation failed
+ * Functions are reentrant; all device scratch is stream-ordered (cudaMallocAsync).
+ */
+#ifndef FGT_CUDA_H
+#define FGT_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGT_OK 0
+#define FGT_EINVAL 1
+#define FGT_ECUDA 2
+#define FGT_ERANGE 3
+#define FGT_ENOMEM 4
+
+/* Thread-local text of the last error ("" if none). */
+const char* fgt_last_error(void);
+/* Library version string, e.g. "0.1.0+sm_100a". */
+const char* fgt_version(void);
+/* Number of kernel launches issued by this thread since the last reset. */
+int64_t fgt_launch_count(void);
+void fgt_reset_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Layer 1: kernel drop-ins (host pointers).
+ * ------------------------------------------------------------------------- */
+
+/* Replaces _kernels_py.gauss_direct (_kernels_py.py:14-30):
+ *   out[i] += sum_j exp(-||tgt_i - src_j||^2 * inv_delta) * q_j, skipping pairs with
+ *   r^2 > r2_cut (pass +inf to disable).  periodic != 0 replaces it with
+ *   gauss_direct_periodic (_kernels_py.py:33-46): minimum image diff -= rint(diff). */
+int fgt_gauss_direct(const double* tgt, int64_t nt, const double* src, int64_t ns,
+                     const double* q, int d, double inv_delta, double r2_cut, int periodic,
+                     double* out);
+
+/* Replaces _kernels_py.nufft_spread (_kernels_py.py:65-81): Gaussian-kernel spreading
+ *   grid[(i0+o) mod n_r] += exp(-z^2/(4 tau)) * val, z = x - (rint(x/h_r)+o) h_r,
+ *   o in [-m_sp, m_sp] per axis, h_r = 2 pi / n_r.  x: (M,d) in [0,2pi); vals: (M,)
+ *   complex128; grid: (n_r,)^d complex128 C-order, accumulated (caller zero-fills). */
+int fgt_nufft_spread(const double* x, int64_t M, int d, const double* vals_c128,
+                     int64_t n_r, int m_sp, double tau, double* grid_c128);
+
+/* Replaces _kernels_py.nufft_interp (_kernels_py.py:84-100): out (M,) complex128 is
+ *   overwritten with the adjoint gather of the same taps. */
+int fgt_nufft_interp(const double* x, int64_t M, int d, const double* grid_c128,
+                     int64_t n_r, int m_sp, double tau, double* out_c128);
+
+/* Device-pointer variants of the three kernels (stream = cudaStream_t or NULL). */
+int fgt_gauss_direct_dev(const double* tgt, int64_t nt, const double* src, int64_t ns,
+                         const double* q, int d, double inv_delta, double r2_cut,
+                         int periodic, double* out, void* stream);
+int fgt_nufft_spread_dev(const double* x, int64_t M, int d, const double* vals_c128,
+                         int64_t n_r, int m_sp, double tau, double* grid_c128, void* stream);
+int fgt_nufft_interp_dev(const double* x, int64_t M, int d, const double* grid_c128,
+                         int64_t n_r, int m_sp, double tau, double* out_c128, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Layer 2: discrete FGT pipeline.
+ * ------------------------------------------------------------------------- */
+
+/* Host-side plane-wave parameters.  The Python host computes them with the same
+ * numpy expressions as planewave.pw_params (planewave.py:73-98) and
+ * tree.cutoff_level (tree.py:24-50) so the tree is bit-identical; the library never
+ * re-derives D0 from epsilon. */
+typedef struct fgt_pw_params {
+  int32_t dim;          /* 1, 2 or 3 */
+  int32_t n_f;          /* modes per dimension (even) */
+  double delta;         /* Gaussian variance */
+  double D0;            /* sqrt(log(3/eps_clamped)) */
+  double h;             /* mode spacing 2 pi / (R + D0) */
+  const double* weights_1d; /* (n_f,) host array: h/(2 sqrt(pi)) exp(-m^2 h^2/4) */
+} fgt_pw_params;
+
+/* Tree construction controls (build_point_tree, tree.py:442-527). */
+typedef struct fgt_tree_params {
+  int32_t dim;
+  int32_t periodic;     /* 0 free space, 1 unit cell [-1/2,1/2)^d */
+  int64_t n_s;          /* split boxes with more than n_s sources+targets */
+  double D0;            /* cutoff factor (as above) */
+  double delta;
+  /* periodic trees only: l_c from cutoff_level(kind="density"), root side 1 */
+  int32_t l_c_periodic;
+} fgt_tree_params;
+
+/* Opaque GPU tree + partition, resident on the device. */
+typedef struct fgt_tree fgt_tree;
+
+/* Summary of a built tree. */
+typedef struct fgt_tree_info {
+  int32_t dim;
+  int32_t l_c;
+  int32_t n_levels;
+  int32_t periodic;
+  int64_t n_boxes;
+  int64_t n_leaves;
+  int64_t n_dense;      /* leaves at l_c holding > n_s points (the P-boxes) */
+  int64_t n_sources;
+  int64_t n_targets;
+  double root_center[3];
+  double root_side;
+} fgt_tree_info;
+
+/* Build the level-restricted tree of Alg 1 on the GPU from DEVICE arrays src (ns,d)
+ * and tgt (nt,d).  Box order is canonical: level-major, Morton order within a level
+ * (the reference numbers boxes by creation order; the box SET, parent/leaf relations,
+ * per-leaf ascending index lists and subtree counts are bit-identical). */
+int fgt_tree_build_dev(const double* src, int64_t ns, const double* tgt, int64_t nt,
+                       const fgt_tree_params* prm, void* stream, fgt_tree** out);
+int fgt_tree_get_info(const fgt_tree* t, fgt_tree_info* info);
+/* Copy the tree to caller-owned HOST arrays (any pointer may be NULL to skip):
+ * level (nb) i64, parent (nb) i64, children (nb, 2^d) i64, coords (nb, d) i64,
+ * is_leaf (nb) u8, src_perm (ns) i64, tgt_perm (nt) i64, src_start/src_count/
+ * tgt_start/tgt_count/n_points (nb) i64 -- the fields of tree.Tree (tree.py:53-115)
+ * and tree.PointPartition (tree.py:246-256). */
+int fgt_tree_copy_out(const fgt_tree* t, int64_t* level, int64_t* parent,
+                      int64_t* children, int64_t* coords, uint8_t* is_leaf,
+                      int64_t* src_perm, int64_t* tgt_perm, int64_t* src_start,
+                      int64_t* src_count, int64_t* tgt_start, int64_t* tgt_count,
+                      int64_t* n_points);
+void fgt_tree_free(fgt_tree* t);
+
+/* Interaction-list statistics for the built tree (target-centric P/D lists,
+ * PAPER.md:769-788).  Counts are the entries (T,S,v) of each list. */
+typedef struct fgt_list_info {
+  int64_t n_p_entries;
+  int64_t n_d_entries;
+  int64_t n_psi_boxes;  /* target leaves with a non-empty P-list */
+  int64_t n_direct_pairs; /* sum over D entries of n_tgt(T) * n_src(S) */
+} fgt_list_info;
+int fgt_tree_lists(fgt_tree* t, fgt_list_info* info);
+/* Copy the lists out (host arrays sized from fgt_list_info); v is (n, d) int64. */
+int fgt_tree_copy_lists(const fgt_tree* t, int64_t* p_tgt, int64_t* p_src, int64_t* p_v,
+                        int64_t* d_tgt, int64_t* d_src, int64_t* d_v);
+
+/* Per-phase device timings (ms, CUDA events) of the last fgt_points call. */
+typedef struct fgt_phase_times {
+  double tree_ms, lists_ms, form_ms, gather_ms, eval_ms, direct_ms, total_ms;
+  double h2d_ms, d2h_ms;
+  int64_t launches;
+} fgt_phase_times;
+
+/* Discrete FGT, DEVICE pointers: u (nt) is OVERWRITTEN with
+ *   u_i = sum_j exp(-||x_i - y_j||^2/delta) q_j   (relative l2 error <= ~eps)
+ * following Alg 2 with the tree of fgt_tree_build_dev.  charges (ns) real. */
+int fgt_points_dev(const double* src, int64_t ns, const double* charges,
+                   const double* tgt, int64_t nt, const fgt_tree_params* tp,
+                   const fgt_pw_params* pw, double* u, void* stream,
+                   fgt_phase_times* times);
+/* Same with HOST pointers; the H2D of inputs and D2H of u are inside the call. */
+int fgt_points(const double* src, int64_t ns, const double* charges, const double* tgt,
+               int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, double* u,
+               fgt_phase_times* times);
+
+/* Microbenchmarks used for the roofline denominators (FP64 pipes). */
+int fgt_bench_fp64_peak(int use_dmma, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGT_CUDA_H */

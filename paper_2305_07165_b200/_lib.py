@@ -1,0 +1,131 @@
+"""ctypes binding of libfgtcuda.so (C ABI in include/fgt_cuda.h).
+
+There is no CPU fallback: if the library is missing or cannot be loaded, importing the
+CUDA paths raises immediately (FgtLibraryError) instead of silently computing on the
+host.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfgtcuda.so")
+
+FGT_OK, FGT_EINVAL, FGT_ECUDA, FGT_ERANGE, FGT_ENOMEM = 0, 1, 2, 3, 4
+
+
+class FgtLibraryError(RuntimeError):
+    """libfgtcuda.so is missing or failed to load."""
+
+
+class FgtPwParams(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("n_f", ctypes.c_int32), ("delta", ctypes.c_double),
+                ("D0", ctypes.c_double), ("h", ctypes.c_double),
+                ("weights_1d", ctypes.POINTER(ctypes.c_double))]
+
+
+class FgtTreeParams(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("periodic", ctypes.c_int32), ("n_s", ctypes.c_int64),
+                ("D0", ctypes.c_double), ("delta", ctypes.c_double),
+                ("l_c_periodic", ctypes.c_int32)]
+
+
+class FgtTreeInfo(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("l_c", ctypes.c_int32), ("n_levels", ctypes.c_int32),
+                ("periodic", ctypes.c_int32), ("n_boxes", ctypes.c_int64),
+                ("n_leaves", ctypes.c_int64), ("n_dense", ctypes.c_int64),
+                ("n_sources", ctypes.c_int64), ("n_targets", ctypes.c_int64),
+                ("root_center", ctypes.c_double * 3), ("root_side", ctypes.c_double)]
+
+
+class FgtListInfo(ctypes.Structure):
+    _fields_ = [("n_p_entries", ctypes.c_int64), ("n_d_entries", ctypes.c_int64),
+                ("n_psi_boxes", ctypes.c_int64), ("n_direct_pairs", ctypes.c_int64)]
+
+
+class FgtPhaseTimes(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("tree_ms", "lists_ms", "form_ms", "gather_ms", "eval_ms", "direct_ms",
+                 "total_ms", "h2d_ms", "d2h_ms")] + [("launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+
+# name -> (restype, argtypes); also the list the CPU test checks against the header.
+SIGNATURES = {
+    "fgt_last_error": (ctypes.c_char_p, []),
+    "fgt_version": (ctypes.c_char_p, []),
+    "fgt_launch_count": (_I64, []),
+    "fgt_reset_launch_count": (None, []),
+    "fgt_gauss_direct": (_I, [_P, _I64, _P, _I64, _P, _I, _D, _D, _I, _P]),
+    "fgt_nufft_spread": (_I, [_P, _I64, _I, _P, _I64, _I, _D, _P]),
+    "fgt_nufft_interp": (_I, [_P, _I64, _I, _P, _I64, _I, _D, _P]),
+    "fgt_gauss_direct_dev": (_I, [_P, _I64, _P, _I64, _P, _I, _D, _D, _I, _P, _P]),
+    "fgt_nufft_spread_dev": (_I, [_P, _I64, _I, _P, _I64, _I, _D, _P, _P]),
+    "fgt_nufft_interp_dev": (_I, [_P, _I64, _I, _P, _I64, _I, _D, _P, _P]),
+    "fgt_tree_build_dev": (_I, [_P, _I64, _P, _I64, ctypes.POINTER(FgtTreeParams), _P,
+                                ctypes.POINTER(_P)]),
+    "fgt_tree_get_info": (_I, [_P, ctypes.POINTER(FgtTreeInfo)]),
+    "fgt_tree_copy_out": (_I, [_P] + [_P] * 12),
+    "fgt_tree_free": (None, [_P]),
+    "fgt_tree_lists": (_I, [_P, ctypes.POINTER(FgtListInfo)]),
+    "fgt_tree_copy_lists": (_I, [_P] + [_P] * 6),
+    "fgt_points_dev": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
+                            ctypes.POINTER(FgtPwParams), _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_points": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
+                        ctypes.POINTER(FgtPwParams), _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_bench_fp64_peak": (_I, [_I, ctypes.POINTER(_D)]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes handle; raise FgtLibraryError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FgtLibraryError(
+            f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as e:
+        raise FgtLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status):
+    """Map a C status code to the reference's Python exceptions."""
+    if status == FGT_OK:
+        return
+    msg = load().fgt_last_error().decode(errors="replace")
+    if status in (FGT_EINVAL, FGT_ERANGE):
+        raise ValueError(msg)
+    if status == FGT_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(a):
+    """Raw data pointer of a C-contiguous numpy array (or None)."""
+    if a is None:
+        return None
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def as_c(a, dtype=np.float64):
+    return np.ascontiguousarray(a, dtype=dtype)

@@ -1,0 +1,387 @@
+// extern "C" surface of libfgtcuda.so (declared in include/fgt_cuda.h).
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "k_kernels.cuh"
+#include "k_pw.cuh"
+
+namespace fgt {
+
+static thread_local std::string g_last_error;
+static thread_local int64_t g_launches = 0;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+// RAII stream for host-pointer entry points
+struct OwnedStream {
+  cudaStream_t s = nullptr;
+  OwnedStream() { FGT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~OwnedStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t st;
+  explicit Timer(cudaStream_t s) : st(s) {
+    FGT_CUDA(cudaEventCreate(&a));
+    FGT_CUDA(cudaEventCreate(&b));
+    FGT_CUDA(cudaEventRecord(a, st));
+  }
+  double lap() {
+    FGT_CUDA(cudaEventRecord(b, st));
+    FGT_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    FGT_CUDA(cudaEventElapsedTime(&ms, a, b));
+    std::swap(a, b);
+    return ms;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+__global__ void scatter_kernel(const double* __restrict__ us, const int64_t* __restrict__ perm, int64_t n,
+                               double* __restrict__ u) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    u[perm[i]] = us[i];
+}
+
+static void points_pipeline(const double* src, int64_t ns, const double* q, const double* tgt,
+                            int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw,
+                            double* u, cudaStream_t st, fgt_phase_times* times) {
+  FGT_REQUIRE(tp.dim == pw.dim, FGT_EINVAL, "tree/plane-wave dim mismatch");
+  const int64_t l0 = g_launches;
+  Timer tm(st);
+  fgt_phase_times t{};
+  TreeDev T;
+  build_tree(T, src, ns, tgt, nt, tp, st);
+  gather_sorted_points(T, src, q, tgt);
+  t.tree_ms = tm.lap();
+  build_lists(T);
+  t.lists_ms = tm.lap();
+  DBuf<double> us(nt, st);
+  us.zero();
+  PwDev P;
+  if (T.n_dense > 0) {
+    pw_setup(P, T, pw);
+    pw_form(P, T);
+    t.form_ms = tm.lap();
+    pw_gather(P, T);
+    P.phi.release();
+    t.gather_ms = tm.lap();
+    pw_eval(P, T, us.get());
+    P.psi.release();
+    t.eval_ms = tm.lap();
+  }
+  const double D0 = tp.D0;
+  direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get());
+  if (nt > 0) {
+    scatter_kernel<<<grid_for(nt, 256), 256, 0, st>>>(us.get(), T.tgt_perm.get(), nt, u);
+    FGT_LAUNCHED();
+  }
+  t.direct_ms = tm.lap();
+  t.total_ms = t.tree_ms + t.lists_ms + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
+  t.launches = g_launches - l0;
+  if (times) *times = t;
+}
+
+// ---------------------------------------------------------------- microbenchmarks
+__global__ void fp64_dfma_kernel(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-10, a2 = a0 + 2e-10, a3 = a0 + 3e-10;
+  double a4 = a0 + 4e-10, a5 = a0 + 5e-10, a6 = a0 + 6e-10, a7 = a0 + 7e-10;
+  const double b = 0.999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void fp64_dmma_kernel(double* out, int iters) {
+  double d[8][2];
+  for (int i = 0; i < 8; ++i) d[i][0] = d[i][1] = 0.0;
+  double a = threadIdx.x * 1e-6, b = 1.0 - threadIdx.x * 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[t][0]), "+d"(d[t][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+
+}  // namespace fgt
+
+using namespace fgt;
+
+extern "C" {
+
+const char* fgt_last_error(void) { return g_last_error.c_str(); }
+const char* fgt_version(void) { return "0.1.0+sm_100a"; }
+int64_t fgt_launch_count(void) { return g_launches; }
+void fgt_reset_launch_count(void) { g_launches = 0; }
+
+int fgt_gauss_direct_dev(const double* tgt, int64_t nt, const double* src, int64_t ns,
+                         const double* q, int d, double inv_delta, double r2_cut, int periodic,
+                         double* out, void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(nt >= 0 && ns >= 0, FGT_EINVAL, "negative size");
+    launch_gauss_direct_allpairs(tgt, nt, src, ns, q, d, inv_delta, r2_cut, periodic != 0, out,
+                                 (cudaStream_t)stream);
+  });
+}
+
+int fgt_gauss_direct(const double* tgt, int64_t nt, const double* src, int64_t ns,
+                     const double* q, int d, double inv_delta, double r2_cut, int periodic,
+                     double* out) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(nt >= 0 && ns >= 0, FGT_EINVAL, "negative size");
+    if (nt == 0) return;
+    OwnedStream os;
+    DBuf<double> dt(nt * d, os.s), ds(ns * d, os.s), dq(ns, os.s), dout(nt, os.s);
+    dt.from_host(tgt, nt * d);
+    ds.from_host(src, ns * d);
+    dq.from_host(q, ns);
+    dout.from_host(out, nt);
+    launch_gauss_direct_allpairs(dt.get(), nt, ds.get(), ns, dq.get(), d, inv_delta, r2_cut,
+                                 periodic != 0, dout.get(), os.s);
+    dout.to_host(out, nt);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+  });
+}
+
+int fgt_nufft_spread_dev(const double* x, int64_t M, int d, const double* vals, int64_t n_r,
+                         int m_sp, double tau, double* grid, void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(n_r >= 1 && m_sp >= 0 && tau > 0, FGT_EINVAL, "bad spreading parameters");
+    launch_nufft_spread(x, M, d, vals, n_r, m_sp, tau, grid, (cudaStream_t)stream);
+  });
+}
+
+int fgt_nufft_spread(const double* x, int64_t M, int d, const double* vals, int64_t n_r, int m_sp,
+                     double tau, double* grid) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(n_r >= 1 && m_sp >= 0 && tau > 0, FGT_EINVAL, "bad spreading parameters");
+    int64_t ng = 1;
+    for (int k = 0; k < d; ++k) ng *= n_r;
+    OwnedStream os;
+    DBuf<double> dx(M * d, os.s), dv(2 * M, os.s), dg(2 * ng, os.s);
+    dx.from_host(x, M * d);
+    dv.from_host(vals, 2 * M);
+    dg.from_host(grid, 2 * ng);
+    launch_nufft_spread(dx.get(), M, d, dv.get(), n_r, m_sp, tau, dg.get(), os.s);
+    dg.to_host(grid, 2 * ng);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+  });
+}
+
+int fgt_nufft_interp_dev(const double* x, int64_t M, int d, const double* grid, int64_t n_r,
+                         int m_sp, double tau, double* out, void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(n_r >= 1 && m_sp >= 0 && tau > 0, FGT_EINVAL, "bad spreading parameters");
+    launch_nufft_interp(x, M, d, grid, n_r, m_sp, tau, out, (cudaStream_t)stream);
+  });
+}
+
+int fgt_nufft_interp(const double* x, int64_t M, int d, const double* grid, int64_t n_r, int m_sp,
+                     double tau, double* out) {
+  return guarded([&] {
+    FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(n_r >= 1 && m_sp >= 0 && tau > 0, FGT_EINVAL, "bad spreading parameters");
+    if (M == 0) return;
+    int64_t ng = 1;
+    for (int k = 0; k < d; ++k) ng *= n_r;
+    OwnedStream os;
+    DBuf<double> dx(M * d, os.s), dg(2 * ng, os.s), dout(2 * M, os.s);
+    dx.from_host(x, M * d);
+    dg.from_host(grid, 2 * ng);
+    launch_nufft_interp(dx.get(), M, d, dg.get(), n_r, m_sp, tau, dout.get(), os.s);
+    dout.to_host(out, 2 * M);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+  });
+}
+
+struct fgt_tree {
+  TreeDev T;
+};
+
+int fgt_tree_build_dev(const double* src, int64_t ns, const double* tgt, int64_t nt,
+                       const fgt_tree_params* prm, void* stream, fgt_tree** out) {
+  return guarded([&] {
+    FGT_REQUIRE(prm && out, FGT_EINVAL, "null argument");
+    auto t = std::make_unique<fgt_tree>();
+    build_tree(t->T, src, ns, tgt, nt, *prm, (cudaStream_t)stream);
+    FGT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    *out = t.release();
+  });
+}
+
+int fgt_tree_get_info(const fgt_tree* t, fgt_tree_info* info) {
+  return guarded([&] {
+    FGT_REQUIRE(t && info, FGT_EINVAL, "null argument");
+    const TreeDev& T = t->T;
+    std::memset(info, 0, sizeof(*info));
+    info->dim = T.d;
+    info->l_c = T.l_c;
+    info->n_levels = T.n_levels;
+    info->periodic = T.periodic;
+    info->n_boxes = T.nb;
+    info->n_leaves = T.n_leaves;
+    info->n_dense = T.n_dense;
+    info->n_sources = T.ns;
+    info->n_targets = T.nt;
+    for (int k = 0; k < 3; ++k) info->root_center[k] = T.root_center[k];
+    info->root_side = T.root_side;
+  });
+}
+
+int fgt_tree_copy_out(const fgt_tree* t, int64_t* level, int64_t* parent, int64_t* children,
+                      int64_t* coords, uint8_t* is_leaf, int64_t* src_perm, int64_t* tgt_perm,
+                      int64_t* src_start, int64_t* src_count, int64_t* tgt_start,
+                      int64_t* tgt_count, int64_t* n_points) {
+  return guarded([&] {
+    FGT_REQUIRE(t, FGT_EINVAL, "null tree");
+    const TreeDev& T = t->T;
+    cudaStream_t st = T.st;
+    const int64_t nb = T.nb;
+    if (level) {
+      std::vector<int32_t> l32(nb);
+      T.level.to_host(l32.data(), nb);
+      FGT_CUDA(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < nb; ++i) level[i] = l32[i];
+    }
+    if (parent) T.parent.to_host(parent, nb);
+    if (children) T.children.to_host(children, nb << T.d);
+    if (coords) T.coords.to_host(coords, nb * T.d);
+    if (is_leaf) T.is_leaf.to_host(is_leaf, nb);
+    if (src_perm) T.src_perm.to_host(src_perm, T.ns);
+    if (tgt_perm) T.tgt_perm.to_host(tgt_perm, T.nt);
+    if (src_start) T.src_start.to_host(src_start, nb);
+    if (src_count) T.src_count.to_host(src_count, nb);
+    if (tgt_start) T.tgt_start.to_host(tgt_start, nb);
+    if (tgt_count) T.tgt_count.to_host(tgt_count, nb);
+    if (n_points) T.n_points.to_host(n_points, nb);
+    FGT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fgt_tree_lists(fgt_tree* t, fgt_list_info* info) {
+  return guarded([&] {
+    FGT_REQUIRE(t, FGT_EINVAL, "null tree");
+    build_lists(t->T);
+    FGT_CUDA(cudaStreamSynchronize(t->T.st));
+    if (info) {
+      info->n_p_entries = t->T.n_p;
+      info->n_d_entries = t->T.n_d;
+      info->n_psi_boxes = t->T.n_psi;
+      info->n_direct_pairs = t->T.n_direct_pairs;
+    }
+  });
+}
+
+int fgt_tree_copy_lists(const fgt_tree* t, int64_t* p_tgt, int64_t* p_src, int64_t* p_v,
+                        int64_t* d_tgt, int64_t* d_src, int64_t* d_v) {
+  return guarded([&] {
+    FGT_REQUIRE(t && t->T.lists_built, FGT_EINVAL, "lists not built");
+    const TreeDev& T = t->T;
+    cudaStream_t st = T.st;
+    const int d = T.d;
+    std::vector<int64_t> slot(T.n_p), dense(T.n_dense);
+    std::vector<int32_t> pv(T.n_p * d), dv(T.n_d * d);
+    T.p_src.to_host(slot.data(), T.n_p);
+    T.dense_ids.to_host(dense.data(), T.n_dense);
+    T.p_v.to_host(pv.data(), T.n_p * d);
+    T.d_v.to_host(dv.data(), T.n_d * d);
+    if (p_tgt) T.p_tgt.to_host(p_tgt, T.n_p);
+    if (d_tgt) T.d_tgt.to_host(d_tgt, T.n_d);
+    if (d_src) T.d_src.to_host(d_src, T.n_d);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    if (p_src)
+      for (int64_t i = 0; i < T.n_p; ++i) p_src[i] = dense[slot[i]];
+    if (p_v)
+      for (int64_t i = 0; i < T.n_p * d; ++i) p_v[i] = pv[i];
+    if (d_v)
+      for (int64_t i = 0; i < T.n_d * d; ++i) d_v[i] = dv[i];
+  });
+}
+
+void fgt_tree_free(fgt_tree* t) {
+  if (t) {
+    cudaStreamSynchronize(t->T.st);
+    delete t;
+  }
+}
+
+int fgt_points_dev(const double* src, int64_t ns, const double* charges, const double* tgt,
+                   int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, double* u,
+                   void* stream, fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(tp && pw, FGT_EINVAL, "null parameters");
+    points_pipeline(src, ns, charges, tgt, nt, *tp, *pw, u, (cudaStream_t)stream, times);
+  });
+}
+
+int fgt_points(const double* src, int64_t ns, const double* charges, const double* tgt, int64_t nt,
+               const fgt_tree_params* tp, const fgt_pw_params* pw, double* u,
+               fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(tp && pw, FGT_EINVAL, "null parameters");
+    const int d = tp->dim;
+    OwnedStream os;
+    Timer tm(os.s);
+    DBuf<double> ds(ns * d, os.s), dq(ns, os.s), dt(nt * d, os.s), du(nt, os.s);
+    ds.from_host(src, ns * d);
+    dq.from_host(charges, ns);
+    dt.from_host(tgt, nt * d);
+    double h2d = tm.lap();
+    fgt_phase_times t{};
+    points_pipeline(ds.get(), ns, dq.get(), dt.get(), nt, *tp, *pw, du.get(), os.s, &t);
+    tm.lap();
+    du.to_host(u, nt);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+    t.h2d_ms = h2d;
+    t.d2h_ms = tm.lap();
+    if (times) *times = t;
+  });
+}
+
+int fgt_bench_fp64_peak(int use_dmma, double* tflops) {
+  return guarded([&] {
+    OwnedStream os;
+    DBuf<double> out(1, os.s);
+    int dev = 0, nsm = 0;
+    FGT_CUDA(cudaGetDevice(&dev));
+    FGT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int block = 256, grid = nsm * 8;
+    const int iters = use_dmma ? 4096 : 16384;
+    for (int rep = 0; rep < 2; ++rep) {
+      Timer tm(os.s);
+      if (use_dmma) fp64_dmma_kernel<<<grid, block, 0, os.s>>>(out.get(), iters);
+      else fp64_dfma_kernel<<<grid, block, 0, os.s>>>(out.get(), iters);
+      FGT_LAUNCHED();
+      double ms = tm.lap();
+      double flops = use_dmma ? (double)grid * (block / 32) * iters * 8 * 256 * 2
+                              : (double)grid * block * iters * 8 * 2;
+      *tflops = flops / (ms * 1e-3) / 1e12;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// Shared helpers for libfgtcuda (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdio>
+#include <string>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/fgt_cuda.h"
+
+namespace fgt {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+void count_launch(int n = 1);
+
+#define FGT_CUDA(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      throw ::fgt::Error(_e == cudaErrorMemoryAllocation ? FGT_ENOMEM : FGT_ECUDA,  \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e) +      \
+                             " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+    }                                                                               \
+  } while (0)
+
+#define FGT_LAUNCHED()                 \
+  do {                                 \
+    FGT_CUDA(cudaPeekAtLastError());   \
+    ::fgt::count_launch();             \
+  } while (0)
+
+#define FGT_REQUIRE(cond, code, msg)                   \
+  do {                                                 \
+    if (!(cond)) throw ::fgt::Error((code), (msg));    \
+  } while (0)
+
+// Run a body, translating exceptions into C status codes.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FGT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return FGT_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return FGT_ECUDA;
+  }
+}
+
+// ---------------------------------------------------------------- device buffers
+// Stream-ordered device allocation (cudaMallocAsync pool): frees are ordered after
+// the work already queued on the stream, so scratch never needs a device sync.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) FGT_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+  }
+  void zero() {
+    if (n) FGT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  T* get() const { return p; }
+  size_t size() const { return n; }
+  void to_host(T* h, size_t count) const {
+    if (count) FGT_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void from_host(const T* h, size_t count) {
+    if (count) FGT_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 64) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// ---------------------------------------------------------------- device math
+// Box centre per axis exactly as tree._Builder.center (tree.py:324-326):
+//   (root_center - 0.5*root_side) + (coord + 0.5) * s,  s = root_side / 2**level.
+// Each operation is rounded separately (no FMA contraction), which is what numpy does.
+__device__ __forceinline__ double box_center_1d(double root_low, int64_t coord, double s) {
+  return __dadd_rn(root_low, __dmul_rn((double)coord + 0.5, s));
+}
+
+__host__ __device__ __forceinline__ int pow2i(int k) { return 1 << k; }
+
+// Morton helpers: a box at level l with integer coords g (each < 2^l) has code
+//   sum_{lv<l} childno(lv) << (d*(l-1-lv)),  childno = sum_k bit_k << k
+// (child c has axis-k bit (c>>k)&1, tree.py:314-315), so code(parent) = code >> d.
+__host__ __device__ __forceinline__ uint64_t morton_encode(const int64_t* g, int d, int l) {
+  uint64_t code = 0;
+  for (int b = l - 1; b >= 0; --b) {
+    uint64_t c = 0;
+    for (int k = 0; k < d; ++k) c |= (uint64_t)((g[k] >> b) & 1) << k;
+    code = (code << d) | c;
+  }
+  return code;
+}
+__host__ __device__ __forceinline__ void morton_decode(uint64_t code, int d, int l, int64_t* g) {
+  for (int k = 0; k < d; ++k) g[k] = 0;
+  for (int b = 0; b < l; ++b) {
+    uint64_t c = (code >> (d * b)) & ((1u << d) - 1);
+    for (int k = 0; k < d; ++k) g[k] |= (int64_t)((c >> k) & 1) << b;
+  }
+}
+
+// Global box key: level in the top 6 bits, Morton code below (level-major order).
+constexpr int KEY_LEVEL_SHIFT = 58;
+__host__ __device__ __forceinline__ uint64_t box_key(int level, uint64_t code) {
+  return ((uint64_t)level << KEY_LEVEL_SHIFT) | code;
+}
+__host__ __device__ __forceinline__ int key_level(uint64_t key) {
+  return (int)(key >> KEY_LEVEL_SHIFT);
+}
+__host__ __device__ __forceinline__ uint64_t key_code(uint64_t key) {
+  return key & ((1ull << KEY_LEVEL_SHIFT) - 1);
+}
+
+// lower_bound on a sorted device array.
+template <class T>
+__device__ __forceinline__ int64_t lower_bound_dev(const T* a, int64_t n, T v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+template <class T>
+__device__ __forceinline__ int64_t find_dev(const T* a, int64_t n, T v) {
+  int64_t i = lower_bound_dev(a, n, v);
+  return (i < n && a[i] == v) ? i : -1;
+}
+
+}  // namespace fgt

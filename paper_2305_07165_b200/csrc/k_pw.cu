@@ -1,0 +1,690 @@
+// Plane-wave phases of the discrete FGT (Alg 2) on sm_100a.
+//
+//   form    phi_l(S) = w_l sum_j q_j exp(-i k_l.(y_j - c_S))
+//   gather  psi_l(T) = sum_{(S,v) in L_P(T)} exp(i k_l.(c_T - c_S - v)) phi_l(S)  (:825-828)
+//   eval    u(x)    += Re sum_l exp(i k_l.(x - c_T)) psi_l(T)          (:833-835)
+//   direct  u(x)    += sum_{(S,v) in L_D(T)} sum_{|x-y-v|^2 <= D0^2 delta} exp(-|x-y-v|^2/delta) q
+//
+// The reference evaluates form/eval with nufft_type1/2 (nufft.py:139-183), which at
+// every BASELINE configuration dispatches to the exact tensor-factored sums of
+// dft_oracle (nufft.py:65-103).  Here those sums are complex GEMMs on the FP64 tensor
+// cores (mma.sync m8n8k4 .f64 -> SASS DMMA; tcgen05 has no f64 kind):
+//   form: phi[r, c] = sum_j A[r, j] E_last[j, c],  A[r, j] = q_j prod_{k<d-1} E_k[j, r_k]
+//   eval: T1[j, r]  = sum_c E'_last[j, c] psi[r, c];  u_j = Re sum_r T1[j, r] prod E'_k[j, r_k]
+// with r the flattened leading d-1 mode indices (C order, axis 0 slowest, ModeGrid
+// layout nufft.py:20-48) and c the last-axis mode.  Per-point 1-D phase tables are
+// built in shared memory (sincos per 8-mode segment + rotation recurrence).
+#include "k_pw.cuh"
+
+namespace fgt {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// etab[k][j][mi] = exp(sign * i * m * x_jk), m = mi - n_f/2, x_jk = (p_jk - ctr_k) * sc,
+// zero for j >= cnt or mi >= n_f.  KC rows, NFP (multiple of 8) columns.
+template <int D>
+__device__ void build_etab(double2* __restrict__ etab, int KC, int NFP, const double* __restrict__ pts,
+                           int64_t base, int cnt, const double* ctr, double sc, double sign, int n_f) {
+  const int nseg = NFP >> 3;
+  const int ntask = KC * D * nseg;
+  for (int task = threadIdx.x; task < ntask; task += blockDim.x) {
+    int seg = task % nseg;
+    int rest = task / nseg;
+    int k = rest % D;
+    int j = rest / D;
+    double2* out = etab + ((size_t)k * KC + j) * NFP + seg * 8;
+    if (j >= cnt) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) out[t] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double x = (pts[(base + j) * D + k] - ctr[k]) * sc;
+    int m0 = seg * 8 - n_f / 2;
+    double s0, c0, s1, c1;
+    sincos(sign * (double)m0 * x, &s0, &c0);
+    sincos(sign * x, &s1, &c1);
+    double2 val = make_double2(c0, s0);
+    const double2 step = make_double2(c1, s1);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      out[t] = (seg * 8 + t < n_f) ? val : make_double2(0.0, 0.0);
+      val = cmul(val, step);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ form
+struct FormArgs {
+  const double* src;        // sorted sources (ns, d)
+  const double* q;          // sorted charges
+  const double* center;     // (nb, d)
+  const int64_t* dense_ids; // slot -> box
+  const int64_t* src_start;
+  const int4* units;        // (slot, k0, kn, scratch index or -1)
+  double2* phi;
+  double2* scratch;
+  const double* w1d;
+  int n_f, R, MG, KS;
+  double sc;
+};
+
+constexpr int FORM_KC = 32;
+constexpr int FORM_MT = 2;
+
+template <int D, int NT>
+__global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int KC = FORM_KC, MT = FORM_MT, NFP = NT * 8;
+  double2* etab = sm;
+  double* sq = reinterpret_cast<double*>(etab + D * KC * NFP);
+  const int4 u = a.units[blockIdx.y];
+  const int slot = u.x, k0 = u.y, kn = u.z, oidx = u.w;
+  const int64_t box = a.dense_ids[slot];
+  const int64_t pbase = a.src_start[box] + k0;
+  double ctr[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ctr[k] = a.center[box * D + k];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mg = warp % a.MG, ks = warp / a.MG;
+  const bool active = ks < a.KS;
+  const int row0 = (blockIdx.x * a.MG + mg) * MT * 8;
+  const int n_f = a.n_f;
+
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+
+  int ra[MT], rb[MT];
+  bool rv[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    int r = row0 + mt * 8 + (lane >> 2);
+    rv[mt] = r < a.R;
+    ra[mt] = D == 3 ? r / n_f : r;
+    rb[mt] = D == 3 ? r % n_f : 0;
+  }
+
+  for (int c0 = 0; c0 < kn; c0 += KC) {
+    const int cnt = min(KC, kn - c0);
+    __syncthreads();
+    build_etab<D>(etab, KC, NFP, a.src, pbase + c0, cnt, ctr, a.sc, -1.0, n_f);
+    for (int t = threadIdx.x; t < KC; t += blockDim.x) sq[t] = t < cnt ? a.q[pbase + c0 + t] : 0.0;
+    __syncthreads();
+    if (active) {
+      for (int kk = ks; kk < KC / 4; kk += a.KS) {
+        const int j = kk * 4 + (lane & 3);
+        double2 b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = etab[((D - 1) * KC + j) * NFP + nt * 8 + (lane >> 2)];
+        const double qj = sq[j];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          double2 A = make_double2(0.0, 0.0);
+          if (rv[mt]) {
+            if (D == 1) {
+              A = make_double2(qj, 0.0);
+            } else if (D == 2) {
+              double2 e0 = etab[(0 * KC + j) * NFP + ra[mt]];
+              A = make_double2(qj * e0.x, qj * e0.y);
+            } else {
+              double2 e0 = etab[(0 * KC + j) * NFP + ra[mt]];
+              double2 e1 = etab[(1 * KC + j) * NFP + rb[mt]];
+              double2 p = cmul(e0, e1);
+              A = make_double2(qj * p.x, qj * p.y);
+            }
+          }
+          const double nai = -A.y;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma(acc[mt][nt][0], acc[mt][nt][1], A.x, b[nt].x);
+            dmma(acc[mt][nt][0], acc[mt][nt][1], nai, b[nt].y);
+            dmma(acc[mt][nt][2], acc[mt][nt][3], A.x, b[nt].y);
+            dmma(acc[mt][nt][2], acc[mt][nt][3], A.y, b[nt].x);
+          }
+        }
+      }
+    }
+  }
+
+  // reduce the K-split warps into the ks == 0 warp of each m-group
+  if (a.KS > 1) {
+    double* red = reinterpret_cast<double*>(sm);
+    for (int s = 1; s < a.KS; ++s) {
+      __syncthreads();
+      if (ks == s) {
+        double* dst = red + ((size_t)mg * 32 + lane) * MT * NT * 4;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[(mt * NT + nt) * 4 + e] = acc[mt][nt][e];
+      }
+      __syncthreads();
+      if (ks == 0) {
+        const double* srcp = red + ((size_t)mg * 32 + lane) * MT * NT * 4;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[mt][nt][e] += srcp[(mt * NT + nt) * 4 + e];
+      }
+    }
+  }
+  if (ks != 0) return;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = row0 + mt * 8 + (lane >> 2);
+    if (r >= a.R) continue;
+    double wr = 1.0;
+    if (D == 2) wr = a.w1d[r];
+    if (D == 3) wr = a.w1d[r / n_f] * a.w1d[r % n_f];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = nt * 8 + 2 * (lane & 3) + i;
+        if (c >= n_f) continue;
+        double re = acc[mt][nt][i], im = acc[mt][nt][2 + i];
+        if (oidx < 0) {
+          double w = wr * a.w1d[c];
+          a.phi[((size_t)slot * a.R + r) * n_f + c] = make_double2(re * w, im * w);
+        } else {
+          a.scratch[((size_t)oidx * a.R + r) * n_f + c] = make_double2(re, im);
+        }
+      }
+    }
+  }
+}
+
+// sum the K-split partials of multi-unit boxes (fixed order: deterministic)
+template <int D>
+__global__ void form_reduce_kernel(const double2* __restrict__ scratch, const int4* __restrict__ red,
+                                   int64_t NF, int n_f, const double* __restrict__ w1d,
+                                   double2* __restrict__ phi) {
+  const int4 rj = red[blockIdx.y];  // (slot, first scratch, count, -)
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NF;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int t = 0; t < rj.z; ++t) {
+      double2 v = scratch[(size_t)(rj.y + t) * NF + e];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    int64_t rem = e;
+    double w = 1.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      w *= w1d[rem % n_f];
+      rem /= n_f;
+    }
+    phi[(size_t)rj.x * NF + e] = make_double2(s.x * w, s.y * w);
+  }
+}
+
+__global__ void gather_counts_kernel(const int64_t* __restrict__ ids, int64_t n,
+                                     const int64_t* __restrict__ cnt, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = cnt[ids[i]];
+}
+
+// ------------------------------------------------------------------ gather
+struct GatherArgs {
+  const int64_t* psi_ids;
+  const int64_t* p_off;
+  const int64_t* p_src;   // dense slot
+  const int32_t* p_v;
+  const int64_t* dense_ids;
+  const int64_t* coords;
+  const double2* phase;   // (3, n_f)
+  const double2* phi;
+  double2* psi;
+  int64_t NF;
+  int n_f, l_c;
+};
+
+constexpr int GATHER_MAXE = 64;
+
+template <int D>
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+  __shared__ int s_o[GATHER_MAXE][D];
+  __shared__ int64_t s_slot[GATHER_MAXE];
+  const int64_t i = blockIdx.y;
+  const int64_t T = a.psi_ids[i];
+  const int64_t e0 = a.p_off[i];
+  const int64_t ne64 = a.p_off[i + 1] - e0;
+  const int ne = (int)(ne64 < GATHER_MAXE ? ne64 : GATHER_MAXE);
+  const int64_t side = (int64_t)1 << a.l_c;
+  for (int t = threadIdx.x; t < ne; t += blockDim.x) {
+    const int64_t slot = a.p_src[e0 + t];
+    const int64_t S = a.dense_ids[slot];
+    s_slot[t] = slot;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      int64_t o = a.coords[T * D + k] - (a.coords[S * D + k] + (int64_t)a.p_v[(e0 + t) * D + k] * side);
+      s_o[t][k] = (int)o + 1;  // index into phase rows (-1, 0, 1)
+    }
+  }
+  __syncthreads();
+  const int n_f = a.n_f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.NF;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int m[D];
+    int64_t rem = e;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      m[k] = (int)(rem % n_f);
+      rem /= n_f;
+    }
+    double2 acc = make_double2(0.0, 0.0);
+    for (int t = 0; t < ne; ++t) {
+      double2 p = a.phase[s_o[t][0] * n_f + m[0]];
+#pragma unroll
+      for (int k = 1; k < D; ++k) p = cmul(p, a.phase[s_o[t][k] * n_f + m[k]]);
+      double2 f = a.phi[(size_t)s_slot[t] * a.NF + e];
+      acc.x += p.x * f.x - p.y * f.y;
+      acc.y += p.x * f.y + p.y * f.x;
+    }
+    a.psi[(size_t)i * a.NF + e] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ eval
+struct EvalArgs {
+  const double* tgt;      // sorted targets
+  const double* center;
+  const int64_t* psi_ids;
+  const int64_t* tgt_start;
+  const int64_t* tgt_count;
+  const double2* psi;
+  double* u;
+  int n_f, R, ksteps;
+  double sc;
+};
+
+constexpr int EVAL_TB = 32;
+constexpr int EVAL_MT = 4;
+
+template <int D, int NT>
+__global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int TB = EVAL_TB, MT = EVAL_MT, NFP = NT * 8;
+  double2* etab = sm;
+  double* s_u = reinterpret_cast<double*>(etab + D * TB * NFP);
+  const int64_t i = blockIdx.x;
+  const int64_t T = a.psi_ids[i];
+  const int64_t t0 = a.tgt_start[T];
+  const int ntg = (int)a.tgt_count[T];
+  double ctr[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ctr[k] = a.center[T * D + k];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int n_f = a.n_f, R = a.R;
+  const int ntiles = (R + 7) / 8;
+  const double2* psi = a.psi + (size_t)i * R * n_f;
+
+  for (int p0 = 0; p0 < ntg; p0 += TB) {
+    const int cnt = min(TB, ntg - p0);
+    __syncthreads();
+    build_etab<D>(etab, TB, NFP, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
+    __syncthreads();
+    double part[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) part[mt] = 0.0;
+    for (int nt = warp; nt < ntiles; nt += nwarps) {
+      double acc[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mt][e] = 0.0;
+      const int rb = nt * 8 + (lane >> 2);
+      for (int kk = 0; kk < a.ksteps; ++kk) {
+        const int c = kk * 4 + (lane & 3);
+        double2 B = make_double2(0.0, 0.0);
+        if (rb < R && c < n_f) B = psi[(size_t)rb * n_f + c];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double2 A = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * NFP + c];
+          dmma(acc[mt][0], acc[mt][1], A.x, B.x);
+          dmma(acc[mt][0], acc[mt][1], -A.y, B.y);
+          dmma(acc[mt][2], acc[mt][3], A.x, B.y);
+          dmma(acc[mt][2], acc[mt][3], A.y, B.x);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int j = mt * 8 + (lane >> 2);
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          const int r = nt * 8 + 2 * (lane & 3) + i2;
+          if (r >= R) continue;
+          double2 f = make_double2(1.0, 0.0);
+          if (D == 2) f = etab[(0 * TB + j) * NFP + r];
+          if (D == 3) f = cmul(etab[(0 * TB + j) * NFP + r / n_f], etab[(1 * TB + j) * NFP + r % n_f]);
+          part[mt] += acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y;
+        }
+      }
+    }
+    // deterministic cross-warp sum: per-warp partials, then a fixed-order reduction
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      double v = part[mt];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if ((lane & 3) == 0) s_u[warp * TB + mt * 8 + (lane >> 2)] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < nwarps; ++w) s += s_u[w * TB + t];
+      a.u[t0 + p0 + t] += s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ direct
+struct DirectArgs {
+  const int64_t* d_tgt_ids;
+  const int64_t* d_off;
+  const int64_t* d_src;
+  const int32_t* d_v;
+  const int64_t* src_start;
+  const int64_t* src_count;
+  const int64_t* tgt_start;
+  const int64_t* tgt_count;
+  const double* src;   // sorted
+  const double* q;     // sorted
+  const double* tgt;   // sorted
+  double* u;
+  double inv_delta, r2_cut, root_side;
+  int64_t n;
+};
+
+template <int D>
+__global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
+  constexpr int TILE = 128;
+  __shared__ double s_y[TILE * D];
+  __shared__ double s_q[TILE];
+  for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
+    const int64_t T = a.d_tgt_ids[i];
+    const int64_t e0 = a.d_off[i], e1 = a.d_off[i + 1];
+    if (e0 == e1) continue;
+    const int64_t t0 = a.tgt_start[T];
+    const int ntg = (int)a.tgt_count[T];
+    for (int tb = 0; tb < ntg; tb += blockDim.x) {
+      const int j = tb + threadIdx.x;
+      const bool valid = j < ntg;
+      double x[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = valid ? a.tgt[(t0 + j) * D + k] : 0.0;
+      double acc = 0.0;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t S = a.d_src[e];
+        const int64_t s0 = a.src_start[S];
+        const int nsrc = (int)a.src_count[S];
+        double shift[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) shift[k] = (double)a.d_v[e * D + k] * a.root_side;
+        for (int sb = 0; sb < nsrc; sb += TILE) {
+          const int nj = min(TILE, nsrc - sb);
+          __syncthreads();
+          for (int t = threadIdx.x; t < nj; t += blockDim.x) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) s_y[t * D + k] = a.src[(s0 + sb + t) * D + k] + shift[k];
+            s_q[t] = a.q[s0 + sb + t];
+          }
+          __syncthreads();
+          if (valid) {
+            for (int t = 0; t < nj; ++t) {
+              double r2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                double df = x[k] - s_y[t * D + k];
+                r2 += df * df;
+              }
+              if (r2 <= a.r2_cut) acc += exp(-r2 * a.inv_delta) * s_q[t];
+            }
+          }
+        }
+      }
+      if (valid) a.u[t0 + j] += acc;
+    }
+  }
+}
+
+template <int D, int NT>
+void launch_form(PwDev& P, TreeDev& T, const FormArgs& fa, int nrowblk, int nunits, size_t smem,
+                 cudaStream_t st) {
+  FGT_CUDA(cudaFuncSetAttribute(form_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(nrowblk, nunits);
+  form_kernel<D, NT><<<grid, 256, smem, st>>>(fa);
+  FGT_LAUNCHED();
+}
+
+template <int D, int NT>
+void launch_eval(const EvalArgs& ea, int64_t n_psi, cudaStream_t st) {
+  size_t smem = (size_t)D * EVAL_TB * NT * 8 * sizeof(double2) + 8 * EVAL_TB * sizeof(double);
+  FGT_CUDA(cudaFuncSetAttribute(eval_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  eval_kernel<D, NT><<<(unsigned)n_psi, 256, smem, st>>>(ea);
+  FGT_LAUNCHED();
+}
+
+}  // namespace
+
+// ====================================================================== host side
+
+void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
+  FGT_REQUIRE(pw.dim == T.d, FGT_EINVAL, "plane-wave dim != tree dim");
+  FGT_REQUIRE(pw.n_f >= 2 && pw.n_f % 2 == 0, FGT_EINVAL, "n_f must be even and >= 2");
+  FGT_REQUIRE(pw.n_f <= 64, FGT_ERANGE, "n_f > 64 not supported by the plane-wave kernels");
+  cudaStream_t st = T.st;
+  P.d = T.d;
+  P.n_f = pw.n_f;
+  P.R = 1;
+  for (int k = 0; k < P.d - 1; ++k) P.R *= P.n_f;
+  P.NF = P.R * P.n_f;
+  P.sc = pw.h / std::sqrt(pw.delta);
+  P.side_lc = T.root_side;
+  for (int l = 0; l < T.l_c; ++l) P.side_lc *= 0.5;
+  P.w1d.alloc(P.n_f, st);
+  P.w1d.from_host(pw.weights_1d, P.n_f);
+  std::vector<double> ph(3 * 2 * P.n_f);
+  for (int o = 0; o < 3; ++o)
+    for (int mi = 0; mi < P.n_f; ++mi) {
+      double m = (double)(mi - P.n_f / 2);
+      double arg = m * P.sc * (double)(o - 1) * P.side_lc;
+      ph[(o * P.n_f + mi) * 2] = std::cos(arg);
+      ph[(o * P.n_f + mi) * 2 + 1] = std::sin(arg);
+    }
+  P.phase.alloc(ph.size(), st);
+  P.phase.from_host(ph.data(), ph.size());
+}
+
+template <int D>
+static void pw_form_impl(PwDev& P, TreeDev& T) {
+  cudaStream_t st = T.st;
+  const int64_t nd = T.n_dense;
+  P.phi.alloc((size_t)nd * P.NF * 2, st);
+  if (nd == 0) return;
+  P.phi.zero();
+  // per-box source counts -> work units of at most KU points (split-K for big boxes)
+  DBuf<int64_t> cnt_d(nd, st);
+  gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), cnt_d.get());
+  FGT_LAUNCHED();
+  std::vector<int64_t> cnt(nd);
+  cnt_d.to_host(cnt.data(), nd);
+  FGT_CUDA(cudaStreamSynchronize(st));
+  const int KU = 2048;
+  std::vector<int4> units, reds;
+  int nscratch = 0;
+  for (int64_t s = 0; s < nd; ++s) {
+    int64_t n = cnt[s];
+    if (n == 0) continue;
+    int nu = (int)((n + KU - 1) / KU);
+    if (nu == 1) {
+      units.push_back(make_int4((int)s, 0, (int)n, -1));
+    } else {
+      reds.push_back(make_int4((int)s, nscratch, nu, 0));
+      for (int t = 0; t < nu; ++t) {
+        int k0 = t * KU;
+        units.push_back(make_int4((int)s, k0, (int)std::min<int64_t>(KU, n - k0), nscratch++));
+      }
+    }
+  }
+  if (units.empty()) return;
+  DBuf<int4> units_d(units.size(), st);
+  units_d.from_host(units.data(), units.size());
+  DBuf<double> scratch((size_t)nscratch * P.NF * 2, st);
+
+  const int n_f = P.n_f;
+  const int NT = (n_f + 7) / 8;
+  const int mtiles = (int)((P.R + 7) / 8);
+  const int groups = (mtiles + FORM_MT - 1) / FORM_MT;
+  int MG, KS, nrowblk;
+  if (groups >= 8) { MG = 8; KS = 1; nrowblk = (groups + 7) / 8; }
+  else { MG = groups; KS = 8 / MG; nrowblk = 1; }
+  FormArgs fa;
+  fa.src = T.src_sorted.get();
+  fa.q = T.q_sorted.get();
+  fa.center = T.center.get();
+  fa.dense_ids = T.dense_ids.get();
+  fa.src_start = T.src_start.get();
+  fa.units = units_d.get();
+  fa.phi = reinterpret_cast<double2*>(P.phi.get());
+  fa.scratch = reinterpret_cast<double2*>(scratch.get());
+  fa.w1d = P.w1d.get();
+  fa.n_f = n_f;
+  fa.R = (int)P.R;
+  fa.MG = MG;
+  fa.KS = KS;
+  fa.sc = P.sc;
+  const size_t etab_bytes = (size_t)D * FORM_KC * NT * 8 * sizeof(double2) + FORM_KC * sizeof(double);
+  const size_t red_bytes = (size_t)MG * 32 * FORM_MT * NT * 4 * sizeof(double);
+  const size_t smem = std::max(etab_bytes, red_bytes);
+  const int nunits = (int)units.size();
+  switch (NT) {
+#define FGT_FORM_CASE(NTV) case NTV: launch_form<D, NTV>(P, T, fa, nrowblk, nunits, smem, st); break;
+    FGT_FORM_CASE(1) FGT_FORM_CASE(2) FGT_FORM_CASE(3) FGT_FORM_CASE(4)
+    FGT_FORM_CASE(5) FGT_FORM_CASE(6) FGT_FORM_CASE(7) FGT_FORM_CASE(8)
+#undef FGT_FORM_CASE
+    default: throw Error(FGT_ERANGE, "n_f too large");
+  }
+  if (!reds.empty()) {
+    DBuf<int4> reds_d(reds.size(), st);
+    reds_d.from_host(reds.data(), reds.size());
+    dim3 grid(grid_for(P.NF, 256, 64), (unsigned)reds.size());
+    form_reduce_kernel<D><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(scratch.get()), reds_d.get(),
+                                                P.NF, n_f, P.w1d.get(), reinterpret_cast<double2*>(P.phi.get()));
+    FGT_LAUNCHED();
+  }
+}
+
+void pw_form(PwDev& P, TreeDev& T) {
+  if (T.d == 1) pw_form_impl<1>(P, T);
+  else if (T.d == 2) pw_form_impl<2>(P, T);
+  else pw_form_impl<3>(P, T);
+}
+
+void pw_gather(PwDev& P, TreeDev& T) {
+  cudaStream_t st = T.st;
+  P.psi.alloc((size_t)T.n_psi * P.NF * 2, st);
+  if (T.n_psi == 0) return;
+  GatherArgs ga;
+  ga.psi_ids = T.psi_ids.get();
+  ga.p_off = T.p_off.get();
+  ga.p_src = T.p_src.get();
+  ga.p_v = T.p_v.get();
+  ga.dense_ids = T.dense_ids.get();
+  ga.coords = T.coords.get();
+  ga.phase = reinterpret_cast<const double2*>(P.phase.get());
+  ga.phi = reinterpret_cast<const double2*>(P.phi.get());
+  ga.psi = reinterpret_cast<double2*>(P.psi.get());
+  ga.NF = P.NF;
+  ga.n_f = P.n_f;
+  ga.l_c = T.l_c;
+  dim3 grid(grid_for(P.NF, 256, 256), (unsigned)T.n_psi);
+  if (T.d == 1) gather_kernel<1><<<grid, 256, 0, st>>>(ga);
+  else if (T.d == 2) gather_kernel<2><<<grid, 256, 0, st>>>(ga);
+  else gather_kernel<3><<<grid, 256, 0, st>>>(ga);
+  FGT_LAUNCHED();
+}
+
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
+  if (T.n_psi == 0) return;
+  cudaStream_t st = T.st;
+  EvalArgs ea;
+  ea.tgt = T.tgt_sorted.get();
+  ea.center = T.center.get();
+  ea.psi_ids = T.psi_ids.get();
+  ea.tgt_start = T.tgt_start.get();
+  ea.tgt_count = T.tgt_count.get();
+  ea.psi = reinterpret_cast<const double2*>(P.psi.get());
+  ea.u = u_sorted;
+  ea.n_f = P.n_f;
+  ea.R = (int)P.R;
+  ea.ksteps = (P.n_f + 3) / 4;
+  ea.sc = P.sc;
+  const int NT = (P.n_f + 7) / 8;
+#define FGT_EVAL_D(DD)                                              \
+  switch (NT) {                                                     \
+    case 1: launch_eval<DD, 1>(ea, T.n_psi, st); break;             \
+    case 2: launch_eval<DD, 2>(ea, T.n_psi, st); break;             \
+    case 3: launch_eval<DD, 3>(ea, T.n_psi, st); break;             \
+    case 4: launch_eval<DD, 4>(ea, T.n_psi, st); break;             \
+    case 5: launch_eval<DD, 5>(ea, T.n_psi, st); break;             \
+    case 6: launch_eval<DD, 6>(ea, T.n_psi, st); break;             \
+    case 7: launch_eval<DD, 7>(ea, T.n_psi, st); break;             \
+    case 8: launch_eval<DD, 8>(ea, T.n_psi, st); break;             \
+    default: throw Error(FGT_ERANGE, "n_f too large");              \
+  }
+  if (T.d == 1) { FGT_EVAL_D(1) }
+  else if (T.d == 2) { FGT_EVAL_D(2) }
+  else { FGT_EVAL_D(3) }
+#undef FGT_EVAL_D
+}
+
+void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted) {
+  if (T.n_d == 0 || T.n_dtgt == 0) return;
+  cudaStream_t st = T.st;
+  DirectArgs da;
+  da.d_tgt_ids = T.d_tgt_ids.get();
+  da.d_off = T.d_off.get();
+  da.d_src = T.d_src.get();
+  da.d_v = T.d_v.get();
+  da.src_start = T.src_start.get();
+  da.src_count = T.src_count.get();
+  da.tgt_start = T.tgt_start.get();
+  da.tgt_count = T.tgt_count.get();
+  da.src = T.src_sorted.get();
+  da.q = T.q_sorted.get();
+  da.tgt = T.tgt_sorted.get();
+  da.u = u_sorted;
+  da.inv_delta = inv_delta;
+  da.r2_cut = r2_cut;
+  da.root_side = T.root_side;
+  da.n = T.n_dtgt;
+  unsigned g = (unsigned)std::min<int64_t>(T.n_dtgt, 148 * 16);
+  if (T.d == 1) direct_kernel<1><<<g, 128, 0, st>>>(da);
+  else if (T.d == 2) direct_kernel<2><<<g, 128, 0, st>>>(da);
+  else direct_kernel<3><<<g, 128, 0, st>>>(da);
+  FGT_LAUNCHED();
+}
+
+}  // namespace fgt

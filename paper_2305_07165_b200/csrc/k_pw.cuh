@@ -1,0 +1,29 @@
+#pragma once
+#include "k_tree.cuh"
+
+namespace fgt {
+
+// Plane-wave data of one discrete FGT evaluation.
+struct PwDev {
+  int d = 0, n_f = 0;
+  int64_t R = 0;       // rows n_f^(d-1)
+  int64_t NF = 0;      // n_f^d modes
+  double sc = 0;       // coordinate scale h / sqrt(delta)
+  double side_lc = 0;  // cutoff box side
+  DBuf<double> w1d;    // (n_f) pre-multiplied 1-D weights (planewave.py:33-70)
+  DBuf<double> phase;  // (3, n_f) complex: exp(+i m sc o side_lc), o = -1, 0, 1
+  DBuf<double> phi;    // (n_dense, R, n_f) complex outgoing expansions
+  DBuf<double> psi;    // (n_psi, R, n_f) complex incoming expansions
+};
+
+void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
+// Form outgoing expansions of all P-boxes: type-1 exponential sums.
+void pw_form(PwDev& P, TreeDev& T);
+// Diagonal translation phi -> psi over the P-lists.
+void pw_gather(PwDev& P, TreeDev& T);
+// Type-2 evaluation of psi at the targets of every psi box; u_sorted += Re(...).
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted);
+// Direct near field over the D-lists (ball cut PAPER.md:909-915).
+void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted);
+
+}  // namespace fgt

@@ -1,0 +1,940 @@
+// GPU construction of the level-restricted point tree (Alg 1) and
+// of the target-centric P/D interaction lists.
+//
+// Reference behaviour reproduced bit-exactly (tree.py line numbers):
+//   * root: free space centre = midpoint of the bbox, side 2^l_c D0 sqrt(delta) with
+//     the roundoff guard (:463-472); periodic root centre 0, side 1 (:458-461);
+//   * a point's child is chosen by p_k >= centre_k of the box being split (:486-491),
+//     centres from _Builder.center (:324-326) rounded op-by-op (no FMA);
+//   * level-synchronous refinement of boxes with > n_s points up to l_c (:493-502);
+//   * 2:1 balance (:378-403) and the dense-cutoff-leaf fix (:506-523).
+// The balance / dense-fix closures are monotone, so their unique least fixpoint is
+// reached by parallel rounds (every split made is forced in any closed superset);
+// the box set, leaf relation and per-leaf ascending index lists therefore match the
+// sequential LIFO build.  Boxes are numbered level-major, Morton within a level.
+//
+// Representation: each point carries its Morton code at level l_c (the path of child
+// numbers it would take through every split).  A box (level l, code c) holds exactly
+// the points whose code >> d(l_c-l) == c, so subtree counts are two binary searches
+// in the sorted point codes.  Boxes live in one sorted array of keys (l<<58 | c).
+#include <cub/cub.cuh>
+#include "k_tree.cuh"
+
+namespace fgt {
+
+namespace {
+
+struct CubTmp {
+  DBuf<uint8_t> buf;
+  void* get(size_t bytes, cudaStream_t st) {
+    if (bytes > buf.size()) buf.alloc(bytes + 256, st);
+    return buf.get();
+  }
+};
+
+template <class T>
+T read_scalar(const T* dptr, cudaStream_t st) {
+  T h;
+  FGT_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
+  FGT_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+struct Root {
+  double low[3];
+  double side;
+};
+
+// ------------------------------------------------------------------ bbox
+template <int D>
+__global__ void __launch_bounds__(256) bbox_partial_kernel(const double* __restrict__ a, int64_t n,
+                                                           double* __restrict__ part) {
+  double lo[D], hi[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) { lo[k] = INFINITY; hi[k] = -INFINITY; }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double v = a[i * D + k];
+      lo[k] = fmin(lo[k], v);
+      hi[k] = fmax(hi[k], v);
+    }
+  }
+  __shared__ double s[2 * D][256];
+#pragma unroll
+  for (int k = 0; k < D; ++k) { s[k][threadIdx.x] = lo[k]; s[D + k][threadIdx.x] = hi[k]; }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        s[k][threadIdx.x] = fmin(s[k][threadIdx.x], s[k][threadIdx.x + w]);
+        s[D + k][threadIdx.x] = fmax(s[D + k][threadIdx.x], s[D + k][threadIdx.x + w]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 2 * D; ++k) part[blockIdx.x * 2 * D + k] = s[k][0];
+  }
+}
+
+void device_bbox(const double* src, int64_t ns, const double* tgt, int64_t nt, int d,
+                 double* lo, double* hi, cudaStream_t st) {
+  const int nblk = 296;
+  DBuf<double> part(2 * nblk * 2 * d, st);
+  for (int k = 0; k < d; ++k) { lo[k] = INFINITY; hi[k] = -INFINITY; }
+  int used = 0;
+  for (int which = 0; which < 2; ++which) {
+    const double* a = which ? tgt : src;
+    int64_t n = which ? nt : ns;
+    if (n == 0) continue;
+    double* p = part.get() + which * nblk * 2 * d;
+    if (d == 1) bbox_partial_kernel<1><<<nblk, 256, 0, st>>>(a, n, p);
+    else if (d == 2) bbox_partial_kernel<2><<<nblk, 256, 0, st>>>(a, n, p);
+    else bbox_partial_kernel<3><<<nblk, 256, 0, st>>>(a, n, p);
+    FGT_LAUNCHED();
+    used |= 1 << which;
+  }
+  std::vector<double> h(2 * nblk * 2 * d);
+  part.to_host(h.data(), h.size());
+  FGT_CUDA(cudaStreamSynchronize(st));
+  for (int which = 0; which < 2; ++which) {
+    if (!(used >> which & 1)) continue;
+    for (int b = 0; b < nblk; ++b) {
+      const double* p = h.data() + (which * nblk + b) * 2 * d;
+      for (int k = 0; k < d; ++k) {
+        lo[k] = std::fmin(lo[k], p[k]);
+        hi[k] = std::fmax(hi[k], p[d + k]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ point codes
+template <int D>
+__global__ void __launch_bounds__(256) point_codes_kernel(
+    const double* __restrict__ src, int64_t ns, const double* __restrict__ tgt, int64_t nt,
+    int l_c, Root root, uint64_t* __restrict__ code, int64_t* __restrict__ idx) {
+  const int64_t ntot = ns + nt;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* p = (i < ns) ? src + i * D : tgt + (i - ns) * D;
+    double x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = p[k];
+    int64_t g[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = 0;
+    double s = root.side;  // side of the box being split at level l (exact halvings)
+    for (int l = 0; l < l_c; ++l) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        double c = box_center_1d(root.low[k], g[k], s);
+        g[k] = 2 * g[k] + (x[k] >= c ? 1 : 0);
+      }
+      s *= 0.5;
+    }
+    code[i] = morton_encode(g, D, l_c);
+    idx[i] = i;
+  }
+}
+
+// subtree point count of box (l, c): codes in [c << sh, (c+1) << sh)
+__device__ __forceinline__ int64_t prefix_lo(const uint64_t* pkey, int64_t n, uint64_t c, int sh) {
+  return lower_bound_dev(pkey, n, c << sh);
+}
+__device__ __forceinline__ int64_t prefix_hi(const uint64_t* pkey, int64_t n, uint64_t c, int sh) {
+  return lower_bound_dev(pkey, n, (c + 1) << sh);
+}
+
+// deepest existing box at level <= l containing cell `code` at level l (tree.py:290-298)
+__device__ __forceinline__ int64_t find_covering_dev(const uint64_t* keys, int64_t nb, int d, int l,
+                                                     uint64_t code) {
+  for (int lv = l; lv >= 0; --lv) {
+    int64_t i = find_dev(keys, nb, box_key(lv, code));
+    if (i >= 0) return i;
+    code >>= d;
+  }
+  return -1;
+}
+
+// neighbour cell of g at level l by offset o; returns false if outside (free space).
+// Periodic: v = n div 2^l, n -= v 2^l (tree.py:369-371).
+template <int D>
+__device__ __forceinline__ bool neighbor_cell(const int64_t* g, const int* o, int l, bool periodic,
+                                              int64_t* n, int* v) {
+  const int64_t side = (int64_t)1 << l;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    int64_t c = g[k] + o[k];
+    if (periodic) {
+      int64_t vv = (c >= 0) ? c / side : -((-c + side - 1) / side);
+      v[k] = (int)vv;
+      c -= vv * side;
+    } else {
+      v[k] = 0;
+      if (c < 0 || c >= side) return false;
+    }
+    n[k] = c;
+  }
+  return true;
+}
+
+// offsets in tree._offsets order (:419-426): axis 0 slowest, each in (-1, 0, 1)
+template <int D>
+__device__ __forceinline__ void offset_of(int t, int* o) {
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) {
+    o[k] = t % 3 - 1;
+    t /= 3;
+  }
+}
+
+__global__ void count_flag_kernel(const uint64_t* __restrict__ keys, int64_t lo, int64_t hi,
+                                  const uint64_t* __restrict__ pkey, int64_t npts, int d, int l_c,
+                                  int64_t n_s, uint8_t* __restrict__ flag) {
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    int l = key_level(k);
+    int sh = d * (l_c - l);
+    uint64_t c = key_code(k);
+    int64_t cnt = prefix_hi(pkey, npts, c, sh) - prefix_lo(pkey, npts, c, sh);
+    flag[i - lo] = cnt > n_s ? 1 : 0;
+  }
+}
+
+__global__ void make_children_kernel(const uint64_t* __restrict__ parents, int64_t np, int d,
+                                     uint64_t* __restrict__ out) {
+  const int nc = 1 << d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np * nc;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t p = parents[i / nc];
+    out[i] = box_key(key_level(p) + 1, (key_code(p) << d) | (uint64_t)(i % nc));
+  }
+}
+
+__global__ void leaf_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int d,
+                                 uint8_t* __restrict__ leaf) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    leaf[i] = find_dev(keys, nb, box_key(key_level(k) + 1, key_code(k) << d)) < 0 ? 1 : 0;
+  }
+}
+
+// 2:1 balance round (tree.py:378-403): a leaf b at level l >= 2 forces the split of any
+// leaf neighbour covering at level <= l-2.
+template <int D>
+__global__ void balance_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb,
+                                    const uint8_t* __restrict__ leaf, int periodic,
+                                    uint8_t* __restrict__ split, int* __restrict__ any) {
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!leaf[i]) continue;
+    uint64_t key = keys[i];
+    int l = key_level(key);
+    if (l < 2) continue;
+    int64_t g[D];
+    morton_decode(key_code(key), D, l, g);
+    for (int t = 0; t < NOFF; ++t) {
+      int o[D];
+      offset_of<D>(t, o);
+      bool self = true;
+#pragma unroll
+      for (int k = 0; k < D; ++k) self &= (o[k] == 0);
+      if (self) continue;
+      int64_t n[D];
+      int v[D];
+      if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
+      int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
+      if (j >= 0 && leaf[j] && l - key_level(keys[j]) >= 2) {
+        split[j] = 1;
+        *any = 1;
+      }
+    }
+  }
+}
+
+// dense-cutoff-leaf fix (tree.py:506-523): a level-l_c leaf with > n_s points forces
+// the split of every leaf neighbour at level l_c-1.
+template <int D>
+__global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int64_t lo,
+                                     int64_t hi, const uint8_t* __restrict__ leaf,
+                                     const uint64_t* __restrict__ pkey, int64_t npts, int l_c,
+                                     int64_t n_s, int periodic, uint8_t* __restrict__ split,
+                                     int* __restrict__ any) {
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!leaf[i]) continue;
+    uint64_t key = keys[i];
+    uint64_t c = key_code(key);
+    int64_t cnt = prefix_hi(pkey, npts, c, 0) - prefix_lo(pkey, npts, c, 0);
+    if (cnt <= n_s) continue;
+    int64_t g[D];
+    morton_decode(c, D, l_c, g);
+    for (int t = 0; t < NOFF; ++t) {
+      int o[D];
+      offset_of<D>(t, o);
+      bool self = true;
+#pragma unroll
+      for (int k = 0; k < D; ++k) self &= (o[k] == 0);
+      if (self) continue;
+      int64_t n[D];
+      int v[D];
+      if (!neighbor_cell<D>(g, o, l_c, periodic, n, v)) continue;
+      int64_t j = find_covering_dev(keys, nb, D, l_c, morton_encode(n, D, l_c));
+      if (j >= 0 && leaf[j] && key_level(keys[j]) == l_c - 1) {
+        split[j] = 1;
+        *any = 1;
+      }
+    }
+  }
+}
+
+__global__ void level_offsets_kernel(const uint64_t* __restrict__ keys, int64_t nb, int nlev,
+                                     int64_t* __restrict__ off) {
+  int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l <= nlev) off[l] = lower_bound_dev(keys, nb, box_key(l, 0));
+}
+
+// Per-box finalisation: the Tree fields (tree.py:236-254) + subtree counts.
+template <int D>
+__global__ void finalize_boxes_kernel(const uint64_t* __restrict__ keys, int64_t nb,
+                                      const uint64_t* __restrict__ pkey, int64_t npts,
+                                      const int64_t* __restrict__ srcpre, int l_c, Root root,
+                                      int32_t* __restrict__ level, int64_t* __restrict__ parent,
+                                      int64_t* __restrict__ children, int64_t* __restrict__ coords,
+                                      uint8_t* __restrict__ is_leaf, int64_t* __restrict__ npoints,
+                                      int64_t* __restrict__ scount, int64_t* __restrict__ tcount,
+                                      double* __restrict__ center) {
+  constexpr int NC = 1 << D;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = keys[i];
+    int l = key_level(key);
+    uint64_t c = key_code(key);
+    level[i] = l;
+    int64_t g[D];
+    morton_decode(c, D, l, g);
+    double s = root.side;
+    for (int t = 0; t < l; ++t) s *= 0.5;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      coords[i * D + k] = g[k];
+      center[i * D + k] = box_center_1d(root.low[k], g[k], s);
+    }
+    parent[i] = l > 0 ? find_dev(keys, nb, box_key(l - 1, c >> D)) : -1;
+    int64_t c0 = find_dev(keys, nb, box_key(l + 1, c << D));
+#pragma unroll
+    for (int t = 0; t < NC; ++t) children[i * NC + t] = c0 >= 0 ? c0 + t : -1;
+    is_leaf[i] = c0 < 0;
+    int sh = D * (l_c - l);
+    int64_t lo = prefix_lo(pkey, npts, c, sh), hi = prefix_hi(pkey, npts, c, sh);
+    npoints[i] = hi - lo;
+    int64_t sc = srcpre[hi] - srcpre[lo];
+    scount[i] = c0 < 0 ? sc : 0;
+    tcount[i] = c0 < 0 ? (hi - lo - sc) : 0;
+  }
+}
+
+__global__ void source_flag_kernel(const int64_t* __restrict__ pidx, int64_t npts, int64_t ns,
+                                   int64_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= npts;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i < npts && pidx[i] < ns) ? 1 : 0;
+}
+
+// leaf of every point (the deepest box containing its l_c cell), scattered to the
+// original (combined) index, so a stable sort by leaf keeps ascending indices
+template <int D>
+__global__ void point_leaf_kernel(const uint64_t* __restrict__ keys, int64_t nb,
+                                  const uint64_t* __restrict__ pkey, const int64_t* __restrict__ pidx,
+                                  int64_t npts, int l_c, int64_t* __restrict__ leaf_of) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npts;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    leaf_of[pidx[i]] = find_covering_dev(keys, nb, D, l_c, pkey[i]);
+  }
+}
+
+__global__ void iota_kernel(int64_t* a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = i;
+}
+
+__global__ void leaf_start_kernel(const int64_t* __restrict__ sorted_leaf, int64_t n,
+                                  const uint8_t* __restrict__ is_leaf, int64_t nb,
+                                  int64_t* __restrict__ start) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    start[b] = is_leaf[b] ? lower_bound_dev(sorted_leaf, n, b) : 0;
+}
+
+__global__ void dense_flag_kernel(const int32_t* __restrict__ level, const uint8_t* __restrict__ leaf,
+                                  const int64_t* __restrict__ npoints, int64_t nb, int l_c,
+                                  int64_t n_s, uint8_t* __restrict__ flag) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    flag[b] = (leaf[b] && level[b] == l_c && npoints[b] > n_s) ? 1 : 0;
+}
+
+__global__ void dense_slot_kernel(const int64_t* __restrict__ ids, int64_t n, int64_t* __restrict__ slot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    slot[ids[i]] = i;
+}
+
+__global__ void fill_i64_kernel(int64_t* a, int64_t n, int64_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+template <int D>
+__global__ void gather_rows_kernel(const double* __restrict__ a, const int64_t* __restrict__ perm,
+                                   int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = perm[i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) out[i * D + k] = a[j * D + k];
+  }
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 63 && ((int64_t)1 << b) <= n) ++b;
+  return b;
+}
+
+// Box-set state during construction.
+struct BoxSet {
+  DBuf<uint64_t> keys;
+  int64_t n = 0;
+};
+
+void sort_keys(BoxSet& B, CubTmp& tmp, cudaStream_t st) {
+  DBuf<uint64_t> out(B.n, st);
+  size_t bytes = 0;
+  FGT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, B.keys.get(), out.get(), (int)B.n, 0, 64, st));
+  FGT_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(bytes, st), bytes, B.keys.get(), out.get(), (int)B.n, 0, 64, st));
+  count_launch();
+  B.keys = std::move(out);
+}
+
+// Split the boxes flagged in `flag` (aligned with keys[lo, lo+n)): append their 2^d
+// children and re-sort.  Returns the number of boxes split.
+int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int d, CubTmp& tmp,
+                      cudaStream_t st) {
+  if (n == 0) return 0;
+  DBuf<uint64_t> sel(n, st);
+  DBuf<int64_t> nsel(1, st);
+  size_t bytes = 0;
+  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, B.keys.get() + lo, flag, sel.get(), nsel.get(), (int)n, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, B.keys.get() + lo, flag, sel.get(), nsel.get(), (int)n, st));
+  count_launch();
+  int64_t k = read_scalar(nsel.get(), st);
+  if (k == 0) return 0;
+  const int64_t nc = (int64_t)k << d;
+  DBuf<uint64_t> grown(B.n + nc, st);
+  FGT_CUDA(cudaMemcpyAsync(grown.get(), B.keys.get(), B.n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  make_children_kernel<<<grid_for(nc, 256), 256, 0, st>>>(sel.get(), k, d, grown.get() + B.n);
+  FGT_LAUNCHED();
+  B.keys = std::move(grown);
+  B.n += nc;
+  sort_keys(B, tmp, st);
+  return k;
+}
+
+std::vector<int64_t> level_offsets(const BoxSet& B, int nlev, cudaStream_t st) {
+  DBuf<int64_t> off(nlev + 1, st);
+  level_offsets_kernel<<<1, 64, 0, st>>>(B.keys.get(), B.n, nlev, off.get());
+  FGT_LAUNCHED();
+  std::vector<int64_t> h(nlev + 1);
+  off.to_host(h.data(), nlev + 1);
+  FGT_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+template <int D>
+void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st) {
+  DBuf<int> any(1, st);
+  for (int round = 0; round < 4096; ++round) {
+    DBuf<uint8_t> leaf(B.n, st), split(B.n, st);
+    split.zero();
+    any.zero();
+    leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
+    FGT_LAUNCHED();
+    balance_flag_kernel<D><<<grid_for(B.n, 128), 128, 0, st>>>(B.keys.get(), B.n, leaf.get(), periodic,
+                                                                 split.get(), any.get());
+    FGT_LAUNCHED();
+    if (!read_scalar(any.get(), st)) return;
+    split_flagged(B, 0, B.n, split.get(), D, tmp, st);
+  }
+  throw Error(FGT_ECUDA, "tree balance did not converge");
+}
+
+template <int D>
+void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tgt, int64_t nt,
+                     const fgt_tree_params& tp, cudaStream_t st) {
+  T.st = st;
+  T.d = D;
+  T.ns = ns;
+  T.nt = nt;
+  T.ntot = ns + nt;
+  T.n_s = tp.n_s;
+  T.periodic = tp.periodic;
+  FGT_REQUIRE(T.ntot > 0, FGT_EINVAL, "need at least one source or target");
+  FGT_REQUIRE(tp.n_s >= 1, FGT_EINVAL, "n_s must be >= 1");
+  FGT_REQUIRE(T.ntot < ((int64_t)1 << 31), FGT_ERANGE, "more than 2^31 points");
+
+  // ---- root and cutoff level (tree.py:458-472, cutoff_level :207-233)
+  if (tp.periodic) {
+    for (int k = 0; k < D; ++k) T.root_center[k] = 0.0;
+    T.root_side = 1.0;
+    T.l_c = tp.l_c_periodic;
+  } else {
+    double lo[3], hi[3];
+    device_bbox(src, ns, tgt, nt, D, lo, hi, st);
+    double spread = 0.0;
+    for (int k = 0; k < D; ++k) {
+      T.root_center[k] = 0.5 * (lo[k] + hi[k]);
+      double e = hi[k] - lo[k];
+      spread = (k == 0) ? e : std::fmax(spread, e);
+    }
+    const double cut = tp.D0 * std::sqrt(tp.delta);
+    int l_c;
+    if (spread <= cut) l_c = 0;
+    else l_c = std::min((int)std::ceil(std::log2(spread / cut) - 1e-12), 30);
+    double side = std::ldexp(tp.D0, l_c) * std::sqrt(tp.delta);
+    if (side < spread) { l_c += 1; side *= 2.0; }
+    T.l_c = l_c;
+    T.root_side = side;
+  }
+  for (int k = 0; k < D; ++k) T.root_low[k] = T.root_center[k] - 0.5 * T.root_side;
+  FGT_REQUIRE(D * T.l_c <= 57, FGT_ERANGE, "cutoff level too deep for 64-bit Morton keys");
+  const int l_c = T.l_c;
+  Root root;
+  for (int k = 0; k < 3; ++k) root.low[k] = k < D ? T.root_low[k] : 0.0;
+  root.side = T.root_side;
+
+  // ---- point codes, stable radix sort
+  const int64_t np = T.ntot;
+  CubTmp tmp;
+  {
+    DBuf<uint64_t> code(np, st);
+    DBuf<int64_t> idx(np, st);
+    point_codes_kernel<D><<<grid_for(np, 256), 256, 0, st>>>(src, ns, tgt, nt, l_c, root, code.get(), idx.get());
+    FGT_LAUNCHED();
+    if (D * l_c > 0) {
+      T.pkey.alloc(np, st);
+      T.pidx.alloc(np, st);
+      size_t bytes = 0;
+      FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, code.get(), T.pkey.get(), idx.get(), T.pidx.get(), (int)np, 0, D * l_c, st));
+      FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes, st), bytes, code.get(), T.pkey.get(), idx.get(), T.pidx.get(), (int)np, 0, D * l_c, st));
+      count_launch();
+    } else {
+      T.pkey = std::move(code);
+      T.pidx = std::move(idx);
+    }
+  }
+
+  // ---- level-synchronous refinement (tree.py:493-502)
+  BoxSet B;
+  B.keys.alloc(1, st);
+  {
+    uint64_t k0 = box_key(0, 0);
+    B.keys.from_host(&k0, 1);
+    B.n = 1;
+  }
+  for (int l = 0; l < l_c; ++l) {
+    std::vector<int64_t> off = level_offsets(B, l + 1, st);
+    int64_t lo = off[l], hi = off[l + 1];
+    if (hi == lo) break;
+    DBuf<uint8_t> flag(hi - lo, st);
+    count_flag_kernel<<<grid_for(hi - lo, 256), 256, 0, st>>>(B.keys.get(), lo, hi, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
+    FGT_LAUNCHED();
+    if (split_flagged(B, lo, hi - lo, flag.get(), D, tmp, st) == 0) break;
+  }
+
+  // ---- balance + dense-cutoff-leaf fix to the joint fixpoint (tree.py:504-523)
+  balance_rounds<D>(B, tp.periodic, tmp, st);
+  if (l_c >= 1) {
+    DBuf<int> any(1, st);
+    for (int round = 0; round < 4096; ++round) {
+      std::vector<int64_t> off = level_offsets(B, l_c + 1, st);
+      int64_t lo = off[l_c], hi = off[l_c + 1];
+      DBuf<uint8_t> leaf(B.n, st), split(B.n, st);
+      split.zero();
+      any.zero();
+      leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
+      FGT_LAUNCHED();
+      if (hi > lo) {
+        densefix_flag_kernel<D><<<grid_for(hi - lo, 128), 128, 0, st>>>(
+            B.keys.get(), B.n, lo, hi, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
+            split.get(), any.get());
+        FGT_LAUNCHED();
+      }
+      if (!read_scalar(any.get(), st)) break;
+      split_flagged(B, 0, B.n, split.get(), D, tmp, st);
+      balance_rounds<D>(B, tp.periodic, tmp, st);
+    }
+  }
+
+  // ---- finalise boxes
+  const int64_t nb = B.n;
+  T.nb = nb;
+  T.level_off = level_offsets(B, l_c + 1, st);  // l_c+2 entries
+  T.bkey = std::move(B.keys);
+  T.n_levels = 0;
+  for (int l = 0; l <= l_c; ++l)
+    if (T.level_off[l + 1] > T.level_off[l]) T.n_levels = l + 1;
+
+  DBuf<int64_t> srcpre(np + 1, st);
+  {
+    DBuf<int64_t> flag(np + 1, st);
+    source_flag_kernel<<<grid_for(np + 1, 256), 256, 0, st>>>(T.pidx.get(), np, ns, flag.get());
+    FGT_LAUNCHED();
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag.get(), srcpre.get(), (int)(np + 1), st));
+    FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, flag.get(), srcpre.get(), (int)(np + 1), st));
+    count_launch();
+  }
+  T.level.alloc(nb, st);
+  T.parent.alloc(nb, st);
+  T.children.alloc(nb << D, st);
+  T.coords.alloc(nb * D, st);
+  T.is_leaf.alloc(nb, st);
+  T.n_points.alloc(nb, st);
+  T.src_count.alloc(nb, st);
+  T.tgt_count.alloc(nb, st);
+  T.center.alloc(nb * D, st);
+  finalize_boxes_kernel<D><<<grid_for(nb, 128), 128, 0, st>>>(
+      T.bkey.get(), nb, T.pkey.get(), np, srcpre.get(), l_c, root, T.level.get(), T.parent.get(),
+      T.children.get(), T.coords.get(), T.is_leaf.get(), T.n_points.get(), T.src_count.get(),
+      T.tgt_count.get(), T.center.get());
+  FGT_LAUNCHED();
+
+  // ---- per-point leaves, stable sorts -> src_perm / tgt_perm (tree.py:533-564)
+  {
+    DBuf<int64_t> leaf_of(np, st);
+    point_leaf_kernel<D><<<grid_for(np, 256), 256, 0, st>>>(T.bkey.get(), nb, T.pkey.get(), T.pidx.get(), np, l_c, leaf_of.get());
+    FGT_LAUNCHED();
+    const int bits = bits_for(nb);
+    for (int which = 0; which < 2; ++which) {
+      int64_t n = which ? nt : ns;
+      DBuf<int64_t>& perm = which ? T.tgt_perm : T.src_perm;
+      DBuf<int64_t>& start = which ? T.tgt_start : T.src_start;
+      perm.alloc(n, st);
+      start.alloc(nb, st);
+      DBuf<int64_t> sorted_leaf(n, st);
+      if (n > 0) {
+        DBuf<int64_t> iota(n, st);
+        iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota.get(), n);
+        FGT_LAUNCHED();
+        const int64_t* keys_in = leaf_of.get() + (which ? ns : 0);
+        size_t bytes = 0;
+        FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sorted_leaf.get(), iota.get(), perm.get(), (int)n, 0, bits, st));
+        FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes, st), bytes, keys_in, sorted_leaf.get(), iota.get(), perm.get(), (int)n, 0, bits, st));
+        count_launch();
+      }
+      leaf_start_kernel<<<grid_for(nb, 256), 256, 0, st>>>(sorted_leaf.get(), n, T.is_leaf.get(), nb, start.get());
+      FGT_LAUNCHED();
+    }
+  }
+
+  // ---- P-boxes: leaves at l_c with > n_s points
+  {
+    DBuf<uint8_t> flag(nb, st);
+    dense_flag_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.level.get(), T.is_leaf.get(), T.n_points.get(), nb, l_c, T.n_s, flag.get());
+    FGT_LAUNCHED();
+    DBuf<int64_t> iota(nb, st), sel(nb, st), nsel(1, st);
+    iota_kernel<<<grid_for(nb, 256), 256, 0, st>>>(iota.get(), nb);
+    FGT_LAUNCHED();
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), sel.get(), nsel.get(), (int)nb, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), sel.get(), nsel.get(), (int)nb, st));
+    count_launch();
+    T.n_dense = read_scalar(nsel.get(), st);
+    T.dense_ids.alloc(T.n_dense, st);
+    if (T.n_dense)
+      FGT_CUDA(cudaMemcpyAsync(T.dense_ids.get(), sel.get(), T.n_dense * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    T.dense_slot.alloc(nb, st);
+    fill_i64_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.dense_slot.get(), nb, -1);
+    FGT_LAUNCHED();
+    if (T.n_dense) {
+      dense_slot_kernel<<<grid_for(T.n_dense, 256), 256, 0, st>>>(T.dense_ids.get(), T.n_dense, T.dense_slot.get());
+      FGT_LAUNCHED();
+    }
+    // leaf count
+    DBuf<int64_t> nl(1, st);
+    size_t b2 = 0;
+    FGT_CUDA(cub::DeviceReduce::Sum(nullptr, b2, T.is_leaf.get(), nl.get(), (int)nb, st));
+    FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), nl.get(), (int)nb, st));
+    count_launch();
+    T.n_leaves = read_scalar(nl.get(), st);
+  }
+}
+
+}  // namespace
+
+void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, int64_t nt,
+                const fgt_tree_params& tp, cudaStream_t st) {
+  FGT_REQUIRE(tp.dim >= 1 && tp.dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+  FGT_REQUIRE(tp.delta > 0, FGT_EINVAL, "delta must be positive");
+  if (tp.dim == 1) build_tree_impl<1>(T, src, ns, tgt, nt, tp, st);
+  else if (tp.dim == 2) build_tree_impl<2>(T, src, ns, tgt, nt, tp, st);
+  else build_tree_impl<3>(T, src, ns, tgt, nt, tp, st);
+}
+
+void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt) {
+  cudaStream_t st = T.st;
+  const int d = T.d;
+  T.src_sorted.alloc(T.ns * d, st);
+  T.tgt_sorted.alloc(T.nt * d, st);
+  auto gather = [&](const double* a, const int64_t* perm, int64_t n, double* out, int dd) {
+    if (n == 0) return;
+    unsigned g = grid_for(n, 256);
+    if (dd == 1) gather_rows_kernel<1><<<g, 256, 0, st>>>(a, perm, n, out);
+    else if (dd == 2) gather_rows_kernel<2><<<g, 256, 0, st>>>(a, perm, n, out);
+    else gather_rows_kernel<3><<<g, 256, 0, st>>>(a, perm, n, out);
+    FGT_LAUNCHED();
+  };
+  gather(src, T.src_perm.get(), T.ns, T.src_sorted.get(), d);
+  gather(tgt, T.tgt_perm.get(), T.nt, T.tgt_sorted.get(), d);
+  if (q) {
+    T.q_sorted.alloc(T.ns, st);
+    gather(q, T.src_perm.get(), T.ns, T.q_sorted.get(), 1);
+  }
+}
+
+// ====================================================================== lists
+namespace {
+
+// Enumerate the neighbour leaves of leaf T (tree recipe of SURVEY §8c, matching
+// neighbor_cells tree.py:359-376 + find_covering :290-298): for each offset, the
+// covering leaf (colleague or coarse) or, when the colleague is subdivided, its
+// children touching T (fine neighbours; leaves by balance).  Deduplicated on (S, v).
+template <int D>
+struct NbrEntry {
+  int64_t box;
+  int v[D];
+};
+
+template <int D>
+__device__ int enumerate_neighbors(const uint64_t* __restrict__ keys, int64_t nb,
+                                   const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
+                                   const int64_t* __restrict__ children, int64_t T, int periodic,
+                                   NbrEntry<D>* out) {
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  constexpr int NC = 1 << D;
+  uint64_t key = keys[T];
+  int l = key_level(key);
+  int64_t g[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) g[k] = coords[T * D + k];
+  int cnt = 0;
+  auto push = [&](int64_t b, const int* v) {
+    for (int e = 0; e < cnt; ++e) {
+      bool same = out[e].box == b;
+#pragma unroll
+      for (int k = 0; k < D; ++k) same &= out[e].v[k] == v[k];
+      if (same) return;
+    }
+    out[cnt].box = b;
+#pragma unroll
+    for (int k = 0; k < D; ++k) out[cnt].v[k] = v[k];
+    ++cnt;
+  };
+  for (int t = 0; t < NOFF; ++t) {
+    int o[D];
+    offset_of<D>(t, o);
+    int64_t n[D];
+    int v[D];
+    if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
+    int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
+    if (j < 0) continue;
+    if (leaf[j]) {
+      push(j, v);
+    } else {
+      const int64_t side = (int64_t)1 << l;
+      for (int c = 0; c < NC; ++c) {
+        int64_t ch = children[j * NC + c];
+        bool touch = true;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          int64_t gc = coords[ch * D + k] + 2 * (int64_t)v[k] * side;
+          touch &= (gc >= 2 * g[k] - 1) && (gc <= 2 * g[k] + 2);
+        }
+        if (touch) push(ch, v);
+      }
+    }
+  }
+  return cnt;
+}
+
+// pass 0: count entries per target leaf; pass 1: write them
+template <int D>
+__global__ void __launch_bounds__(128) lists_kernel(
+    int pass, const int64_t* __restrict__ tleaves, int64_t ntl, const uint64_t* __restrict__ keys,
+    int64_t nb, const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
+    const int64_t* __restrict__ children, const int32_t* __restrict__ level,
+    const int64_t* __restrict__ npoints, const int64_t* __restrict__ scount,
+    const int64_t* __restrict__ tcount, const int64_t* __restrict__ dense_slot, int periodic,
+    int64_t* __restrict__ pcnt, int64_t* __restrict__ dcnt, const int64_t* __restrict__ poff,
+    const int64_t* __restrict__ doff, int64_t* __restrict__ p_src, int32_t* __restrict__ p_v,
+    int64_t* __restrict__ p_tgt, int64_t* __restrict__ d_src, int32_t* __restrict__ d_v,
+    int64_t* __restrict__ d_tgt, unsigned long long* __restrict__ pairs) {
+  constexpr int CAP = D == 1 ? 4 : (D == 2 ? 16 : 64);
+  NbrEntry<D> ent[CAP];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntl;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t T = tleaves[i];
+    int cnt = enumerate_neighbors<D>(keys, nb, leaf, coords, children, T, periodic, ent);
+    int64_t np_ = 0, nd_ = 0;
+    int64_t po = pass ? poff[i] : 0, dof = pass ? doff[i] : 0;
+    unsigned long long pr = 0;
+    for (int e = 0; e < cnt; ++e) {
+      int64_t S = ent[e].box;
+      int64_t slot = dense_slot[S];
+      if (slot >= 0) {
+        if (pass) {
+          p_src[po + np_] = slot;
+          p_tgt[po + np_] = T;
+#pragma unroll
+          for (int k = 0; k < D; ++k) p_v[(po + np_) * D + k] = ent[e].v[k];
+        }
+        ++np_;
+      } else if (scount[S] > 0) {
+        if (pass) {
+          d_src[dof + nd_] = S;
+          d_tgt[dof + nd_] = T;
+#pragma unroll
+          for (int k = 0; k < D; ++k) d_v[(dof + nd_) * D + k] = ent[e].v[k];
+          pr += (unsigned long long)(scount[S] * tcount[T]);
+        }
+        ++nd_;
+      }
+    }
+    if (!pass) {
+      pcnt[i] = np_;
+      dcnt[i] = nd_;
+    } else if (pr) {
+      atomicAdd(pairs, pr);
+    }
+  }
+}
+
+__global__ void target_leaf_flag_kernel(const uint8_t* __restrict__ leaf, const int64_t* __restrict__ tcount,
+                                        int64_t nb, uint8_t* __restrict__ flag) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    flag[b] = leaf[b] && tcount[b] > 0;
+}
+
+__global__ void nonzero_flag_kernel(const int64_t* __restrict__ a, int64_t n, uint8_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = a[i] > 0;
+}
+
+}  // namespace
+
+template <int D>
+static void build_lists_impl(TreeDev& T) {
+  cudaStream_t st = T.st;
+  CubTmp tmp;
+  const int64_t nb = T.nb;
+  // target leaves (leaves with targets), canonical order
+  DBuf<uint8_t> flag(nb, st);
+  target_leaf_flag_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.is_leaf.get(), T.tgt_count.get(), nb, flag.get());
+  FGT_LAUNCHED();
+  DBuf<int64_t> iota(nb, st), tl(nb, st), ntl_d(1, st);
+  iota_kernel<<<grid_for(nb, 256), 256, 0, st>>>(iota.get(), nb);
+  FGT_LAUNCHED();
+  size_t bytes = 0;
+  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), tl.get(), ntl_d.get(), (int)nb, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), tl.get(), ntl_d.get(), (int)nb, st));
+  count_launch();
+  const int64_t ntl = read_scalar(ntl_d.get(), st);
+  T.n_dtgt = ntl;
+
+  DBuf<int64_t> pcnt(ntl + 1, st), dcnt(ntl + 1, st), poff(ntl + 1, st), doff(ntl + 1, st);
+  pcnt.zero();
+  dcnt.zero();
+  DBuf<unsigned long long> pairs(1, st);
+  pairs.zero();
+  if (ntl > 0) {
+    lists_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
+        0, tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
+        T.level.get(), T.n_points.get(), T.src_count.get(), T.tgt_count.get(), T.dense_slot.get(),
+        T.periodic, pcnt.get(), dcnt.get(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, pairs.get());
+    FGT_LAUNCHED();
+  }
+  bytes = 0;
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, pcnt.get(), poff.get(), (int)(ntl + 1), st));
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, pcnt.get(), poff.get(), (int)(ntl + 1), st));
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, dcnt.get(), doff.get(), (int)(ntl + 1), st));
+  count_launch(2);
+  int64_t tot[2];
+  FGT_CUDA(cudaMemcpyAsync(&tot[0], poff.get() + ntl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FGT_CUDA(cudaMemcpyAsync(&tot[1], doff.get() + ntl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FGT_CUDA(cudaStreamSynchronize(st));
+  T.n_p = tot[0];
+  T.n_d = tot[1];
+  T.p_src.alloc(T.n_p, st);
+  T.p_v.alloc(T.n_p * D, st);
+  T.p_tgt.alloc(T.n_p, st);
+  T.d_src.alloc(T.n_d, st);
+  T.d_v.alloc(T.n_d * D, st);
+  T.d_tgt.alloc(T.n_d, st);
+  if (ntl > 0) {
+    lists_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
+        1, tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
+        T.level.get(), T.n_points.get(), T.src_count.get(), T.tgt_count.get(), T.dense_slot.get(),
+        T.periodic, nullptr, nullptr, poff.get(), doff.get(), T.p_src.get(), T.p_v.get(),
+        T.p_tgt.get(), T.d_src.get(), T.d_v.get(), T.d_tgt.get(), pairs.get());
+    FGT_LAUNCHED();
+  }
+  // direct CSR over all target leaves
+  T.d_tgt_ids = std::move(tl);
+  T.d_off = std::move(doff);
+  // psi boxes: target leaves with P entries -> compact CSR
+  {
+    DBuf<uint8_t> f2(ntl + 1, st);
+    nonzero_flag_kernel<<<grid_for(ntl, 256), 256, 0, st>>>(pcnt.get(), ntl, f2.get());
+    FGT_LAUNCHED();
+    DBuf<int64_t> sel(ntl + 1, st), nsel(1, st), seloff(ntl + 1, st);
+    bytes = 0;
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, T.d_tgt_ids.get(), f2.get(), sel.get(), nsel.get(), (int)ntl, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, T.d_tgt_ids.get(), f2.get(), sel.get(), nsel.get(), (int)ntl, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), nsel.get(), (int)ntl, st));
+    count_launch(2);
+    T.n_psi = read_scalar(nsel.get(), st);
+    T.psi_ids.alloc(T.n_psi, st);
+    T.p_off.alloc(T.n_psi + 1, st);
+    if (T.n_psi) {
+      FGT_CUDA(cudaMemcpyAsync(T.psi_ids.get(), sel.get(), T.n_psi * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      FGT_CUDA(cudaMemcpyAsync(T.p_off.get(), seloff.get(), T.n_psi * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    }
+    FGT_CUDA(cudaMemcpyAsync(T.p_off.get() + T.n_psi, &T.n_p, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  T.n_direct_pairs = (int64_t)read_scalar(pairs.get(), st);
+  T.lists_built = true;
+}
+
+void build_lists(TreeDev& T) {
+  if (T.lists_built) return;
+  if (T.d == 1) build_lists_impl<1>(T);
+  else if (T.d == 2) build_lists_impl<2>(T);
+  else build_lists_impl<3>(T);
+}
+
+}  // namespace fgt

@@ -1,0 +1,109 @@
+"""Discrete plane-wave FGT (Alg 2 of arXiv 2305.07165) on the GPU.
+
+Entry point `fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary)`
+keeps the contract of the reference's (specified, unshipped) point_fgt module,
+/root/reference/SPEC.md:408-412 and :149-163:
+
+    u_i = sum_j exp(-||x_i - y_j||^2 / delta) q_j,   relative l2 error <= ~10 eps.
+
+Host work is parameter selection only (bit-identical numpy expressions, see
+planewave.py); the tree, lists, outgoing expansions, translations, evaluation and
+direct sums all run in libfgtcuda.so.  `fgt_points_device` takes torch CUDA tensors
+(inputs already resident in HBM) and runs on torch's current stream.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, pw_params
+from .tree import tree_params
+
+
+class FgtParams:
+    """Resolved parameters of one transform (tree + plane-wave quadrature)."""
+
+    def __init__(self, dim, delta, epsilon, n_s, periodic):
+        if not delta > 0:
+            raise ValueError("delta must be positive")
+        eps = clamp_tolerance(epsilon)
+        self.tp, self.l_c_periodic, self.R = tree_params(dim, n_s, delta, eps, periodic)
+        if periodic and not (delta < PERIODIC_IMAGE_DELTA and self.l_c_periodic >= 2):
+            raise ValueError(
+                "periodic transform implemented for the image regime (delta < 1/36, "
+                "cutoff level >= 2); the root Fourier-series regime is not supported")
+        # NUFFT/plane-wave rule for the cutoff boxes
+        self.pwq = pw_params(float(epsilon), delta, R=self.R, dim=dim)
+        self._w = np.ascontiguousarray(self.pwq.weights_1d, dtype=np.float64)
+        pw = _lib.FgtPwParams()
+        pw.dim = dim
+        pw.n_f = self.pwq.n_f
+        pw.delta = float(delta)
+        pw.D0 = float(self.pwq.D0)
+        pw.h = float(self.pwq.h)
+        pw.weights_1d = self._w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        self.pw = pw
+
+
+def _prep(sources, charges, targets, periodic):
+    src = np.atleast_2d(np.asarray(sources, dtype=np.float64))
+    tgt = np.atleast_2d(np.asarray(targets, dtype=np.float64))
+    q = np.asarray(charges, dtype=np.float64).reshape(-1)
+    if src.size == 0 and tgt.size == 0:
+        raise ValueError("need at least one source or target")
+    dim = src.shape[1] if src.size else tgt.shape[1]
+    src = src.reshape(-1, dim)
+    tgt = tgt.reshape(-1, dim)
+    if q.shape[0] != src.shape[0]:
+        raise ValueError("sources/charges length mismatch")
+    if periodic:
+        # the unit cell is [-1/2, 1/2)^d; wrap points given outside it
+        if src.size and (src.min() < -0.5 or src.max() >= 0.5):
+            src = src - np.floor(src + 0.5)
+        if tgt.size and (tgt.min() < -0.5 or tgt.max() >= 0.5):
+            tgt = tgt - np.floor(tgt + 0.5)
+    return np.ascontiguousarray(src), np.ascontiguousarray(q), np.ascontiguousarray(tgt), dim
+
+
+def _boundary(boundary):
+    if boundary not in ("free", "periodic"):
+        raise ValueError(f"unknown boundary {boundary!r}")
+    return boundary == "periodic"
+
+
+def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free",
+               return_times=False):
+    """Potentials u (M,) at the targets; host arrays in, host array out."""
+    periodic = _boundary(boundary)
+    src, q, tgt, dim = _prep(sources, charges, targets, periodic)
+    prm = FgtParams(dim, delta, epsilon, n_s, periodic)
+    u = np.empty(tgt.shape[0], dtype=np.float64)
+    times = _lib.FgtPhaseTimes()
+    P = _lib.ptr
+    _lib.check(_lib.load().fgt_points(P(src), src.shape[0], P(q), P(tgt), tgt.shape[0],
+                                      ctypes.byref(prm.tp), ctypes.byref(prm.pw), P(u),
+                                      ctypes.byref(times)))
+    return (u, times.as_dict()) if return_times else u
+
+
+def fgt_points_device(sources, charges, targets, delta, epsilon, n_s, boundary="free",
+                      out=None, params=None, return_times=False):
+    """Same transform on torch CUDA float64 tensors (resident in HBM)."""
+    import torch
+    periodic = _boundary(boundary)
+    for name, t in (("sources", sources), ("charges", charges), ("targets", targets)):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CUDA float64 tensor")
+    dim = sources.shape[1] if sources.dim() == 2 else targets.shape[1]
+    prm = params or FgtParams(dim, delta, epsilon, n_s, periodic)
+    nt = targets.shape[0]
+    if out is None:
+        out = torch.empty(nt, dtype=torch.float64, device=targets.device)
+    times = _lib.FgtPhaseTimes()
+    stream = torch.cuda.current_stream().cuda_stream
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(_lib.load().fgt_points_dev(vp(sources), sources.shape[0], vp(charges), vp(targets),
+                                          nt, ctypes.byref(prm.tp), ctypes.byref(prm.pw),
+                                          vp(out), ctypes.c_void_p(stream), ctypes.byref(times)))
+    return (out, times.as_dict()) if return_times else out
