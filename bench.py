@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the discrete plane-wave FGT hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1): BASELINE.json configs[1] ("config 2"): d=3 free space, N=M=10^6,
+sources from 8 isotropic Gaussian clusters (sigma 0.02, clipped to the unit box),
+uniform targets, standard-normal charges, delta=1e-4, eps=1e-9, s=200.  Inputs are
+generated with the SURVEY.md §8(d) recipe (numpy default_rng seeds 1 and 2).
+
+A step is one full transform: tree + lists + form + gather + eval + direct.
+`value`   = (N+M) points/s with inputs resident in HBM (fgt_points_device), CUDA events
+            on the launching stream, L2 flushed (512 MB write) between steps.
+`e2e`     = same metric through the host API fgt_points(): pinned host inputs copied
+            H2D and potentials copied D2H inside every timed step.
+`roofline`= the dominant kernel (the FP64-tensor-core form kernel): algorithmic
+            flops 8*N_F per source in a P-box / its CUDA-event time, against the
+            measured FP64 DMMA peak of this GPU.
+Under torchrun (N>1) each rank evaluates a cost-balanced contiguous share of the
+target leaves of the same problem (strong scaling; tree replicated, P-box halo
+recomputed, no data-path collective); time = max over ranks.
+`--impl reference` times the CPU oracle (numpy restatement of the reference; the
+reference ships no compiled path) on a bounded, extrapolated sample of the same
+workload, on rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FGT (N+M) points/sec at fixed ε on 1/2/4/8 B200; % of HBM/FP64 roofline"
+CFG = dict(N=1_000_000, M=1_000_000, d=3, delta=1e-4, eps=1e-9, n_s=200, boundary="free")
+WORKLOAD = ("config2: discrete free-space FGT, d=3, N=M=1e6, sources 8 Gaussian clusters "
+            "(sigma=0.02, clipped), uniform targets, delta=1e-4, eps=1e-9, s=200")
+
+
+def gen_config2(N, M):
+    """SURVEY.md §8(d) item 2 generator."""
+    r = np.random.default_rng(1)
+    C = r.uniform(-0.5, 0.5, (8, 3))
+    lab = r.integers(0, 8, N)
+    y = np.clip(C[lab] + 0.02 * r.standard_normal((N, 3)), -0.5, 0.5)
+    q = r.standard_normal(N)
+    x = np.random.default_rng(2).uniform(-0.5, 0.5, (M, 3))
+    return y, q, x
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                self.out, _ = self.p.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(y, q, x, seed, budget=(2.0, 2.0, 1.0)):
+    """Time the CPU oracle (restated reference Alg 2) on config 2: the full tree, then
+    random samples of P-boxes (form), psi boxes (gather+eval) and direct target
+    leaves, each extrapolated by its work share.  Returns (seconds, description)."""
+    from oracle import point_fgt as op
+    rng = np.random.default_rng(seed)
+    a = op.Alg2(y, q, x, CFG["delta"], CFG["eps"], CFG["n_s"], CFG["boundary"])
+    t0 = time.perf_counter()
+    t = a.build_tree()
+    t_tree = time.perf_counter() - t0
+
+    def sample(items, weight, fn, limit):
+        order = rng.permutation(len(items))
+        done_w, t_spent = 0.0, 0.0
+        for i in order:
+            s = time.perf_counter()
+            fn(items[i])
+            t_spent += time.perf_counter() - s
+            done_w += weight[i]
+            if t_spent >= limit:
+                break
+        total = float(np.sum(weight))
+        return t_spent * (total / done_w if done_w else 0.0), done_w / total if total else 1.0
+
+    dense = a.dense
+    w_form = t.src_count[dense].astype(float) + 1.0
+    t_form, f_form = sample(dense, w_form, lambda S: a.form([S]), budget[0])
+    # gather+eval cost does not depend on the expansion values: use zeros for P-boxes
+    # whose expansions were not sampled
+    zero = np.zeros((a.pw.n_f,) * a.dim, dtype=np.complex128)
+    for S in dense:
+        a.phi.setdefault(S, zero)
+    psi_boxes = np.array([T for T in a.tleaves if t.level[T] == t.l_c and
+                          any(a.is_dense[S] for S, _ in a.list_of(T))])
+    w_ge = np.array([t.tgt_count[T] + 1.0 for T in psi_boxes])
+    t_ge, f_ge = sample(psi_boxes, w_ge, lambda T: a.gather_eval([T]), budget[1])
+    w_d = np.array([t.tgt_count[T] * sum(t.src_count[S] for S, _ in a.list_of(T)
+                                         if not a.is_dense[S]) + 1.0 for T in a.tleaves])
+    t_dir, f_dir = sample(a.tleaves, w_d, lambda T: a.direct([T]), budget[2])
+    total = t_tree + t_form + t_ge + t_dir
+    desc = (f"config-2 input, full oracle tree ({t_tree:.1f} s) + random samples "
+            f"extrapolated by work share: form {100 * f_form:.2f}% of P-box sources, "
+            f"gather+eval {100 * f_ge:.1f}% of psi boxes, direct {100 * f_dir:.1f}% of pairs; "
+            f"extrapolated total {total:.0f} s")
+    return total, desc
+
+
+# ------------------------------------------------------------------ distributed helpers
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    y, q, x = gen_config2(CFG["N"], CFG["M"])
+    times, desc = [], ""
+    for s in range(args.warmup + args.steps):
+        tot, desc = oracle_sample(y, q, x, seed=s)
+        if s >= args.warmup:
+            times.append(tot)
+    sec = float(np.mean(times))
+    value = (CFG["N"] + CFG["M"]) / sec
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 generator, seeds 1/2)",
+        "config": {"workload": WORKLOAD, **CFG},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2305_07165_b200 import _lib, fgt_points, fgt_points_device
+    from paper_2305_07165_b200.point_fgt import FgtParams
+    import ctypes
+
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    N, M = args.n or CFG["N"], args.n or CFG["M"]
+    y, q, x = gen_config2(N, M)
+    share = (rank, world)
+    prm = FgtParams(3, CFG["delta"], CFG["eps"], CFG["n_s"], False, share)
+    dy, dq, dx = (torch.from_numpy(a).to(dev) for a in (y, q, x))
+    u = torch.empty(M, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return fgt_points_device(dy, dq, dx, CFG["delta"], CFG["eps"], CFG["n_s"], out=u,
+                                 params=prm, return_times=True)[1]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    phases = []
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = lib.fgt_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))          # L2 flush, outside the events
+            ev[i][0].record(stream)
+            phases.append(step())
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = lib.fgt_launch_count() - l0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(float(np.sum(step_ms)), world)
+    ms_per_step = total_ms / args.steps
+    value = (N + M) / (ms_per_step * 1e-3)
+
+    # ---- end-to-end through the host API (pinned host buffers, H2D + D2H per step)
+    hy, hq, hx = (torch.from_numpy(a).pin_memory() for a in (y, q, x))
+    hu = torch.empty(M, dtype=torch.float64).pin_memory()
+    ny, nq, nx, nu = hy.numpy(), hq.numpy(), hx.numpy(), hu.numpy()
+    e2e_s = []
+    barrier(world)
+    for i in range(max(1, args.steps)):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nu[:] = fgt_points(ny, nq, nx, CFG["delta"], CFG["eps"], CFG["n_s"], share=share)
+        e2e_s.append(time.perf_counter() - t0)
+    barrier(world)
+    e2e_sec = max_over_ranks(float(np.mean(e2e_s)), world)
+    h2d = (y.nbytes + q.nbytes + x.nbytes)
+    d2h = M * 8
+
+    # ---- roofline of the dominant kernel (form: FP64 DMMA)
+    ph = phases[-1]
+    k_form = float(np.mean([p["k_form_ms"] for p in phases]))
+    flops_form = 8.0 * ph["n_modes"] * ph["n_src_dense"]
+    peak = ctypes.c_double()
+    _lib.check(lib.fgt_bench_fp64_peak(1, ctypes.byref(peak)))
+    achieved = flops_form / (k_form * 1e-3) / 1e12 if k_form > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "form_kernel_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    res = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-2 generator, seeds 1/2)",
+        "config": {"workload": WORKLOAD, **CFG, "N": N, "M": M,
+                   "parallelism": f"target-leaf shares x{world}",
+                   "l2": "flushed between steps (512 MB write, untimed)"},
+        "e2e": {"value": (N + M) / e2e_sec, "unit": "points/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_sec * 1e3},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak.value,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
+                     "traffic": traffic, "kernel": "form_kernel (FP64 DMMA m8n8k4)",
+                     "alg_flops_per_launch": flops_form, "kernel_ms": k_form,
+                     "peak_source": "FP64 DMMA microbenchmark on this GPU "
+                                    "(fgt_bench_fp64_peak; not in MEASURED_PEAKS.json)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "phases_ms": {k: ph[k] for k in ("tree_ms", "lists_ms", "form_ms", "gather_ms",
+                                          "eval_ms", "direct_ms", "k_form_ms", "k_gather_ms",
+                                          "k_eval_ms", "k_direct_ms")},
+        "work": {k: ph[k] for k in ("n_boxes", "n_dense", "n_psi", "n_src_dense", "n_tgt_psi",
+                                     "n_p_entries", "n_direct_pairs", "n_modes")},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sec, desc = oracle_sample(y, q, x, seed=0)
+        res["cpu_baseline"] = {"value": (N + M) / sec, "unit": "points/s", "cores": 1,
+                               "kind": "port", "sample": desc}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override N=M (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        res = run_reference(args, world, rank)
+    else:
+        res = run_ours(args, world, rank, local)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

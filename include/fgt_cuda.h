@@ -107,7 +107,18 @@ typedef struct fgt_tree_params {
   double delta;
   /* periodic trees only: l_c from cutoff_level(kind="density"), root side 1 */
   int32_t l_c_periodic;
+  /* multi-GPU share (fgt_points only): this process evaluates the targets of the
+   * part_rank-th of part_size cost-balanced contiguous ranges (Morton order) of the
+   * target leaves; outgoing expansions are formed for exactly the P-boxes its range
+   * needs (halo recomputed, no exchange).  part_size <= 1 means everything.  Targets
+   * outside the share get u = 0. */
+  int32_t part_rank;
+  int32_t part_size;
 } fgt_tree_params;
+
+/* Split n items with non-negative costs into `parts` contiguous ranges of nearly
+ * equal total cost: bounds[0..parts] (bounds[0] = 0, bounds[parts] = n).  Host-only. */
+int fgt_partition_bounds(const double* cost, int64_t n, int32_t parts, int64_t* bounds);
 
 /* Opaque GPU tree + partition, resident on the device. */
 typedef struct fgt_tree fgt_tree;
@@ -164,6 +175,11 @@ typedef struct fgt_phase_times {
   double tree_ms, lists_ms, form_ms, gather_ms, eval_ms, direct_ms, total_ms;
   double h2d_ms, d2h_ms;
   int64_t launches;
+  /* device time of the hot kernels alone (CUDA events around each launch) */
+  double k_form_ms, k_gather_ms, k_eval_ms, k_direct_ms;
+  /* workload counters for algorithmic byte/flop accounting */
+  int64_t n_boxes, n_dense, n_psi, n_src_dense, n_tgt_psi, n_p_entries, n_direct_pairs;
+  int64_t n_modes; /* N_F = n_f^d */
 } fgt_phase_times;
 
 /* Discrete FGT, DEVICE pointers: u (nt) is OVERWRITTEN with

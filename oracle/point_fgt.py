@@ -89,6 +89,7 @@ class Alg2:
         self.is_dense[self.dense] = True
         self.tleaves = np.nonzero(t.is_leaf & (t.tgt_count > 0))[0]
         self.u_sorted = np.zeros(self.tgt.shape[0])
+        self.tgt_sorted = self.tgt[t.tgt_perm]
         self.lists = {}
         return t
 
@@ -125,7 +126,7 @@ class Alg2:
     def gather_eval(self, targets=None):
         """Translate (gather) then evaluate incoming expansions (Alg 2 steps 2-3)."""
         t = self.tree
-        tgt_sorted = self.tgt[t.tgt_perm]
+        tgt_sorted = self.tgt_sorted
         for T in (self.tleaves if targets is None else targets):
             if t.level[T] != t.l_c:
                 continue
@@ -143,7 +144,7 @@ class Alg2:
     def direct(self, targets=None):
         """Direct interactions over the D-lists with the ball cut (Alg 2 step 4)."""
         t = self.tree
-        tgt_sorted = self.tgt[t.tgt_perm]
+        tgt_sorted = self.tgt_sorted
         r2 = self.pw.D0 ** 2 * self.delta
         for T in (self.tleaves if targets is None else targets):
             sl = self._tgt_slice(T)

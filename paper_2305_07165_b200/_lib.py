@@ -29,7 +29,8 @@ class FgtPwParams(ctypes.Structure):
 class FgtTreeParams(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("periodic", ctypes.c_int32), ("n_s", ctypes.c_int64),
                 ("D0", ctypes.c_double), ("delta", ctypes.c_double),
-                ("l_c_periodic", ctypes.c_int32)]
+                ("l_c_periodic", ctypes.c_int32), ("part_rank", ctypes.c_int32),
+                ("part_size", ctypes.c_int32)]
 
 
 class FgtTreeInfo(ctypes.Structure):
@@ -46,9 +47,14 @@ class FgtListInfo(ctypes.Structure):
 
 
 class FgtPhaseTimes(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_double) for n in
-                ("tree_ms", "lists_ms", "form_ms", "gather_ms", "eval_ms", "direct_ms",
-                 "total_ms", "h2d_ms", "d2h_ms")] + [("launches", ctypes.c_int64)]
+    _fields_ = ([(n, ctypes.c_double) for n in
+                 ("tree_ms", "lists_ms", "form_ms", "gather_ms", "eval_ms", "direct_ms",
+                  "total_ms", "h2d_ms", "d2h_ms")] + [("launches", ctypes.c_int64)]
+                + [(n, ctypes.c_double) for n in
+                   ("k_form_ms", "k_gather_ms", "k_eval_ms", "k_direct_ms")]
+                + [(n, ctypes.c_int64) for n in
+                   ("n_boxes", "n_dense", "n_psi", "n_src_dense", "n_tgt_psi", "n_p_entries",
+                    "n_direct_pairs", "n_modes")])
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -83,6 +89,7 @@ SIGNATURES = {
     "fgt_points": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
                         ctypes.POINTER(FgtPwParams), _P, ctypes.POINTER(FgtPhaseTimes)]),
     "fgt_bench_fp64_peak": (_I, [_I, ctypes.POINTER(_D)]),
+    "fgt_partition_bounds": (_I, [_P, _I64, ctypes.c_int32, _P]),
 }
 
 _lib = None

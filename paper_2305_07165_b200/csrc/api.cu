@@ -12,6 +12,18 @@ static thread_local std::string g_last_error;
 static thread_local int64_t g_launches = 0;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void ensure_pool_retained() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
 void count_launch(int n) { g_launches += n; }
 
 // RAII stream for host-pointer entry points
@@ -55,18 +67,131 @@ __global__ void scatter_kernel(const double* __restrict__ us, const int64_t* __r
     u[perm[i]] = us[i];
 }
 
+__global__ void leaf_direct_cost_kernel(const int64_t* __restrict__ tl, int64_t n,
+                                        const int64_t* __restrict__ d_off, const int64_t* __restrict__ d_src,
+                                        const int64_t* __restrict__ scount, const int64_t* __restrict__ tcount,
+                                        double* __restrict__ nt_out, double* __restrict__ pairs_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0;
+    for (int64_t e = d_off[i]; e < d_off[i + 1]; ++e) s += (double)scount[d_src[e]];
+    double t = (double)tcount[tl[i]];
+    nt_out[i] = t;
+    pairs_out[i] = t * s;
+  }
+}
+
+std::vector<int64_t> partition_bounds(const std::vector<double>& cost, int parts) {
+  const int64_t n = (int64_t)cost.size();
+  std::vector<int64_t> b(parts + 1, n);
+  b[0] = 0;
+  double total = 0;
+  for (double c : cost) total += c;
+  double acc = 0;
+  int r = 1;
+  for (int64_t i = 0; i < n && r < parts; ++i) {
+    acc += cost[i];
+    while (r < parts && acc >= total * r / parts) b[r++] = i + 1;
+  }
+  for (; r < parts; ++r) b[r] = n;
+  return b;
+}
+
+// Restrict the target-side work of T to this rank's cost-balanced contiguous range of
+// target leaves (canonical = Morton order at each level).  P-boxes needed by the
+// range's P-lists are flagged in T.dense_need (their expansions are recomputed on
+// every rank that needs them: a one-box halo, no exchange).
+static void restrict_to_share(TreeDev& T, int rank, int size, int64_t NF) {
+  cudaStream_t st = T.st;
+  const int64_t n = T.n_dtgt;
+  std::vector<double> nt(n), pairs(n);
+  std::vector<int64_t> tl(n), doff(n + 1), psi(T.n_psi), poff(T.n_psi + 1);
+  if (n > 0) {
+    DBuf<double> ntd(n, st), prd(n, st);
+    leaf_direct_cost_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.d_tgt_ids.get(), n, T.d_off.get(), T.d_src.get(),
+                                                              T.src_count.get(), T.tgt_count.get(), ntd.get(), prd.get());
+    FGT_LAUNCHED();
+    ntd.to_host(nt.data(), n);
+    prd.to_host(pairs.data(), n);
+    T.d_tgt_ids.to_host(tl.data(), n);
+  }
+  T.d_off.to_host(doff.data(), n + 1);
+  T.psi_ids.to_host(psi.data(), T.n_psi);
+  T.p_off.to_host(poff.data(), T.n_psi + 1);
+  FGT_CUDA(cudaStreamSynchronize(st));
+  // cost in flop-equivalents: eval 8 N_F per target, gather ~100 N_F per P entry
+  // (HBM-bound, ridge ~6 flop/B x 16 B), direct ~40 per pair
+  std::vector<double> cost(n);
+  std::vector<int64_t> psi_of(n, -1);
+  for (int64_t i = 0, j = 0; i < n; ++i) {
+    while (j < T.n_psi && psi[j] < tl[i]) ++j;
+    double c = 40.0 * pairs[i];
+    if (j < T.n_psi && psi[j] == tl[i]) {
+      psi_of[i] = j;
+      c += 8.0 * NF * nt[i] + 100.0 * NF * (double)(poff[j + 1] - poff[j]);
+    }
+    cost[i] = c;
+  }
+  std::vector<int64_t> b = partition_bounds(cost, size);
+  const int64_t lo = b[rank], hi = b[rank + 1];
+  // psi index range covered by target leaves [lo, hi)
+  int64_t plo = 0, phi = 0;
+  {
+    auto first_psi = [&](int64_t i) {
+      for (; i < n; ++i)
+        if (psi_of[i] >= 0) return psi_of[i];
+      return T.n_psi;
+    };
+    plo = first_psi(lo);
+    phi = first_psi(hi);
+  }
+  // restrict direct CSR (absolute offsets stay valid)
+  {
+    DBuf<int64_t> ids(hi - lo, st), off(hi - lo + 1, st);
+    if (hi > lo) FGT_CUDA(cudaMemcpyAsync(ids.get(), T.d_tgt_ids.get() + lo, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    FGT_CUDA(cudaMemcpyAsync(off.get(), T.d_off.get() + lo, (hi - lo + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    T.d_tgt_ids = std::move(ids);
+    T.d_off = std::move(off);
+    T.n_dtgt = hi - lo;
+  }
+  // restrict psi boxes and flag the P-boxes they need
+  T.dense_need.assign(T.n_dense, 0);
+  {
+    const int64_t e0 = poff[plo], e1 = poff[phi];
+    std::vector<int64_t> slots(e1 - e0);
+    if (e1 > e0) {
+      FGT_CUDA(cudaMemcpyAsync(slots.data(), T.p_src.get() + e0, (e1 - e0) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FGT_CUDA(cudaStreamSynchronize(st));
+    }
+    for (int64_t s : slots) T.dense_need[s] = 1;
+    DBuf<int64_t> ids(phi - plo, st), off(phi - plo + 1, st);
+    if (phi > plo) FGT_CUDA(cudaMemcpyAsync(ids.get(), T.psi_ids.get() + plo, (phi - plo) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    FGT_CUDA(cudaMemcpyAsync(off.get(), T.p_off.get() + plo, (phi - plo + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    T.psi_ids = std::move(ids);
+    T.p_off = std::move(off);
+    T.n_psi = phi - plo;
+  }
+}
+
 static void points_pipeline(const double* src, int64_t ns, const double* q, const double* tgt,
                             int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw,
                             double* u, cudaStream_t st, fgt_phase_times* times) {
   FGT_REQUIRE(tp.dim == pw.dim, FGT_EINVAL, "tree/plane-wave dim mismatch");
   const int64_t l0 = g_launches;
   Timer tm(st);
-  fgt_phase_times t{};
+  fgt_phase_times t;
+  std::memset(&t, 0, sizeof(t));
   TreeDev T;
   build_tree(T, src, ns, tgt, nt, tp, st);
   gather_sorted_points(T, src, q, tgt);
   t.tree_ms = tm.lap();
   build_lists(T);
+  if (tp.part_size > 1) {
+    FGT_REQUIRE(tp.part_rank >= 0 && tp.part_rank < tp.part_size, FGT_EINVAL, "bad part_rank");
+    int64_t NF = 1;
+    for (int k = 0; k < pw.dim; ++k) NF *= pw.n_f;
+    restrict_to_share(T, tp.part_rank, tp.part_size, NF);
+  }
   t.lists_ms = tm.lap();
   DBuf<double> us(nt, st);
   us.zero();
@@ -83,7 +208,7 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     t.eval_ms = tm.lap();
   }
   const double D0 = tp.D0;
-  direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get());
+  direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get(), &P.k_direct);
   if (nt > 0) {
     scatter_kernel<<<grid_for(nt, 256), 256, 0, st>>>(us.get(), T.tgt_perm.get(), nt, u);
     FGT_LAUNCHED();
@@ -91,6 +216,18 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.direct_ms = tm.lap();
   t.total_ms = t.tree_ms + t.lists_ms + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
   t.launches = g_launches - l0;
+  t.k_form_ms = P.k_form.ms();
+  t.k_gather_ms = P.k_gather.ms();
+  t.k_eval_ms = P.k_eval.ms();
+  t.k_direct_ms = P.k_direct.ms();
+  t.n_boxes = T.nb;
+  t.n_dense = T.n_dense;
+  t.n_psi = T.n_psi;
+  t.n_src_dense = P.n_src_dense;
+  t.n_tgt_psi = P.n_tgt_psi;
+  t.n_p_entries = T.n_p;
+  t.n_direct_pairs = T.n_direct_pairs;
+  t.n_modes = P.NF;
   if (times) *times = t;
 }
 
@@ -351,7 +488,8 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
     dq.from_host(charges, ns);
     dt.from_host(tgt, nt * d);
     double h2d = tm.lap();
-    fgt_phase_times t{};
+    fgt_phase_times t;
+    std::memset(&t, 0, sizeof(t));
     points_pipeline(ds.get(), ns, dq.get(), dt.get(), nt, *tp, *pw, du.get(), os.s, &t);
     tm.lap();
     du.to_host(u, nt);
@@ -359,6 +497,16 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
     t.h2d_ms = h2d;
     t.d2h_ms = tm.lap();
     if (times) *times = t;
+  });
+}
+
+int fgt_partition_bounds(const double* cost, int64_t n, int32_t parts, int64_t* bounds) {
+  return guarded([&] {
+    FGT_REQUIRE(parts >= 1 && n >= 0 && (n == 0 || cost) && bounds, FGT_EINVAL, "bad arguments");
+    std::vector<double> c(cost, cost + n);
+    for (double v : c) FGT_REQUIRE(v >= 0, FGT_EINVAL, "negative cost");
+    std::vector<int64_t> b = partition_bounds(c, parts);
+    for (int r = 0; r <= parts; ++r) bounds[r] = b[r];
   });
 }
 

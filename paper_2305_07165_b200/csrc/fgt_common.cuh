@@ -59,6 +59,10 @@ int guarded(F&& f) {
   }
 }
 
+// Keep freed pool memory mapped (default release threshold 0 trims the pool at every
+// synchronisation, so multi-GB scratch would be unmapped/remapped on each call).
+void ensure_pool_retained();
+
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered device allocation (cudaMallocAsync pool): frees are ordered after
 // the work already queued on the stream, so scratch never needs a device sync.
@@ -71,6 +75,7 @@ struct DBuf {
   DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
   void alloc(size_t count, cudaStream_t st) {
     release();
+    ensure_pool_retained();
     s = st;
     n = count;
     if (count) FGT_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
@@ -98,6 +103,35 @@ struct DBuf {
   }
   void from_host(const T* h, size_t count) {
     if (count) FGT_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// CUDA-event pair bracketing one kernel launch (device time of that kernel alone).
+struct KClock {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool used = false;
+  void begin(cudaStream_t st) {
+    if (!a) {
+      FGT_CUDA(cudaEventCreate(&a));
+      FGT_CUDA(cudaEventCreate(&b));
+    }
+    FGT_CUDA(cudaEventRecord(a, st));
+    used = true;
+  }
+  void end(cudaStream_t st) { FGT_CUDA(cudaEventRecord(b, st)); }
+  double ms() const {
+    if (!used) return 0.0;
+    float v = 0.f;
+    FGT_CUDA(cudaEventSynchronize(b));
+    FGT_CUDA(cudaEventElapsedTime(&v, a, b));
+    return v;
+  }
+  KClock() = default;
+  KClock(const KClock&) = delete;
+  KClock& operator=(const KClock&) = delete;
+  ~KClock() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
   }
 };
 

@@ -537,6 +537,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   for (int64_t s = 0; s < nd; ++s) {
     int64_t n = cnt[s];
     if (n == 0) continue;
+    if (!T.dense_need.empty() && !T.dense_need[s]) continue;
     int nu = (int)((n + KU - 1) / KU);
     if (nu == 1) {
       units.push_back(make_int4((int)s, 0, (int)n, -1));
@@ -548,6 +549,8 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
       }
     }
   }
+  P.n_src_dense = 0;
+  for (int64_t s = 0; s < nd; ++s) P.n_src_dense += cnt[s];
   if (units.empty()) return;
   DBuf<int4> units_d(units.size(), st);
   units_d.from_host(units.data(), units.size());
@@ -579,6 +582,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   const size_t red_bytes = (size_t)MG * 32 * FORM_MT * NT * 4 * sizeof(double);
   const size_t smem = std::max(etab_bytes, red_bytes);
   const int nunits = (int)units.size();
+  P.k_form.begin(st);
   switch (NT) {
 #define FGT_FORM_CASE(NTV) case NTV: launch_form<D, NTV>(P, T, fa, nrowblk, nunits, smem, st); break;
     FGT_FORM_CASE(1) FGT_FORM_CASE(2) FGT_FORM_CASE(3) FGT_FORM_CASE(4)
@@ -586,6 +590,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
 #undef FGT_FORM_CASE
     default: throw Error(FGT_ERANGE, "n_f too large");
   }
+  P.k_form.end(st);
   if (!reds.empty()) {
     DBuf<int4> reds_d(reds.size(), st);
     reds_d.from_host(reds.data(), reds.size());
@@ -620,15 +625,27 @@ void pw_gather(PwDev& P, TreeDev& T) {
   ga.n_f = P.n_f;
   ga.l_c = T.l_c;
   dim3 grid(grid_for(P.NF, 256, 256), (unsigned)T.n_psi);
+  P.k_gather.begin(st);
   if (T.d == 1) gather_kernel<1><<<grid, 256, 0, st>>>(ga);
   else if (T.d == 2) gather_kernel<2><<<grid, 256, 0, st>>>(ga);
   else gather_kernel<3><<<grid, 256, 0, st>>>(ga);
   FGT_LAUNCHED();
+  P.k_gather.end(st);
 }
 
 void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
   if (T.n_psi == 0) return;
   cudaStream_t st = T.st;
+  {
+    DBuf<int64_t> c(T.n_psi, st);
+    gather_counts_kernel<<<grid_for(T.n_psi, 256), 256, 0, st>>>(T.psi_ids.get(), T.n_psi, T.tgt_count.get(), c.get());
+    FGT_LAUNCHED();
+    std::vector<int64_t> h(T.n_psi);
+    c.to_host(h.data(), T.n_psi);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    P.n_tgt_psi = 0;
+    for (int64_t v : h) P.n_tgt_psi += v;
+  }
   EvalArgs ea;
   ea.tgt = T.tgt_sorted.get();
   ea.center = T.center.get();
@@ -654,13 +671,15 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
     case 8: launch_eval<DD, 8>(ea, T.n_psi, st); break;             \
     default: throw Error(FGT_ERANGE, "n_f too large");              \
   }
+  P.k_eval.begin(st);
   if (T.d == 1) { FGT_EVAL_D(1) }
   else if (T.d == 2) { FGT_EVAL_D(2) }
   else { FGT_EVAL_D(3) }
+  P.k_eval.end(st);
 #undef FGT_EVAL_D
 }
 
-void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted) {
+void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk) {
   if (T.n_d == 0 || T.n_dtgt == 0) return;
   cudaStream_t st = T.st;
   DirectArgs da;
@@ -681,10 +700,12 @@ void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted)
   da.root_side = T.root_side;
   da.n = T.n_dtgt;
   unsigned g = (unsigned)std::min<int64_t>(T.n_dtgt, 148 * 16);
+  if (clk) clk->begin(st);
   if (T.d == 1) direct_kernel<1><<<g, 128, 0, st>>>(da);
   else if (T.d == 2) direct_kernel<2><<<g, 128, 0, st>>>(da);
   else direct_kernel<3><<<g, 128, 0, st>>>(da);
   FGT_LAUNCHED();
+  if (clk) clk->end(st);
 }
 
 }  // namespace fgt

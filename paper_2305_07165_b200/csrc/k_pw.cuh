@@ -14,6 +14,8 @@ struct PwDev {
   DBuf<double> phase;  // (3, n_f) complex: exp(+i m sc o side_lc), o = -1, 0, 1
   DBuf<double> phi;    // (n_dense, R, n_f) complex outgoing expansions
   DBuf<double> psi;    // (n_psi, R, n_f) complex incoming expansions
+  KClock k_form, k_gather, k_eval, k_direct;
+  int64_t n_src_dense = 0, n_tgt_psi = 0;
 };
 
 void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
@@ -24,6 +26,6 @@ void pw_gather(PwDev& P, TreeDev& T);
 // Type-2 evaluation of psi at the targets of every psi box; u_sorted += Re(...).
 void pw_eval(PwDev& P, TreeDev& T, double* u_sorted);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
-void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted);
+void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 
 }  // namespace fgt

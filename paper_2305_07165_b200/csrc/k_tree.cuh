@@ -45,6 +45,9 @@ struct TreeDev {
   DBuf<int32_t> d_v;     // (n_d * d)
   DBuf<int64_t> d_tgt;   // (n_d) target box id
 
+  // multi-GPU share: P-boxes whose expansions this rank needs (empty = all)
+  std::vector<uint8_t> dense_need;
+
   // sorted point data (leaf-contiguous)
   DBuf<double> src_sorted, q_sorted, tgt_sorted;
 };

@@ -24,11 +24,15 @@ from .tree import tree_params
 class FgtParams:
     """Resolved parameters of one transform (tree + plane-wave quadrature)."""
 
-    def __init__(self, dim, delta, epsilon, n_s, periodic):
+    def __init__(self, dim, delta, epsilon, n_s, periodic, share=(0, 1)):
         if not delta > 0:
             raise ValueError("delta must be positive")
         eps = clamp_tolerance(epsilon)
         self.tp, self.l_c_periodic, self.R = tree_params(dim, n_s, delta, eps, periodic)
+        rank, size = share
+        if not 0 <= rank < size:
+            raise ValueError(f"bad share {share!r}")
+        self.tp.part_rank, self.tp.part_size = int(rank), int(size)
         if periodic and not (delta < PERIODIC_IMAGE_DELTA and self.l_c_periodic >= 2):
             raise ValueError(
                 "periodic transform implemented for the image regime (delta < 1/36, "
@@ -73,11 +77,15 @@ def _boundary(boundary):
 
 
 def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free",
-               return_times=False):
-    """Potentials u (M,) at the targets; host arrays in, host array out."""
+               return_times=False, share=(0, 1)):
+    """Potentials u (M,) at the targets; host arrays in, host array out.
+
+    share=(rank, size) evaluates only this rank's cost-balanced range of target leaves
+    (other targets get 0); summing the outputs of all ranks gives the full transform.
+    """
     periodic = _boundary(boundary)
     src, q, tgt, dim = _prep(sources, charges, targets, periodic)
-    prm = FgtParams(dim, delta, epsilon, n_s, periodic)
+    prm = FgtParams(dim, delta, epsilon, n_s, periodic, share)
     u = np.empty(tgt.shape[0], dtype=np.float64)
     times = _lib.FgtPhaseTimes()
     P = _lib.ptr
@@ -88,7 +96,7 @@ def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free",
 
 
 def fgt_points_device(sources, charges, targets, delta, epsilon, n_s, boundary="free",
-                      out=None, params=None, return_times=False):
+                      out=None, params=None, return_times=False, share=(0, 1)):
     """Same transform on torch CUDA float64 tensors (resident in HBM)."""
     import torch
     periodic = _boundary(boundary)
@@ -96,7 +104,7 @@ def fgt_points_device(sources, charges, targets, delta, epsilon, n_s, boundary="
         if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
             raise ValueError(f"{name} must be a contiguous CUDA float64 tensor")
     dim = sources.shape[1] if sources.dim() == 2 else targets.shape[1]
-    prm = params or FgtParams(dim, delta, epsilon, n_s, periodic)
+    prm = params or FgtParams(dim, delta, epsilon, n_s, periodic, share)
     nt = targets.shape[0]
     if out is None:
         out = torch.empty(nt, dtype=torch.float64, device=targets.device)
