@@ -21,7 +21,8 @@ namespace fgt {
 namespace {
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  // not volatile: lets the scheduler interleave independent accumulators
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -31,9 +32,10 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 // etab[k][j][mi] = exp(sign * i * m * x_jk), m = mi - n_f/2, x_jk = (p_jk - ctr_k) * sc,
-// zero for j >= cnt or mi >= n_f.  KC rows, NFP (multiple of 8) columns.
+// zero for j >= cnt or mi >= n_f.  KC rows of NFP (multiple of 8) columns, row stride RS
+// (>= NFP, padded so the fragment loads of consecutive rows hit distinct banks).
 template <int D>
-__device__ void build_etab(double2* __restrict__ etab, int KC, int NFP, const double* __restrict__ pts,
+__device__ void build_etab(double2* __restrict__ etab, int KC, int NFP, int RS, const double* __restrict__ pts,
                            int64_t base, int cnt, const double* ctr, double sc, double sign, int n_f) {
   const int nseg = NFP >> 3;
   const int ntask = KC * D * nseg;
@@ -42,7 +44,7 @@ __device__ void build_etab(double2* __restrict__ etab, int KC, int NFP, const do
     int rest = task / nseg;
     int k = rest % D;
     int j = rest / D;
-    double2* out = etab + ((size_t)k * KC + j) * NFP + seg * 8;
+    double2* out = etab + ((size_t)k * KC + j) * RS + seg * 8;
     if (j >= cnt) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) out[t] = make_double2(0.0, 0.0);
@@ -84,9 +86,9 @@ constexpr int FORM_MT = 2;
 template <int D, int NT>
 __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
   extern __shared__ double2 sm[];
-  constexpr int KC = FORM_KC, MT = FORM_MT, NFP = NT * 8;
+  constexpr int KC = FORM_KC, MT = FORM_MT, NFP = NT * 8, RS = NFP + 2;
   double2* etab = sm;
-  double* sq = reinterpret_cast<double*>(etab + D * KC * NFP);
+  double* sq = reinterpret_cast<double*>(etab + D * KC * RS);
   const int4 u = a.units[blockIdx.y];
   const int slot = u.x, k0 = u.y, kn = u.z, oidx = u.w;
   const int64_t box = a.dense_ids[slot];
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
   for (int c0 = 0; c0 < kn; c0 += KC) {
     const int cnt = min(KC, kn - c0);
     __syncthreads();
-    build_etab<D>(etab, KC, NFP, a.src, pbase + c0, cnt, ctr, a.sc, -1.0, n_f);
+    build_etab<D>(etab, KC, NFP, RS, a.src, pbase + c0, cnt, ctr, a.sc, -1.0, n_f);
     for (int t = threadIdx.x; t < KC; t += blockDim.x) sq[t] = t < cnt ? a.q[pbase + c0 + t] : 0.0;
     __syncthreads();
     if (active) {
@@ -129,33 +131,43 @@ __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
         const int j = kk * 4 + (lane & 3);
         double2 b[NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = etab[((D - 1) * KC + j) * NFP + nt * 8 + (lane >> 2)];
+        for (int nt = 0; nt < NT; ++nt) b[nt] = etab[((D - 1) * KC + j) * RS + nt * 8 + (lane >> 2)];
         const double qj = sq[j];
+        double2 A[MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          double2 A = make_double2(0.0, 0.0);
+          A[mt] = make_double2(0.0, 0.0);
           if (rv[mt]) {
             if (D == 1) {
-              A = make_double2(qj, 0.0);
+              A[mt] = make_double2(qj, 0.0);
             } else if (D == 2) {
-              double2 e0 = etab[(0 * KC + j) * NFP + ra[mt]];
-              A = make_double2(qj * e0.x, qj * e0.y);
+              double2 e0 = etab[(0 * KC + j) * RS + ra[mt]];
+              A[mt] = make_double2(qj * e0.x, qj * e0.y);
             } else {
-              double2 e0 = etab[(0 * KC + j) * NFP + ra[mt]];
-              double2 e1 = etab[(1 * KC + j) * NFP + rb[mt]];
+              double2 e0 = etab[(0 * KC + j) * RS + ra[mt]];
+              double2 e1 = etab[(1 * KC + j) * RS + rb[mt]];
               double2 p = cmul(e0, e1);
-              A = make_double2(qj * p.x, qj * p.y);
+              A[mt] = make_double2(qj * p.x, qj * p.y);
             }
           }
-          const double nai = -A.y;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma(acc[mt][nt][0], acc[mt][nt][1], A.x, b[nt].x);
-            dmma(acc[mt][nt][0], acc[mt][nt][1], nai, b[nt].y);
-            dmma(acc[mt][nt][2], acc[mt][nt][3], A.x, b[nt].y);
-            dmma(acc[mt][nt][2], acc[mt][nt][3], A.y, b[nt].x);
-          }
         }
+        // four passes so consecutive DMMAs never share an accumulator
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], A[mt].x, b[nt].x);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][2], acc[mt][nt][3], A[mt].x, b[nt].y);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], -A[mt].y, b[nt].y);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][2], acc[mt][nt][3], A[mt].y, b[nt].x);
       }
     }
   }
@@ -324,9 +336,9 @@ constexpr int EVAL_MT = 4;
 template <int D, int NT>
 __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   extern __shared__ double2 sm[];
-  constexpr int TB = EVAL_TB, MT = EVAL_MT, NFP = NT * 8;
+  constexpr int TB = EVAL_TB, MT = EVAL_MT, NFP = NT * 8, RS = NFP + 4;
   double2* etab = sm;
-  double* s_u = reinterpret_cast<double*>(etab + D * TB * NFP);
+  double* s_u = reinterpret_cast<double*>(etab + D * TB * RS);
   const int64_t i = blockIdx.x;
   const int64_t T = a.psi_ids[i];
   const int64_t t0 = a.tgt_start[T];
@@ -343,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   for (int p0 = 0; p0 < ntg; p0 += TB) {
     const int cnt = min(TB, ntg - p0);
     __syncthreads();
-    build_etab<D>(etab, TB, NFP, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
+    build_etab<D>(etab, TB, NFP, RS, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
     __syncthreads();
     double part[MT];
 #pragma unroll
@@ -359,14 +371,17 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
         const int c = kk * 4 + (lane & 3);
         double2 B = make_double2(0.0, 0.0);
         if (rb < R && c < n_f) B = psi[(size_t)rb * n_f + c];
+        double2 A[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const double2 A = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * NFP + c];
-          dmma(acc[mt][0], acc[mt][1], A.x, B.x);
-          dmma(acc[mt][0], acc[mt][1], -A.y, B.y);
-          dmma(acc[mt][2], acc[mt][3], A.x, B.y);
-          dmma(acc[mt][2], acc[mt][3], A.y, B.x);
-        }
+        for (int mt = 0; mt < MT; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], A[mt].x, B.x);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].x, B.y);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], -A[mt].y, B.y);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].y, B.x);
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -376,8 +391,8 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
           const int r = nt * 8 + 2 * (lane & 3) + i2;
           if (r >= R) continue;
           double2 f = make_double2(1.0, 0.0);
-          if (D == 2) f = etab[(0 * TB + j) * NFP + r];
-          if (D == 3) f = cmul(etab[(0 * TB + j) * NFP + r / n_f], etab[(1 * TB + j) * NFP + r % n_f]);
+          if (D == 2) f = etab[(0 * TB + j) * RS + r];
+          if (D == 3) f = cmul(etab[(0 * TB + j) * RS + r / n_f], etab[(1 * TB + j) * RS + r % n_f]);
           part[mt] += acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y;
         }
       }
@@ -480,7 +495,7 @@ void launch_form(PwDev& P, TreeDev& T, const FormArgs& fa, int nrowblk, int nuni
 
 template <int D, int NT>
 void launch_eval(const EvalArgs& ea, int64_t n_psi, cudaStream_t st) {
-  size_t smem = (size_t)D * EVAL_TB * NT * 8 * sizeof(double2) + 8 * EVAL_TB * sizeof(double);
+  size_t smem = (size_t)D * EVAL_TB * (NT * 8 + 4) * sizeof(double2) + 8 * EVAL_TB * sizeof(double);
   FGT_CUDA(cudaFuncSetAttribute(eval_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   eval_kernel<D, NT><<<(unsigned)n_psi, 256, smem, st>>>(ea);
   FGT_LAUNCHED();
@@ -578,7 +593,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   fa.MG = MG;
   fa.KS = KS;
   fa.sc = P.sc;
-  const size_t etab_bytes = (size_t)D * FORM_KC * NT * 8 * sizeof(double2) + FORM_KC * sizeof(double);
+  const size_t etab_bytes = (size_t)D * FORM_KC * (NT * 8 + 2) * sizeof(double2) + FORM_KC * sizeof(double);
   const size_t red_bytes = (size_t)MG * 32 * FORM_MT * NT * 4 * sizeof(double);
   const size_t smem = std::max(etab_bytes, red_bytes);
   const int nunits = (int)units.size();

@@ -1,0 +1,119 @@
+"""Pin the CPU oracle against golden fixtures produced by the real reference package
+(tests/golden/make_golden.py).  CPU only."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import kernels as ok
+from oracle import nufft as on
+from oracle import params as op
+from oracle import point_fgt as ofgt
+from oracle import tree as ot
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_table1_and_weights_exact():
+    g = load("params.npz")
+    for i, e in enumerate(g["eps"]):
+        assert op.d0_of(e) == g["D0"][i]
+        for k, f in enumerate((2.0, 3.0, 4.0)):
+            q = op.quad(e, 1e-3, R=f * op.d0_of(e), dim=2)
+            assert q.n_f == g["nf"][k, i] and q.h == g["h"][k, i]
+    # the paper's Table 1
+    assert list(g["nf"][0, [0, 2, 4, 6, 8, 10]]) == [12, 20, 30, 38, 48, 56]
+    assert list(g["nf"][2, [0, 2, 4, 6, 8, 10]]) == [20, 34, 48, 64, 78, 92]
+    assert np.array_equal(op.quad(1e-6, 1e-3, dim=3).w1, g["w30"])
+
+
+def test_table2_and_cutoff_level_exact():
+    g = load("params.npz")
+    for i, e in enumerate(g["np_eps"]):
+        for j, dl in enumerate(g["np_delta"]):
+            assert op.periodic_np(e, dl) == g["n_p"][i, j]
+    for c, out in zip(g["cl_cases"], g["cl_out"]):
+        l_c, R = op.cut_level(c[0], c[1], c[2], "point" if c[3] else "density")
+        assert l_c == out[0] and R == out[1]
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_kernels(d):
+    g = load("kernels.npz")
+    t, s, q = g[f"gd_t{d}"], g[f"gd_s{d}"], g[f"gd_q{d}"]
+    assert rel(ok.gauss_sum(t, s, q, 50.0, 0.05, np.zeros(64)), g[f"gd_free{d}"]) < 1e-14
+    assert rel(ok.gauss_sum(t, s, q, 50.0, np.inf, np.zeros(64)), g[f"gd_inf{d}"]) < 1e-14
+    assert rel(ok.gauss_sum(t, s, q, 50.0, np.inf, np.zeros(64), periodic=True),
+               g[f"gd_per{d}"]) < 1e-14
+    n_r, m = (48, 6) if d < 3 else (20, 4)
+    x, v = g[f"sp_x{d}"], g[f"sp_v{d}"]
+    assert rel(ok.spread(x, v, n_r, m, 0.02, np.zeros((n_r,) * d, complex)), g[f"sp_g{d}"]) < 1e-14
+    assert rel(ok.interp(x, g[f"ip_grid{d}"], n_r, m, 0.02), g[f"ip_out{d}"]) < 1e-14
+
+
+@pytest.mark.parametrize("d,n_f", [(1, 30), (2, 20), (3, 12)])
+def test_nufft(d, n_f):
+    g = load("nufft.npz")
+    x, f, c = g[f"x{d}"], g[f"f{d}"], g[f"c{d}"]
+    assert rel(on.exact_sums(x, f, n_f, d, "type1", -1), g[f"t1dft_{d}"]) < 1e-13
+    assert rel(on.exact_sums(x, c, n_f, d, "type2", +1), g[f"t2dft_{d}"]) < 1e-13
+    assert tuple(on.plan(n_f, 1e-10)) == tuple(g[f"plan_{d}"])
+    for eps in (1e-4, 1e-8, 1e-12):
+        tag = f"{d}_{int(-np.log10(eps))}"
+        a1 = on.type1(x, f, n_f, d, eps, -1, method="grid")
+        a2 = on.type2(x, c, n_f, d, eps, +1, method="grid")
+        # same algorithm; numpy FFT vs the reference's radix-2/3/5 FFT (roundoff only)
+        assert rel(a1, g[f"t1grid_{tag}"]) < 1e-12
+        assert rel(a2, g[f"t2grid_{tag}"]) < 1e-12
+        # NUFFT contract vs exact sums
+        assert rel(a1, g[f"t1dft_{d}"]) < eps
+        assert rel(a2, g[f"t2dft_{d}"]) < eps
+
+
+def tree_inputs(gen):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("mg", os.path.join(GOLD, "make_golden.py"))
+    # make_golden imports the reference at module import; replicate only its generators
+    src = open(spec.origin).read()
+    start = src.index("def tree_inputs")
+    ns = {"np": np}
+    exec(src[start:src.index("def trees")], ns)
+    return ns["tree_inputs"](gen)
+
+
+TREES = {"cfg1": ("uniform2", 100, 1e-3, 1e-6, False),
+         "clust3d": ("clust3", 40, 1e-4, 1e-9, False),
+         "periodic2d": ("uniform2p", 50, 1e-4, 1e-8, True),
+         "shell3d": ("shell3", 10, 1e-5, 1e-6, False)}
+
+
+@pytest.mark.parametrize("name", list(TREES))
+def test_tree_bit_exact_vs_reference(name):
+    gen, n_s, delta, eps, periodic = TREES[name]
+    y, x, _ = tree_inputs(gen)
+    t = ot.build(y, x, n_s, delta, eps, periodic=periodic)
+    g = load(f"tree_{name}.npz")
+    assert t.l_c == int(g["l_c"]) and t.R == float(g["R"])
+    assert np.array_equal(t.root_center, g["root_center"]) and t.root_side == float(g["root_side"])
+    for f in ("level", "parent", "children", "coords", "is_leaf", "src_start", "src_count",
+              "tgt_start", "tgt_count", "n_points"):
+        assert np.array_equal(getattr(t, f), g[f]), f
+    assert np.array_equal(t.src_perm, g["src_perm"]) and np.array_equal(t.tgt_perm, g["tgt_perm"])
+
+
+def test_alg2_config1_vs_reference_primitives():
+    y, x, q = tree_inputs("uniform2")
+    g = load("alg2_cfg1.npz")
+    u = ofgt.fgt_points(y, q, x, 1e-3, 1e-6, 100)
+    assert rel(u, g["u"]) < 1e-12          # same algorithm on the reference primitives
+    assert rel(u, g["exact"]) <= 10 * 1e-6  # SPEC.md:425 accuracy bar
+    assert rel(g["u"], g["exact"]) <= 10 * 1e-6
