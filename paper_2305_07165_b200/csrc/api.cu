@@ -4,7 +4,7 @@
 #include <memory>
 
 #include "k_kernels.cuh"
-#include "k_pw.cuh"
+#include "k_nufft.cuh"
 
 namespace fgt {
 
@@ -196,14 +196,19 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   DBuf<double> us(nt, st);
   us.zero();
   PwDev P;
+  NufftPlan NP;
   if (T.n_dense > 0) {
     pw_setup(P, T, pw);
-    pw_form(P, T);
+    // box-local NUFFT plan at tolerance eps/10; eps = 3 exp(-D0^2)
+    const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
+    const double X = 0.5 * P.side_lc * P.sc * (1.0 + 1e-12);
+    nufft_plan(NP, pw.n_f, tol, X, pw.weights_1d, st);
+    pw_form(P, T, &NP);
     t.form_ms = tm.lap();
     pw_gather(P, T);
     P.phi.release();
     t.gather_ms = tm.lap();
-    pw_eval(P, T, us.get());
+    pw_eval(P, T, us.get(), &NP);
     P.psi.release();
     t.eval_ms = tm.lap();
   }

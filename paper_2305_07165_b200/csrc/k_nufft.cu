@@ -1,0 +1,588 @@
+// Box-local NUFFT (spread / separable DFT / interpolate) for heavy P-boxes and psi boxes.
+//
+// The reference forms phi with nufft_type1 (nufft.py:139-162: Gaussian spreading onto a
+// periodic 2x grid, radix-2/3/5 FFT, bin selection, deconvolution) and evaluates psi
+// with nufft_type2 (nufft.py:165-183).  On B200 the same transform is organised as:
+//   1. spreading with the exponential-of-semicircle kernel (w taps/axis instead of the
+//      reference Gaussian's 2w+1) into a NON-periodic grid that covers only the box
+//      (2X/Delta + w cells per axis), held in shared-memory plane slabs in which every
+//      warp owns whole planes: plain read-modify-write, no atomics;
+//   2. the grid -> mode map as d separable complex GEMMs on the FP64 tensor cores
+//      (mma.sync m8n8k4 .f64) with the deconvolution 1/fh(m) and the plane-wave weights
+//      folded into the 1-D matrices, written straight into phi (no FFT, no bin gather:
+//      only n_f of the 2 n_f modes are ever needed);
+//   3. evaluation runs the transposed chain and interpolates with the same kernel.
+// Partial grids of K-split boxes are summed in a fixed order (deterministic).
+#include <cmath>
+
+#include "k_nufft.cuh"
+
+namespace fgt {
+
+namespace {
+
+__device__ __forceinline__ void dmma2(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__host__ __device__ __forceinline__ double es_kernel(double z, double beta) {
+  double s = 1.0 - z * z;
+  return s > 0.0 ? exp(beta * (sqrt(s) - 1.0)) : 0.0;
+}
+
+constexpr int MAXW = 16;
+
+// ------------------------------------------------------------------ batched GEMM
+// C[b] = A[b] (M x K) * B[b] (K x N), row-major with leading dims, batch strides in
+// elements; complex operands are interleaved (re, im).  CRE: store Re(C) only.
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, batch;
+  int64_t lda, ldb, ldc, sA, sB, sC;
+  const int64_t* cidx;  // optional C batch index
+  const int64_t* bidx;  // optional B batch index
+};
+
+template <bool AC, bool BC, bool CRE>
+__global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t b = blockIdx.z;
+  const int m0 = blockIdx.y * 32 + wm * 16;
+  const int n0 = blockIdx.x * 48 + wn * 24;
+  const double* A = g.A + b * g.sA * (AC ? 2 : 1);
+  const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
+  const int64_t cb = g.cidx ? g.cidx[b] : b;
+  double* C = g.C + cb * g.sC * (CRE ? 1 : 2);
+  double acc[2][3][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+  for (int k0 = 0; k0 < g.K; k0 += 4) {
+    const int k = k0 + (lane & 3);
+    double ar[2], ai[2], br[3], bi[3];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = m0 + mt * 8 + (lane >> 2);
+      ar[mt] = ai[mt] = 0.0;
+      if (r < g.M && k < g.K) {
+        if (AC) {
+          double2 v = *reinterpret_cast<const double2*>(A + 2 * (r * g.lda + k));
+          ar[mt] = v.x;
+          ai[mt] = v.y;
+        } else {
+          ar[mt] = A[r * g.lda + k];
+        }
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int c = n0 + nt * 8 + (lane >> 2);
+      br[nt] = bi[nt] = 0.0;
+      if (c < g.N && k < g.K) {
+        if (BC) {
+          double2 v = *reinterpret_cast<const double2*>(B + 2 * (k * g.ldb + c));
+          br[nt] = v.x;
+          bi[nt] = v.y;
+        } else {
+          br[nt] = B[k * g.ldb + c];
+        }
+      }
+    }
+    // re += ar br - ai bi ; im += ar bi + ai br   (terms with a real operand vanish)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
+    if (AC && BC) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
+    }
+    if (!CRE) {
+      if (BC) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
+      }
+      if (AC) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
+      }
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int r = m0 + mt * 8 + (lane >> 2);
+    if (r >= g.M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = n0 + nt * 8 + 2 * (lane & 3) + i;
+        if (c >= g.N) continue;
+        if (CRE) C[r * g.ldc + c] = acc[mt][nt][i];
+        else *reinterpret_cast<double2*>(C + 2 * (r * g.ldc + c)) = make_double2(acc[mt][nt][i], acc[mt][nt][2 + i]);
+      }
+    }
+  }
+}
+
+template <bool AC, bool BC, bool CRE>
+void bgemm(const GemmArgs& g, cudaStream_t st) {
+  if (g.batch == 0 || g.M == 0 || g.N == 0) return;
+  dim3 grid((g.N + 47) / 48, (g.M + 31) / 32, g.batch);
+  FGT_REQUIRE(g.batch <= 65535, FGT_ERANGE, "GEMM batch too large");
+  bgemm_kernel<AC, BC, CRE><<<grid, 128, 0, st>>>(g);
+  FGT_LAUNCHED();
+}
+
+GemmArgs gemm(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB,
+              double* C, int64_t ldc, int64_t sC, int M, int N, int K, int batch,
+              const int64_t* cidx = nullptr, const int64_t* bidx = nullptr) {
+  GemmArgs g;
+  g.A = A; g.B = B; g.C = C;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.sA = sA; g.sB = sB; g.sC = sC;
+  g.cidx = cidx;
+  g.bidx = bidx;
+  return g;
+}
+
+// ------------------------------------------------------------------ spreading
+struct SpreadArgs {
+  const double* src;
+  const double* q;
+  const double* center;
+  const int64_t* dense_ids;
+  const int64_t* src_start;
+  const int64_t* slots;  // list index -> dense slot
+  const int4* units;     // (list index, k0, kn, scratch index or -1)
+  double* grid;          // (list, G^D)
+  double* scratch;       // (nscratch, G^D)
+  double sc, inv_delta, beta;
+  int w, gmin, G, SP;
+};
+
+constexpr int SPREAD_PC = 64;
+
+template <int D>
+__global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a) {
+  extern __shared__ double sm[];
+  const int G = a.G, w = a.w;
+  const int64_t plane = D == 3 ? (int64_t)G * G : (D == 2 ? G : 1);
+  const int gs0 = blockIdx.y * a.SP;
+  const int np = min(a.SP, G - gs0);
+  double* sl = sm;
+  double* s_w = sl + (size_t)a.SP * plane;
+  double* s_q = s_w + SPREAD_PC * D * MAXW;
+  int* s_a = reinterpret_cast<int*>(s_q + SPREAD_PC);
+  for (int64_t e = threadIdx.x; e < np * plane; e += blockDim.x) sl[e] = 0.0;
+  const int4 u = a.units[blockIdx.x];
+  const int64_t box = a.dense_ids[a.slots[u.x]];
+  const int64_t base = a.src_start[box] + u.y;
+  double ctr[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ctr[k] = a.center[box * D + k];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double s = a.sc * a.inv_delta, half = 0.5 * w, inv_half = 2.0 / w;
+  for (int c0 = 0; c0 < u.z; c0 += SPREAD_PC) {
+    const int cnt = min(SPREAD_PC, u.z - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt * D; t += blockDim.x) {
+      const int j = t / D, k = t % D;
+      const double tt = (a.src[(base + c0 + j) * D + k] - ctr[k]) * s;
+      const double a0 = ceil(tt - half);
+      int ai = (int)a0 - a.gmin;
+      ai = max(0, min(ai, G - w));  // never taken for in-box points (grid has margin)
+      s_a[j * D + k] = ai;
+      double* wp = s_w + (j * D + k) * MAXW;
+      for (int o = 0; o < w; ++o) wp[o] = es_kernel((a0 + o - tt) * inv_half, a.beta);
+    }
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) s_q[t] = a.q[base + c0 + t];
+    __syncthreads();
+    for (int j = 0; j < cnt; ++j) {
+      const int a0 = s_a[j * D];
+      const int plo = max(a0, gs0), phi = min(a0 + w, gs0 + np);
+      if (plo >= phi) continue;
+      int p = plo + ((warp - plo % 8) + 8) % 8;  // first plane this warp owns
+      for (; p < phi; p += 8) {
+        const double c = s_q[j] * s_w[(j * D) * MAXW + (p - a0)];
+        double* pl = sl + (int64_t)(p - gs0) * plane;
+        if (D == 3) {
+          const int a1 = s_a[j * D + 1], a2 = s_a[j * D + 2];
+          const double* w1 = s_w + (j * D + 1) * MAXW;
+          const double* w2 = s_w + (j * D + 2) * MAXW;
+          for (int idx = lane; idx < w * w; idx += 32) {
+            const int o1 = idx / w, o2 = idx - o1 * w;
+            pl[(a1 + o1) * G + a2 + o2] += c * w1[o1] * w2[o2];
+          }
+        } else if (D == 2) {
+          const int a1 = s_a[j * D + 1];
+          const double* w1 = s_w + (j * D + 1) * MAXW;
+          for (int o1 = lane; o1 < w; o1 += 32) pl[a1 + o1] += c * w1[o1];
+        } else if (lane == 0) {
+          pl[0] += c;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t GD = plane * G;
+  double* out = (u.w < 0 ? a.grid + (int64_t)u.x * GD : a.scratch + (int64_t)u.w * GD) + gs0 * plane;
+  for (int64_t e = threadIdx.x; e < np * plane; e += blockDim.x) out[e] = sl[e];
+}
+
+__global__ void grid_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red,
+                                   int64_t GD, double* __restrict__ grid) {
+  const int4 r = red[blockIdx.y];  // (list index, first scratch, count, -)
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < GD;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < r.z; ++t) s += scratch[(int64_t)(r.y + t) * GD + e];
+    grid[(int64_t)r.x * GD + e] = s;
+  }
+}
+
+// ------------------------------------------------------------------ interpolation
+struct InterpArgs {
+  const double* tgt;
+  const double* center;
+  const int64_t* psi_ids;
+  const int64_t* list;   // list index -> psi index
+  const int64_t* tgt_start;
+  const int64_t* tgt_count;
+  const double* grid;    // (list, G^D) real
+  double* u;
+  double sc, inv_delta, beta;
+  int w, gmin, G;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
+  __shared__ double s_w[8][D][MAXW];
+  const int64_t li = blockIdx.x;
+  const int64_t T = a.psi_ids[a.list[li]];
+  const int64_t t0 = a.tgt_start[T];
+  const int nt = (int)a.tgt_count[T];
+  const int G = a.G, w = a.w;
+  const int64_t GD = D == 3 ? (int64_t)G * G * G : (D == 2 ? (int64_t)G * G : G);
+  const double* grid = a.grid + li * GD;
+  double ctr[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ctr[k] = a.center[T * D + k];
+  const double s = a.sc * a.inv_delta, half = 0.5 * w, inv_half = 2.0 / w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (D == 3) {
+    // one warp per target; lanes over the (o1, o2) taps of each o0 plane
+    for (int j = warp; j < nt; j += 8) {
+      int ai[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double tt = (a.tgt[(t0 + j) * D + k] - ctr[k]) * s;
+        const double a0 = ceil(tt - half);
+        ai[k] = max(0, min((int)a0 - a.gmin, G - w));
+        for (int o = lane; o < w; o += 32) s_w[warp][k][o] = es_kernel((a0 + o - tt) * inv_half, a.beta);
+      }
+      __syncwarp();
+      double acc = 0.0;
+      for (int o0 = 0; o0 < w; ++o0) {
+        const double* pl = grid + ((int64_t)(ai[0] + o0) * G) * G;
+        double part = 0.0;
+        for (int idx = lane; idx < w * w; idx += 32) {
+          const int o1 = idx / w, o2 = idx - o1 * w;
+          part += s_w[warp][1][o1] * s_w[warp][2][o2] * pl[(ai[1] + o1) * G + ai[2] + o2];
+        }
+        acc += s_w[warp][0][o0] * part;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) a.u[t0 + j] += acc;
+      __syncwarp();
+    }
+  } else {
+    for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+      double wk[D][MAXW];
+      int ai[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double tt = (a.tgt[(t0 + j) * D + k] - ctr[k]) * s;
+        const double a0 = ceil(tt - half);
+        ai[k] = max(0, min((int)a0 - a.gmin, G - w));
+        for (int o = 0; o < MAXW; ++o) wk[k][o] = o < w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
+      }
+      double acc = 0.0;
+      if (D == 2) {
+        for (int o0 = 0; o0 < w; ++o0) {
+          const double* row = grid + (int64_t)(ai[0] + o0) * G + ai[1];
+          double part = 0.0;
+          for (int o1 = 0; o1 < w; ++o1) part += wk[1][o1] * row[o1];
+          acc += wk[0][o0] * part;
+        }
+      } else {
+        for (int o0 = 0; o0 < w; ++o0) acc += wk[0][o0] * grid[ai[0] + o0];
+      }
+      a.u[t0 + j] += acc;
+    }
+  }
+}
+
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wq) {
+  x.resize(n);
+  wq.resize(n);
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    x[i] = z;
+    wq[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+}  // namespace
+
+void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
+  N.n_f = n_f;
+  N.tol = tol;
+  N.X = X;
+  N.w = (int)std::ceil(std::log10(1.0 / tol)) + 1;
+  N.w = std::max(2, std::min(N.w, MAXW));
+  N.beta = 2.30 * N.w;
+  N.Delta = M_PI / n_f;  // 2 pi / (sigma n_f), sigma = 2
+  const double Xg = X / N.Delta;
+  N.gmin = (int)std::floor(-Xg - 0.5 * N.w) - 1;
+  const int gmax = (int)std::ceil(Xg + 0.5 * N.w) + 1;
+  N.G = gmax - N.gmin + 1;
+  std::vector<double> xs, ws;
+  gauss_legendre(4 * N.w + 40, xs, ws);
+  N.fh.assign(n_f, 0.0);
+  for (int mi = 0; mi < n_f; ++mi) {
+    const double m = mi - n_f / 2;
+    double s = 0;
+    for (size_t q = 0; q < xs.size(); ++q) {
+      const double t = 0.5 * N.w * xs[q];
+      s += 0.5 * N.w * ws[q] * es_kernel(xs[q], N.beta) * std::cos(m * N.Delta * t);
+    }
+    N.fh[mi] = s;
+  }
+  const int G = N.G;
+  std::vector<double> Ef(2 * n_f * G), EfT(2 * n_f * G), Ee(2 * n_f * G), EeT(2 * n_f * G);
+  for (int mi = 0; mi < n_f; ++mi) {
+    const double m = mi - n_f / 2;
+    for (int g = 0; g < G; ++g) {
+      const double arg = m * (N.gmin + g) * N.Delta;
+      const double c = std::cos(arg), sn = std::sin(arg);
+      const double wf = (w1d ? w1d[mi] : 1.0) / N.fh[mi], we = 1.0 / N.fh[mi];
+      Ef[2 * (mi * G + g)] = wf * c;
+      Ef[2 * (mi * G + g) + 1] = -wf * sn;
+      EfT[2 * (g * n_f + mi)] = wf * c;
+      EfT[2 * (g * n_f + mi) + 1] = -wf * sn;
+      Ee[2 * (g * n_f + mi)] = we * c;
+      Ee[2 * (g * n_f + mi) + 1] = we * sn;
+      EeT[2 * (mi * G + g)] = we * c;
+      EeT[2 * (mi * G + g) + 1] = we * sn;
+    }
+  }
+  N.Ef.alloc(Ef.size(), st);
+  N.Ef.from_host(Ef.data(), Ef.size());
+  N.EfT.alloc(EfT.size(), st);
+  N.EfT.from_host(EfT.data(), EfT.size());
+  N.Ee.alloc(Ee.size(), st);
+  N.Ee.from_host(Ee.data(), Ee.size());
+  N.EeT.alloc(EeT.size(), st);
+  N.EeT.from_host(EeT.data(), EeT.size());
+  FGT_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+}
+
+namespace {
+int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  while (e--) r *= b;
+  return r;
+}
+
+template <int D>
+void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots) {
+  if (slots.empty()) return;
+  cudaStream_t st = T.st;
+  const int G = N.G, n_f = N.n_f, w = N.w;
+  const int64_t GD = ipow(G, D);
+  const int64_t plane = GD / G;
+  // per-slot source counts
+  std::vector<int64_t> dense(T.n_dense), scount(T.nb);
+  T.dense_ids.to_host(dense.data(), T.n_dense);
+  T.src_count.to_host(scount.data(), T.nb);
+  FGT_CUDA(cudaStreamSynchronize(st));
+  // shared-memory slab: as many axis-0 planes as fit beside the point staging area
+  const size_t stage = (size_t)SPREAD_PC * (D * MAXW + 1) * sizeof(double) + SPREAD_PC * D * sizeof(int);
+  const size_t budget = 227 * 1024 - stage - 1024;
+  int SP = (int)std::min<int64_t>(G, (int64_t)(budget / (plane * sizeof(double))));
+  FGT_REQUIRE(SP >= 1, FGT_ERANGE, "spreading grid plane does not fit in shared memory");
+  const int nslab = (G + SP - 1) / SP;
+  SP = (G + nslab - 1) / nslab;
+  const size_t smem = (size_t)SP * plane * sizeof(double) + stage;
+  FGT_CUDA(cudaFuncSetAttribute(spread_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // batches bounded by ~1.5 GB of grid + stage buffers
+  const int64_t per_box = GD * 8 + (D >= 2 ? plane * n_f * 16 : 0) + (D == 3 ? (int64_t)G * n_f * n_f * 16 : 0);
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)1536 * 1024 * 1024 / per_box));
+  const int KU = 4096;
+  for (size_t b0 = 0; b0 < slots.size(); b0 += nb_max) {
+    const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)slots.size() - b0);
+    std::vector<int4> units, reds;
+    int nscr = 0;
+    for (int64_t i = 0; i < nbat; ++i) {
+      const int64_t n = scount[dense[slots[b0 + i]]];
+      const int nu = (int)((n + KU - 1) / KU);
+      if (nu <= 1) {
+        units.push_back(make_int4((int)i, 0, (int)n, -1));
+      } else {
+        reds.push_back(make_int4((int)i, nscr, nu, 0));
+        for (int t = 0; t < nu; ++t)
+          units.push_back(make_int4((int)i, t * KU, (int)std::min<int64_t>(KU, n - (int64_t)t * KU), nscr++));
+      }
+    }
+    DBuf<int64_t> sl_d(nbat, st);
+    sl_d.from_host(slots.data() + b0, nbat);
+    DBuf<int4> units_d(units.size(), st), reds_d(reds.size(), st);
+    units_d.from_host(units.data(), units.size());
+    if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
+    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * GD, st);
+    SpreadArgs sa;
+    sa.src = T.src_sorted.get();
+    sa.q = T.q_sorted.get();
+    sa.center = T.center.get();
+    sa.dense_ids = T.dense_ids.get();
+    sa.src_start = T.src_start.get();
+    sa.slots = sl_d.get();
+    sa.units = units_d.get();
+    sa.grid = grid.get();
+    sa.scratch = scratch.get();
+    sa.sc = P.sc;
+    sa.inv_delta = 1.0 / N.Delta;
+    sa.beta = N.beta;
+    sa.w = w;
+    sa.gmin = N.gmin;
+    sa.G = G;
+    sa.SP = SP;
+    spread_kernel<D><<<dim3((unsigned)units.size(), nslab), 256, smem, st>>>(sa);
+    FGT_LAUNCHED();
+    if (!reds.empty()) {
+      grid_reduce_kernel<<<dim3(grid_for(GD, 256, 64), (unsigned)reds.size()), 256, 0, st>>>(
+          scratch.get(), reds_d.get(), GD, grid.get());
+      FGT_LAUNCHED();
+    }
+    scratch.release();
+    // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
+    double* phi = P.phi.get();
+    const int64_t NF = P.NF;
+    if (D == 1) {
+      bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid.get(), 1, G, phi, 1, NF, n_f, 1, G, (int)nbat, sl_d.get()), st);
+    } else if (D == 2) {
+      DBuf<double> t1(2 * nbat * G * n_f, st);
+      // T1[g1][m2] = sum_g2 grid[g1][g2] EfT[g2][m2]
+      bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
+      // phi[m1][m2] = sum_g1 Ef[m1][g1] T1[g1][m2]
+      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NF, n_f, n_f, G, (int)nbat, sl_d.get()), st);
+    } else {
+      DBuf<double> t1(2 * nbat * plane * n_f, st), t2(2 * nbat * G * n_f * n_f, st);
+      // T1[(g1 g2)][m3] = sum_g3 grid[(g1 g2)][g3] EfT[g3][m3]
+      bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, plane * n_f, (int)plane, n_f, G, (int)nbat), st);
+      // T2[g1][m2][m3] = sum_g2 Ef[m2][g2] T1[g1][g2][m3]      (batch = box x g1)
+      FGT_REQUIRE(nbat * G <= 65535, FGT_ERANGE, "GEMM batch too large");
+      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, t2.get(), n_f, (int64_t)n_f * n_f, n_f, n_f, G, (int)(nbat * G)), st);
+      // phi[m1][(m2 m3)] = sum_g1 Ef[m1][g1] T2[g1][(m2 m3)]
+      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t2.get(), (int64_t)n_f * n_f, (int64_t)G * n_f * n_f, phi, (int64_t)n_f * n_f, NF, n_f, n_f * n_f, G, (int)nbat, sl_d.get()), st);
+    }
+  }
+}
+
+template <int D>
+void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& idx,
+                     double* u_sorted) {
+  if (idx.empty()) return;
+  cudaStream_t st = T.st;
+  const int G = N.G, n_f = N.n_f;
+  const int64_t GD = ipow(G, D), plane = GD / G, NF = P.NF;
+  const int64_t per_box = GD * 8 + (D >= 2 ? (int64_t)G * ipow(n_f, D - 1) * 16 : 0) + (D == 3 ? plane * n_f * 16 : 0);
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)1536 * 1024 * 1024 / per_box));
+  for (size_t b0 = 0; b0 < idx.size(); b0 += nb_max) {
+    const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)idx.size() - b0);
+    DBuf<int64_t> li(nbat, st);
+    li.from_host(idx.data() + b0, nbat);
+    DBuf<double> grid(nbat * GD, st);
+    const double* psi = P.psi.get();  // first stage reads psi[list[b]] through bidx
+    if (D == 1) {
+      // grid[g] = Re sum_m Ee[g][m] psi[m]
+      bgemm<true, true, true>(gemm(N.Ee.get(), n_f, 0, psi, 1, NF, grid.get(), 1, GD, G, 1, n_f, (int)nbat, nullptr, li.get()), st);
+    } else if (D == 2) {
+      DBuf<double> v1(2 * nbat * G * n_f, st);
+      // V1[g1][m2] = sum_m1 Ee[g1][m1] psi[m1][m2]
+      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, psi, n_f, NF, v1.get(), n_f, (int64_t)G * n_f, G, n_f, n_f, (int)nbat, nullptr, li.get()), st);
+      // grid[g1][g2] = Re sum_m2 V1[g1][m2] EeT[m2][g2]
+      bgemm<true, true, true>(gemm(v1.get(), n_f, (int64_t)G * n_f, N.EeT.get(), G, 0, grid.get(), G, GD, G, G, n_f, (int)nbat), st);
+    } else {
+      DBuf<double> v1(2 * nbat * G * n_f * n_f, st), v2(2 * nbat * plane * n_f, st);
+      // V1[g1][(m2 m3)] = sum_m1 Ee[g1][m1] psi[m1][(m2 m3)]
+      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, psi, (int64_t)n_f * n_f, NF, v1.get(), (int64_t)n_f * n_f, (int64_t)G * n_f * n_f, G, n_f * n_f, n_f, (int)nbat, nullptr, li.get()), st);
+      // V2[g1][g2][m3] = sum_m2 Ee[g2][m2] V1[g1][m2][m3]     (batch = box x g1)
+      FGT_REQUIRE(nbat * G <= 65535, FGT_ERANGE, "GEMM batch too large");
+      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, v1.get(), n_f, (int64_t)n_f * n_f, v2.get(), n_f, (int64_t)G * n_f, G, n_f, n_f, (int)(nbat * G)), st);
+      // grid[(g1 g2)][g3] = Re sum_m3 V2[(g1 g2)][m3] EeT[m3][g3]
+      bgemm<true, true, true>(gemm(v2.get(), n_f, plane * n_f, N.EeT.get(), G, 0, grid.get(), G, GD, (int)plane, G, n_f, (int)nbat), st);
+    }
+    InterpArgs ia;
+    ia.tgt = T.tgt_sorted.get();
+    ia.center = T.center.get();
+    ia.psi_ids = T.psi_ids.get();
+    ia.list = li.get();
+    ia.tgt_start = T.tgt_start.get();
+    ia.tgt_count = T.tgt_count.get();
+    ia.grid = grid.get();
+    ia.u = u_sorted;
+    ia.sc = P.sc;
+    ia.inv_delta = 1.0 / N.Delta;
+    ia.beta = N.beta;
+    ia.w = N.w;
+    ia.gmin = N.gmin;
+    ia.G = G;
+    interp_kernel<D><<<(unsigned)nbat, 256, 0, st>>>(ia);
+    FGT_LAUNCHED();
+  }
+}
+}  // namespace
+
+void nufft_form(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots) {
+  if (T.d == 1) nufft_form_impl<1>(N, P, T, slots);
+  else if (T.d == 2) nufft_form_impl<2>(N, P, T, slots);
+  else nufft_form_impl<3>(N, P, T, slots);
+}
+
+void nufft_eval(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& idx,
+                double* u_sorted) {
+  if (T.d == 1) nufft_eval_impl<1>(N, P, T, idx, u_sorted);
+  else if (T.d == 2) nufft_eval_impl<2>(N, P, T, idx, u_sorted);
+  else nufft_eval_impl<3>(N, P, T, idx, u_sorted);
+}
+
+}  // namespace fgt

@@ -1,0 +1,30 @@
+// Box-local NUFFT path for forming / evaluating plane-wave expansions of heavy boxes.
+#pragma once
+#include "k_pw.cuh"
+
+namespace fgt {
+
+// Exponential-of-semicircle spreading kernel psi(t) = exp(beta (sqrt(1 - (2t/w)^2) - 1)),
+// |t| <= w/2 grid cells, on a NON-periodic grid g*Delta, g in [gmin, gmin+G), that
+// covers the scaled coordinates of one cutoff box (|x_k| <= X) plus the kernel support.
+// Delta = 2 pi / (sigma n_f), sigma = 2.  Then, for |m| <= n_f/2,
+//   exp(-i m x) ~= (1/fh(m)) sum_g psi(g - x/Delta) exp(-i m g Delta),
+//   fh(m) = int psi(s) cos(m Delta s) ds           (Gauss-Legendre on the host)
+// with aliasing error ~ tol (no FFT, no wrap: the grid is only 2X/Delta + w wide).
+struct NufftPlan {
+  int n_f = 0, w = 0, gmin = 0, G = 0;
+  double beta = 0, Delta = 0, X = 0, tol = 0;
+  std::vector<double> fh;   // (n_f)
+  DBuf<double> Ef, EfT;     // form: (n_f, G) and (G, n_f) complex  w1d[m]/fh[m] e^{-i m g Delta}
+  DBuf<double> Ee, EeT;     // eval: (G, n_f) and (n_f, G) complex        e^{+i m g Delta}/fh[m]
+};
+
+void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
+
+// phi[slot] for the listed P-box slots, by spreading + separable DFT (DMMA GEMMs).
+void nufft_form(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots);
+// u_sorted += Re(psi_i evaluated at the targets of psi box i) for the listed psi indices.
+void nufft_eval(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& psi_idx,
+                double* u_sorted);
+
+}  // namespace fgt

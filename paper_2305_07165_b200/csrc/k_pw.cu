@@ -14,9 +14,42 @@
 // with r the flattened leading d-1 mode indices (C order, axis 0 slowest, ModeGrid
 // layout nufft.py:20-48) and c the last-axis mode.  Per-point 1-D phase tables are
 // built in shared memory (sincos per 8-mode segment + rotation recurrence).
-#include "k_pw.cuh"
+#include <cstdlib>
+#include <cstring>
+
+#include "k_nufft.cuh"
 
 namespace fgt {
+
+int nufft_mode() {
+  const char* e = std::getenv("FGT_NUFFT_MODE");
+  if (!e) return 0;
+  if (!std::strcmp(e, "direct")) return 1;
+  if (!std::strcmp(e, "spread")) return 2;
+  return 0;
+}
+
+namespace {
+// complex-MAC equivalents of the separable grid <-> mode transform of one box
+double box_dft_cost(int D, int G, int n_f) {
+  const double g = G, n = n_f;
+  if (D == 1) return n * g;
+  if (D == 2) return 0.5 * g * g * n + n * n * g;
+  return 0.5 * g * g * g * n + g * g * n * n + n * n * n * g;
+}
+// true if the box-local NUFFT beats the exact sums for a box with npts points
+bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double tap_cost) {
+  if (!N) return false;
+  const int mode = nufft_mode();
+  if (mode == 1) return false;
+  if (mode == 2) return npts > 0;
+  double taps = 1;
+  for (int k = 0; k < D; ++k) taps *= N->w;
+  const double direct = (double)npts * NF;
+  const double spread = tap_cost * npts * taps + box_dft_cost(D, N->G, N->n_f) + 32.0 * NF;
+  return direct > spread;
+}
+}  // namespace
 
 namespace {
 
@@ -324,6 +357,7 @@ struct EvalArgs {
   const int64_t* psi_ids;
   const int64_t* tgt_start;
   const int64_t* tgt_count;
+  const int64_t* list;    // blockIdx.x -> psi index
   const double2* psi;
   double* u;
   int n_f, R, ksteps;
@@ -339,7 +373,7 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   constexpr int TB = EVAL_TB, MT = EVAL_MT, NFP = NT * 8, RS = NFP + 4;
   double2* etab = sm;
   double* s_u = reinterpret_cast<double*>(etab + D * TB * RS);
-  const int64_t i = blockIdx.x;
+  const int64_t i = a.list[blockIdx.x];
   const int64_t T = a.psi_ids[i];
   const int64_t t0 = a.tgt_start[T];
   const int ntg = (int)a.tgt_count[T];
@@ -533,7 +567,7 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
 }
 
 template <int D>
-static void pw_form_impl(PwDev& P, TreeDev& T) {
+static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   cudaStream_t st = T.st;
   const int64_t nd = T.n_dense;
   P.phi.alloc((size_t)nd * P.NF * 2, st);
@@ -548,11 +582,16 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   FGT_CUDA(cudaStreamSynchronize(st));
   const int KU = 2048;
   std::vector<int4> units, reds;
+  std::vector<int64_t> spread_slots;
   int nscratch = 0;
   for (int64_t s = 0; s < nd; ++s) {
     int64_t n = cnt[s];
     if (n == 0) continue;
     if (!T.dense_need.empty() && !T.dense_need[s]) continue;
+    if (prefer_nufft(N, D, P.NF, n, 3.0)) {
+      spread_slots.push_back(s);
+      continue;
+    }
     int nu = (int)((n + KU - 1) / KU);
     if (nu == 1) {
       units.push_back(make_int4((int)s, 0, (int)n, -1));
@@ -566,7 +605,13 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   }
   P.n_src_dense = 0;
   for (int64_t s = 0; s < nd; ++s) P.n_src_dense += cnt[s];
-  if (units.empty()) return;
+  P.n_spread_boxes = (int64_t)spread_slots.size();
+  P.k_form.begin(st);
+  if (!spread_slots.empty()) nufft_form(*N, P, T, spread_slots);
+  if (units.empty()) {
+    P.k_form.end(st);
+    return;
+  }
   DBuf<int4> units_d(units.size(), st);
   units_d.from_host(units.data(), units.size());
   DBuf<double> scratch((size_t)nscratch * P.NF * 2, st);
@@ -597,7 +642,6 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   const size_t red_bytes = (size_t)MG * 32 * FORM_MT * NT * 4 * sizeof(double);
   const size_t smem = std::max(etab_bytes, red_bytes);
   const int nunits = (int)units.size();
-  P.k_form.begin(st);
   switch (NT) {
 #define FGT_FORM_CASE(NTV) case NTV: launch_form<D, NTV>(P, T, fa, nrowblk, nunits, smem, st); break;
     FGT_FORM_CASE(1) FGT_FORM_CASE(2) FGT_FORM_CASE(3) FGT_FORM_CASE(4)
@@ -616,10 +660,10 @@ static void pw_form_impl(PwDev& P, TreeDev& T) {
   }
 }
 
-void pw_form(PwDev& P, TreeDev& T) {
-  if (T.d == 1) pw_form_impl<1>(P, T);
-  else if (T.d == 2) pw_form_impl<2>(P, T);
-  else pw_form_impl<3>(P, T);
+void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N) {
+  if (T.d == 1) pw_form_impl<1>(P, T, N);
+  else if (T.d == 2) pw_form_impl<2>(P, T, N);
+  else pw_form_impl<3>(P, T, N);
 }
 
 void pw_gather(PwDev& P, TreeDev& T) {
@@ -648,9 +692,10 @@ void pw_gather(PwDev& P, TreeDev& T) {
   P.k_gather.end(st);
 }
 
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N) {
   if (T.n_psi == 0) return;
   cudaStream_t st = T.st;
+  std::vector<int64_t> direct_list, spread_list;
   {
     DBuf<int64_t> c(T.n_psi, st);
     gather_counts_kernel<<<grid_for(T.n_psi, 256), 256, 0, st>>>(T.psi_ids.get(), T.n_psi, T.tgt_count.get(), c.get());
@@ -659,14 +704,29 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
     c.to_host(h.data(), T.n_psi);
     FGT_CUDA(cudaStreamSynchronize(st));
     P.n_tgt_psi = 0;
-    for (int64_t v : h) P.n_tgt_psi += v;
+    for (int64_t i = 0; i < T.n_psi; ++i) {
+      P.n_tgt_psi += h[i];
+      if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) spread_list.push_back(i);
+      else direct_list.push_back(i);
+    }
   }
+  P.n_spread_psi = (int64_t)spread_list.size();
+  P.k_eval.begin(st);
+  if (!spread_list.empty()) nufft_eval(*N, P, T, spread_list, u_sorted);
+  if (direct_list.empty()) {
+    P.k_eval.end(st);
+    return;
+  }
+  DBuf<int64_t> list_d(direct_list.size(), st);
+  list_d.from_host(direct_list.data(), direct_list.size());
+  const int64_t n_direct = (int64_t)direct_list.size();
   EvalArgs ea;
   ea.tgt = T.tgt_sorted.get();
   ea.center = T.center.get();
   ea.psi_ids = T.psi_ids.get();
   ea.tgt_start = T.tgt_start.get();
   ea.tgt_count = T.tgt_count.get();
+  ea.list = list_d.get();
   ea.psi = reinterpret_cast<const double2*>(P.psi.get());
   ea.u = u_sorted;
   ea.n_f = P.n_f;
@@ -676,17 +736,16 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted) {
   const int NT = (P.n_f + 7) / 8;
 #define FGT_EVAL_D(DD)                                              \
   switch (NT) {                                                     \
-    case 1: launch_eval<DD, 1>(ea, T.n_psi, st); break;             \
-    case 2: launch_eval<DD, 2>(ea, T.n_psi, st); break;             \
-    case 3: launch_eval<DD, 3>(ea, T.n_psi, st); break;             \
-    case 4: launch_eval<DD, 4>(ea, T.n_psi, st); break;             \
-    case 5: launch_eval<DD, 5>(ea, T.n_psi, st); break;             \
-    case 6: launch_eval<DD, 6>(ea, T.n_psi, st); break;             \
-    case 7: launch_eval<DD, 7>(ea, T.n_psi, st); break;             \
-    case 8: launch_eval<DD, 8>(ea, T.n_psi, st); break;             \
+    case 1: launch_eval<DD, 1>(ea, n_direct, st); break;            \
+    case 2: launch_eval<DD, 2>(ea, n_direct, st); break;            \
+    case 3: launch_eval<DD, 3>(ea, n_direct, st); break;            \
+    case 4: launch_eval<DD, 4>(ea, n_direct, st); break;            \
+    case 5: launch_eval<DD, 5>(ea, n_direct, st); break;            \
+    case 6: launch_eval<DD, 6>(ea, n_direct, st); break;            \
+    case 7: launch_eval<DD, 7>(ea, n_direct, st); break;            \
+    case 8: launch_eval<DD, 8>(ea, n_direct, st); break;            \
     default: throw Error(FGT_ERANGE, "n_f too large");              \
   }
-  P.k_eval.begin(st);
   if (T.d == 1) { FGT_EVAL_D(1) }
   else if (T.d == 2) { FGT_EVAL_D(2) }
   else { FGT_EVAL_D(3) }

@@ -15,16 +15,22 @@ struct PwDev {
   DBuf<double> phi;    // (n_dense, R, n_f) complex outgoing expansions
   DBuf<double> psi;    // (n_psi, R, n_f) complex incoming expansions
   KClock k_form, k_gather, k_eval, k_direct;
-  int64_t n_src_dense = 0, n_tgt_psi = 0;
+  int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
 };
+
+struct NufftPlan;
+
+// Per-box path selection between the exact tensor-factored sums (DMMA) and the box-local
+// NUFFT (spread + separable DFT): FGT_NUFFT_MODE=direct|spread forces one (tests).
+int nufft_mode();
 
 void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
 // Form outgoing expansions of all P-boxes: type-1 exponential sums.
-void pw_form(PwDev& P, TreeDev& T);
+void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N);
 // Diagonal translation phi -> psi over the P-lists.
 void pw_gather(PwDev& P, TreeDev& T);
 // Type-2 evaluation of psi at the targets of every psi box; u_sorted += Re(...).
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted);
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 

@@ -181,9 +181,14 @@ PIPE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["auto", "spread", "direct"])
 @pytest.mark.parametrize("case", PIPE_CASES, ids=[c[0] for c in PIPE_CASES])
-def test_fgt_points_vs_oracle(cuda, case):
+def test_fgt_points_vs_oracle(cuda, case, mode, monkeypatch):
+    """Both plane-wave paths (exact sums on DMMA / box-local ES-kernel NUFFT) and the
+    automatic per-box choice meet the 10 eps bar against the oracle."""
     from paper_2305_07165_b200 import fgt_points
+    if mode != "auto":
+        monkeypatch.setenv("FGT_NUFFT_MODE", mode)
     name, d, n, delta, eps, n_s, boundary, dist, same = case
     r = np.random.default_rng(11)
     y = make_points(r, dist, n, d)
@@ -247,3 +252,19 @@ def test_single_point_and_flat_kernel(cuda):
     q = r.uniform(-1, 1, 2000)
     u = fgt_points(y, q, y, 1e6, 1e-9, 50)  # kernel ~ 1 everywhere
     assert rel(u, np.full(2000, q.sum())) < 1e-6
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_shares_sum_to_full(cuda, size):
+    """Multi-GPU shares run one after another on one GPU: disjoint, and their sum is
+    bitwise the full transform (each target is owned by exactly one share)."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(8)
+    y = clustered(r, 20000, 3)
+    x = r.uniform(-0.5, 0.5, (20000, 3))
+    q = r.standard_normal(20000)
+    full = fgt_points(y, q, x, 1e-4, 1e-9, 100)
+    parts = [fgt_points(y, q, x, 1e-4, 1e-9, 100, share=(k, size)) for k in range(size)]
+    nz = sum((p != 0).astype(int) for p in parts)
+    assert nz.max() <= 1
+    assert np.array_equal(sum(parts), full)
