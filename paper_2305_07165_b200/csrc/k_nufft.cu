@@ -15,11 +15,42 @@
 // Partial grids of K-split boxes are summed in a fixed order (deterministic).
 #include <cmath>
 
+#include <cub/cub.cuh>
+
 #include "k_nufft.cuh"
 
 namespace fgt {
 
 namespace {
+
+struct CubTmpBuf {
+  DBuf<uint8_t> buf;
+  void* get(size_t bytes, cudaStream_t st) {
+    if (bytes > buf.size()) buf.alloc(bytes + 256, st);
+    return buf.get();
+  }
+};
+
+__global__ void iota_i64_kernel(int64_t* a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = i;
+}
+
+void iota_i64(int64_t* a, int64_t n, cudaStream_t st) {
+  if (n == 0) return;
+  iota_i64_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, n);
+  FGT_LAUNCHED();
+}
+
+void sort_pairs_u32(CubTmpBuf& tmp, const uint32_t* kin, uint32_t* kout, const int64_t* vin,
+                    int64_t* vout, int64_t n, int bits, cudaStream_t st) {
+  if (n == 0) return;
+  size_t bytes = 0;
+  FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, bits, st));
+  FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes, st), bytes, kin, kout, vin, vout, (int)n, 0, bits, st));
+  count_launch();
+}
 
 __device__ __forceinline__ void dmma2(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -161,97 +192,172 @@ GemmArgs gemm(const double* A, int64_t lda, int64_t sA, const double* B, int64_t
 }
 
 // ------------------------------------------------------------------ spreading
-struct SpreadArgs {
+// Pass 1 (one thread per point and axis): kernel weights of every source of the batch,
+// computed once: first tap a_k (0-based grid index) and w weights per axis, plus the
+// sort key (box, a_0).  Pass 2: points sorted by (box, a_0), so the points touching
+// grid plane p of a box (a_0 in [p-w+1, p]) form one contiguous range.  Pass 3: one warp
+// per (box, plane, point chunk) accumulates the plane in its own shared-memory buffer
+// (plain read-modify-write: lanes of one instruction hit distinct cells, no other warp
+// touches the buffer), then writes it out once.
+struct WeightArgs {
   const double* src;
   const double* q;
   const double* center;
   const int64_t* dense_ids;
   const int64_t* src_start;
-  const int64_t* slots;  // list index -> dense slot
-  const int4* units;     // (list index, k0, kn, scratch index or -1)
-  double* grid;          // (list, G^D)
-  double* scratch;       // (nscratch, G^D)
+  const int64_t* slots;  // batch box -> dense slot
+  const int64_t* boff;   // (nbat+1) point offsets of the batch boxes
+  int64_t npts, nbat;
+  double* wts;           // (npts, D, MAXW)
+  int* ai;               // (npts, D)
+  double* qb;            // (npts)
+  uint32_t* key;         // (npts)
   double sc, inv_delta, beta;
-  int w, gmin, G, SP;
+  int w, gmin, G;
 };
 
-constexpr int SPREAD_PC = 64;
-
 template <int D>
-__global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a) {
-  extern __shared__ double sm[];
-  const int G = a.G, w = a.w;
-  const int64_t plane = D == 3 ? (int64_t)G * G : (D == 2 ? G : 1);
-  const int gs0 = blockIdx.y * a.SP;
-  const int np = min(a.SP, G - gs0);
-  double* sl = sm;
-  double* s_w = sl + (size_t)a.SP * plane;
-  double* s_q = s_w + SPREAD_PC * D * MAXW;
-  int* s_a = reinterpret_cast<int*>(s_q + SPREAD_PC);
-  for (int64_t e = threadIdx.x; e < np * plane; e += blockDim.x) sl[e] = 0.0;
-  const int4 u = a.units[blockIdx.x];
-  const int64_t box = a.dense_ids[a.slots[u.x]];
-  const int64_t base = a.src_start[box] + u.y;
-  double ctr[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) ctr[k] = a.center[box * D + k];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double s = a.sc * a.inv_delta, half = 0.5 * w, inv_half = 2.0 / w;
-  for (int c0 = 0; c0 < u.z; c0 += SPREAD_PC) {
-    const int cnt = min(SPREAD_PC, u.z - c0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt * D; t += blockDim.x) {
-      const int j = t / D, k = t % D;
-      const double tt = (a.src[(base + c0 + j) * D + k] - ctr[k]) * s;
-      const double a0 = ceil(tt - half);
-      int ai = (int)a0 - a.gmin;
-      ai = max(0, min(ai, G - w));  // never taken for in-box points (grid has margin)
-      s_a[j * D + k] = ai;
-      double* wp = s_w + (j * D + k) * MAXW;
-      for (int o = 0; o < w; ++o) wp[o] = es_kernel((a0 + o - tt) * inv_half, a.beta);
+__global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
+  const double s = a.sc * a.inv_delta, half = 0.5 * a.w, inv_half = 2.0 / a.w;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.npts * D;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / D;
+    const int k = (int)(t - i * D);
+    // batch box of point i
+    int64_t lo = 0, hi = a.nbat;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (a.boff[mid] <= i) lo = mid; else hi = mid;
     }
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) s_q[t] = a.q[base + c0 + t];
-    __syncthreads();
-    for (int j = 0; j < cnt; ++j) {
-      const int a0 = s_a[j * D];
-      const int plo = max(a0, gs0), phi = min(a0 + w, gs0 + np);
-      if (plo >= phi) continue;
-      int p = plo + ((warp - plo % 8) + 8) % 8;  // first plane this warp owns
-      for (; p < phi; p += 8) {
-        const double c = s_q[j] * s_w[(j * D) * MAXW + (p - a0)];
-        double* pl = sl + (int64_t)(p - gs0) * plane;
-        if (D == 3) {
-          const int a1 = s_a[j * D + 1], a2 = s_a[j * D + 2];
-          const double* w1 = s_w + (j * D + 1) * MAXW;
-          const double* w2 = s_w + (j * D + 2) * MAXW;
-          for (int idx = lane; idx < w * w; idx += 32) {
-            const int o1 = idx / w, o2 = idx - o1 * w;
-            pl[(a1 + o1) * G + a2 + o2] += c * w1[o1] * w2[o2];
-          }
-        } else if (D == 2) {
-          const int a1 = s_a[j * D + 1];
-          const double* w1 = s_w + (j * D + 1) * MAXW;
-          for (int o1 = lane; o1 < w; o1 += 32) pl[a1 + o1] += c * w1[o1];
-        } else if (lane == 0) {
-          pl[0] += c;
-        }
-      }
+    const int64_t box = a.dense_ids[a.slots[lo]];
+    const int64_t sidx = a.src_start[box] + (i - a.boff[lo]);
+    const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
+    const double a0 = ceil(tt - half);
+    const int aa = max(0, min((int)a0 - a.gmin, a.G - a.w));
+    a.ai[i * D + k] = aa;
+    double* wp = a.wts + (i * D + k) * MAXW;
+#pragma unroll
+    for (int o = 0; o < MAXW; ++o) wp[o] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
+    if (k == 0) {
+      a.qb[i] = a.q[sidx];
+      a.key[i] = ((uint32_t)lo << 8) | (uint32_t)aa;
     }
   }
-  __syncthreads();
-  const int64_t GD = plane * G;
-  double* out = (u.w < 0 ? a.grid + (int64_t)u.x * GD : a.scratch + (int64_t)u.w * GD) + gs0 * plane;
-  for (int64_t e = threadIdx.x; e < np * plane; e += blockDim.x) out[e] = sl[e];
 }
 
-__global__ void grid_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red,
-                                   int64_t GD, double* __restrict__ grid) {
-  const int4 r = red[blockIdx.y];  // (list index, first scratch, count, -)
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < GD;
-       e += (int64_t)gridDim.x * blockDim.x) {
+// (box, plane) -> [lo, hi) of the sorted points whose first plane is in [p-w+1, p]
+__global__ void plane_ranges_kernel(const uint32_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
+                                    int w, int* __restrict__ range) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nbat * G;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)(t / G), p = (uint32_t)(t % G);
+    const uint32_t k0 = (b << 8) | (uint32_t)max(0, (int)p - w + 1), k1 = ((b << 8) | p) + 1;
+    range[2 * t] = (int)lower_bound_dev(key, npts, k0);
+    range[2 * t + 1] = (int)lower_bound_dev(key, npts, k1);
+  }
+}
+
+struct PlaneArgs {
+  const int4* jobs;       // (box*G + plane, first sorted point, count, scratch index or -1)
+  int njobs;
+  const int64_t* perm;    // sorted position -> batch point
+  const double* wts;
+  const int* ai;
+  const double* qb;
+  double* grid;           // (nbat, G^D)
+  double* scratch;        // (nscratch, G^(D-1))
+  int w, G;
+};
+
+template <int D, int NIT>
+__global__ void __launch_bounds__(128) spread_plane_kernel(PlaneArgs a) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * 4 + warp;
+  if (job >= a.njobs) return;  // warp-uniform; no block barriers below
+  const int G = a.G, w = a.w;
+  const int plane = D == 3 ? G * G : (D == 2 ? G : 1);
+  double* pl = sm + (size_t)warp * plane;
+  for (int e = lane; e < plane; e += 32) pl[e] = 0.0;
+  __syncwarp();
+  const int4 jb = a.jobs[job];
+  const int p = jb.x % G;
+  // this lane's taps: (o1, o2) = divmod(lane + 32 it, w), it < NIT (w^2 <= 32 NIT)
+  int o1s[NIT], o2s[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int idx = lane + 32 * it;
+    const bool ok = D == 3 ? idx < w * w : (D == 2 ? lane < w : lane == 0);
+    o1s[it] = ok ? (D == 3 ? idx / w : idx) : -1;
+    o2s[it] = ok && D == 3 ? idx % w : 0;
+  }
+  const int jend = jb.y + jb.z;
+  for (int base = jb.y; base < jend; base += 32) {
+    const int cnt = min(32, jend - base);
+    // lane-parallel fetch of the per-point scalars of 32 points
+    int64_t il = 0;
+    double cl = 0.0;
+    int a1l = 0, a2l = 0;
+    if (lane < cnt) {
+      il = a.perm[base + lane];
+      const int a0 = a.ai[il * D];
+      cl = a.qb[il] * a.wts[(il * D) * MAXW + (p - a0)];
+      if (D >= 2) a1l = a.ai[il * D + 1];
+      if (D == 3) a2l = a.ai[il * D + 2];
+    }
+    if (D == 1) {
+      double sum = cl;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) pl[0] += sum;
+      continue;
+    }
+    auto wload = [&](int jj) {
+      const int64_t i = __shfl_sync(0xffffffffu, il, jj);
+      return (D == 3 && lane >= 16) ? a.wts[(i * D + 2) * MAXW + (lane - 16)]
+                                    : a.wts[(i * D + 1) * MAXW + (lane & 15)];
+    };
+    double wnext = wload(0);
+    for (int jj = 0; jj < cnt; ++jj) {
+      const double wv = wnext;
+      if (jj + 1 < cnt) wnext = wload(jj + 1);  // prefetch the next point's weights
+      const double c = __shfl_sync(0xffffffffu, cl, jj);
+      const int a1 = __shfl_sync(0xffffffffu, a1l, jj);
+      const int a2 = __shfl_sync(0xffffffffu, a2l, jj);
+      double val[NIT], cur[NIT];
+      int off[NIT];
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) {
+        const int o1 = max(o1s[it], 0);
+        const double w1 = __shfl_sync(0xffffffffu, wv, o1);
+        const double w2 = D == 3 ? __shfl_sync(0xffffffffu, wv, 16 + o2s[it]) : 1.0;
+        val[it] = c * w1 * w2;
+        off[it] = D == 3 ? (a1 + o1) * G + a2 + o2s[it] : a1 + o1;
+      }
+#pragma unroll
+      for (int it = 0; it < NIT; ++it) cur[it] = o1s[it] >= 0 ? pl[off[it]] : 0.0;
+#pragma unroll
+      for (int it = 0; it < NIT; ++it)
+        if (o1s[it] >= 0) pl[off[it]] = cur[it] + val[it];
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  const int64_t GD = (int64_t)plane * G;
+  const int b = jb.x / G;
+  double* out = jb.w < 0 ? a.grid + (int64_t)b * GD + (int64_t)p * plane : a.scratch + (int64_t)jb.w * plane;
+  for (int e = lane; e < plane; e += 32) out[e] = pl[e];
+}
+
+__global__ void plane_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red,
+                                    int plane, int G, double* __restrict__ grid) {
+  const int4 r = red[blockIdx.y];  // (box*G + plane, first scratch, count, -)
+  const int64_t GD = (int64_t)plane * G;
+  double* out = grid + (int64_t)(r.x / G) * GD + (int64_t)(r.x % G) * plane;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < plane; e += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int t = 0; t < r.z; ++t) s += scratch[(int64_t)(r.y + t) * GD + e];
-    grid[(int64_t)r.x * GD + e] = s;
+    for (int t = 0; t < r.z; ++t) s += scratch[(int64_t)(r.y + t) * plane + e];
+    out[e] = s;
   }
 }
 
@@ -434,65 +540,117 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   T.dense_ids.to_host(dense.data(), T.n_dense);
   T.src_count.to_host(scount.data(), T.nb);
   FGT_CUDA(cudaStreamSynchronize(st));
-  // shared-memory slab: as many axis-0 planes as fit beside the point staging area
-  const size_t stage = (size_t)SPREAD_PC * (D * MAXW + 1) * sizeof(double) + SPREAD_PC * D * sizeof(int);
-  const size_t budget = 227 * 1024 - stage - 1024;
-  int SP = (int)std::min<int64_t>(G, (int64_t)(budget / (plane * sizeof(double))));
-  FGT_REQUIRE(SP >= 1, FGT_ERANGE, "spreading grid plane does not fit in shared memory");
-  const int nslab = (G + SP - 1) / SP;
-  SP = (G + nslab - 1) / nslab;
-  const size_t smem = (size_t)SP * plane * sizeof(double) + stage;
-  FGT_CUDA(cudaFuncSetAttribute(spread_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // batches bounded by ~1.5 GB of grid + stage buffers
+  const size_t psmem = 4 * (size_t)plane * sizeof(double);
+  FGT_REQUIRE(psmem <= 227 * 1024, FGT_ERANGE, "spreading plane does not fit in shared memory");
+  FGT_REQUIRE(G < 256, FGT_ERANGE, "spreading grid too large");
+  const int nit = D == 3 ? (w * w + 31) / 32 : 1;
+  FGT_REQUIRE(nit <= 8, FGT_ERANGE, "spreading width too large");
+  auto plane_kernel = [&](int k) -> void (*)(PlaneArgs) {
+    switch (k) {
+      case 1: return spread_plane_kernel<D, 1>;
+      case 2: return spread_plane_kernel<D, 2>;
+      case 3: return spread_plane_kernel<D, 3>;
+      case 4: return spread_plane_kernel<D, 4>;
+      case 5: return spread_plane_kernel<D, 5>;
+      case 6: return spread_plane_kernel<D, 6>;
+      case 7: return spread_plane_kernel<D, 7>;
+      default: return spread_plane_kernel<D, 8>;
+    }
+  };
+  void (*pk)(PlaneArgs) = plane_kernel(nit);
+  FGT_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  // batches bounded by ~1.5 GB of grid + stage buffers + per-point weights
   const int64_t per_box = GD * 8 + (D >= 2 ? plane * n_f * 16 : 0) + (D == 3 ? (int64_t)G * n_f * n_f * 16 : 0);
-  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)1536 * 1024 * 1024 / per_box));
-  const int KU = 4096;
-  for (size_t b0 = 0; b0 < slots.size(); b0 += nb_max) {
-    const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)slots.size() - b0);
-    std::vector<int4> units, reds;
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
+  const int CH = 1024;  // points per plane job
+  CubTmpBuf tmp;
+  size_t b0 = 0;
+  while (b0 < slots.size()) {
+    // grow the batch up to nb_max boxes and ~4M points
+    int64_t nbat = 0, npts = 0;
+    std::vector<int64_t> boff(1, 0);
+    while (b0 + nbat < slots.size() && nbat < nb_max) {
+      const int64_t n = scount[dense[slots[b0 + nbat]]];
+      if (nbat > 0 && npts + n > (int64_t)4 << 20) break;
+      npts += n;
+      boff.push_back(npts);
+      ++nbat;
+    }
+    DBuf<int64_t> sl_d(nbat, st), boff_d(nbat + 1, st);
+    sl_d.from_host(slots.data() + b0, nbat);
+    boff_d.from_host(boff.data(), nbat + 1);
+    DBuf<double> wts(npts * D * MAXW, st), qb(npts, st);
+    DBuf<int> ai(npts * D, st);
+    DBuf<uint32_t> key(npts, st), skey(npts, st);
+    DBuf<int64_t> iota(npts, st), perm(npts, st);
+    WeightArgs wa;
+    wa.src = T.src_sorted.get();
+    wa.q = T.q_sorted.get();
+    wa.center = T.center.get();
+    wa.dense_ids = T.dense_ids.get();
+    wa.src_start = T.src_start.get();
+    wa.slots = sl_d.get();
+    wa.boff = boff_d.get();
+    wa.npts = npts;
+    wa.nbat = nbat;
+    wa.wts = wts.get();
+    wa.ai = ai.get();
+    wa.qb = qb.get();
+    wa.key = key.get();
+    wa.sc = P.sc;
+    wa.inv_delta = 1.0 / N.Delta;
+    wa.beta = N.beta;
+    wa.w = w;
+    wa.gmin = N.gmin;
+    wa.G = G;
+    spread_weights_kernel<D><<<grid_for(npts * D, 256), 256, 0, st>>>(wa);
+    FGT_LAUNCHED();
+    iota_i64(iota.get(), npts, st);
+    int bits = 8;
+    while (((int64_t)1 << (bits - 8)) < nbat) ++bits;
+    sort_pairs_u32(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
+    DBuf<int> range(2 * nbat * G, st);
+    plane_ranges_kernel<<<grid_for(nbat * G, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
+    FGT_LAUNCHED();
+    std::vector<int> hr(2 * nbat * G);
+    range.to_host(hr.data(), hr.size());
+    FGT_CUDA(cudaStreamSynchronize(st));
+    std::vector<int4> jobs, reds;
     int nscr = 0;
-    for (int64_t i = 0; i < nbat; ++i) {
-      const int64_t n = scount[dense[slots[b0 + i]]];
-      const int nu = (int)((n + KU - 1) / KU);
-      if (nu <= 1) {
-        units.push_back(make_int4((int)i, 0, (int)n, -1));
+    for (int64_t bp = 0; bp < nbat * G; ++bp) {
+      const int lo = hr[2 * bp], n = hr[2 * bp + 1] - lo;
+      if (n <= CH) {
+        jobs.push_back(make_int4((int)bp, lo, n, -1));
       } else {
-        reds.push_back(make_int4((int)i, nscr, nu, 0));
-        for (int t = 0; t < nu; ++t)
-          units.push_back(make_int4((int)i, t * KU, (int)std::min<int64_t>(KU, n - (int64_t)t * KU), nscr++));
+        const int nc = (n + CH - 1) / CH;
+        reds.push_back(make_int4((int)bp, nscr, nc, 0));
+        for (int c = 0; c < nc; ++c) jobs.push_back(make_int4((int)bp, lo + c * CH, std::min(CH, n - c * CH), nscr++));
       }
     }
-    DBuf<int64_t> sl_d(nbat, st);
-    sl_d.from_host(slots.data() + b0, nbat);
-    DBuf<int4> units_d(units.size(), st), reds_d(reds.size(), st);
-    units_d.from_host(units.data(), units.size());
+    DBuf<int4> jobs_d(jobs.size(), st), reds_d(reds.size(), st);
+    jobs_d.from_host(jobs.data(), jobs.size());
     if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
-    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * GD, st);
-    SpreadArgs sa;
-    sa.src = T.src_sorted.get();
-    sa.q = T.q_sorted.get();
-    sa.center = T.center.get();
-    sa.dense_ids = T.dense_ids.get();
-    sa.src_start = T.src_start.get();
-    sa.slots = sl_d.get();
-    sa.units = units_d.get();
-    sa.grid = grid.get();
-    sa.scratch = scratch.get();
-    sa.sc = P.sc;
-    sa.inv_delta = 1.0 / N.Delta;
-    sa.beta = N.beta;
-    sa.w = w;
-    sa.gmin = N.gmin;
-    sa.G = G;
-    sa.SP = SP;
-    spread_kernel<D><<<dim3((unsigned)units.size(), nslab), 256, smem, st>>>(sa);
+    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * plane, st);
+    PlaneArgs pa;
+    pa.jobs = jobs_d.get();
+    pa.njobs = (int)jobs.size();
+    pa.perm = perm.get();
+    pa.wts = wts.get();
+    pa.ai = ai.get();
+    pa.qb = qb.get();
+    pa.grid = grid.get();
+    pa.scratch = scratch.get();
+    pa.w = w;
+    pa.G = G;
+    pk<<<(unsigned)((jobs.size() + 3) / 4), 128, psmem, st>>>(pa);
     FGT_LAUNCHED();
     if (!reds.empty()) {
-      grid_reduce_kernel<<<dim3(grid_for(GD, 256, 64), (unsigned)reds.size()), 256, 0, st>>>(
-          scratch.get(), reds_d.get(), GD, grid.get());
+      plane_reduce_kernel<<<dim3(grid_for(plane, 256, 8), (unsigned)reds.size()), 256, 0, st>>>(
+          scratch.get(), reds_d.get(), (int)plane, G, grid.get());
       FGT_LAUNCHED();
     }
     scratch.release();
+    wts.release();
     // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
     double* phi = P.phi.get();
     const int64_t NF = P.NF;
@@ -514,6 +672,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       // phi[m1][(m2 m3)] = sum_g1 Ef[m1][g1] T2[g1][(m2 m3)]
       bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t2.get(), (int64_t)n_f * n_f, (int64_t)G * n_f * n_f, phi, (int64_t)n_f * n_f, NF, n_f, n_f * n_f, G, (int)nbat, sl_d.get()), st);
     }
+    b0 += nbat;
   }
 }
 
@@ -525,7 +684,7 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   const int G = N.G, n_f = N.n_f;
   const int64_t GD = ipow(G, D), plane = GD / G, NF = P.NF;
   const int64_t per_box = GD * 8 + (D >= 2 ? (int64_t)G * ipow(n_f, D - 1) * 16 : 0) + (D == 3 ? plane * n_f * 16 : 0);
-  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)1536 * 1024 * 1024 / per_box));
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
   for (size_t b0 = 0; b0 < idx.size(); b0 += nb_max) {
     const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)idx.size() - b0);
     DBuf<int64_t> li(nbat, st);
