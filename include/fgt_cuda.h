@@ -180,6 +180,9 @@ typedef struct fgt_phase_times {
   /* workload counters for algorithmic byte/flop accounting */
   int64_t n_boxes, n_dense, n_psi, n_src_dense, n_tgt_psi, n_p_entries, n_direct_pairs;
   int64_t n_modes; /* N_F = n_f^d */
+  /* box-local NUFFT path: boxes / points routed to it and its kernel width and grid */
+  int64_t n_spread_boxes, n_src_spread, n_spread_psi, n_tgt_spread;
+  int32_t nufft_w, nufft_G;
 } fgt_phase_times;
 
 /* Discrete FGT, DEVICE pointers: u (nt) is OVERWRITTEN with

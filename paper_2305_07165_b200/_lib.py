@@ -54,7 +54,9 @@ class FgtPhaseTimes(ctypes.Structure):
                    ("k_form_ms", "k_gather_ms", "k_eval_ms", "k_direct_ms")]
                 + [(n, ctypes.c_int64) for n in
                    ("n_boxes", "n_dense", "n_psi", "n_src_dense", "n_tgt_psi", "n_p_entries",
-                    "n_direct_pairs", "n_modes")])
+                    "n_direct_pairs", "n_modes", "n_spread_boxes", "n_src_spread",
+                    "n_spread_psi", "n_tgt_spread")]
+                + [("nufft_w", ctypes.c_int32), ("nufft_G", ctypes.c_int32)])
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -233,6 +233,12 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.n_p_entries = T.n_p;
   t.n_direct_pairs = T.n_direct_pairs;
   t.n_modes = P.NF;
+  t.n_spread_boxes = P.n_spread_boxes;
+  t.n_src_spread = P.n_src_spread;
+  t.n_spread_psi = P.n_spread_psi;
+  t.n_tgt_spread = P.n_tgt_spread;
+  t.nufft_w = NP.w;
+  t.nufft_G = NP.G;
   if (times) *times = t;
 }
 

@@ -590,6 +590,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
     if (!T.dense_need.empty() && !T.dense_need[s]) continue;
     if (prefer_nufft(N, D, P.NF, n, 3.0)) {
       spread_slots.push_back(s);
+      P.n_src_spread += n;
       continue;
     }
     int nu = (int)((n + KU - 1) / KU);
@@ -706,8 +707,12 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N) {
     P.n_tgt_psi = 0;
     for (int64_t i = 0; i < T.n_psi; ++i) {
       P.n_tgt_psi += h[i];
-      if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) spread_list.push_back(i);
-      else direct_list.push_back(i);
+      if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) {
+        spread_list.push_back(i);
+        P.n_tgt_spread += h[i];
+      } else {
+        direct_list.push_back(i);
+      }
     }
   }
   P.n_spread_psi = (int64_t)spread_list.size();

@@ -16,6 +16,7 @@ struct PwDev {
   DBuf<double> psi;    // (n_psi, R, n_f) complex incoming expansions
   KClock k_form, k_gather, k_eval, k_direct;
   int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
+  int64_t n_src_spread = 0, n_tgt_spread = 0;
 };
 
 struct NufftPlan;
