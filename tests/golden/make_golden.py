@@ -197,9 +197,41 @@ def alg2_cfg1():
     save("alg2_cfg1.npz", u=u, exact=exact)
 
 
+def sigma_f(d):
+    """Sum of two Gaussians (the density used by the volume fixtures)."""
+    C = np.array([[0.1, -0.05, 0.02][:d], [-0.2, 0.15, -0.1][:d]])
+    W, A = [0.05, 0.1], [1.0, 0.7]
+    return lambda p: sum(a * np.exp(-np.sum((p - c) ** 2, axis=-1) / w ** 2) for c, w, a in zip(C, W, A))
+
+
+def volume():
+    from fgt import poly1d as rpoly
+    out = {}
+    # Gaussian moments: recurrence window and quadrature window (poly1d.py:129-195)
+    t = np.linspace(-3, 3, 61)
+    for lam in (1 / 64, 1 / 32, 1 / 16, 1 / 8, 0.25, 0.64):
+        out[f"J_{lam:.6f}"] = rpoly.gauss_moment_J(lam, 15, t)
+    tI = np.linspace(-100, 100, 401)
+    out["I"] = rpoly.fourier_moment_I(23, tI)
+    b = rpoly.LegendreBasis.build(12)
+    out["nodes12"], out["v2p12"], out["p2v12"] = b.nodes, b.val_to_pol, b.pol_to_val
+    r = np.random.default_rng(3)
+    c = r.standard_normal((6, 6, 6))
+    out["tail_c"], out["tail"] = c, np.array(rpoly.tail_error(c))
+    save("poly1d.npz", **out)
+    for d, k, eps in ((2, 10, 1e-9), (3, 6, 1e-7)):
+        t, vals, _ = rt.build_density_tree(sigma_f(d), d, k, eps)
+        leaves = np.nonzero(t.is_leaf)[0]
+        V = np.stack([vals[b] for b in leaves]).reshape(len(leaves), -1)
+        save(f"dtree_{d}d.npz", level=t.level, parent=t.parent, children=t.children,
+             coords=t.coords, is_leaf=t.is_leaf, leaves=leaves,
+             vsum=V.sum(axis=1), vsq=(V * V).sum(axis=1))
+
+
 if __name__ == "__main__":
     params()
     kernels()
     nufft()
     trees()
     alg2_cfg1()
+    volume()

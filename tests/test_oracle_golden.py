@@ -117,3 +117,70 @@ def test_alg2_config1_vs_reference_primitives():
     assert rel(u, g["u"]) < 1e-12          # same algorithm on the reference primitives
     assert rel(u, g["exact"]) <= 10 * 1e-6  # SPEC.md:425 accuracy bar
     assert rel(g["u"], g["exact"]) <= 10 * 1e-6
+
+
+# ------------------------------------------------------------------ volume (Alg 3/4)
+def test_poly1d_vs_reference():
+    from oracle import volume as ov
+    g = load("poly1d.npz")
+    t = np.linspace(-3, 3, 61)
+    for lam in (1 / 64, 1 / 32, 1 / 16, 1 / 8, 0.25, 0.64):
+        ref = g[f"J_{lam:.6f}"]
+        got = ov.gauss_J(lam, 15, t)
+        # relative to the table scale lam*sqrt(pi) (poly1d.py:181)
+        assert np.max(np.abs(got - ref)) < 1e-11 * lam * np.sqrt(np.pi)
+    tI = np.linspace(-100, 100, 401)
+    assert np.max(np.abs(ov.fourier_I(23, tI) - g["I"])) < 1e-14
+    b = ov.Basis(12)
+    assert np.allclose(b.nodes, g["nodes12"], atol=1e-15, rtol=0)
+    assert np.allclose(b.v2p, g["v2p12"], atol=1e-14, rtol=0)
+    assert ov.tail_error(g["tail_c"]) == float(g["tail"])
+
+
+def sigma_f(d):
+    C = np.array([[0.1, -0.05, 0.02][:d], [-0.2, 0.15, -0.1][:d]])
+    W, A = [0.05, 0.1], [1.0, 0.7]
+    return (lambda p: sum(a * np.exp(-np.sum((p - c) ** 2, axis=-1) / w ** 2)
+                          for c, w, a in zip(C, W, A))), C, W, A
+
+
+@pytest.mark.parametrize("d,k,eps", [(2, 10, 1e-9), (3, 6, 1e-7)])
+def test_density_tree_vs_reference(d, k, eps):
+    from oracle import volume as ov
+    g = load(f"dtree_{d}d.npz")
+    t = ov.density_tree(sigma_f(d)[0], d, k, eps)
+    for f in ("level", "parent", "children", "coords", "is_leaf"):
+        assert np.array_equal(getattr(t, f), g[f]), f
+    V = np.stack([t.values[b] for b in g["leaves"]]).reshape(len(g["leaves"]), -1)
+    assert np.allclose(V.sum(axis=1), g["vsum"], rtol=1e-13, atol=1e-13)
+    assert np.allclose((V * V).sum(axis=1), g["vsq"], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("d,k,delta,eps", [(1, 12, 1e-3, 1e-9), (2, 10, 1e-3, 1e-8),
+                                           (3, 6, 1e-2, 1e-5)])
+def test_volume_oracle_closed_form(d, k, delta, eps):
+    """SPEC.md:651 acceptance 7(a): sum-of-Gaussians density, closed-form convolution."""
+    from oracle import volume as ov
+    dens, C, W, A = sigma_f(d)
+    t = ov.density_tree(dens, d, k, eps * 0.1)
+    u = ov.fgt_box(t, delta, eps)
+    num = den = 0.0
+    for b, ub in u.items():
+        ex = ov.gaussian_box_convolution(t.leaf_points(b), delta, C, W, A)
+        num += np.sum((ub - ex) ** 2)
+        den += np.sum(ex ** 2)
+    assert np.sqrt(num / den) <= 10 * eps
+
+
+def test_volume_oracle_constant_density():
+    """SPEC.md:259 / acceptance 7(c): sigma = 1 -> product of erf differences."""
+    from scipy.special import erf
+    from oracle import volume as ov
+    t = ov.density_tree(lambda p: np.ones(p.shape[:-1]), 2, 8, 1e-10)
+    delta, eps = 1e-2, 1e-9
+    u = ov.fgt_box(t, delta, eps)
+    for b, ub in u.items():
+        x = t.leaf_points(b)
+        ex = np.prod(np.sqrt(np.pi * delta) / 2 * (erf((0.5 - x) / np.sqrt(delta))
+                                                   + erf((0.5 + x) / np.sqrt(delta))), axis=-1)
+        assert np.max(np.abs(ub - ex)) <= 10 * eps * np.max(np.abs(ex))
