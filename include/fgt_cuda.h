@@ -197,6 +197,55 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
                int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, double* u,
                fgt_phase_times* times);
 
+/* ---------------------------------------------------------------------------
+ * Layer 3: continuous (box) FGT, Alg 4.
+ *
+ * The density tree (Alg 3, tree.py:577-644) needs the user's sigma callable, so it is
+ * built on the host; the host also builds the per-level 1-D tables (J/I moments,
+ * poly1d.py:129-210) and the schedules below.  Everything else runs on the GPU:
+ * leaf->PW and PW->grid as d separable FP64-DMMA GEMMs per level, the diagonal
+ * merge / gather / push shifts, and the direct near field as separable k x k
+ * contractions.  All index arrays are HOST int64 arrays; complex = interleaved.
+ * ------------------------------------------------------------------------- */
+typedef struct fgt_box_plan {
+  int32_t dim, k, n_f, n_levels, l_c;
+  int64_t n_leaves;     /* leaf grids (values / u are (n_leaves, k^d)) */
+  int64_t n_pw;         /* boxes with a plane-wave slot (f(B) = 1) */
+  /* per-level 1-D matrices, complex (n_levels, n_f, k) and (n_levels, k, n_f) */
+  const double* val2pw; /* (L/2) w_m conj(I[P_n](L m h / 2 sqrt(delta))) T_val->pol */
+  const double* pw2val; /* exp(+i m h L xi_n / 2 sqrt(delta)) */
+  /* phase rows, complex (n_rows, n_f); rows are referenced by the shift schedules */
+  int64_t n_rows;
+  const double* rows;
+  /* direct tables, real (n_tables, k, k): (L/2) J_lam[P_n](2 o + r xi_i) T_val->pol */
+  int64_t n_tables;
+  const double* dtab;
+  /* leaf -> PW: (leaf slot, pw slot, level) */
+  int64_t n_form;
+  const int64_t *form_leaf, *form_pw, *form_level;
+  /* diagonal shifts, executed as stages in order; stage s covers destinations
+   * [stage_off[s], stage_off[s+1]); kind 0 = merge (phi -> phi), 1 = gather
+   * (phi -> psi), 2 = push (psi -> psi).  Per destination: pw slot, accumulate (1) or
+   * overwrite (0), entries (src pw slot, d phase-row indices) summed in order. */
+  int64_t n_stages, n_dst, n_entries;
+  const int64_t *stage_off;  /* (n_stages+1) into dst list */
+  const int64_t *stage_kind; /* (n_stages) */
+  const int64_t *dst, *dst_acc, *dst_off; /* (n_dst), (n_dst), (n_dst+1) into entries */
+  const int64_t *ent_src, *ent_rows;      /* (n_entries), (n_entries, d) */
+  /* PW -> grid: (leaf slot, pw slot, level) */
+  int64_t n_eval;
+  const int64_t *eval_leaf, *eval_pw, *eval_level;
+  /* direct pairs sorted by target leaf: (target leaf, source leaf, d table ids) */
+  int64_t n_dpairs;
+  const int64_t *d_tgt, *d_src, *d_tab;
+} fgt_box_plan;
+
+/* u (n_leaves, k^d) = box FGT of values (n_leaves, k^d); DEVICE pointers. */
+int fgt_box_dev(const fgt_box_plan* plan, const double* values, double* u, void* stream,
+                fgt_phase_times* times);
+/* Same with HOST pointers (H2D / D2H inside). */
+int fgt_box(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times);
+
 /* Microbenchmarks used for the roofline denominators (FP64 pipes). */
 int fgt_bench_fp64_peak(int use_dmma, double* tflops);
 

@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "..", "build", "obj")
 LIB = os.path.join(HERE, "libfgtcuda.so")
 
-SOURCES = ["k_kernels.cu", "k_tree.cu", "k_pw.cu", "k_nufft.cu", "api.cu"]
+SOURCES = ["k_kernels.cu", "k_tree.cu", "k_pw.cu", "k_nufft.cu", "k_volume.cu", "api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -62,6 +62,28 @@ class FgtPhaseTimes(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+_PD = ctypes.POINTER(ctypes.c_double)
+
+
+class FgtBoxPlan(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("k", ctypes.c_int32), ("n_f", ctypes.c_int32),
+                ("n_levels", ctypes.c_int32), ("l_c", ctypes.c_int32),
+                ("n_leaves", ctypes.c_int64), ("n_pw", ctypes.c_int64),
+                ("val2pw", _PD), ("pw2val", _PD), ("n_rows", ctypes.c_int64), ("rows", _PD),
+                ("n_tables", ctypes.c_int64), ("dtab", _PD),
+                ("n_form", ctypes.c_int64), ("form_leaf", _PI64), ("form_pw", _PI64),
+                ("form_level", _PI64),
+                ("n_stages", ctypes.c_int64), ("n_dst", ctypes.c_int64),
+                ("n_entries", ctypes.c_int64), ("stage_off", _PI64), ("stage_kind", _PI64),
+                ("dst", _PI64), ("dst_acc", _PI64), ("dst_off", _PI64), ("ent_src", _PI64),
+                ("ent_rows", _PI64),
+                ("n_eval", ctypes.c_int64), ("eval_leaf", _PI64), ("eval_pw", _PI64),
+                ("eval_level", _PI64),
+                ("n_dpairs", ctypes.c_int64), ("d_tgt", _PI64), ("d_src", _PI64),
+                ("d_tab", _PI64)]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I64 = ctypes.c_int64
@@ -92,6 +114,8 @@ SIGNATURES = {
                         ctypes.POINTER(FgtPwParams), _P, ctypes.POINTER(FgtPhaseTimes)]),
     "fgt_bench_fp64_peak": (_I, [_I, ctypes.POINTER(_D)]),
     "fgt_partition_bounds": (_I, [_P, _I64, ctypes.c_int32, _P]),
+    "fgt_box_dev": (_I, [ctypes.POINTER(FgtBoxPlan), _P, _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_box": (_I, [ctypes.POINTER(FgtBoxPlan), _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
 }
 
 _lib = None

@@ -511,6 +511,44 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
   });
 }
 
+int fgt_box_dev(const fgt_box_plan* plan, const double* values, double* u, void* stream,
+                fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(plan, FGT_EINVAL, "null plan");
+    const int64_t l0 = g_launches;
+    fgt_phase_times t;
+    std::memset(&t, 0, sizeof(t));
+    box_fgt(*plan, values, u, (cudaStream_t)stream, &t);
+    t.launches = g_launches - l0;
+    if (times) *times = t;
+  });
+}
+
+int fgt_box(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(plan, FGT_EINVAL, "null plan");
+    int64_t kd = 1;
+    for (int i = 0; i < plan->dim; ++i) kd *= plan->k;
+    const int64_t n = plan->n_leaves * kd;
+    OwnedStream os;
+    Timer tm(os.s);
+    DBuf<double> dv(n, os.s), du(n, os.s);
+    dv.from_host(values, n);
+    const double h2d = tm.lap();
+    const int64_t l0 = g_launches;
+    fgt_phase_times t;
+    std::memset(&t, 0, sizeof(t));
+    box_fgt(*plan, dv.get(), du.get(), os.s, &t);
+    t.launches = g_launches - l0;
+    tm.lap();
+    du.to_host(u, n);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+    t.h2d_ms = h2d;
+    t.d2h_ms = tm.lap();
+    if (times) *times = t;
+  });
+}
+
 int fgt_partition_bounds(const double* cost, int64_t n, int32_t parts, int64_t* bounds) {
   return guarded([&] {
     FGT_REQUIRE(parts >= 1 && n >= 0 && (n == 0 || cost) && bounds, FGT_EINVAL, "bad arguments");

@@ -1,0 +1,157 @@
+// Batched small GEMMs on the FP64 tensor cores (mma.sync m8n8k4 .f64 -> SASS DMMA).
+// Shared by the NUFFT grid<->mode transforms and the volume FGT per-axis contractions
+// (the separable `_apply_per_axis` pattern of poly1d.py:76-81).
+#pragma once
+#include "fgt_common.cuh"
+
+namespace fgt {
+
+__device__ __forceinline__ void dmma2(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// C[b] = A[b] (M x K) * B[b] (K x N), row-major with leading dims, batch strides in
+// elements; complex operands are interleaved (re, im).  CRE: store Re(C) only.
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K;
+  int64_t batch;
+  int64_t lda, ldb, ldc, sA, sB, sC;
+  const int64_t* cidx;  // optional C batch index
+  const int64_t* bidx;  // optional B batch index
+  const int64_t* aidx;  // optional A batch index
+  int64_t boff;         // batch offset of this launch (grid.z limit)
+};
+
+template <bool AC, bool BC, bool CRE, bool ACC>
+__global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t b = blockIdx.z + g.boff;
+  const int m0 = blockIdx.y * 32 + wm * 16;
+  const int n0 = blockIdx.x * 48 + wn * 24;
+  const double* A = g.A + (g.aidx ? g.aidx[b] : b) * g.sA * (AC ? 2 : 1);
+  const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
+  const int64_t cb = g.cidx ? g.cidx[b] : b;
+  double* C = g.C + cb * g.sC * (CRE ? 1 : 2);
+  double acc[2][3][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+  for (int k0 = 0; k0 < g.K; k0 += 4) {
+    const int k = k0 + (lane & 3);
+    double ar[2], ai[2], br[3], bi[3];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = m0 + mt * 8 + (lane >> 2);
+      ar[mt] = ai[mt] = 0.0;
+      if (r < g.M && k < g.K) {
+        if (AC) {
+          double2 v = *reinterpret_cast<const double2*>(A + 2 * (r * g.lda + k));
+          ar[mt] = v.x;
+          ai[mt] = v.y;
+        } else {
+          ar[mt] = A[r * g.lda + k];
+        }
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int c = n0 + nt * 8 + (lane >> 2);
+      br[nt] = bi[nt] = 0.0;
+      if (c < g.N && k < g.K) {
+        if (BC) {
+          double2 v = *reinterpret_cast<const double2*>(B + 2 * (k * g.ldb + c));
+          br[nt] = v.x;
+          bi[nt] = v.y;
+        } else {
+          br[nt] = B[k * g.ldb + c];
+        }
+      }
+    }
+    // re += ar br - ai bi ; im += ar bi + ai br   (terms with a real operand vanish)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
+    if (AC && BC) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
+    }
+    if (!CRE) {
+      if (BC) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
+      }
+      if (AC) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
+      }
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int r = m0 + mt * 8 + (lane >> 2);
+    if (r >= g.M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = n0 + nt * 8 + 2 * (lane & 3) + i;
+        if (c >= g.N) continue;
+        if (CRE) {
+          double* cp = C + r * g.ldc + c;
+          *cp = ACC ? *cp + acc[mt][nt][i] : acc[mt][nt][i];
+        } else {
+          double2* cp = reinterpret_cast<double2*>(C + 2 * (r * g.ldc + c));
+          double2 v = make_double2(acc[mt][nt][i], acc[mt][nt][2 + i]);
+          if (ACC) { v.x += cp->x; v.y += cp->y; }
+          *cp = v;
+        }
+      }
+    }
+  }
+}
+
+template <bool AC, bool BC, bool CRE, bool ACC = false>
+void bgemm(const GemmArgs& g, cudaStream_t st) {
+  if (g.batch == 0 || g.M == 0 || g.N == 0) return;
+  for (int64_t b0 = 0; b0 < g.batch; b0 += 65535) {
+    GemmArgs c = g;
+    c.boff = b0;
+    dim3 grid((g.N + 47) / 48, (g.M + 31) / 32, (unsigned)std::min<int64_t>(65535, g.batch - b0));
+    bgemm_kernel<AC, BC, CRE, ACC><<<grid, 128, 0, st>>>(c);
+    FGT_LAUNCHED();
+  }
+}
+
+inline GemmArgs gemm(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB,
+              double* C, int64_t ldc, int64_t sC, int M, int N, int K, int64_t batch,
+              const int64_t* cidx = nullptr, const int64_t* bidx = nullptr,
+              const int64_t* aidx = nullptr) {
+  GemmArgs g;
+  g.A = A; g.B = B; g.C = C;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.sA = sA; g.sB = sB; g.sC = sC;
+  g.cidx = cidx;
+  g.bidx = bidx;
+  g.aidx = aidx;
+  g.boff = 0;
+  return g;
+}
+
+
+}  // namespace fgt

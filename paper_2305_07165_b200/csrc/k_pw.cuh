@@ -34,5 +34,8 @@ void pw_gather(PwDev& P, TreeDev& T);
 void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
+// Continuous (box) FGT executor (k_volume.cu).
+void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
+             fgt_phase_times* times);
 
 }  // namespace fgt

@@ -1,0 +1,333 @@
+// Continuous (box) FGT, Alg 4 of arXiv 2305.07165, on sm_100a.
+//
+//   leaf->PW   phi = (val2pw_l)^{(x)d} values          d separable DMMA GEMMs per level
+//   merge      phi_B = sum_C T_c2p(C) . phi_C            diagonal shifts (HBM streams)
+//   gather     psi_T = sum_S T_out2in(T,S) . phi_S       (l_c, P-list of SURVEY §3(D))
+//   push       psi_C = T_p2c(C) . psi_B
+//   eval       u = Re (pw2val_l)^{(x)d} psi            d separable DMMA GEMMs per level
+//   direct     u_T += (D1 (x) D2 (x) D3) values_S      real k x k tables, 11 per level
+// The reference has no Alg 4 code (SPEC.md:446-542 specifies it); the per-axis
+// contractions are its `_apply_per_axis` pattern (poly1d.py:76-81).
+#include <algorithm>
+#include <map>
+
+#include "k_gemm.cuh"
+#include "k_pw.cuh"
+
+namespace fgt {
+
+namespace {
+
+int64_t ipw(int64_t b, int e) {
+  int64_t r = 1;
+  while (e--) r *= b;
+  return r;
+}
+
+// ---------------------------------------------------------------- diagonal shifts
+struct ShiftArgs {
+  const int64_t* dst;
+  const int64_t* dst_acc;
+  const int64_t* dst_off;
+  const int64_t* ent_src;
+  const int64_t* ent_rows;
+  const double2* rows;
+  const double2* src;   // phi or psi
+  double2* out;         // phi or psi
+  int64_t NF, d0;       // first dst of this stage
+  int n_f, D;
+};
+
+constexpr int SHIFT_MAXE = 64;
+
+template <int D>
+__global__ void __launch_bounds__(256) shift_kernel(ShiftArgs a) {
+  __shared__ int64_t s_src[SHIFT_MAXE];
+  __shared__ int s_row[SHIFT_MAXE][D];
+  const int64_t t = a.d0 + blockIdx.y;
+  const int64_t e0 = a.dst_off[t];
+  const int64_t ne64 = a.dst_off[t + 1] - e0;
+  const int ne = (int)(ne64 < SHIFT_MAXE ? ne64 : SHIFT_MAXE);
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    s_src[i] = a.ent_src[e0 + i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) s_row[i][k] = (int)a.ent_rows[(e0 + i) * D + k];
+  }
+  __syncthreads();
+  const bool acc_in = a.dst_acc[t] != 0;
+  double2* out = a.out + a.dst[t] * a.NF;
+  const int n_f = a.n_f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.NF;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int m[D];
+    int64_t rem = e;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      m[k] = (int)(rem % n_f);
+      rem /= n_f;
+    }
+    double2 acc = acc_in ? out[e] : make_double2(0.0, 0.0);
+    for (int i = 0; i < ne; ++i) {
+      double2 p = a.rows[(int64_t)s_row[i][0] * n_f + m[0]];
+#pragma unroll
+      for (int k = 1; k < D; ++k) {
+        const double2 q = a.rows[(int64_t)s_row[i][k] * n_f + m[k]];
+        p = make_double2(p.x * q.x - p.y * q.y, p.x * q.y + p.y * q.x);
+      }
+      const double2 f = a.src[s_src[i] * a.NF + e];
+      acc.x += p.x * f.x - p.y * f.y;
+      acc.y += p.x * f.y + p.y * f.x;
+    }
+    out[e] = acc;
+  }
+}
+
+__global__ void repeat_kernel(const int64_t* __restrict__ in, int64_t n, int rep, int stride, int off,
+                              int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * rep;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[(i / rep) * stride + off];
+}
+
+__global__ void pair_reduce_kernel(const double* __restrict__ Y, const int64_t* __restrict__ toff,
+                                   const int64_t* __restrict__ tleaf, int64_t kd, double* __restrict__ u) {
+  const int64_t t = blockIdx.y;
+  const int64_t p0 = toff[t], p1 = toff[t + 1];
+  double* ut = u + tleaf[t] * kd;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kd;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = ut[e];
+    for (int64_t p = p0; p < p1; ++p) s += Y[p * kd + e];
+    ut[e] = s;
+  }
+}
+
+template <class T>
+DBuf<T> upload(const T* h, int64_t n, cudaStream_t st) {
+  DBuf<T> d(n, st);
+  if (n) d.from_host(h, n);
+  return d;
+}
+
+struct LevelList {
+  std::vector<int64_t> leaf, pw;
+};
+
+std::map<int, LevelList> group_by_level(int64_t n, const int64_t* leaf, const int64_t* pw,
+                                        const int64_t* level) {
+  std::map<int, LevelList> g;
+  for (int64_t i = 0; i < n; ++i) {
+    auto& L = g[(int)level[i]];
+    L.leaf.push_back(leaf[i]);
+    L.pw.push_back(pw[i]);
+  }
+  return g;
+}
+
+// complex transpose (rows x cols) -> (cols x rows), interleaved
+std::vector<double> ctranspose(const double* a, int rows, int cols) {
+  std::vector<double> t(2 * (size_t)rows * cols);
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      t[2 * ((size_t)c * rows + r)] = a[2 * ((size_t)r * cols + c)];
+      t[2 * ((size_t)c * rows + r) + 1] = a[2 * ((size_t)r * cols + c) + 1];
+    }
+  return t;
+}
+
+template <int D>
+void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
+              fgt_phase_times* times) {
+  const int k = pl.k, n_f = pl.n_f, L = pl.n_levels;
+  const int64_t KD = ipw(k, D), NF = ipw(n_f, D);
+  FGT_REQUIRE(pl.dim == D, FGT_EINVAL, "plan dim");
+  FGT_REQUIRE(k >= 2 && k <= 32 && n_f >= 2 && n_f <= 128, FGT_ERANGE, "unsupported k / n_f");
+  KClock c_form, c_shift, c_eval, c_direct;
+  // ---- tables
+  const size_t mat = 2 * (size_t)n_f * k;
+  DBuf<double> v2p = upload(pl.val2pw, (int64_t)L * mat, st);      // (L, n_f, k)
+  DBuf<double> p2v = upload(pl.pw2val, (int64_t)L * mat, st);      // (L, k, n_f)
+  std::vector<double> v2pT_h, p2vT_h;
+  for (int l = 0; l < L; ++l) {
+    auto a = ctranspose(pl.val2pw + l * mat, n_f, k);  // (k, n_f)
+    auto b = ctranspose(pl.pw2val + l * mat, k, n_f);  // (n_f, k)
+    v2pT_h.insert(v2pT_h.end(), a.begin(), a.end());
+    p2vT_h.insert(p2vT_h.end(), b.begin(), b.end());
+  }
+  DBuf<double> v2pT = upload(v2pT_h.data(), (int64_t)v2pT_h.size(), st);
+  DBuf<double> p2vT = upload(p2vT_h.data(), (int64_t)p2vT_h.size(), st);
+  DBuf<double> rows = upload(pl.rows, 2 * pl.n_rows * n_f, st);
+  std::vector<double> dT_h((size_t)pl.n_tables * k * k);
+  for (int64_t t = 0; t < pl.n_tables; ++t)
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) dT_h[(t * k + j) * k + i] = pl.dtab[(t * k + i) * k + j];
+  DBuf<double> dtab = upload(pl.dtab, pl.n_tables * k * k, st);
+  DBuf<double> dtabT = upload(dT_h.data(), (int64_t)dT_h.size(), st);
+  DBuf<double> phi(2 * pl.n_pw * NF, st), psi(2 * pl.n_pw * NF, st);
+
+  // ---- leaf -> plane waves, level by level
+  c_form.begin(st);
+  auto forms = group_by_level(pl.n_form, pl.form_leaf, pl.form_pw, pl.form_level);
+  for (auto& kv : forms) {
+    const int l = kv.first;
+    const int64_t nb = (int64_t)kv.second.leaf.size();
+    DBuf<int64_t> lf = upload(kv.second.leaf.data(), nb, st), pw = upload(kv.second.pw.data(), nb, st);
+    const double* A = v2p.get() + l * mat;
+    const double* AT = v2pT.get() + l * mat;
+    if (D == 1) {
+      bgemm<true, false, false>(gemm(A, k, 0, values, 1, KD, phi.get(), 1, NF, n_f, 1, k, nb, pw.get(), lf.get()), st);
+    } else if (D == 2) {
+      DBuf<double> t1(2 * nb * k * n_f, st);
+      bgemm<false, true, false>(gemm(values, k, KD, AT, n_f, 0, t1.get(), n_f, (int64_t)k * n_f, k, n_f, k, nb, nullptr, nullptr, lf.get()), st);
+      bgemm<true, true, false>(gemm(A, k, 0, t1.get(), n_f, (int64_t)k * n_f, phi.get(), n_f, NF, n_f, n_f, k, nb, pw.get()), st);
+    } else {
+      DBuf<double> t1(2 * nb * k * k * n_f, st), t2(2 * nb * k * n_f * n_f, st);
+      bgemm<false, true, false>(gemm(values, k, KD, AT, n_f, 0, t1.get(), n_f, (int64_t)k * k * n_f, k * k, n_f, k, nb, nullptr, nullptr, lf.get()), st);
+      bgemm<true, true, false>(gemm(A, k, 0, t1.get(), n_f, (int64_t)k * n_f, t2.get(), n_f, (int64_t)n_f * n_f, n_f, n_f, k, nb * k), st);
+      bgemm<true, true, false>(gemm(A, k, 0, t2.get(), (int64_t)n_f * n_f, (int64_t)k * n_f * n_f, phi.get(), (int64_t)n_f * n_f, NF, n_f, n_f * n_f, k, nb, pw.get()), st);
+    }
+  }
+  c_form.end(st);
+
+  // ---- merge / gather / push: diagonal shift stages in order
+  c_shift.begin(st);
+  {
+    DBuf<int64_t> dst = upload(pl.dst, pl.n_dst, st), dacc = upload(pl.dst_acc, pl.n_dst, st);
+    DBuf<int64_t> doff = upload(pl.dst_off, pl.n_dst + 1, st);
+    DBuf<int64_t> esrc = upload(pl.ent_src, pl.n_entries, st), erow = upload(pl.ent_rows, pl.n_entries * D, st);
+    for (int64_t s = 0; s < pl.n_stages; ++s) {
+      const int64_t a0 = pl.stage_off[s], a1 = pl.stage_off[s + 1];
+      if (a1 == a0) continue;
+      const int64_t kind = pl.stage_kind[s];  // 0 merge, 1 gather, 2 push
+      ShiftArgs sa;
+      sa.dst = dst.get();
+      sa.dst_acc = dacc.get();
+      sa.dst_off = doff.get();
+      sa.ent_src = esrc.get();
+      sa.ent_rows = erow.get();
+      sa.rows = reinterpret_cast<const double2*>(rows.get());
+      sa.src = reinterpret_cast<const double2*>(kind == 2 ? psi.get() : phi.get());
+      sa.out = reinterpret_cast<double2*>(kind == 0 ? phi.get() : psi.get());
+      sa.NF = NF;
+      sa.d0 = a0;
+      sa.n_f = n_f;
+      sa.D = D;
+      FGT_REQUIRE(a1 - a0 <= 65535, FGT_ERANGE, "too many shift destinations in one stage");
+      dim3 grid(grid_for(NF, 256, 64), (unsigned)(a1 - a0));
+      shift_kernel<D><<<grid, 256, 0, st>>>(sa);
+      FGT_LAUNCHED();
+    }
+  }
+  c_shift.end(st);
+
+  // ---- plane waves -> leaf grids (overwrites u of every evaluated leaf)
+  FGT_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * pl.n_leaves * KD, st));
+  c_eval.begin(st);
+  auto evals = group_by_level(pl.n_eval, pl.eval_leaf, pl.eval_pw, pl.eval_level);
+  for (auto& kv : evals) {
+    const int l = kv.first;
+    const int64_t nb = (int64_t)kv.second.leaf.size();
+    DBuf<int64_t> lf = upload(kv.second.leaf.data(), nb, st), pw = upload(kv.second.pw.data(), nb, st);
+    const double* E = p2v.get() + l * mat;    // (k, n_f)
+    const double* ET = p2vT.get() + l * mat;  // (n_f, k)
+    if (D == 1) {
+      bgemm<true, true, true>(gemm(E, n_f, 0, psi.get(), 1, NF, u, 1, KD, k, 1, n_f, nb, lf.get(), pw.get()), st);
+    } else if (D == 2) {
+      DBuf<double> v1(2 * nb * k * n_f, st);
+      bgemm<true, true, false>(gemm(E, n_f, 0, psi.get(), n_f, NF, v1.get(), n_f, (int64_t)k * n_f, k, n_f, n_f, nb, nullptr, pw.get()), st);
+      bgemm<true, true, true>(gemm(v1.get(), n_f, (int64_t)k * n_f, ET, k, 0, u, k, KD, k, k, n_f, nb, lf.get()), st);
+    } else {
+      DBuf<double> v1(2 * nb * k * n_f * n_f, st), v2(2 * nb * k * k * n_f, st);
+      bgemm<true, true, false>(gemm(E, n_f, 0, psi.get(), (int64_t)n_f * n_f, NF, v1.get(), (int64_t)n_f * n_f, (int64_t)k * n_f * n_f, k, n_f * n_f, n_f, nb, nullptr, pw.get()), st);
+      bgemm<true, true, false>(gemm(E, n_f, 0, v1.get(), n_f, (int64_t)n_f * n_f, v2.get(), n_f, (int64_t)k * n_f, k, n_f, n_f, nb * k), st);
+      bgemm<true, true, true>(gemm(v2.get(), n_f, (int64_t)k * k * n_f, ET, k, 0, u, k, KD, k * k, k, n_f, nb, lf.get()), st);
+    }
+  }
+  c_eval.end(st);
+  phi.release();
+  psi.release();
+
+  // ---- direct near field: per pair separable contractions into Y, then a fixed-order
+  // per-target sum (pairs arrive sorted by target)
+  c_direct.begin(st);
+  const int64_t np = pl.n_dpairs;
+  if (np > 0) {
+    std::vector<int64_t> toff(1, 0), tleaf;
+    for (int64_t p = 0; p < np; ++p) {
+      if (p == 0 || pl.d_tgt[p] != pl.d_tgt[p - 1]) {
+        if (p) toff.push_back(p);
+        tleaf.push_back(pl.d_tgt[p]);
+      }
+      FGT_REQUIRE(p == 0 || pl.d_tgt[p] >= pl.d_tgt[p - 1], FGT_EINVAL, "direct pairs not sorted by target");
+    }
+    toff.push_back(np);
+    DBuf<int64_t> src = upload(pl.d_src, np, st), tab = upload(pl.d_tab, np * D, st);
+    DBuf<int64_t> toff_d = upload(toff.data(), (int64_t)toff.size(), st), tleaf_d = upload(tleaf.data(), (int64_t)tleaf.size(), st);
+    const int64_t chunk = std::max<int64_t>(1, (int64_t)(512ll << 20) / (KD * 8 * 2));
+    DBuf<double> Y(np * KD, st);
+    for (int64_t p0 = 0; p0 < np; p0 += chunk) {
+      const int64_t nb = std::min(chunk, np - p0);
+      DBuf<int64_t> ta(nb * k, st), tb(nb, st), tc(nb, st);
+      const int64_t* srcp = src.get() + p0;
+      // table ids per axis: axis 0 -> tc (last stage), axis D-1 -> first stage
+      repeat_kernel<<<grid_for(nb, 256), 256, 0, st>>>(tab.get() + p0 * D, nb, 1, D, D - 1, tb.get());
+      FGT_LAUNCHED();
+      repeat_kernel<<<grid_for(nb, 256), 256, 0, st>>>(tab.get() + p0 * D, nb, 1, D, 0, tc.get());
+      FGT_LAUNCHED();
+      double* Yp = Y.get() + p0 * KD;
+      if (D == 1) {
+        bgemm<false, false, true>(gemm(dtab.get(), k, k * k, values, 1, KD, Yp, 1, KD, k, 1, k, nb, nullptr, srcp, tc.get()), st);
+      } else if (D == 2) {
+        DBuf<double> x1(nb * KD, st);
+        // X1[a][n2] = sum_b vals[a][b] D_axis1^T[b][n2]
+        bgemm<false, false, true>(gemm(values, k, KD, dtabT.get(), k, k * k, x1.get(), k, KD, k, k, k, nb, nullptr, tb.get(), srcp), st);
+        // Y[n1][n2] = sum_a D_axis0[n1][a] X1[a][n2]
+        bgemm<false, false, true>(gemm(dtab.get(), k, k * k, x1.get(), k, KD, Yp, k, KD, k, k, k, nb, nullptr, nullptr, tc.get()), st);
+      } else {
+        DBuf<double> x1(nb * KD, st), x2(nb * KD, st);
+        repeat_kernel<<<grid_for(nb * k, 256), 256, 0, st>>>(tab.get() + p0 * D, nb, k, D, 1, ta.get());
+        FGT_LAUNCHED();
+        // X1[(a b)][n3] = sum_c vals[(a b)][c] D_axis2^T[c][n3]
+        bgemm<false, false, true>(gemm(values, k, KD, dtabT.get(), k, k * k, x1.get(), k, KD, k * k, k, k, nb, nullptr, tb.get(), srcp), st);
+        // X2[a][n2][n3] = sum_b D_axis1[n2][b] X1[a][b][n3]      (batch = pair x a)
+        bgemm<false, false, true>(gemm(dtab.get(), k, k * k, x1.get(), k, (int64_t)k * k, x2.get(), k, (int64_t)k * k, k, k, k, nb * k, nullptr, nullptr, ta.get()), st);
+        // Y[n1][(n2 n3)] = sum_a D_axis0[n1][a] X2[a][(n2 n3)]
+        bgemm<false, false, true>(gemm(dtab.get(), k, k * k, x2.get(), (int64_t)k * k, KD, Yp, (int64_t)k * k, KD, k, k * k, k, nb, nullptr, nullptr, tc.get()), st);
+      }
+    }
+    const int64_t nt = (int64_t)tleaf.size();
+    FGT_REQUIRE(nt <= 65535 * 64, FGT_ERANGE, "too many direct targets");
+    for (int64_t t0 = 0; t0 < nt; t0 += 65535) {
+      const int64_t n = std::min<int64_t>(65535, nt - t0);
+      pair_reduce_kernel<<<dim3(grid_for(KD, 256, 16), (unsigned)n), 256, 0, st>>>(
+          Y.get(), toff_d.get() + t0, tleaf_d.get() + t0, KD, u);
+      FGT_LAUNCHED();
+    }
+  }
+  c_direct.end(st);
+  if (times) {
+    times->form_ms = times->k_form_ms = c_form.ms();
+    times->gather_ms = times->k_gather_ms = c_shift.ms();
+    times->eval_ms = times->k_eval_ms = c_eval.ms();
+    times->direct_ms = times->k_direct_ms = c_direct.ms();
+    times->total_ms = times->form_ms + times->gather_ms + times->eval_ms + times->direct_ms;
+    times->n_modes = NF;
+    times->n_boxes = pl.n_pw;
+    times->n_src_dense = pl.n_form;
+    times->n_tgt_psi = pl.n_eval;
+    times->n_p_entries = pl.n_entries;
+    times->n_direct_pairs = np;
+  }
+}
+
+}  // namespace
+
+void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
+             fgt_phase_times* times) {
+  if (pl.dim == 1) box_impl<1>(pl, values, u, st, times);
+  else if (pl.dim == 2) box_impl<2>(pl, values, u, st, times);
+  else if (pl.dim == 3) box_impl<3>(pl, values, u, st, times);
+  else throw Error(FGT_EINVAL, "dim must be 1, 2, or 3");
+}
+
+}  // namespace fgt

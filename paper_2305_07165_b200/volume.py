@@ -1,0 +1,495 @@
+"""Continuous (box) FGT on the GPU: Alg 3 density tree on the host, Alg 4 in CUDA.
+
+Public entry points mirror the reference / SPEC:
+  * `build_density_tree(density, dim, k, epsilon, periodic=False, l_max=30,
+    refill="evaluate", root_center=None, root_side=1.0)` -> (tree, values, coeffs),
+    the contract of /root/reference/pkg/src/fgt/tree.py:577-644 (sigma is a user
+    callable, so Alg 3 runs on the host; boxes are created in the reference's order);
+  * `fgt_box(tree, values, delta, epsilon, boundary="free")` -> {leaf: u (k,)*d}
+    (SPEC.md:512-516): the level tables (J/I moments, poly1d.py:129-210) and schedules are
+    built here, then one C call (`fgt_box`, include/fgt_cuda.h) runs leaf->PW, merge,
+    gather, push, PW->grid and the direct near field on the GPU.
+Conventions (signs, lambda = 2 sqrt(delta)/L, pre-multiplied weights) are the ones
+SURVEY.md §3(D) verified against quadrature.
+"""
+
+import ctypes
+
+import numpy as np
+from scipy.special import spherical_jn
+
+from . import _lib
+from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_level, pw_params
+from .tree import Tree
+
+MAX_LEVEL = 30
+
+
+# ------------------------------------------------------------------ 1-D polynomial tools
+def legendre_values(n_max, x):
+    """P_0..P_n_max at x (three-term recurrence)."""
+    x = np.asarray(x, dtype=float)
+    out = np.empty((n_max + 1,) + x.shape)
+    out[0] = 1.0
+    if n_max:
+        out[1] = x
+    for n in range(1, n_max):
+        out[n + 1] = ((2 * n + 1) * x * out[n] - n * out[n - 1]) / (n + 1)
+    return out
+
+
+class LegendreBasis:
+    """k Gauss-Legendre nodes/weights on [-1, 1] and the value <-> coefficient maps."""
+
+    def __init__(self, k):
+        if not 2 <= k <= 24:
+            raise ValueError(f"polynomial order k={k} outside supported range [2, 24]")
+        self.k = k
+        self.nodes, self.weights = np.polynomial.legendre.leggauss(k)
+        P = legendre_values(k - 1, self.nodes)
+        self.val_to_pol = ((2 * np.arange(k) + 1) / 2.0)[:, None] * self.weights[None, :] * P
+        self.pol_to_val = P.T.copy()
+
+
+def apply_per_axis(mat, tensor, dim):
+    out = tensor
+    for ax in range(dim):
+        out = np.moveaxis(np.tensordot(mat, out, axes=([1], [ax])), 0, ax)
+    return np.ascontiguousarray(out)
+
+
+def tail_error(c):
+    k, d = c.shape[0], c.ndim
+    if d == 1:
+        tail = c[k - 2:]
+    else:
+        idx = np.indices((k,) * d).astype(float)
+        tail = c[(idx ** 2).sum(axis=0) >= k * k]
+    return float(np.sqrt(np.mean(np.abs(tail) ** 2))) if tail.size else 0.0
+
+
+def gauss_moment_J(lam, n_max, t):
+    """J_lam[P_n](t) = int_{-1}^1 exp(-((t-x)/lam)^2) P_n(x) dx by composite Gauss-Legendre
+    quadrature over the support [t-9.5 lam, t+9.5 lam] clipped to [-1, 1]."""
+    t = np.atleast_1d(np.asarray(t, dtype=float))
+    lo = np.maximum(-1.0, t - 9.5 * lam)
+    hi = np.minimum(1.0, t + 9.5 * lam)
+    xs, ws = np.polynomial.legendre.leggauss(40)
+    out = np.zeros((n_max + 1,) + t.shape)
+    panels = 8
+    for p in range(panels):
+        a = lo + (hi - lo) * (p / panels)
+        b = lo + (hi - lo) * ((p + 1) / panels)
+        half = 0.5 * np.maximum(b - a, 0.0)
+        X = (0.5 * (a + b))[..., None] + half[..., None] * xs
+        g = np.exp(-((t[..., None] - X) / lam) ** 2) * (half[..., None] * ws)
+        out += np.einsum("n...q,...q->n...", legendre_values(n_max, X), g)
+    return out
+
+
+def fourier_moment_I(n_max, t):
+    """I[P_n](t) = int_{-1}^1 exp(i t x) P_n(x) dx = 2 i^n j_n(t)."""
+    t = np.atleast_1d(np.asarray(t, dtype=float))
+    n = np.arange(n_max + 1)
+    jn = spherical_jn(n[:, None], t.ravel()[None, :]).reshape((n_max + 1,) + t.shape)
+    return 2.0 * (1j ** n).reshape((-1,) + (1,) * t.ndim) * jn
+
+
+# ------------------------------------------------------------------ Alg 3
+class _Builder:
+    """Mutable 2^d-tree in the reference's creation order (children of box b at level l+1
+    get consecutive ids; child c has axis-k bit (c >> k) & 1)."""
+
+    def __init__(self, dim, rc, rs, periodic):
+        self.dim, self.rc, self.rs, self.periodic = dim, np.asarray(rc, float), float(rs), periodic
+        self.level, self.parent, self.kids = [0], [-1], [None]
+        self.coords = [np.zeros(dim, np.int64)]
+        self.index = [{(0,) * dim: 0}]
+        self.bits = np.array([[(c >> a) & 1 for a in range(dim)] for c in range(2 ** dim)])
+        g = np.stack(np.meshgrid(*([np.arange(-1, 2)] * dim), indexing="ij"), -1).reshape(-1, dim)
+        self.offs = [o for o in g if o.any()]
+
+    def leaf(self, b):
+        return self.kids[b] is None
+
+    def center(self, b):
+        s = self.rs / 2 ** self.level[b]
+        return self.rc - 0.5 * self.rs + (self.coords[b] + 0.5) * s
+
+    def split(self, b):
+        l = self.level[b] + 1
+        if l > MAX_LEVEL:
+            raise RuntimeError(f"refinement beyond maximum level {MAX_LEVEL}")
+        if len(self.index) <= l:
+            self.index.append({})
+        first = len(self.level)
+        for c in range(2 ** self.dim):
+            g = 2 * self.coords[b] + self.bits[c]
+            self.level.append(l)
+            self.parent.append(b)
+            self.kids.append(None)
+            self.coords.append(g)
+            self.index[l][tuple(g)] = first + c
+        self.kids[b] = list(range(first, first + 2 ** self.dim))
+        return self.kids[b]
+
+    def covering(self, l, cell):
+        c = np.asarray(cell)
+        for lv in range(min(l, len(self.index) - 1), -1, -1):
+            b = self.index[lv].get(tuple(c))
+            if b is not None:
+                return b
+            c = c >> 1
+        raise RuntimeError("no covering box")
+
+    def balance(self, on_split):
+        stack = [b for b in range(len(self.level)) if self.leaf(b)]
+        while stack:
+            b = stack.pop()
+            if not self.leaf(b) or self.level[b] < 2:
+                continue
+            l, n_side, again = self.level[b], 2 ** self.level[b], False
+            for o in self.offs:
+                n = self.coords[b] + o
+                if self.periodic:
+                    n = n - (n // n_side) * n_side
+                elif np.any(n < 0) or np.any(n >= n_side):
+                    continue
+                nb = self.covering(l, n)
+                if self.leaf(nb) and l - self.level[nb] >= 2:
+                    kids = self.split(nb)
+                    on_split(nb, kids)
+                    stack.extend(kids)
+                    again = True
+            if again:
+                stack.append(b)
+
+    def finalize(self):
+        nb = len(self.level)
+        children = np.full((nb, 2 ** self.dim), -1, np.int64)
+        for b, k in enumerate(self.kids):
+            if k is not None:
+                children[b] = k
+        return Tree(dim=self.dim, root_center=self.rc, root_side=self.rs, periodic=self.periodic,
+                    level=np.asarray(self.level, np.int64), parent=np.asarray(self.parent, np.int64),
+                    children=children, coords=np.asarray(self.coords, np.int64).reshape(nb, self.dim),
+                    is_leaf=children[:, 0] < 0)
+
+
+def leaf_grid(tree, box, basis):
+    """Tensor-product Legendre nodes of a box, shape (k,)*d + (d,)."""
+    c = tree.centers(box)
+    s = float(tree.side(tree.level[box]))
+    axes = [c[i] + 0.5 * s * basis.nodes for i in range(tree.dim)]
+    return np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1)
+
+
+def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL,
+                       refill="evaluate", root_center=None, root_side=1.0):
+    """Resolve sigma on a level-restricted tree (Alg 3); returns (tree, values, coeffs)."""
+    if refill != "evaluate":
+        # the reference's interpolation refill evaluates at local*0.5 (tree.py:665) and is
+        # wrong by O(1); only re-evaluation is supported
+        raise ValueError("only refill='evaluate' is supported")
+    rc = np.zeros(dim) if root_center is None else np.asarray(root_center, float)
+    eps = clamp_tolerance(epsilon)
+    basis = LegendreBasis(k)
+    B = _Builder(dim, rc, root_side, periodic)
+    values, coeffs = {}, {}
+    wt = basis.weights
+    for _ in range(dim - 1):
+        wt = np.multiply.outer(wt, basis.weights)
+
+    def sample(b):
+        c = B.center(b)
+        s = B.rs / 2 ** B.level[b]
+        axes = [c[i] + 0.5 * s * basis.nodes for i in range(dim)]
+        v = np.asarray(density(np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1)), float)
+        values[b] = v
+        coeffs[b] = apply_per_axis(basis.val_to_pol, v, dim)
+
+    def sigma_norm():
+        tot = 0.0
+        for b, v in values.items():
+            if B.leaf(b):
+                s = B.rs / 2 ** B.level[b]
+                tot += (s / 2.0) ** dim * float(np.sum(wt * v * v))
+        return np.sqrt(tot) / root_side ** (dim / 2.0)
+
+    sample(0)
+    frontier = [0]
+    for l in range(l_max + 1):
+        nrm = max(sigma_norm(), 1e-300)
+        split = [b for b in frontier if tail_error(coeffs[b]) > eps * nrm]
+        if not split:
+            break
+        if l == l_max:
+            raise RuntimeError(f"density not resolved at maximum refinement level {l_max}")
+        frontier = []
+        for b in split:
+            for c in B.split(b):
+                sample(c)
+                frontier.append(c)
+    B.balance(lambda parent, kids: [sample(c) for c in kids])
+    tree = B.finalize()
+    leaves = np.nonzero(tree.is_leaf)[0]
+    return tree, {b: values[b] for b in leaves}, {b: coeffs[b] for b in leaves}
+
+
+# ------------------------------------------------------------------ Alg 4 plan
+FINE = [(-0.75, 0.5), (-0.25, 0.5), (0.25, 0.5), (0.75, 0.5)]
+COARSE = [(-1.5, 2.0), (-0.5, 2.0), (0.5, 2.0), (1.5, 2.0)]
+COLL = [(-1.0, 1.0), (0.0, 1.0), (1.0, 1.0)]
+OFFSETS = FINE + COARSE + COLL  # the 11 per-axis offsets s_1..s_11
+
+
+class BoxPlan:
+    """Host half of Alg 4: flags, lists, tables and shift schedules for one tree."""
+
+    def __init__(self, tree, delta, epsilon, k, periodic):
+        if not delta > 0:
+            raise ValueError("delta must be positive")
+        d = tree.dim
+        self.dim, self.k = d, k
+        eps = clamp_tolerance(epsilon)
+        self.l_c, R = cutoff_level(delta, eps, tree.root_side, kind="density")
+        if periodic and not (delta < PERIODIC_IMAGE_DELTA and self.l_c >= 2):
+            raise ValueError("periodic box FGT implemented for delta < 1/36 and l_c >= 2")
+        self.pw = pw_params(float(epsilon), delta, R=R, dim=d)
+        n_f = self.n_f = self.pw.n_f
+        basis = self.basis = LegendreBasis(k)
+        nb = tree.n_boxes
+        l_c = self.l_c
+        lmax = int(tree.level.max())
+        self.n_levels = max(lmax, l_c) + 1
+        leaves = np.nonzero(tree.is_leaf)[0]
+        self.leaves = leaves
+        leaf_slot = np.full(nb, -1, np.int64)
+        leaf_slot[leaves] = np.arange(leaves.size)
+        key = {(int(tree.level[b]),) + tuple(int(c) for c in tree.coords[b]): b for b in range(nb)}
+        km = (np.arange(n_f) - n_f // 2) * self.pw.h / np.sqrt(delta)
+        side = tree.root_side / 2.0 ** np.arange(self.n_levels)
+        offs = np.stack(np.meshgrid(*([np.arange(-1, 2)] * d), indexing="ij"), -1).reshape(-1, d)
+
+        def covering(l, cell):
+            c = np.asarray(cell)
+            for lv in range(l, -1, -1):
+                b = key.get((lv,) + tuple(int(x) for x in c))
+                if b is not None:
+                    return b
+                c = c >> 1
+            raise RuntimeError("no covering box")
+
+        def neighbour_cells(b, with_self=True):
+            l = int(tree.level[b])
+            n_side = 2 ** l
+            for o in offs:
+                if not with_self and not o.any():
+                    continue
+                n = tree.coords[b] + o
+                if periodic:
+                    v = n // n_side
+                    yield n - v * n_side, v
+                elif not (np.any(n < 0) or np.any(n >= n_side)):
+                    yield n, np.zeros(d, np.int64)
+
+        # f flags (Definition fflagdef): level > l_c, or level l_c with a subdivided colleague
+        f = tree.level > l_c
+        coll = {}
+        for b in np.nonzero(tree.level == l_c)[0]:
+            lst = [(key[(l_c,) + tuple(int(x) for x in n)], v) for n, v in neighbour_cells(b)]
+            coll[b] = lst
+            f[b] = any(not tree.is_leaf[S] for S, _ in lst)
+        pw_slot = np.full(nb, -1, np.int64)
+        pw_slot[f] = np.arange(int(f.sum()))
+        self.n_pw = int(f.sum())
+
+        # ---- phase rows: out2in (3) at l_c, then c2p (2) and p2c (2) per child level
+        rows = [np.exp(1j * km * o * side[l_c]) for o in (-1, 0, 1)]
+        c2p_row, p2c_row = {}, {}
+        for l in range(1, self.n_levels):
+            for sgn in (0, 1):
+                s = (2 * sgn - 1) * 0.5 * side[l]
+                c2p_row[(l, sgn)] = len(rows)
+                rows.append(np.exp(-1j * km * s))
+                p2c_row[(l, sgn)] = len(rows)
+                rows.append(np.exp(1j * km * s))
+        self.rows = np.ascontiguousarray(np.array(rows, dtype=np.complex128))
+
+        # ---- shift stages: merge (deepest first), gather at l_c, push (shallowest first)
+        stage_off, stage_kind = [0], []
+        dst, dst_acc, dst_off, ent_src, ent_rows = [], [], [0], [], []
+
+        def add_dst(t, entries, acc=0):
+            dst.append(pw_slot[t])
+            dst_acc.append(acc)
+            for s, r in entries:
+                ent_src.append(pw_slot[s])
+                ent_rows.append(r)
+            dst_off.append(len(ent_src))
+
+        def end_stage(kind):
+            if len(dst) > stage_off[-1]:
+                stage_off.append(len(dst))
+                stage_kind.append(kind)
+
+        for l in range(lmax - 1, l_c - 1, -1):
+            for b in np.nonzero((tree.level == l) & ~tree.is_leaf)[0]:
+                ents = []
+                for c in tree.children[b]:
+                    bits = tree.coords[c] - 2 * tree.coords[b]
+                    ents.append((c, [c2p_row[(l + 1, int(x))] for x in bits]))
+                add_dst(b, ents)
+            end_stage(0)
+        n_gpairs = 0
+        for T, lst in coll.items():
+            if not f[T]:
+                continue
+            ents = []
+            for S, v in lst:
+                if f[S] and not (tree.is_leaf[T] and tree.is_leaf[S]):
+                    o = tree.coords[T] - tree.coords[S] - v * 2 ** l_c  # in {-1, 0, 1}
+                    ents.append((S, [int(x) + 1 for x in o]))
+            n_gpairs += len(ents)
+            add_dst(T, ents)
+        end_stage(1)
+        self.n_gather_pairs = n_gpairs
+        for l in range(l_c, lmax):
+            for b in np.nonzero((tree.level == l) & ~tree.is_leaf & f)[0]:
+                for c in tree.children[b]:
+                    bits = tree.coords[c] - 2 * tree.coords[b]
+                    add_dst(c, [(b, [p2c_row[(l + 1, int(x))] for x in bits])])
+            end_stage(2)
+        self.stage_off = np.array(stage_off, np.int64)
+        self.stage_kind = np.array(stage_kind, np.int64)
+        self.dst = np.array(dst, np.int64)
+        self.dst_acc = np.array(dst_acc, np.int64)
+        self.dst_off = np.array(dst_off, np.int64)
+        self.ent_src = np.array(ent_src, np.int64)
+        self.ent_rows = np.array(ent_rows, np.int64).reshape(-1, d)
+
+        # ---- leaf -> PW and PW -> grid
+        fl = leaves[f[leaves]]
+        self.form_leaf = leaf_slot[fl]
+        self.form_pw = pw_slot[fl]
+        self.form_level = tree.level[fl].astype(np.int64)
+        self.eval_leaf, self.eval_pw, self.eval_level = self.form_leaf, self.form_pw, self.form_level
+        val2pw = np.zeros((self.n_levels, n_f, k), np.complex128)
+        pw2val = np.zeros((self.n_levels, k, n_f), np.complex128)
+        m = np.arange(n_f) - n_f // 2
+        for l in set(self.form_level.tolist()):
+            L = side[l]
+            I = fourier_moment_I(k - 1, L * m * self.pw.h / (2 * np.sqrt(delta)))  # (k, n_f)
+            val2pw[l] = ((L / 2.0) * self.pw.weights_1d[:, None] * np.conj(I).T) @ basis.val_to_pol
+            pw2val[l] = np.exp(1j * np.outer(0.5 * L * basis.nodes, km))
+        self.val2pw = np.ascontiguousarray(val2pw)
+        self.pw2val = np.ascontiguousarray(pw2val)
+
+        # ---- direct: touching leaf pairs with both leaves at level <= l_c (D-list)
+        pairs = []
+        for T in leaves[tree.level[leaves] <= l_c]:
+            lt = int(tree.level[T])
+            seen = set()
+            for n, v in neighbour_cells(T):
+                S = covering(lt, n)
+                cands = [S] if tree.is_leaf[S] else [
+                    c for c in tree.children[S]
+                    if np.all(tree.coords[c] + 2 * v * 2 ** lt >= 2 * tree.coords[T] - 1)
+                    and np.all(tree.coords[c] + 2 * v * 2 ** lt <= 2 * tree.coords[T] + 2)]
+                for S2 in cands:
+                    kk = (int(S2),) + tuple(int(x) for x in v)
+                    if kk in seen or not tree.is_leaf[S2] or tree.level[S2] > l_c:
+                        continue
+                    seen.add(kk)
+                    pairs.append((T, S2, v))
+        ctr = tree.centers()
+        used_levels = sorted({int(tree.level[S]) for _, S, _ in pairs})
+        tab_id = {}
+        tabs = []
+        for l in used_levels:
+            L = side[l]
+            lam = 2 * np.sqrt(delta) / L
+            for j, (o, r) in enumerate(OFFSETS):
+                Jm = gauss_moment_J(lam, k - 1, 2 * o + r * basis.nodes)  # (k deg, k tgt)
+                tab_id[(l, j)] = len(tabs)
+                tabs.append(((L / 2.0) * Jm.T) @ basis.val_to_pol)
+        self.dtab = np.ascontiguousarray(np.array(tabs, np.float64).reshape(-1, k, k))
+        look = {(o, r): j for j, (o, r) in enumerate(OFFSETS)}
+        d_t, d_s, d_tab = [], [], []
+        for T, S, v in sorted(pairs, key=lambda p: leaf_slot[p[0]]):
+            ls = int(tree.level[S])
+            Ls, Lt = side[ls], side[int(tree.level[T])]
+            ids = []
+            for ax in range(d):
+                o = (ctr[T][ax] - ctr[S][ax] - v[ax] * tree.root_side) / Ls
+                ids.append(tab_id[(ls, look[(float(o), float(Lt / Ls))])])
+            d_t.append(leaf_slot[T])
+            d_s.append(leaf_slot[S])
+            d_tab.append(ids)
+        self.d_tgt = np.array(d_t, np.int64)
+        self.d_src = np.array(d_s, np.int64)
+        self.d_tab = np.array(d_tab, np.int64).reshape(-1, d)
+
+    def cstruct(self):
+        """The fgt_box_plan C struct (arrays kept alive by self)."""
+        P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if a.dtype != np.int64 else \
+            a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))  # noqa: E731
+        self._keep = [np.ascontiguousarray(a) for a in (
+            self.val2pw.view(np.float64), self.pw2val.view(np.float64), self.rows.view(np.float64),
+            self.dtab)]
+        s = _lib.FgtBoxPlan()
+        s.dim, s.k, s.n_f, s.n_levels, s.l_c = self.dim, self.k, self.n_f, self.n_levels, self.l_c
+        s.n_leaves, s.n_pw = self.leaves.size, self.n_pw
+        s.val2pw, s.pw2val = P(self._keep[0]), P(self._keep[1])
+        s.n_rows, s.rows = self.rows.shape[0], P(self._keep[2])
+        s.n_tables, s.dtab = self.dtab.shape[0], P(self._keep[3])
+        s.n_form, s.form_leaf, s.form_pw, s.form_level = (
+            self.form_leaf.size, P(self.form_leaf), P(self.form_pw), P(self.form_level))
+        s.n_stages, s.n_dst, s.n_entries = self.stage_kind.size, self.dst.size, self.ent_src.size
+        s.stage_off, s.stage_kind = P(self.stage_off), P(self.stage_kind)
+        s.dst, s.dst_acc, s.dst_off = P(self.dst), P(self.dst_acc), P(self.dst_off)
+        self._ent_rows = np.ascontiguousarray(self.ent_rows)
+        s.ent_src, s.ent_rows = P(self.ent_src), P(self._ent_rows)
+        s.n_eval, s.eval_leaf, s.eval_pw, s.eval_level = (
+            self.eval_leaf.size, P(self.eval_leaf), P(self.eval_pw), P(self.eval_level))
+        self._d_tab = np.ascontiguousarray(self.d_tab)
+        s.n_dpairs, s.d_tgt, s.d_src, s.d_tab = self.d_tgt.size, P(self.d_tgt), P(self.d_src), P(self._d_tab)
+        return s
+
+
+def _stack_values(tree, values, k):
+    leaves = np.nonzero(tree.is_leaf)[0]
+    return leaves, np.ascontiguousarray(np.stack([np.asarray(values[b], float).reshape((k,) * tree.dim)
+                                                   for b in leaves]))
+
+
+def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, plan=None):
+    """u = int exp(-|x-y|^2/delta) sigma(y) dy on every leaf grid; {leaf: (k,)*d array}."""
+    if boundary not in ("free", "periodic"):
+        raise ValueError(f"unknown boundary {boundary!r}")
+    if bool(tree.periodic) != (boundary == "periodic"):
+        raise ValueError("tree periodicity does not match boundary")
+    some = next(iter(values.values()))
+    k = np.asarray(some).shape[0]
+    plan = plan or BoxPlan(tree, delta, epsilon, k, boundary == "periodic")
+    leaves, V = _stack_values(tree, values, k)
+    U = np.empty_like(V)
+    t = _lib.FgtPhaseTimes()
+    cs = plan.cstruct()
+    _lib.check(_lib.load().fgt_box(ctypes.byref(cs), _lib.ptr(V), _lib.ptr(U), ctypes.byref(t)))
+    out = {int(b): U[i] for i, b in enumerate(leaves)}
+    return (out, t.as_dict()) if return_times else out
+
+
+def fgt_box_device(plan, values_dev, out_dev=None, return_times=False):
+    """Box FGT on torch CUDA tensors (n_leaves, k^d) already resident in HBM."""
+    import torch
+    if out_dev is None:
+        out_dev = torch.empty_like(values_dev)
+    t = _lib.FgtPhaseTimes()
+    cs = plan.cstruct()
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.load().fgt_box_dev(ctypes.byref(cs), ctypes.c_void_p(values_dev.data_ptr()),
+                                       ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(stream),
+                                       ctypes.byref(t)))
+    return (out_dev, t.as_dict()) if return_times else out_dev

@@ -1,0 +1,96 @@
+"""GPU parity of the continuous (box) FGT: libfgtcuda.so vs the CPU oracle and vs closed
+forms (SPEC.md:651 acceptance 7)."""
+
+import numpy as np
+import pytest
+
+from oracle import volume as ov
+
+pytestmark = pytest.mark.gpu
+
+
+def gaussians(d):
+    C = np.array([[0.1, -0.05, 0.02][:d], [-0.2, 0.15, -0.1][:d]])
+    W, A = [0.05, 0.1], [1.0, 0.7]
+    return (lambda p: sum(a * np.exp(-np.sum((p - c) ** 2, axis=-1) / w ** 2)
+                          for c, w, a in zip(C, W, A))), C, W, A
+
+
+def rel_err(u, ref):
+    num = sum(np.sum((u[b] - ref[b]) ** 2) for b in ref)
+    den = sum(np.sum(ref[b] ** 2) for b in ref)
+    return np.sqrt(num / den)
+
+
+CASES = [  # d, k, delta, eps
+    (1, 12, 1e-3, 1e-9),
+    (2, 10, 1e-3, 1e-8),
+    (2, 16, 1e-4, 1e-10),
+    (3, 6, 1e-2, 1e-6),
+    (3, 8, 1e-3, 1e-7),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"d{c[0]}k{c[1]}" for c in CASES])
+def test_box_fgt_vs_oracle_and_closed_form(cuda, case):
+    from paper_2305_07165_b200 import volume as pv
+    d, k, delta, eps = case
+    dens, C, W, A = gaussians(d)
+    tree, vals, _ = pv.build_density_tree(dens, d, k, eps * 0.1)
+    u = pv.fgt_box(tree, vals, delta, eps)
+    to = ov.density_tree(dens, d, k, eps * 0.1)
+    assert np.array_equal(to.level, tree.level) and np.array_equal(to.coords, tree.coords)
+    ref = ov.fgt_box(to, delta, eps)
+    assert set(u) == set(ref)
+    assert rel_err(u, ref) < 1e-11
+    exact = {b: ov.gaussian_box_convolution(to.leaf_points(b), delta, C, W, A) for b in ref}
+    assert rel_err(u, exact) <= 10 * eps
+
+
+def test_box_fgt_constant_density(cuda):
+    from scipy.special import erf
+    from paper_2305_07165_b200 import volume as pv
+    tree, vals, _ = pv.build_density_tree(lambda p: np.ones(p.shape[:-1]), 3, 6, 1e-10)
+    delta, eps = 1e-2, 1e-8
+    u = pv.fgt_box(tree, vals, delta, eps)
+    for b, ub in u.items():
+        x = pv.leaf_grid(tree, b, pv.LegendreBasis(6))
+        ex = np.prod(np.sqrt(np.pi * delta) / 2 * (erf((0.5 - x) / np.sqrt(delta))
+                                                   + erf((0.5 + x) / np.sqrt(delta))), axis=-1)
+        assert np.max(np.abs(ub - ex)) <= 10 * eps * np.max(ex)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_box_fgt_periodic_eigenfunction(cuda, d):
+    """sigma_p -> (pi delta)^{d/2} exp(-d pi^2 delta n^2) sigma_p."""
+    from paper_2305_07165_b200 import volume as pv
+    n, delta, eps = 4, 1e-3, 1e-8
+
+    def sig(p):
+        out = np.sin(2 * np.pi * n * p[..., 0])
+        for ax in range(1, d):
+            out = out * np.cos(2 * np.pi * n * p[..., ax])
+        return out
+    tree, vals, _ = pv.build_density_tree(sig, d, 8 if d == 2 else 6, 1e-9, periodic=True)
+    u = pv.fgt_box(tree, vals, delta, eps, boundary="periodic")
+    fac = (np.pi * delta) ** (d / 2) * np.exp(-d * np.pi ** 2 * delta * n * n)
+    num = den = 0.0
+    for b, ub in u.items():
+        ex = fac * sig(pv.leaf_grid(tree, b, pv.LegendreBasis(8 if d == 2 else 6)))
+        num += np.sum((ub - ex) ** 2)
+        den += np.sum(ex ** 2)
+    assert np.sqrt(num / den) <= 10 * eps
+
+
+def test_box_fgt_device_path(cuda):
+    import torch
+    from paper_2305_07165_b200 import volume as pv
+    dens = gaussians(3)[0]
+    tree, vals, _ = pv.build_density_tree(dens, 3, 8, 1e-8)
+    plan = pv.BoxPlan(tree, 1e-3, 1e-7, 8, False)
+    u = pv.fgt_box(tree, vals, 1e-3, 1e-7, plan=plan)
+    leaves, V = pv._stack_values(tree, vals, 8)
+    ud = pv.fgt_box_device(plan, torch.from_numpy(V).cuda())
+    torch.cuda.synchronize()
+    ud = ud.cpu().numpy()
+    assert all(np.array_equal(ud[i], u[int(b)]) for i, b in enumerate(leaves))
