@@ -297,7 +297,9 @@ class BoxPlan:
         f = tree.level > l_c
         coll = {}
         for b in np.nonzero(tree.level == l_c)[0]:
-            lst = [(key[(l_c,) + tuple(int(x) for x in n)], v) for n, v in neighbour_cells(b)]
+            # colleagues that exist at l_c (a coarser covering leaf interacts directly)
+            lst = [(key[kk], v) for n, v in neighbour_cells(b)
+                   if (kk := (l_c,) + tuple(int(x) for x in n)) in key]
             coll[b] = lst
             f[b] = any(not tree.is_leaf[S] for S, _ in lst)
         pw_slot = np.full(nb, -1, np.int64)

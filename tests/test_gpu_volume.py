@@ -64,14 +64,16 @@ def test_box_fgt_constant_density(cuda):
 def test_box_fgt_periodic_eigenfunction(cuda, d):
     """sigma_p -> (pi delta)^{d/2} exp(-d pi^2 delta n^2) sigma_p."""
     from paper_2305_07165_b200 import volume as pv
-    n, delta, eps = 4, 1e-3, 1e-8
+    # 3-D kept small: phi/psi are stored for every f=1 box (n_f^3 modes each)
+    n, delta, eps = (4, 1e-3, 1e-8) if d == 2 else (2, 2e-3, 1e-6)
 
     def sig(p):
         out = np.sin(2 * np.pi * n * p[..., 0])
         for ax in range(1, d):
             out = out * np.cos(2 * np.pi * n * p[..., ax])
         return out
-    tree, vals, _ = pv.build_density_tree(sig, d, 8 if d == 2 else 6, 1e-9, periodic=True)
+    tree, vals, _ = pv.build_density_tree(sig, d, 8 if d == 2 else 6, 1e-9 if d == 2 else 1e-7,
+                                           periodic=True)
     u = pv.fgt_box(tree, vals, delta, eps, boundary="periodic")
     fac = (np.pi * delta) ** (d / 2) * np.exp(-d * np.pi ** 2 * delta * n * n)
     num = den = 0.0
