@@ -362,7 +362,49 @@ def run_ours(args, world, rank, local):
         sec, desc = oracle_sample(y, q, x, seed=0)
         res["cpu_baseline"] = {"value": (N + M) / sec, "unit": "points/s", "cores": 1,
                                "kind": "port", "sample": desc}
+    if rank == 0 and not args.no_volume:
+        res["volume"] = run_volume_leg(args, flush)
     return res
+
+
+def run_volume_leg(args, flush):
+    """Secondary line: BASELINE configs[3] (volume FGT, d=3, k=16, delta=1e-4, eps=1e-10,
+    5 Gaussians): device time of fgt_box_device per step (plan prebuilt), grid points/s;
+    e2e adds the host plan and the H2D/D2H of the leaf grids."""
+    import torch
+    from paper_2305_07165_b200 import volume as pv
+    from tools.prof_volume import build
+    tree, vals, plan, t_tree, t_plan = build()
+    leaves, V = pv._stack_values(tree, vals, 16)
+    dv = torch.from_numpy(V).cuda()
+    out = torch.empty_like(dv)
+    for _ in range(3):
+        pv.fgt_box_device(plan, dv, out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ms, ph = [], None
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _, ph = pv.fgt_box_device(plan, dv, out, return_times=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    npts = V.size
+    t0 = time.perf_counter()
+    u = pv.fgt_box(tree, vals, 1e-4, 1e-10)
+    e2e = time.perf_counter() - t0
+    return {"workload": "config4: volume FGT d=3, k=16, 5 Gaussians (w 0.01-0.1), "
+                        "delta=1e-4, eps=1e-10, tree eps 1e-10",
+            "metric": "grid points/s (N = N_leaf k^d)", "grid_points": int(npts),
+            "n_leaves": int(len(leaves)), "n_boxes": int(tree.n_boxes),
+            "value": npts / (float(np.mean(ms)) * 1e-3), "ms_per_step": float(np.mean(ms)),
+            "e2e": {"value": npts / e2e, "ms_per_step": e2e * 1e3,
+                    "includes": "host tables/schedules + H2D + GPU + D2H"},
+            "host_density_tree_s": t_tree, "host_plan_s": t_plan,
+            "phases_ms": {k: ph[k] for k in ("form_ms", "gather_ms", "eval_ms", "direct_ms")},
+            "checksum": float(sum(np.sum(v) for v in u.values()))}
 
 
 def main():
@@ -373,6 +415,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override N=M (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-volume", action="store_true", help="skip the config-4 volume leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, local = dist_setup(args.gpus)

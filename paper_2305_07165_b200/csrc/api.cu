@@ -205,12 +205,19 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     nufft_plan(NP, pw.n_f, tol, X, pw.weights_1d, st);
     pw_form(P, T, &NP);
     t.form_ms = tm.lap();
-    pw_gather(P, T);
+    // psi is produced and consumed in batches of bounded size (<= ~4 GB)
+    const int64_t per = P.NF * 16;
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)4 << 30) / per));
+    for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
+      const int64_t hi = std::min(T.n_psi, lo + batch);
+      pw_gather(P, T, lo, hi);
+      pw_eval(P, T, us.get(), &NP, lo, hi);
+    }
     P.phi.release();
-    t.gather_ms = tm.lap();
-    pw_eval(P, T, us.get(), &NP);
     P.psi.release();
-    t.eval_ms = tm.lap();
+    const double ge = tm.lap();
+    t.gather_ms = P.k_gather.ms();
+    t.eval_ms = ge - t.gather_ms;
   }
   const double D0 = tp.D0;
   direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get(), &P.k_direct);

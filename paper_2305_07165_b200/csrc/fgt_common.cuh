@@ -107,31 +107,33 @@ struct DBuf {
 };
 
 // CUDA-event pair bracketing one kernel launch (device time of that kernel alone).
+// Several begin/end intervals may be recorded; ms() returns their sum.
 struct KClock {
-  cudaEvent_t a = nullptr, b = nullptr;
-  bool used = false;
+  std::vector<cudaEvent_t> ev;
   void begin(cudaStream_t st) {
-    if (!a) {
-      FGT_CUDA(cudaEventCreate(&a));
-      FGT_CUDA(cudaEventCreate(&b));
-    }
+    cudaEvent_t a, b;
+    FGT_CUDA(cudaEventCreate(&a));
+    FGT_CUDA(cudaEventCreate(&b));
     FGT_CUDA(cudaEventRecord(a, st));
-    used = true;
+    ev.push_back(a);
+    ev.push_back(b);
   }
-  void end(cudaStream_t st) { FGT_CUDA(cudaEventRecord(b, st)); }
+  void end(cudaStream_t st) { FGT_CUDA(cudaEventRecord(ev.back(), st)); }
   double ms() const {
-    if (!used) return 0.0;
-    float v = 0.f;
-    FGT_CUDA(cudaEventSynchronize(b));
-    FGT_CUDA(cudaEventElapsedTime(&v, a, b));
-    return v;
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float v = 0.f;
+      FGT_CUDA(cudaEventSynchronize(ev[i + 1]));
+      FGT_CUDA(cudaEventElapsedTime(&v, ev[i], ev[i + 1]));
+      tot += v;
+    }
+    return tot;
   }
   KClock() = default;
   KClock(const KClock&) = delete;
   KClock& operator=(const KClock&) = delete;
   ~KClock() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
 };
 

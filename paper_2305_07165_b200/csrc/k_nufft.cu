@@ -560,7 +560,7 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     DBuf<int64_t> li(nbat, st);
     li.from_host(idx.data() + b0, nbat);
     DBuf<double> grid(nbat * GD, st);
-    const double* psi = P.psi.get();  // first stage reads psi[list[b]] through bidx
+    const double* psi = P.psi_view();  // first stage reads psi[list[b]] through bidx
     if (D == 1) {
       // grid[g] = Re sum_m Ee[g][m] psi[m]
       bgemm<true, true, true>(gemm(N.Ee.get(), n_f, 0, psi, 1, NF, grid.get(), 1, GD, G, 1, n_f, (int)nbat, nullptr, li.get()), st);

@@ -299,8 +299,8 @@ struct GatherArgs {
   const int64_t* coords;
   const double2* phase;   // (3, n_f)
   const double2* phi;
-  double2* psi;
-  int64_t NF;
+  double2* psi;   // batch-local output
+  int64_t NF, i0; // first psi index of the batch
   int n_f, l_c;
 };
 
@@ -310,7 +310,7 @@ template <int D>
 __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
   __shared__ int s_o[GATHER_MAXE][D];
   __shared__ int64_t s_slot[GATHER_MAXE];
-  const int64_t i = blockIdx.y;
+  const int64_t i = a.i0 + blockIdx.y;
   const int64_t T = a.psi_ids[i];
   const int64_t e0 = a.p_off[i];
   const int64_t ne64 = a.p_off[i + 1] - e0;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
       acc.x += p.x * f.x - p.y * f.y;
       acc.y += p.x * f.y + p.y * f.x;
     }
-    a.psi[(size_t)i * a.NF + e] = acc;
+    a.psi[(size_t)blockIdx.y * a.NF + e] = acc;
   }
 }
 
@@ -667,10 +667,12 @@ void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N) {
   else pw_form_impl<3>(P, T, N);
 }
 
-void pw_gather(PwDev& P, TreeDev& T) {
+void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   cudaStream_t st = T.st;
-  P.psi.alloc((size_t)T.n_psi * P.NF * 2, st);
-  if (T.n_psi == 0) return;
+  if (P.psi.size() < (size_t)(hi - lo) * P.NF * 2) P.psi.alloc((size_t)(hi - lo) * P.NF * 2, st);
+  P.psi_lo = lo;
+  P.psi_hi = hi;
+  if (hi == lo) return;
   GatherArgs ga;
   ga.psi_ids = T.psi_ids.get();
   ga.p_off = T.p_off.get();
@@ -682,9 +684,11 @@ void pw_gather(PwDev& P, TreeDev& T) {
   ga.phi = reinterpret_cast<const double2*>(P.phi.get());
   ga.psi = reinterpret_cast<double2*>(P.psi.get());
   ga.NF = P.NF;
+  ga.i0 = lo;
   ga.n_f = P.n_f;
   ga.l_c = T.l_c;
-  dim3 grid(grid_for(P.NF, 256, 256), (unsigned)T.n_psi);
+  FGT_REQUIRE(hi - lo <= 65535, FGT_ERANGE, "psi batch too large");
+  dim3 grid(grid_for(P.NF, 256, 256), (unsigned)(hi - lo));
   P.k_gather.begin(st);
   if (T.d == 1) gather_kernel<1><<<grid, 256, 0, st>>>(ga);
   else if (T.d == 2) gather_kernel<2><<<grid, 256, 0, st>>>(ga);
@@ -693,29 +697,29 @@ void pw_gather(PwDev& P, TreeDev& T) {
   P.k_gather.end(st);
 }
 
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N) {
-  if (T.n_psi == 0) return;
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi) {
+  if (hi == lo) return;
   cudaStream_t st = T.st;
   std::vector<int64_t> direct_list, spread_list;
   {
-    DBuf<int64_t> c(T.n_psi, st);
-    gather_counts_kernel<<<grid_for(T.n_psi, 256), 256, 0, st>>>(T.psi_ids.get(), T.n_psi, T.tgt_count.get(), c.get());
+    const int64_t n = hi - lo;
+    DBuf<int64_t> c(n, st);
+    gather_counts_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get() + lo, n, T.tgt_count.get(), c.get());
     FGT_LAUNCHED();
-    std::vector<int64_t> h(T.n_psi);
-    c.to_host(h.data(), T.n_psi);
+    std::vector<int64_t> h(n);
+    c.to_host(h.data(), n);
     FGT_CUDA(cudaStreamSynchronize(st));
-    P.n_tgt_psi = 0;
-    for (int64_t i = 0; i < T.n_psi; ++i) {
+    for (int64_t i = 0; i < n; ++i) {
       P.n_tgt_psi += h[i];
       if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) {
-        spread_list.push_back(i);
+        spread_list.push_back(lo + i);
         P.n_tgt_spread += h[i];
       } else {
-        direct_list.push_back(i);
+        direct_list.push_back(lo + i);
       }
     }
   }
-  P.n_spread_psi = (int64_t)spread_list.size();
+  P.n_spread_psi += (int64_t)spread_list.size();
   P.k_eval.begin(st);
   if (!spread_list.empty()) nufft_eval(*N, P, T, spread_list, u_sorted);
   if (direct_list.empty()) {
@@ -732,7 +736,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N) {
   ea.tgt_start = T.tgt_start.get();
   ea.tgt_count = T.tgt_count.get();
   ea.list = list_d.get();
-  ea.psi = reinterpret_cast<const double2*>(P.psi.get());
+  ea.psi = reinterpret_cast<const double2*>(P.psi_view());
   ea.u = u_sorted;
   ea.n_f = P.n_f;
   ea.R = (int)P.R;

@@ -13,7 +13,10 @@ struct PwDev {
   DBuf<double> w1d;    // (n_f) pre-multiplied 1-D weights (planewave.py:33-70)
   DBuf<double> phase;  // (3, n_f) complex: exp(+i m sc o side_lc), o = -1, 0, 1
   DBuf<double> phi;    // (n_dense, R, n_f) complex outgoing expansions
-  DBuf<double> psi;    // (n_psi, R, n_f) complex incoming expansions
+  DBuf<double> psi;    // (psi_hi - psi_lo, R, n_f) complex incoming expansions (one batch)
+  int64_t psi_lo = 0, psi_hi = 0;
+  // base pointer such that psi_view() + 2 * i * NF addresses psi box i of the batch
+  double* psi_view() const { return psi.get() - 2 * psi_lo * NF; }
   KClock k_form, k_gather, k_eval, k_direct;
   int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
   int64_t n_src_spread = 0, n_tgt_spread = 0;
@@ -29,9 +32,9 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
 // Form outgoing expansions of all P-boxes: type-1 exponential sums.
 void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N);
 // Diagonal translation phi -> psi over the P-lists.
-void pw_gather(PwDev& P, TreeDev& T);
+void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi);
 // Type-2 evaluation of psi at the targets of every psi box; u_sorted += Re(...).
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N);
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 // Continuous (box) FGT executor (k_volume.cu).
