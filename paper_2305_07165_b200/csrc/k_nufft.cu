@@ -62,13 +62,17 @@ __host__ __device__ __forceinline__ double es_kernel(double z, double beta) {
 constexpr int MAXW = 16;
 
 // ------------------------------------------------------------------ spreading
-// Pass 1 (one thread per point and axis): kernel weights of every source of the batch,
-// computed once: first tap a_k (0-based grid index) and w weights per axis, plus the
-// sort key (box, a_0).  Pass 2: points sorted by (box, a_0), so the points touching
-// grid plane p of a box (a_0 in [p-w+1, p]) form one contiguous range.  Pass 3: one warp
-// per (box, plane, point chunk) accumulates the plane in its own shared-memory buffer
-// (plain read-modify-write: lanes of one instruction hit distinct cells, no other warp
-// touches the buffer), then writes it out once.
+// Pass 1 (one thread per point): first tap a_k (0-based grid index) and the w kernel
+// weights of every axis, computed once, plus a sort key.  Pass 2: points sorted by the
+// key, so every job's points form one contiguous range:
+//   d = 3: key (box, a_0, a_1); job = (box, grid plane p), points with a_0 in [p-w+1, p];
+//   d = 2: key (box, a_0);      job = (box), the whole G x G grid;
+//   d = 1: key (box, a_0);      job = (box, cell p).
+// Pass 3 (d = 2, 3) spreads on the FP64 tensor cores: a point's contribution to a plane
+// is the rank-1 update c w1 (x) w2, so four points make one m8n8k4 DMMA per 8 x 8 tile;
+// one warp keeps its whole plane (NB x NB tiles) in registers -- no shared-memory
+// read-modify-write, no atomics.  Per group of 4 points only the tiles their taps touch
+// are issued (warp-uniform predicates).
 struct WeightArgs {
   const double* src;
   const double* q;
@@ -89,142 +93,228 @@ struct WeightArgs {
 template <int D>
 __global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
   const double s = a.sc * a.inv_delta, half = 0.5 * a.w, inv_half = 2.0 / a.w;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.npts * D;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / D;
-    const int k = (int)(t - i * D);
-    // batch box of point i
-    int64_t lo = 0, hi = a.nbat;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.npts;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = a.nbat;  // batch box of point i
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
       if (a.boff[mid] <= i) lo = mid; else hi = mid;
     }
     const int64_t box = a.dense_ids[a.slots[lo]];
     const int64_t sidx = a.src_start[box] + (i - a.boff[lo]);
-    const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
-    const double a0 = ceil(tt - half);
-    const int aa = max(0, min((int)a0 - a.gmin, a.G - a.w));
-    a.ai[i * D + k] = aa;
-    double* wp = a.wts + (i * D + k) * MAXW;
+    int aa[D];
 #pragma unroll
-    for (int o = 0; o < MAXW; ++o) wp[o] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
-    if (k == 0) {
-      a.qb[i] = a.q[sidx];
-      a.key[i] = ((uint32_t)lo << 8) | (uint32_t)aa;
+    for (int k = 0; k < D; ++k) {
+      const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
+      const double a0 = ceil(tt - half);
+      aa[k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
+      a.ai[i * D + k] = aa[k];
+      double* wp = a.wts + (i * D + k) * MAXW;
+#pragma unroll
+      for (int o = 0; o < MAXW; ++o) wp[o] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
     }
+    a.qb[i] = a.q[sidx];
+    a.key[i] = D == 3 ? (((uint32_t)lo << 16) | ((uint32_t)aa[0] << 8) | (uint32_t)aa[D > 1 ? 1 : 0])
+                      : (((uint32_t)lo << 8) | (uint32_t)aa[0]);
   }
 }
 
-// (box, plane) -> [lo, hi) of the sorted points whose first plane is in [p-w+1, p]
-__global__ void plane_ranges_kernel(const uint32_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
-                                    int w, int* __restrict__ range) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nbat * G;
+// job ranges in the sorted keys: d = 3 per (box, plane), d = 1 per (box, cell), d = 2 per box
+template <int D>
+__global__ void job_ranges_kernel(const uint32_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
+                                  int w, int* __restrict__ range) {
+  const int64_t njob = D == 2 ? nbat : nbat * G;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < njob;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = (uint32_t)(t / G), p = (uint32_t)(t % G);
-    const uint32_t k0 = (b << 8) | (uint32_t)max(0, (int)p - w + 1), k1 = ((b << 8) | p) + 1;
+    uint32_t k0, k1;
+    if (D == 2) {
+      k0 = (uint32_t)t << 8;
+      k1 = (uint32_t)(t + 1) << 8;
+    } else {
+      const uint32_t b = (uint32_t)(t / G), p = (uint32_t)(t % G);
+      const uint32_t plo = (uint32_t)max(0, (int)p - w + 1);
+      if (D == 3) {
+        k0 = (b << 16) | (plo << 8);
+        k1 = (b << 16) | ((p + 1) << 8);
+      } else {
+        k0 = (b << 8) | plo;
+        k1 = ((b << 8) | p) + 1;
+      }
+    }
     range[2 * t] = (int)lower_bound_dev(key, npts, k0);
     range[2 * t + 1] = (int)lower_bound_dev(key, npts, k1);
   }
 }
 
+// Sorted point records for the tile kernel: rw (n, 32) = [row-axis weights | column-axis
+// weights], rq (n) charge, ra (n, 4) first taps (a_0, a_1, a_2), rw0 (n, 16) axis-0 weights
+// (d = 3 plane factor).  One gather after the sort makes every job's staging a contiguous,
+// coalesced copy instead of a perm -> index -> weights pointer chase.
+template <int D>
+__global__ void sort_records_kernel(const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ wts,
+                                    const int* __restrict__ ai, const double* __restrict__ qb,
+                                    double* __restrict__ rw, double* __restrict__ rq, int* __restrict__ ra,
+                                    double* __restrict__ rw0) {
+  const int RA = D == 3 ? 1 : 0, CA = D == 3 ? 2 : 1;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 32;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t >> 5;
+    const int o = (int)(t & 31);
+    const int64_t i = perm[j];
+    rw[t] = wts[(i * D + (o < 16 ? RA : CA)) * MAXW + (o & 15)];
+    if (D == 3 && o < 16) rw0[j * 16 + o] = wts[(i * D) * MAXW + o];
+    if (o < 4) ra[j * 4 + o] = o < D ? ai[i * D + o] : 0;
+    if (o == 0) rq[j] = qb[i];
+  }
+}
+
 struct PlaneArgs {
-  const int4* jobs;       // (box*G + plane, first sorted point, count, scratch index or -1)
+  const int4* jobs;       // (job id, first sorted point, count, scratch index or -1)
   int njobs;
   const int64_t* perm;    // sorted position -> batch point
   const double* wts;
   const int* ai;
   const double* qb;
   double* grid;           // (nbat, G^D)
-  double* scratch;        // (nscratch, G^(D-1))
+  double* scratch;        // (nscratch, plane)
+  const double* rw;       // sorted records (tile kernel)
+  const double* rq;
+  const int* ra;
+  const double* rw0;
   int w, G;
 };
 
-template <int D, int NIT>
-__global__ void __launch_bounds__(128) spread_plane_kernel(PlaneArgs a) {
-  extern __shared__ double sm[];
+// staged weights per point: w1 at [0, 16), w2 at [20, 36); row stride 40 doubles (80 words,
+// = 16 mod 32) so the 4 point rows read by one fragment load fall on 2 disjoint bank sets
+constexpr int TILE_RS = 40;
+constexpr int TILE_W2 = 20;
+
+template <int D, int NB>
+__global__ void __launch_bounds__(128) spread_tile_kernel(PlaneArgs a) {
+  __shared__ double s_w[4][32 * TILE_RS];
+  __shared__ double s_c[4][32];
+  __shared__ int s_a1[4][32], s_a2[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int job = blockIdx.x * 4 + warp;
-  if (job >= a.njobs) return;  // warp-uniform; no block barriers below
+  if (job >= a.njobs) return;  // warp-uniform; only __syncwarp below
   const int G = a.G, w = a.w;
-  const int plane = D == 3 ? G * G : (D == 2 ? G : 1);
-  double* pl = sm + (size_t)warp * plane;
-  for (int e = lane; e < plane; e += 32) pl[e] = 0.0;
-  __syncwarp();
   const int4 jb = a.jobs[job];
-  const int p = jb.x % G;
-  // this lane's taps: (o1, o2) = divmod(lane + 32 it, w), it < NIT (w^2 <= 32 NIT)
-  int o1s[NIT], o2s[NIT];
+  const int p = D == 3 ? jb.x % G : 0;
+  const int RA = D == 3 ? 1 : 0, CA = D == 3 ? 2 : 1;  // row / column axes of the plane
+  double* w1 = s_w[warp];
+  double* w2 = s_w[warp] + TILE_W2;
+  double acc[NB][NB][2];
 #pragma unroll
-  for (int it = 0; it < NIT; ++it) {
-    const int idx = lane + 32 * it;
-    const bool ok = D == 3 ? idx < w * w : (D == 2 ? lane < w : lane == 0);
-    o1s[it] = ok ? (D == 3 ? idx / w : idx) : -1;
-    o2s[it] = ok && D == 3 ? idx % w : 0;
-  }
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int t = 0; t < NB; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
   const int jend = jb.y + jb.z;
   for (int base = jb.y; base < jend; base += 32) {
     const int cnt = min(32, jend - base);
-    // lane-parallel fetch of the per-point scalars of 32 points
-    int64_t il = 0;
-    double cl = 0.0;
-    int a1l = 0, a2l = 0;
+    __syncwarp();
     if (lane < cnt) {
-      il = a.perm[base + lane];
-      const int a0 = a.ai[il * D];
-      cl = a.qb[il] * a.wts[(il * D) * MAXW + (p - a0)];
-      if (D >= 2) a1l = a.ai[il * D + 1];
-      if (D == 3) a2l = a.ai[il * D + 2];
+      const int64_t j = base + lane;
+      const int4 r = *reinterpret_cast<const int4*>(a.ra + 4 * j);
+      double c = a.rq[j];
+      if (D == 3) c *= a.rw0[j * 16 + (p - r.x)];
+      s_c[warp][lane] = c;
+      s_a1[warp][lane] = D == 3 ? r.y : r.x;
+      s_a2[warp][lane] = D == 3 ? r.z : r.y;
     }
-    if (D == 1) {
-      double sum = cl;
+    // stage the row / column weights of the 32 points: a contiguous copy
+    {
+      const double* src = a.rw + (int64_t)base * 32;
+      double v[32];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      if (lane == 0) pl[0] += sum;
-      continue;
+      for (int it = 0; it < 32; ++it) v[it] = it < cnt ? src[it * 32 + lane] : 0.0;
+      const int o = lane;
+#pragma unroll
+      for (int it = 0; it < 32; ++it)
+        if (it < cnt) w1[it * TILE_RS + (o < 16 ? o : TILE_W2 + o - 16)] = v[it];
     }
-    auto wload = [&](int jj) {
-      const int64_t i = __shfl_sync(0xffffffffu, il, jj);
-      return (D == 3 && lane >= 16) ? a.wts[(i * D + 2) * MAXW + (lane - 16)]
-                                    : a.wts[(i * D + 1) * MAXW + (lane & 15)];
-    };
-    double wnext = wload(0);
-    for (int jj = 0; jj < cnt; ++jj) {
-      const double wv = wnext;
-      if (jj + 1 < cnt) wnext = wload(jj + 1);  // prefetch the next point's weights
-      const double c = __shfl_sync(0xffffffffu, cl, jj);
-      const int a1 = __shfl_sync(0xffffffffu, a1l, jj);
-      const int a2 = __shfl_sync(0xffffffffu, a2l, jj);
-      double val[NIT], cur[NIT];
-      int off[NIT];
+    __syncwarp();
+    for (int g = 0; 4 * g < cnt; ++g) {
+      const int j = 4 * g + (lane & 3);
+      const bool valid = j < cnt;
+      const double cj = valid ? s_c[warp][j] : 0.0;
+      const int a1 = valid ? s_a1[warp][j] : 0, a2 = valid ? s_a2[warp][j] : 0;
+      // rows / columns the group touches (warp-uniform)
+      int rlo = 1 << 20, rhi = -1, clo = 1 << 20, chi = -1;
 #pragma unroll
-      for (int it = 0; it < NIT; ++it) {
-        const int o1 = max(o1s[it], 0);
-        const double w1 = __shfl_sync(0xffffffffu, wv, o1);
-        const double w2 = D == 3 ? __shfl_sync(0xffffffffu, wv, 16 + o2s[it]) : 1.0;
-        val[it] = c * w1 * w2;
-        off[it] = D == 3 ? (a1 + o1) * G + a2 + o2s[it] : a1 + o1;
+      for (int k = 0; k < 4; ++k) {
+        if (4 * g + k < cnt) {
+          rlo = min(rlo, s_a1[warp][4 * g + k]);
+          rhi = max(rhi, s_a1[warp][4 * g + k] + w - 1);
+          clo = min(clo, s_a2[warp][4 * g + k]);
+          chi = max(chi, s_a2[warp][4 * g + k] + w - 1);
+        }
+      }
+      const int bl = rlo >> 3, bh = rhi >> 3, tl = clo >> 3, th = chi >> 3;
+      double A[NB], B[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int d = 8 * b + (lane >> 2) - a1;
+        A[b] = (valid && (unsigned)d < (unsigned)w) ? cj * w1[j * TILE_RS + d] : 0.0;
+        const int e = 8 * b + (lane >> 2) - a2;
+        B[b] = (valid && (unsigned)e < (unsigned)w) ? w2[j * TILE_RS + e] : 0.0;
       }
 #pragma unroll
-      for (int it = 0; it < NIT; ++it) cur[it] = o1s[it] >= 0 ? pl[off[it]] : 0.0;
+      for (int b = 0; b < NB; ++b) {
+        if (b < bl || b > bh) continue;
 #pragma unroll
-      for (int it = 0; it < NIT; ++it)
-        if (o1s[it] >= 0) pl[off[it]] = cur[it] + val[it];
-      __syncwarp();
+        for (int t = 0; t < NB; ++t) {
+          if (t < tl || t > th) continue;
+          dmma2(acc[b][t][0], acc[b][t][1], A[b], B[t]);
+        }
+      }
     }
   }
-  __syncwarp();
-  const int64_t GD = (int64_t)plane * G;
-  const int b = jb.x / G;
-  double* out = jb.w < 0 ? a.grid + (int64_t)b * GD + (int64_t)p * plane : a.scratch + (int64_t)jb.w * plane;
-  for (int e = lane; e < plane; e += 32) out[e] = pl[e];
+  // write the plane: lane holds cells (8b + lane/4, 8t + 2 (lane%4) + {0, 1})
+  const int64_t plane = (int64_t)G * G;
+  const int bx = D == 3 ? jb.x / G : jb.x;
+  double* out = jb.w < 0 ? a.grid + (int64_t)bx * plane * (D == 3 ? G : 1) + (int64_t)p * plane
+                         : a.scratch + (int64_t)jb.w * plane;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int r = 8 * b + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2) {
+        const int c = 8 * t + 2 * (lane & 3) + i2;
+        if (r < G && c < G) out[(int64_t)r * G + c] = acc[b][t][i2];
+      }
+    }
+  }
+}
+
+// d = 1: one warp per (box, cell) job sums c w0[p - a0] over its points
+__global__ void __launch_bounds__(128) spread_line_kernel(PlaneArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * 4 + warp;
+  if (job >= a.njobs) return;
+  const int4 jb = a.jobs[job];
+  const int G = a.G, p = jb.x % G;
+  double sum = 0.0;
+  for (int j = jb.y + lane; j < jb.y + jb.z; j += 32) {
+    const int64_t i = a.perm[j];
+    sum += a.qb[i] * a.wts[i * MAXW + (p - a.ai[i])];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if (lane == 0) {
+    if (jb.w < 0) a.grid[(int64_t)(jb.x / G) * G + p] = sum;
+    else a.scratch[jb.w] = sum;
+  }
 }
 
 __global__ void plane_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red,
-                                    int plane, int G, double* __restrict__ grid) {
-  const int4 r = red[blockIdx.y];  // (box*G + plane, first scratch, count, -)
-  const int64_t GD = (int64_t)plane * G;
-  double* out = grid + (int64_t)(r.x / G) * GD + (int64_t)(r.x % G) * plane;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < plane; e += gridDim.x * blockDim.x) {
+                                    int64_t plane, int64_t job_stride, double* __restrict__ grid) {
+  const int4 r = red[blockIdx.y];  // (job id, first scratch, count, -); job id -> offset job*plane
+  double* out = grid + (int64_t)r.x * plane;
+  (void)job_stride;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < plane;
+       e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int t = 0; t < r.z; ++t) s += scratch[(int64_t)(r.y + t) * plane + e];
     out[e] = s;
@@ -342,7 +432,9 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.n_f = n_f;
   N.tol = tol;
   N.X = X;
-  N.w = (int)std::ceil(std::log10(1.0 / tol)) + 1;
+  // w = ceil(log10(1/tol)) + 1 taps per axis; the 1e-9 guard keeps tol = 1e-10 at 11
+  // taps instead of 12 when log10 lands a hair above an integer
+  N.w = (int)std::ceil(std::log10(1.0 / tol) - 1e-9) + 1;
   N.w = std::max(2, std::min(N.w, MAXW));
   N.beta = 2.30 * N.w;
   N.Delta = M_PI / n_f;  // 2 pi / (sigma n_f), sigma = 2
@@ -410,29 +502,13 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   T.dense_ids.to_host(dense.data(), T.n_dense);
   T.src_count.to_host(scount.data(), T.nb);
   FGT_CUDA(cudaStreamSynchronize(st));
-  const size_t psmem = 4 * (size_t)plane * sizeof(double);
-  FGT_REQUIRE(psmem <= 227 * 1024, FGT_ERANGE, "spreading plane does not fit in shared memory");
-  FGT_REQUIRE(G < 256, FGT_ERANGE, "spreading grid too large");
-  const int nit = D == 3 ? (w * w + 31) / 32 : 1;
-  FGT_REQUIRE(nit <= 8, FGT_ERANGE, "spreading width too large");
-  auto plane_kernel = [&](int k) -> void (*)(PlaneArgs) {
-    switch (k) {
-      case 1: return spread_plane_kernel<D, 1>;
-      case 2: return spread_plane_kernel<D, 2>;
-      case 3: return spread_plane_kernel<D, 3>;
-      case 4: return spread_plane_kernel<D, 4>;
-      case 5: return spread_plane_kernel<D, 5>;
-      case 6: return spread_plane_kernel<D, 6>;
-      case 7: return spread_plane_kernel<D, 7>;
-      default: return spread_plane_kernel<D, 8>;
-    }
-  };
-  void (*pk)(PlaneArgs) = plane_kernel(nit);
-  FGT_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  FGT_REQUIRE(G < 256 && G <= 64, FGT_ERANGE, "spreading grid too large (G > 64)");
   // batches bounded by ~1.5 GB of grid + stage buffers + per-point weights
   const int64_t per_box = GD * 8 + (D >= 2 ? plane * n_f * 16 : 0) + (D == 3 ? (int64_t)G * n_f * n_f * 16 : 0);
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
-  const int CH = 1024;  // points per plane job
+  const int CH = D == 2 ? 4096 : 2048;  // points per job
+  // grid cells written by one job: a plane (d = 3), the whole grid (d = 2), a cell (d = 1)
+  const int64_t job_cells = D == 3 ? plane : (D == 2 ? GD : 1);
   CubTmpBuf tmp;
   size_t b0 = 0;
   while (b0 < slots.size()) {
@@ -473,35 +549,51 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     wa.w = w;
     wa.gmin = N.gmin;
     wa.G = G;
-    spread_weights_kernel<D><<<grid_for(npts * D, 256), 256, 0, st>>>(wa);
+    spread_weights_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(wa);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
-    int bits = 8;
-    while (((int64_t)1 << (bits - 8)) < nbat) ++bits;
+    int bits = D == 3 ? 16 : 8;
+    while (((int64_t)1 << (bits - (D == 3 ? 16 : 8))) < nbat) ++bits;
     sort_pairs_u32(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
-    DBuf<int> range(2 * nbat * G, st);
-    plane_ranges_kernel<<<grid_for(nbat * G, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
+    const int64_t njob = D == 2 ? nbat : nbat * G;
+    DBuf<int> range(2 * njob, st);
+    job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
     FGT_LAUNCHED();
-    std::vector<int> hr(2 * nbat * G);
+    std::vector<int> hr(2 * njob);
     range.to_host(hr.data(), hr.size());
     FGT_CUDA(cudaStreamSynchronize(st));
     std::vector<int4> jobs, reds;
     int nscr = 0;
-    for (int64_t bp = 0; bp < nbat * G; ++bp) {
-      const int lo = hr[2 * bp], n = hr[2 * bp + 1] - lo;
+    for (int64_t jid = 0; jid < njob; ++jid) {
+      const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
       if (n <= CH) {
-        jobs.push_back(make_int4((int)bp, lo, n, -1));
+        jobs.push_back(make_int4((int)jid, lo, n, -1));
       } else {
         const int nc = (n + CH - 1) / CH;
-        reds.push_back(make_int4((int)bp, nscr, nc, 0));
-        for (int c = 0; c < nc; ++c) jobs.push_back(make_int4((int)bp, lo + c * CH, std::min(CH, n - c * CH), nscr++));
+        reds.push_back(make_int4((int)jid, nscr, nc, 0));
+        for (int c = 0; c < nc; ++c) jobs.push_back(make_int4((int)jid, lo + c * CH, std::min(CH, n - c * CH), nscr++));
       }
     }
     DBuf<int4> jobs_d(jobs.size(), st), reds_d(reds.size(), st);
     jobs_d.from_host(jobs.data(), jobs.size());
     if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
-    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * plane, st);
+    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * job_cells, st);
+    DBuf<double> rw, rq, rw0;
+    DBuf<int> ra;
+    if (D >= 2) {
+      rw.alloc(npts * 32, st);
+      rq.alloc(npts, st);
+      ra.alloc(npts * 4, st);
+      if (D == 3) rw0.alloc(npts * 16, st);
+      sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
+          perm.get(), npts, wts.get(), ai.get(), qb.get(), rw.get(), rq.get(), ra.get(), rw0.get());
+      FGT_LAUNCHED();
+    }
     PlaneArgs pa;
+    pa.rw = rw.get();
+    pa.rq = rq.get();
+    pa.ra = ra.get();
+    pa.rw0 = rw0.get();
     pa.jobs = jobs_d.get();
     pa.njobs = (int)jobs.size();
     pa.perm = perm.get();
@@ -512,11 +604,22 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     pa.scratch = scratch.get();
     pa.w = w;
     pa.G = G;
-    pk<<<(unsigned)((jobs.size() + 3) / 4), 128, psmem, st>>>(pa);
+    const unsigned nblk = (unsigned)((jobs.size() + 3) / 4);
+    if constexpr (D == 1) {
+      spread_line_kernel<<<nblk, 128, 0, st>>>(pa);
+    } else {
+      const int NB = (G + 7) / 8;
+      switch (NB) {
+#define FGT_TILE(NBV) case NBV: spread_tile_kernel<D, NBV><<<nblk, 128, 0, st>>>(pa); break;
+        FGT_TILE(1) FGT_TILE(2) FGT_TILE(3) FGT_TILE(4) FGT_TILE(5) FGT_TILE(6) FGT_TILE(7) FGT_TILE(8)
+#undef FGT_TILE
+        default: throw Error(FGT_ERANGE, "spreading grid too large");
+      }
+    }
     FGT_LAUNCHED();
     if (!reds.empty()) {
-      plane_reduce_kernel<<<dim3(grid_for(plane, 256, 8), (unsigned)reds.size()), 256, 0, st>>>(
-          scratch.get(), reds_d.get(), (int)plane, G, grid.get());
+      plane_reduce_kernel<<<dim3(grid_for(job_cells, 256, 16), (unsigned)reds.size()), 256, 0, st>>>(
+          scratch.get(), reds_d.get(), job_cells, 0, grid.get());
       FGT_LAUNCHED();
     }
     scratch.release();
