@@ -90,11 +90,16 @@ struct WeightArgs {
   int w, gmin, G;
 };
 
+// one thread per (point, axis, half of the taps): 6 independent exp/sqrt chains per point
 template <int D>
 __global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
   const double s = a.sc * a.inv_delta, half = 0.5 * a.w, inv_half = 2.0 / a.w;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.npts;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.npts * D * 2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int hsel = (int)(t & 1);
+    const int64_t ik = t >> 1;
+    const int64_t i = ik / D;
+    const int k = (int)(ik - i * D);
     int64_t lo = 0, hi = a.nbat;  // batch box of point i
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
@@ -102,20 +107,31 @@ __global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
     }
     const int64_t box = a.dense_ids[a.slots[lo]];
     const int64_t sidx = a.src_start[box] + (i - a.boff[lo]);
-    int aa[D];
+    const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
+    const double a0 = ceil(tt - half);
+    double* wp = a.wts + (i * D + k) * MAXW + hsel * (MAXW / 2);
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
-      const double a0 = ceil(tt - half);
-      aa[k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
-      a.ai[i * D + k] = aa[k];
-      double* wp = a.wts + (i * D + k) * MAXW;
-#pragma unroll
-      for (int o = 0; o < MAXW; ++o) wp[o] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
+    for (int o2 = 0; o2 < MAXW / 2; ++o2) {
+      const int o = hsel * (MAXW / 2) + o2;
+      wp[o2] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
     }
-    a.qb[i] = a.q[sidx];
-    a.key[i] = D == 3 ? (((uint32_t)lo << 16) | ((uint32_t)aa[0] << 8) | (uint32_t)aa[D > 1 ? 1 : 0])
-                      : (((uint32_t)lo << 8) | (uint32_t)aa[0]);
+    if (hsel == 0) {
+      a.ai[i * D + k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
+      if (k == 0) {
+        a.qb[i] = a.q[sidx];
+        a.key[i] = (uint32_t)lo;  // box part; spread_keys_kernel adds the taps
+      }
+    }
+  }
+}
+
+template <int D>
+__global__ void spread_keys_kernel(uint32_t* __restrict__ key, const int* __restrict__ ai, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = key[i];
+    key[i] = D == 3 ? ((b << 16) | ((uint32_t)ai[i * D] << 8) | (uint32_t)ai[i * D + 1])
+                    : ((b << 8) | (uint32_t)ai[i * D]);
   }
 }
 
@@ -549,7 +565,9 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     wa.w = w;
     wa.gmin = N.gmin;
     wa.G = G;
-    spread_weights_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(wa);
+    spread_weights_kernel<D><<<grid_for(npts * D * 2, 256), 256, 0, st>>>(wa);
+    FGT_LAUNCHED();
+    spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
     int bits = D == 3 ? 16 : 8;

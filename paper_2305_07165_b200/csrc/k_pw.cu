@@ -367,10 +367,70 @@ struct EvalArgs {
 constexpr int EVAL_TB = 32;
 constexpr int EVAL_MT = 4;
 
+// One pass over the box's modes for up to 8*MTP targets whose phase tables are in etab;
+// per-warp partial sums go to s_u[warp][target].  MTP is the number of 8-target m-tiles
+// actually used, fixed at compile time so the last (partial) pass issues no idle DMMAs.
+template <int D, int NT, int MTP>
+__device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, const double2* __restrict__ psi,
+                                          double* __restrict__ s_u, int R, int n_f, int ksteps) {
+  constexpr int TB = EVAL_TB, NFP = NT * 8, RS = NFP + 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int ntiles = (R + 7) / 8;
+  double part[MTP];
+#pragma unroll
+  for (int mt = 0; mt < MTP; ++mt) part[mt] = 0.0;
+  for (int nt = warp; nt < ntiles; nt += nwarps) {
+    double acc[MTP][4];
+#pragma unroll
+    for (int mt = 0; mt < MTP; ++mt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[mt][e] = 0.0;
+    const int rb = nt * 8 + (lane >> 2);
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const int c = kk * 4 + (lane & 3);
+      double2 B = make_double2(0.0, 0.0);
+      if (rb < R && c < n_f) B = psi[(size_t)rb * n_f + c];
+      double2 A[MTP];
+#pragma unroll
+      for (int mt = 0; mt < MTP; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
+#pragma unroll
+      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][0], acc[mt][1], A[mt].x, B.x);
+#pragma unroll
+      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].x, B.y);
+#pragma unroll
+      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][0], acc[mt][1], -A[mt].y, B.y);
+#pragma unroll
+      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].y, B.x);
+    }
+#pragma unroll
+    for (int mt = 0; mt < MTP; ++mt) {
+      const int j = mt * 8 + (lane >> 2);
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2) {
+        const int r = nt * 8 + 2 * (lane & 3) + i2;
+        if (r >= R) continue;
+        double2 f = make_double2(1.0, 0.0);
+        if (D == 2) f = etab[(0 * TB + j) * RS + r];
+        if (D == 3) f = cmul(etab[(0 * TB + j) * RS + r / n_f], etab[(1 * TB + j) * RS + r % n_f]);
+        part[mt] += acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < MTP; ++mt) {
+    double v = part[mt];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if ((lane & 3) == 0) s_u[warp * TB + mt * 8 + (lane >> 2)] = v;
+  }
+}
+
 template <int D, int NT>
 __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   extern __shared__ double2 sm[];
-  constexpr int TB = EVAL_TB, MT = EVAL_MT, NFP = NT * 8, RS = NFP + 4;
+  constexpr int TB = EVAL_TB, NFP = NT * 8, RS = NFP + 4;
+  static_assert(EVAL_MT == 4, "eval passes are dispatched for 1..4 m-tiles");
   double2* etab = sm;
   double* s_u = reinterpret_cast<double*>(etab + D * TB * RS);
   const int64_t i = a.list[blockIdx.x];
@@ -380,66 +440,22 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   double ctr[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) ctr[k] = a.center[T * D + k];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int n_f = a.n_f, R = a.R;
-  const int ntiles = (R + 7) / 8;
   const double2* psi = a.psi + (size_t)i * R * n_f;
-
   for (int p0 = 0; p0 < ntg; p0 += TB) {
     const int cnt = min(TB, ntg - p0);
     __syncthreads();
     build_etab<D>(etab, TB, NFP, RS, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
     __syncthreads();
-    double part[MT];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) part[mt] = 0.0;
-    for (int nt = warp; nt < ntiles; nt += nwarps) {
-      double acc[MT][4];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[mt][e] = 0.0;
-      const int rb = nt * 8 + (lane >> 2);
-      for (int kk = 0; kk < a.ksteps; ++kk) {
-        const int c = kk * 4 + (lane & 3);
-        double2 B = make_double2(0.0, 0.0);
-        if (rb < R && c < n_f) B = psi[(size_t)rb * n_f + c];
-        double2 A[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], A[mt].x, B.x);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].x, B.y);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], -A[mt].y, B.y);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].y, B.x);
-      }
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int j = mt * 8 + (lane >> 2);
-#pragma unroll
-        for (int i2 = 0; i2 < 2; ++i2) {
-          const int r = nt * 8 + 2 * (lane & 3) + i2;
-          if (r >= R) continue;
-          double2 f = make_double2(1.0, 0.0);
-          if (D == 2) f = etab[(0 * TB + j) * RS + r];
-          if (D == 3) f = cmul(etab[(0 * TB + j) * RS + r / n_f], etab[(1 * TB + j) * RS + r % n_f]);
-          part[mt] += acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y;
-        }
-      }
-    }
-    // deterministic cross-warp sum: per-warp partials, then a fixed-order reduction
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      double v = part[mt];
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      if ((lane & 3) == 0) s_u[warp * TB + mt * 8 + (lane >> 2)] = v;
+    switch ((cnt + 7) >> 3) {
+      case 1: eval_pass<D, NT, 1>(etab, psi, s_u, R, n_f, a.ksteps); break;
+      case 2: eval_pass<D, NT, 2>(etab, psi, s_u, R, n_f, a.ksteps); break;
+      case 3: eval_pass<D, NT, 3>(etab, psi, s_u, R, n_f, a.ksteps); break;
+      default: eval_pass<D, NT, 4>(etab, psi, s_u, R, n_f, a.ksteps); break;
     }
     __syncthreads();
+    // deterministic cross-warp sum in a fixed order
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < nwarps; ++w) s += s_u[w * TB + t];
