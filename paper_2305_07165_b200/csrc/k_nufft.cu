@@ -205,64 +205,93 @@ struct PlaneArgs {
 constexpr int TILE_RS = 40;
 constexpr int TILE_W2 = 20;
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int TILE_BUF = 32 * TILE_RS;                  // doubles per staged batch
+constexpr size_t TILE_SMEM = 4 * (2 * TILE_BUF * sizeof(double) + 32 * (sizeof(double) + 2 * sizeof(int)));
+
 template <int D, int NB>
-__global__ void __launch_bounds__(128) spread_tile_kernel(PlaneArgs a) {
-  __shared__ double s_w[4][32 * TILE_RS];
-  __shared__ double s_c[4][32];
-  __shared__ int s_a1[4][32], s_a2[4][32];
+__global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
+  extern __shared__ double tsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wbuf = tsm + (size_t)warp * 2 * TILE_BUF;             // 2 staged batches
+  double* s_c = tsm + 4 * 2 * TILE_BUF + warp * 32;
+  int* s_a1 = reinterpret_cast<int*>(tsm + 4 * 2 * TILE_BUF + 4 * 32) + warp * 64;
+  int* s_a2 = s_a1 + 32;
   const int job = blockIdx.x * 4 + warp;
   if (job >= a.njobs) return;  // warp-uniform; only __syncwarp below
   const int G = a.G, w = a.w;
   const int4 jb = a.jobs[job];
   const int p = D == 3 ? jb.x % G : 0;
-  const int RA = D == 3 ? 1 : 0, CA = D == 3 ? 2 : 1;  // row / column axes of the plane
-  double* w1 = s_w[warp];
-  double* w2 = s_w[warp] + TILE_W2;
   double acc[NB][NB][2];
 #pragma unroll
   for (int b = 0; b < NB; ++b)
 #pragma unroll
     for (int t = 0; t < NB; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
   const int jend = jb.y + jb.z;
-  for (int base = jb.y; base < jend; base += 32) {
-    const int cnt = min(32, jend - base);
-    __syncwarp();
+  const int nbatch = (jb.z + 31) / 32;
+  // lane layout of one staged weight row: w1 -> [0, 16), w2 -> [TILE_W2, TILE_W2 + 16)
+  const int dst_off = lane < 16 ? lane : TILE_W2 + lane - 16;
+  auto issue = [&](int bi) {
+    const int base = jb.y + 32 * bi, cnt = min(32, jend - base);
+    double* dst = wbuf + (bi & 1) * TILE_BUF;
+    const double* src = a.rw + (int64_t)base * 32 + lane;
+    for (int it = 0; it < cnt; ++it) cp_async8(dst + it * TILE_RS + dst_off, src + it * 32);
+    cp_async_commit();
+  };
+  // per-point scalars of a batch, lane-parallel, kept in registers until published
+  double nc = 0.0;
+  int na1 = 0, na2 = 0;
+  auto fetch = [&](int bi) {
+    const int base = jb.y + 32 * bi, cnt = min(32, jend - base);
     if (lane < cnt) {
       const int64_t j = base + lane;
       const int4 r = *reinterpret_cast<const int4*>(a.ra + 4 * j);
       double c = a.rq[j];
       if (D == 3) c *= a.rw0[j * 16 + (p - r.x)];
-      s_c[warp][lane] = c;
-      s_a1[warp][lane] = D == 3 ? r.y : r.x;
-      s_a2[warp][lane] = D == 3 ? r.z : r.y;
+      nc = c;
+      na1 = D == 3 ? r.y : r.x;
+      na2 = D == 3 ? r.z : r.y;
     }
-    // stage the row / column weights of the 32 points: a contiguous copy
-    {
-      const double* src = a.rw + (int64_t)base * 32;
-      double v[32];
-#pragma unroll
-      for (int it = 0; it < 32; ++it) v[it] = it < cnt ? src[it * 32 + lane] : 0.0;
-      const int o = lane;
-#pragma unroll
-      for (int it = 0; it < 32; ++it)
-        if (it < cnt) w1[it * TILE_RS + (o < 16 ? o : TILE_W2 + o - 16)] = v[it];
+  };
+  issue(0);
+  fetch(0);
+  for (int bi = 0; bi < nbatch; ++bi) {
+    const int cnt = min(32, jend - (jb.y + 32 * bi));
+    __syncwarp();
+    s_c[lane] = nc;
+    s_a1[lane] = na1;
+    s_a2[lane] = na2;
+    if (bi + 1 < nbatch) {
+      issue(bi + 1);
+      fetch(bi + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncwarp();
+    const double* w1 = wbuf + (bi & 1) * TILE_BUF;
+    const double* w2 = w1 + TILE_W2;
     for (int g = 0; 4 * g < cnt; ++g) {
       const int j = 4 * g + (lane & 3);
       const bool valid = j < cnt;
-      const double cj = valid ? s_c[warp][j] : 0.0;
-      const int a1 = valid ? s_a1[warp][j] : 0, a2 = valid ? s_a2[warp][j] : 0;
+      const double cj = valid ? s_c[j] : 0.0;
+      const int a1 = valid ? s_a1[j] : 0, a2 = valid ? s_a2[j] : 0;
       // rows / columns the group touches (warp-uniform)
       int rlo = 1 << 20, rhi = -1, clo = 1 << 20, chi = -1;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (4 * g + k < cnt) {
-          rlo = min(rlo, s_a1[warp][4 * g + k]);
-          rhi = max(rhi, s_a1[warp][4 * g + k] + w - 1);
-          clo = min(clo, s_a2[warp][4 * g + k]);
-          chi = max(chi, s_a2[warp][4 * g + k] + w - 1);
+          rlo = min(rlo, s_a1[4 * g + k]);
+          rhi = max(rhi, s_a1[4 * g + k] + w - 1);
+          clo = min(clo, s_a2[4 * g + k]);
+          chi = max(chi, s_a2[4 * g + k] + w - 1);
         }
       }
       const int bl = rlo >> 3, bh = rhi >> 3, tl = clo >> 3, th = chi >> 3;
@@ -628,7 +657,11 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     } else {
       const int NB = (G + 7) / 8;
       switch (NB) {
-#define FGT_TILE(NBV) case NBV: spread_tile_kernel<D, NBV><<<nblk, 128, 0, st>>>(pa); break;
+#define FGT_TILE(NBV)                                                                          \
+  case NBV:                                                                                    \
+    FGT_CUDA(cudaFuncSetAttribute(spread_tile_kernel<D, NBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TILE_SMEM)); \
+    spread_tile_kernel<D, NBV><<<nblk, 128, TILE_SMEM, st>>>(pa);                              \
+    break;
         FGT_TILE(1) FGT_TILE(2) FGT_TILE(3) FGT_TILE(4) FGT_TILE(5) FGT_TILE(6) FGT_TILE(7) FGT_TILE(8)
 #undef FGT_TILE
         default: throw Error(FGT_ERANGE, "spreading grid too large");

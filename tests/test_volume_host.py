@@ -1,0 +1,67 @@
+"""CPU tests of the volume FGT host side (no GPU): Alg 3 tree vs the reference fixtures,
+the 1-D tables vs the oracle, and the plan's lists / flags vs the oracle's."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import volume as ov
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def sigma_f(d):
+    C = np.array([[0.1, -0.05, 0.02][:d], [-0.2, 0.15, -0.1][:d]])
+    W, A = [0.05, 0.1], [1.0, 0.7]
+    return lambda p: sum(a * np.exp(-np.sum((p - c) ** 2, axis=-1) / w ** 2) for c, w, a in zip(C, W, A))
+
+
+@pytest.mark.parametrize("d,k,eps", [(2, 10, 1e-9), (3, 6, 1e-7)])
+def test_product_density_tree_vs_reference(d, k, eps):
+    from paper_2305_07165_b200 import volume as pv
+    g = np.load(os.path.join(GOLD, f"dtree_{d}d.npz"))
+    t, vals, coeffs = pv.build_density_tree(sigma_f(d), d, k, eps)
+    for f in ("level", "parent", "children", "coords", "is_leaf"):
+        assert np.array_equal(getattr(t, f), g[f]), f
+    V = np.stack([vals[b] for b in g["leaves"]]).reshape(len(g["leaves"]), -1)
+    assert np.allclose(V.sum(axis=1), g["vsum"], rtol=1e-13, atol=1e-13)
+    b0 = int(g["leaves"][0])
+    assert np.allclose(pv.apply_per_axis(pv.LegendreBasis(k).pol_to_val, coeffs[b0], d), vals[b0])
+
+
+def test_refill_interpolate_rejected():
+    from paper_2305_07165_b200 import volume as pv
+    with pytest.raises(ValueError):
+        pv.build_density_tree(sigma_f(2), 2, 6, 1e-6, refill="interpolate")
+
+
+def test_moment_tables_match_oracle():
+    from paper_2305_07165_b200 import volume as pv
+    t = np.linspace(-3, 3, 61)
+    for lam in (1 / 64, 0.1, 0.64, 2.0):
+        a, b = pv.gauss_moment_J(lam, 15, t), ov.gauss_J(lam, 15, t)
+        assert np.max(np.abs(a - b)) < 1e-12 * lam
+    tt = np.linspace(-60, 60, 121)
+    assert np.max(np.abs(pv.fourier_moment_I(20, tt) - ov.fourier_I(20, tt))) < 1e-15
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+def test_box_plan_lists_match_oracle(periodic):
+    from paper_2305_07165_b200 import volume as pv
+    d, k, delta, eps = 2, 8, 1e-4, 1e-8
+    # constant-plus-bump density: leaves at coarse levels give direct pairs as well
+    dens = lambda p: 0.3 + sigma_f(d)(p)  # noqa: E731
+    t, vals, _ = pv.build_density_tree(dens, d, k, 1e-9, periodic=periodic)
+    plan = pv.BoxPlan(t, delta, eps, k, periodic)
+    to = ov.density_tree(dens, d, k, 1e-9, periodic=periodic)
+    f, pw_pairs, d_pairs = ov.box_lists(to, plan.l_c)
+    assert plan.n_pw == int(f.sum())
+    assert plan.n_gather_pairs == len(pw_pairs)
+    leaves = np.nonzero(to.is_leaf)[0]
+    slot = {int(b): i for i, b in enumerate(leaves)}
+    want = sorted((slot[T], slot[S]) for T, S, _ in d_pairs)
+    got = sorted(zip(plan.d_tgt.tolist(), plan.d_src.tolist()))
+    assert got == want
+    # every direct pair references 11-offset tables of the source level only
+    assert plan.d_tab.size > 0 and plan.d_tab.max() < plan.dtab.shape[0]
