@@ -273,6 +273,7 @@ __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t 
        i += (int64_t)gridDim.x * blockDim.x) {
     if (!leaf[i]) continue;
     uint64_t key = keys[i];
+    if (key_level(key) != l_c) continue;
     uint64_t c = key_code(key);
     int64_t cnt = prefix_hi(pkey, npts, c, 0) - prefix_lo(pkey, npts, c, 0);
     if (cnt <= n_s) continue;
@@ -462,20 +463,19 @@ std::vector<int64_t> level_offsets(const BoxSet& B, int nlev, cudaStream_t st) {
   return h;
 }
 
+// One host round trip per round: the count of selected boxes doubles as "changed".
 template <int D>
 void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st) {
   DBuf<int> any(1, st);
   for (int round = 0; round < 4096; ++round) {
     DBuf<uint8_t> leaf(B.n, st), split(B.n, st);
     split.zero();
-    any.zero();
     leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
     FGT_LAUNCHED();
     balance_flag_kernel<D><<<grid_for(B.n, 128), 128, 0, st>>>(B.keys.get(), B.n, leaf.get(), periodic,
                                                                  split.get(), any.get());
     FGT_LAUNCHED();
-    if (!read_scalar(any.get(), st)) return;
-    split_flagged(B, 0, B.n, split.get(), D, tmp, st);
+    if (split_flagged(B, 0, B.n, split.get(), D, tmp, st) == 0) return;
   }
   throw Error(FGT_ECUDA, "tree balance did not converge");
 }
@@ -545,22 +545,44 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     }
   }
 
-  // ---- level-synchronous refinement (tree.py:493-502)
+  // ---- level-synchronous refinement (tree.py:493-502).  The frontier of level l is a
+  // sorted key array; the children of its split boxes (consecutive codes) form the next
+  // sorted frontier, so the level-major box array is their concatenation (no re-sort).
   BoxSet B;
-  B.keys.alloc(1, st);
   {
-    uint64_t k0 = box_key(0, 0);
-    B.keys.from_host(&k0, 1);
-    B.n = 1;
-  }
-  for (int l = 0; l < l_c; ++l) {
-    std::vector<int64_t> off = level_offsets(B, l + 1, st);
-    int64_t lo = off[l], hi = off[l + 1];
-    if (hi == lo) break;
-    DBuf<uint8_t> flag(hi - lo, st);
-    count_flag_kernel<<<grid_for(hi - lo, 256), 256, 0, st>>>(B.keys.get(), lo, hi, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
-    FGT_LAUNCHED();
-    if (split_flagged(B, lo, hi - lo, flag.get(), D, tmp, st) == 0) break;
+    std::vector<DBuf<uint64_t>> levels;
+    std::vector<int64_t> lsize;
+    levels.emplace_back(1, st);
+    const uint64_t k0 = box_key(0, 0);
+    levels.back().from_host(&k0, 1);
+    lsize.push_back(1);
+    for (int l = 0; l < l_c; ++l) {
+      const int64_t fn = lsize.back();
+      DBuf<uint8_t> flag(fn, st);
+      count_flag_kernel<<<grid_for(fn, 256), 256, 0, st>>>(levels.back().get(), 0, fn, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
+      FGT_LAUNCHED();
+      DBuf<uint64_t> sel(fn, st);
+      DBuf<int64_t> nsel(1, st);
+      size_t bytes = 0;
+      FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, levels.back().get(), flag.get(), sel.get(), nsel.get(), (int)fn, st));
+      FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, levels.back().get(), flag.get(), sel.get(), nsel.get(), (int)fn, st));
+      count_launch();
+      const int64_t k = read_scalar(nsel.get(), st);
+      if (k == 0) break;
+      levels.emplace_back(k << D, st);
+      make_children_kernel<<<grid_for(k << D, 256), 256, 0, st>>>(sel.get(), k, D, levels.back().get());
+      FGT_LAUNCHED();
+      lsize.push_back(k << D);
+    }
+    int64_t tot = 0;
+    for (int64_t v : lsize) tot += v;
+    B.keys.alloc(tot, st);
+    B.n = tot;
+    int64_t off = 0;
+    for (size_t l = 0; l < levels.size(); ++l) {
+      FGT_CUDA(cudaMemcpyAsync(B.keys.get() + off, levels[l].get(), lsize[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+      off += lsize[l];
+    }
   }
 
   // ---- balance + dense-cutoff-leaf fix to the joint fixpoint (tree.py:504-523)
@@ -568,21 +590,15 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   if (l_c >= 1) {
     DBuf<int> any(1, st);
     for (int round = 0; round < 4096; ++round) {
-      std::vector<int64_t> off = level_offsets(B, l_c + 1, st);
-      int64_t lo = off[l_c], hi = off[l_c + 1];
       DBuf<uint8_t> leaf(B.n, st), split(B.n, st);
       split.zero();
-      any.zero();
       leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
       FGT_LAUNCHED();
-      if (hi > lo) {
-        densefix_flag_kernel<D><<<grid_for(hi - lo, 128), 128, 0, st>>>(
-            B.keys.get(), B.n, lo, hi, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
-            split.get(), any.get());
-        FGT_LAUNCHED();
-      }
-      if (!read_scalar(any.get(), st)) break;
-      split_flagged(B, 0, B.n, split.get(), D, tmp, st);
+      densefix_flag_kernel<D><<<grid_for(B.n, 128), 128, 0, st>>>(
+          B.keys.get(), B.n, 0, B.n, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
+          split.get(), any.get());
+      FGT_LAUNCHED();
+      if (split_flagged(B, 0, B.n, split.get(), D, tmp, st) == 0) break;
       balance_rounds<D>(B, tp.periodic, tmp, st);
     }
   }
