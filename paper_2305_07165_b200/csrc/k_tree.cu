@@ -795,55 +795,80 @@ __device__ int enumerate_neighbors(const uint64_t* __restrict__ keys, int64_t nb
   return cnt;
 }
 
-// pass 0: count entries per target leaf; pass 1: write them
+template <int D>
+constexpr int list_cap() { return D == 1 ? 4 : (D == 2 ? 16 : 64); }  // <= 4^d entries per leaf
+
+// One enumeration per target leaf: P entries (dense slot) then D entries (box) into the
+// leaf's fixed slots [i*CAP, (i+1)*CAP), plus their counts.
 template <int D>
 __global__ void __launch_bounds__(128) lists_kernel(
-    int pass, const int64_t* __restrict__ tleaves, int64_t ntl, const uint64_t* __restrict__ keys,
-    int64_t nb, const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
-    const int64_t* __restrict__ children, const int32_t* __restrict__ level,
-    const int64_t* __restrict__ npoints, const int64_t* __restrict__ scount,
-    const int64_t* __restrict__ tcount, const int64_t* __restrict__ dense_slot, int periodic,
-    int64_t* __restrict__ pcnt, int64_t* __restrict__ dcnt, const int64_t* __restrict__ poff,
-    const int64_t* __restrict__ doff, int64_t* __restrict__ p_src, int32_t* __restrict__ p_v,
-    int64_t* __restrict__ p_tgt, int64_t* __restrict__ d_src, int32_t* __restrict__ d_v,
-    int64_t* __restrict__ d_tgt, unsigned long long* __restrict__ pairs) {
-  constexpr int CAP = D == 1 ? 4 : (D == 2 ? 16 : 64);
+    const int64_t* __restrict__ tleaves, int64_t ntl, const uint64_t* __restrict__ keys, int64_t nb,
+    const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
+    const int64_t* __restrict__ children, const int64_t* __restrict__ scount,
+    const int64_t* __restrict__ dense_slot, int periodic, int64_t* __restrict__ pcnt,
+    int64_t* __restrict__ dcnt, int64_t* __restrict__ fix_id, int32_t* __restrict__ fix_v) {
+  constexpr int CAP = list_cap<D>();
   NbrEntry<D> ent[CAP];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntl;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t T = tleaves[i];
-    int cnt = enumerate_neighbors<D>(keys, nb, leaf, coords, children, T, periodic, ent);
-    int64_t np_ = 0, nd_ = 0;
-    int64_t po = pass ? poff[i] : 0, dof = pass ? doff[i] : 0;
-    unsigned long long pr = 0;
+    const int64_t T = tleaves[i];
+    const int cnt = enumerate_neighbors<D>(keys, nb, leaf, coords, children, T, periodic, ent);
+    int np_ = 0, nd_ = 0;
+    // P entries from the front of the slot range, D entries from the back
     for (int e = 0; e < cnt; ++e) {
-      int64_t S = ent[e].box;
-      int64_t slot = dense_slot[S];
+      const int64_t S = ent[e].box;
+      const int64_t slot = dense_slot[S];
+      int at;
       if (slot >= 0) {
-        if (pass) {
-          p_src[po + np_] = slot;
-          p_tgt[po + np_] = T;
-#pragma unroll
-          for (int k = 0; k < D; ++k) p_v[(po + np_) * D + k] = ent[e].v[k];
-        }
-        ++np_;
+        at = np_++;
+        fix_id[i * CAP + at] = slot;
       } else if (scount[S] > 0) {
-        if (pass) {
-          d_src[dof + nd_] = S;
-          d_tgt[dof + nd_] = T;
-#pragma unroll
-          for (int k = 0; k < D; ++k) d_v[(dof + nd_) * D + k] = ent[e].v[k];
-          pr += (unsigned long long)(scount[S] * tcount[T]);
-        }
-        ++nd_;
+        at = CAP - 1 - nd_++;
+        fix_id[i * CAP + at] = S;
+      } else {
+        continue;
       }
+#pragma unroll
+      for (int k = 0; k < D; ++k) fix_v[(i * CAP + at) * D + k] = ent[e].v[k];
     }
-    if (!pass) {
-      pcnt[i] = np_;
-      dcnt[i] = nd_;
-    } else if (pr) {
-      atomicAdd(pairs, pr);
+    pcnt[i] = np_;
+    dcnt[i] = nd_;
+  }
+}
+
+template <int D>
+__global__ void lists_compact_kernel(const int64_t* __restrict__ tleaves, int64_t ntl,
+                                     const int64_t* __restrict__ pcnt, const int64_t* __restrict__ dcnt,
+                                     const int64_t* __restrict__ poff, const int64_t* __restrict__ doff,
+                                     const int64_t* __restrict__ fix_id, const int32_t* __restrict__ fix_v,
+                                     const int64_t* __restrict__ scount, const int64_t* __restrict__ tcount,
+                                     int64_t* __restrict__ p_src, int32_t* __restrict__ p_v,
+                                     int64_t* __restrict__ p_tgt, int64_t* __restrict__ d_src,
+                                     int32_t* __restrict__ d_v, int64_t* __restrict__ d_tgt,
+                                     unsigned long long* __restrict__ pairs) {
+  constexpr int CAP = list_cap<D>();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntl;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t T = tleaves[i];
+    for (int e = 0; e < pcnt[i]; ++e) {
+      const int64_t o = poff[i] + e;
+      p_src[o] = fix_id[i * CAP + e];
+      p_tgt[o] = T;
+#pragma unroll
+      for (int k = 0; k < D; ++k) p_v[o * D + k] = fix_v[(i * CAP + e) * D + k];
     }
+    unsigned long long pr = 0;
+    for (int e = 0; e < dcnt[i]; ++e) {
+      const int at = CAP - 1 - e;
+      const int64_t o = doff[i] + e;
+      const int64_t S = fix_id[i * CAP + at];
+      d_src[o] = S;
+      d_tgt[o] = T;
+#pragma unroll
+      for (int k = 0; k < D; ++k) d_v[o * D + k] = fix_v[(i * CAP + at) * D + k];
+      pr += (unsigned long long)(scount[S] * tcount[T]);
+    }
+    if (pr) atomicAdd(pairs, pr);
   }
 }
 
@@ -886,12 +911,14 @@ static void build_lists_impl(TreeDev& T) {
   dcnt.zero();
   DBuf<unsigned long long> pairs(1, st);
   pairs.zero();
+  constexpr int CAP = list_cap<D>();
+  DBuf<int64_t> fix_id(ntl * CAP, st);
+  DBuf<int32_t> fix_v(ntl * CAP * D, st);
   if (ntl > 0) {
     lists_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
-        0, tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
-        T.level.get(), T.n_points.get(), T.src_count.get(), T.tgt_count.get(), T.dense_slot.get(),
-        T.periodic, pcnt.get(), dcnt.get(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, pairs.get());
+        tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
+        T.src_count.get(), T.dense_slot.get(), T.periodic, pcnt.get(), dcnt.get(), fix_id.get(),
+        fix_v.get());
     FGT_LAUNCHED();
   }
   bytes = 0;
@@ -912,13 +939,14 @@ static void build_lists_impl(TreeDev& T) {
   T.d_v.alloc(T.n_d * D, st);
   T.d_tgt.alloc(T.n_d, st);
   if (ntl > 0) {
-    lists_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
-        1, tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
-        T.level.get(), T.n_points.get(), T.src_count.get(), T.tgt_count.get(), T.dense_slot.get(),
-        T.periodic, nullptr, nullptr, poff.get(), doff.get(), T.p_src.get(), T.p_v.get(),
-        T.p_tgt.get(), T.d_src.get(), T.d_v.get(), T.d_tgt.get(), pairs.get());
+    lists_compact_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
+        tl.get(), ntl, pcnt.get(), dcnt.get(), poff.get(), doff.get(), fix_id.get(), fix_v.get(),
+        T.src_count.get(), T.tgt_count.get(), T.p_src.get(), T.p_v.get(), T.p_tgt.get(),
+        T.d_src.get(), T.d_v.get(), T.d_tgt.get(), pairs.get());
     FGT_LAUNCHED();
   }
+  fix_id.release();
+  fix_v.release();
   // direct CSR over all target leaves
   T.d_tgt_ids = std::move(tl);
   T.d_off = std::move(doff);
@@ -933,7 +961,13 @@ static void build_lists_impl(TreeDev& T) {
     FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, T.d_tgt_ids.get(), f2.get(), sel.get(), nsel.get(), (int)ntl, st));
     FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), nsel.get(), (int)ntl, st));
     count_launch(2);
-    T.n_psi = read_scalar(nsel.get(), st);
+    // one round trip for the psi count and the direct-pair statistic
+    int64_t h2[2];
+    FGT_CUDA(cudaMemcpyAsync(&h2[0], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaMemcpyAsync(&h2[1], pairs.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaStreamSynchronize(st));
+    T.n_psi = h2[0];
+    T.n_direct_pairs = h2[1];
     T.psi_ids.alloc(T.n_psi, st);
     T.p_off.alloc(T.n_psi + 1, st);
     if (T.n_psi) {
@@ -942,7 +976,6 @@ static void build_lists_impl(TreeDev& T) {
     }
     FGT_CUDA(cudaMemcpyAsync(T.p_off.get() + T.n_psi, &T.n_p, sizeof(int64_t), cudaMemcpyHostToDevice, st));
   }
-  T.n_direct_pairs = (int64_t)read_scalar(pairs.get(), st);
   T.lists_built = true;
 }
 
