@@ -44,7 +44,8 @@ void iota_i64(int64_t* a, int64_t n, cudaStream_t st) {
   FGT_LAUNCHED();
 }
 
-void sort_pairs_u32(CubTmpBuf& tmp, const uint32_t* kin, uint32_t* kout, const int64_t* vin,
+template <class K>
+void sort_pairs_key(CubTmpBuf& tmp, const K* kin, K* kout, const int64_t* vin,
                     int64_t* vout, int64_t n, int bits, cudaStream_t st) {
   if (n == 0) return;
   size_t bytes = 0;
@@ -85,7 +86,7 @@ struct WeightArgs {
   double* wts;           // (npts, D, MAXW)
   int* ai;               // (npts, D)
   double* qb;            // (npts)
-  uint32_t* key;         // (npts)
+  uint64_t* key;         // (npts)
   double sc, inv_delta, beta;
   int w, gmin, G;
 };
@@ -119,43 +120,42 @@ __global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
       a.ai[i * D + k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
       if (k == 0) {
         a.qb[i] = a.q[sidx];
-        a.key[i] = (uint32_t)lo;  // box part; spread_keys_kernel adds the taps
+        a.key[i] = (uint64_t)lo;  // box part; spread_keys_kernel adds the taps
       }
     }
   }
 }
 
+// key = (box, a_0, ..., a_{d-1}), 8 bits per tap index: a plane job is one key range and
+// consecutive points share rows and columns, so a 4-point DMMA group touches few tiles
 template <int D>
-__global__ void spread_keys_kernel(uint32_t* __restrict__ key, const int* __restrict__ ai, int64_t n) {
+__global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __restrict__ ai, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = key[i];
-    key[i] = D == 3 ? ((b << 16) | ((uint32_t)ai[i * D] << 8) | (uint32_t)ai[i * D + 1])
-                    : ((b << 8) | (uint32_t)ai[i * D]);
+    uint64_t k = key[i];
+#pragma unroll
+    for (int a = 0; a < D; ++a) k = (k << 8) | (uint64_t)ai[i * D + a];
+    key[i] = k;
   }
 }
 
 // job ranges in the sorted keys: d = 3 per (box, plane), d = 1 per (box, cell), d = 2 per box
 template <int D>
-__global__ void job_ranges_kernel(const uint32_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
+__global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
                                   int w, int* __restrict__ range) {
   const int64_t njob = D == 2 ? nbat : nbat * G;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < njob;
        t += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t k0, k1;
+    uint64_t k0, k1;
     if (D == 2) {
-      k0 = (uint32_t)t << 8;
-      k1 = (uint32_t)(t + 1) << 8;
+      k0 = (uint64_t)t << 16;
+      k1 = (uint64_t)(t + 1) << 16;
     } else {
-      const uint32_t b = (uint32_t)(t / G), p = (uint32_t)(t % G);
-      const uint32_t plo = (uint32_t)max(0, (int)p - w + 1);
-      if (D == 3) {
-        k0 = (b << 16) | (plo << 8);
-        k1 = (b << 16) | ((p + 1) << 8);
-      } else {
-        k0 = (b << 8) | plo;
-        k1 = ((b << 8) | p) + 1;
-      }
+      const uint64_t b = (uint64_t)(t / G), p = (uint64_t)(t % G);
+      const uint64_t plo = (uint64_t)max(0, (int)p - w + 1);
+      const int sh = 8 * (D - 1);  // bits below the a_0 byte
+      k0 = (((b << 8) | plo) << sh);
+      k1 = (((b << 8) | (p + 1)) << sh);
     }
     range[2 * t] = (int)lower_bound_dev(key, npts, k0);
     range[2 * t + 1] = (int)lower_bound_dev(key, npts, k1);
@@ -572,7 +572,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     boff_d.from_host(boff.data(), nbat + 1);
     DBuf<double> wts(npts * D * MAXW, st), qb(npts, st);
     DBuf<int> ai(npts * D, st);
-    DBuf<uint32_t> key(npts, st), skey(npts, st);
+    DBuf<uint64_t> key(npts, st), skey(npts, st);
     DBuf<int64_t> iota(npts, st), perm(npts, st);
     WeightArgs wa;
     wa.src = T.src_sorted.get();
@@ -599,9 +599,9 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
-    int bits = D == 3 ? 16 : 8;
-    while (((int64_t)1 << (bits - (D == 3 ? 16 : 8))) < nbat) ++bits;
-    sort_pairs_u32(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
+    int bits = 8 * D;
+    while (((int64_t)1 << (bits - 8 * D)) < nbat) ++bits;
+    sort_pairs_key(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
     const int64_t njob = D == 2 ? nbat : nbat * G;
     DBuf<int> range(2 * njob, st);
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
