@@ -83,7 +83,8 @@ struct WeightArgs {
   const int64_t* slots;  // batch box -> dense slot
   const int64_t* boff;   // (nbat+1) point offsets of the batch boxes
   int64_t npts, nbat;
-  double* wts;           // (npts, D, MAXW)
+  double* wts;           // (npts, MAXW), d = 1 only
+  double* tt;            // (npts, D) coordinates in grid units
   int* ai;               // (npts, D)
   double* qb;            // (npts)
   uint64_t* key;         // (npts)
@@ -91,16 +92,16 @@ struct WeightArgs {
   int w, gmin, G;
 };
 
-// one thread per (point, axis, half of the taps): 6 independent exp/sqrt chains per point
+// Pass 1, one thread per (point, axis): the scaled coordinate tt (grid units) and the
+// first tap a_k; no kernel weights yet (d >= 2 evaluates them after the sort, directly in
+// sorted order; d = 1 evaluates them here for the line kernel).
 template <int D>
-__global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
+__global__ void __launch_bounds__(256) spread_taps_kernel(WeightArgs a) {
   const double s = a.sc * a.inv_delta, half = 0.5 * a.w, inv_half = 2.0 / a.w;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.npts * D * 2;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.npts * D;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int hsel = (int)(t & 1);
-    const int64_t ik = t >> 1;
-    const int64_t i = ik / D;
-    const int k = (int)(ik - i * D);
+    const int64_t i = t / D;
+    const int k = (int)(t - i * D);
     int64_t lo = 0, hi = a.nbat;  // batch box of point i
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
@@ -110,18 +111,16 @@ __global__ void __launch_bounds__(256) spread_weights_kernel(WeightArgs a) {
     const int64_t sidx = a.src_start[box] + (i - a.boff[lo]);
     const double tt = (a.src[sidx * D + k] - a.center[box * D + k]) * s;
     const double a0 = ceil(tt - half);
-    double* wp = a.wts + (i * D + k) * MAXW + hsel * (MAXW / 2);
+    a.tt[i * D + k] = tt;
+    a.ai[i * D + k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
+    if (D == 1) {
+      double* wp = a.wts + i * MAXW;
 #pragma unroll
-    for (int o2 = 0; o2 < MAXW / 2; ++o2) {
-      const int o = hsel * (MAXW / 2) + o2;
-      wp[o2] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
+      for (int o = 0; o < MAXW; ++o) wp[o] = o < a.w ? es_kernel((a0 + o - tt) * inv_half, a.beta) : 0.0;
     }
-    if (hsel == 0) {
-      a.ai[i * D + k] = max(0, min((int)a0 - a.gmin, a.G - a.w));
-      if (k == 0) {
-        a.qb[i] = a.q[sidx];
-        a.key[i] = (uint64_t)lo;  // box part; spread_keys_kernel adds the taps
-      }
+    if (k == 0) {
+      a.qb[i] = a.q[sidx];
+      a.key[i] = (uint64_t)lo;  // box part; spread_keys_kernel adds the taps
     }
   }
 }
@@ -167,18 +166,24 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
 // (d = 3 plane factor).  One gather after the sort makes every job's staging a contiguous,
 // coalesced copy instead of a perm -> index -> weights pointer chase.
 template <int D>
-__global__ void sort_records_kernel(const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ wts,
-                                    const int* __restrict__ ai, const double* __restrict__ qb,
-                                    double* __restrict__ rw, double* __restrict__ rq, int* __restrict__ ra,
-                                    double* __restrict__ rw0) {
+__global__ void sort_records_kernel(const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ tt,
+                                    const int* __restrict__ ai, const double* __restrict__ qb, int w,
+                                    double beta, double* __restrict__ rw, double* __restrict__ rq,
+                                    int* __restrict__ ra, double* __restrict__ rw0) {
   const int RA = D == 3 ? 1 : 0, CA = D == 3 ? 2 : 1;
+  const double half = 0.5 * w, inv_half = 2.0 / w;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 32;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = t >> 5;
     const int o = (int)(t & 31);
     const int64_t i = perm[j];
-    rw[t] = wts[(i * D + (o < 16 ? RA : CA)) * MAXW + (o & 15)];
-    if (D == 3 && o < 16) rw0[j * 16 + o] = wts[(i * D) * MAXW + o];
+    const int ax = o < 16 ? RA : CA, tap = o & 15;
+    const double x = tt[i * D + ax];
+    rw[t] = tap < w ? es_kernel((ceil(x - half) + tap - x) * inv_half, beta) : 0.0;
+    if (D == 3 && o < 16) {
+      const double x0 = tt[i * D];
+      rw0[j * 16 + o] = o < w ? es_kernel((ceil(x0 - half) + o - x0) * inv_half, beta) : 0.0;
+    }
     if (o < 4) ra[j * 4 + o] = o < D ? ai[i * D + o] : 0;
     if (o == 0) rq[j] = qb[i];
   }
@@ -570,7 +575,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     DBuf<int64_t> sl_d(nbat, st), boff_d(nbat + 1, st);
     sl_d.from_host(slots.data() + b0, nbat);
     boff_d.from_host(boff.data(), nbat + 1);
-    DBuf<double> wts(npts * D * MAXW, st), qb(npts, st);
+    DBuf<double> wts(D == 1 ? npts * MAXW : 0, st), tt(npts * D, st), qb(npts, st);
     DBuf<int> ai(npts * D, st);
     DBuf<uint64_t> key(npts, st), skey(npts, st);
     DBuf<int64_t> iota(npts, st), perm(npts, st);
@@ -585,6 +590,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     wa.npts = npts;
     wa.nbat = nbat;
     wa.wts = wts.get();
+    wa.tt = tt.get();
     wa.ai = ai.get();
     wa.qb = qb.get();
     wa.key = key.get();
@@ -594,7 +600,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     wa.w = w;
     wa.gmin = N.gmin;
     wa.G = G;
-    spread_weights_kernel<D><<<grid_for(npts * D * 2, 256), 256, 0, st>>>(wa);
+    spread_taps_kernel<D><<<grid_for(npts * D, 256), 256, 0, st>>>(wa);
     FGT_LAUNCHED();
     spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts);
     FGT_LAUNCHED();
@@ -633,7 +639,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       ra.alloc(npts * 4, st);
       if (D == 3) rw0.alloc(npts * 16, st);
       sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
-          perm.get(), npts, wts.get(), ai.get(), qb.get(), rw.get(), rq.get(), ra.get(), rw0.get());
+          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, rw.get(), rq.get(), ra.get(), rw0.get());
       FGT_LAUNCHED();
     }
     PlaneArgs pa;
