@@ -358,6 +358,7 @@ struct EvalArgs {
   const int64_t* tgt_start;
   const int64_t* tgt_count;
   const int64_t* list;    // blockIdx.x -> psi index
+  const int* pstart;      // blockIdx.x -> first target of this 32-target pass
   const double2* psi;
   double* u;
   int n_f, R, ksteps;
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   static_assert(EVAL_MT == 4, "eval passes are dispatched for 1..4 m-tiles");
   double2* etab = sm;
   double* s_u = reinterpret_cast<double*>(etab + D * TB * RS);
+  // one CTA per 32-target pass of a psi box (work items listed box by box, so the
+  // passes of one box run together and share psi through L2)
   const int64_t i = a.list[blockIdx.x];
   const int64_t T = a.psi_ids[i];
   const int64_t t0 = a.tgt_start[T];
@@ -443,7 +446,8 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   const int nwarps = blockDim.x >> 5;
   const int n_f = a.n_f, R = a.R;
   const double2* psi = a.psi + (size_t)i * R * n_f;
-  for (int p0 = 0; p0 < ntg; p0 += TB) {
+  {
+    const int p0 = a.pstart[blockIdx.x];
     const int cnt = min(TB, ntg - p0);
     __syncthreads();
     build_etab<D>(etab, TB, NFP, RS, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
@@ -717,12 +721,13 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   if (hi == lo) return;
   cudaStream_t st = T.st;
   std::vector<int64_t> direct_list, spread_list;
+  std::vector<int64_t> h_cnt(hi - lo);
   {
     const int64_t n = hi - lo;
     DBuf<int64_t> c(n, st);
     gather_counts_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get() + lo, n, T.tgt_count.get(), c.get());
     FGT_LAUNCHED();
-    std::vector<int64_t> h(n);
+    std::vector<int64_t>& h = h_cnt;
     c.to_host(h.data(), n);
     FGT_CUDA(cudaStreamSynchronize(st));
     for (int64_t i = 0; i < n; ++i) {
@@ -742,9 +747,21 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
     P.k_eval.end(st);
     return;
   }
-  DBuf<int64_t> list_d(direct_list.size(), st);
-  list_d.from_host(direct_list.data(), direct_list.size());
-  const int64_t n_direct = (int64_t)direct_list.size();
+  // work items: (psi box, 32-target pass)
+  std::vector<int64_t> work_box;
+  std::vector<int> work_p0;
+  for (int64_t ii : direct_list) {
+    const int64_t n = h_cnt[ii - lo];
+    for (int64_t p0 = 0; p0 < n; p0 += EVAL_TB) {
+      work_box.push_back(ii);
+      work_p0.push_back((int)p0);
+    }
+  }
+  DBuf<int64_t> list_d(work_box.size(), st);
+  list_d.from_host(work_box.data(), work_box.size());
+  DBuf<int> p0_d(work_p0.size(), st);
+  p0_d.from_host(work_p0.data(), work_p0.size());
+  const int64_t n_direct = (int64_t)work_box.size();
   EvalArgs ea;
   ea.tgt = T.tgt_sorted.get();
   ea.center = T.center.get();
@@ -752,6 +769,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   ea.tgt_start = T.tgt_start.get();
   ea.tgt_count = T.tgt_count.get();
   ea.list = list_d.get();
+  ea.pstart = p0_d.get();
   ea.psi = reinterpret_cast<const double2*>(P.psi_view());
   ea.u = u_sorted;
   ea.n_f = P.n_f;
