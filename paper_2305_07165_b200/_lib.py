@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfgtcuda.so")
+# FGT_LIB_PATH selects an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("FGT_LIB_PATH") or os.path.join(HERE, "libfgtcuda.so")
 
 FGT_OK, FGT_EINVAL, FGT_ECUDA, FGT_ERANGE, FGT_ENOMEM = 0, 1, 2, 3, 4
 

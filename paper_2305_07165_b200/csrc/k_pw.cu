@@ -14,6 +14,7 @@
 // with r the flattened leading d-1 mode indices (C order, axis 0 slowest, ModeGrid
 // layout nufft.py:20-48) and c the last-axis mode.  Per-point 1-D phase tables are
 // built in shared memory (sincos per 8-mode segment + rotation recurrence).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -282,6 +283,16 @@ __global__ void form_reduce_kernel(const double2* __restrict__ scratch, const in
   }
 }
 
+__global__ void psi_meta_kernel(const int64_t* __restrict__ ids, int64_t n,
+                                const int64_t* __restrict__ cnt, const int64_t* __restrict__ parent,
+                                int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = cnt[ids[i]];
+    out[n + i] = parent[ids[i]];
+  }
+}
+
 __global__ void gather_counts_kernel(const int64_t* __restrict__ ids, int64_t n,
                                      const int64_t* __restrict__ cnt, int64_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -300,53 +311,165 @@ struct GatherArgs {
   const double2* phase;   // (3, n_f)
   const double2* phi;
   double2* psi;   // batch-local output
+  const int64_t* goff;  // sibling groups: psi index ranges
   int64_t NF, i0; // first psi index of the batch
   int n_f, l_c;
 };
 
-constexpr int GATHER_MAXE = 64;
+#ifndef FGT_GATHER_MPT
+#define FGT_GATHER_MPT 4
+#endif
+#ifndef FGT_GATHER_MINB
+#define FGT_GATHER_MINB 3
+#endif
+#ifndef FGT_GATHER_UNROLL
+#define FGT_GATHER_UNROLL 1
+#endif
+constexpr int GATHER_THREADS = 256;
+constexpr int GATHER_UNROLL = FGT_GATHER_UNROLL;
+constexpr int GATHER_MPT = FGT_GATHER_MPT;  // modes per thread
+constexpr int GATHER_CHUNK = GATHER_THREADS * GATHER_MPT;
 
+// Diagonal translation is organised by sibling group: the <= 2^d psi boxes under one
+// parent cell (contiguous in the psi list).  Every P entry of a member T (level l_c, child
+// position c of parent p) is a source image S' = coords_S + v * 2^l_c with
+// S' - 2p in [-1, 2]^d, so the sources of a group are indexed by that relative position
+// (4^d slots): each distinct phi_S is loaded once per mode and applied to every member that
+// uses it.  The shift of (T, S') along axis k is o_k = c_k - rel_k in {-1, 0, 1}, so the
+// translation phase is a product of 1, P_k or conj(P_k), P_k = exp(i m_k sc side_lc).
+//
+// group_table_kernel: one CTA per group builds the compacted source table (slot, member
+// mask | relative position) and the psi row of each child position.
 template <int D>
-__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
-  __shared__ int s_o[GATHER_MAXE][D];
-  __shared__ int64_t s_slot[GATHER_MAXE];
-  const int64_t i = a.i0 + blockIdx.y;
-  const int64_t T = a.psi_ids[i];
-  const int64_t e0 = a.p_off[i];
-  const int64_t ne64 = a.p_off[i + 1] - e0;
-  const int ne = (int)(ne64 < GATHER_MAXE ? ne64 : GATHER_MAXE);
+__global__ void group_table_kernel(GatherArgs a, int64_t* __restrict__ gt_slot,
+                                   unsigned* __restrict__ gt_code, int* __restrict__ gt_nu,
+                                   int64_t* __restrict__ gt_out) {
+  constexpr int NSIB = 1 << D;
+  constexpr int NREL = 1 << (2 * D);
+  __shared__ int64_t s_slot[NREL];
+  __shared__ unsigned s_mask[NREL];
+  const int64_t g = blockIdx.x;
+  const int64_t g0 = a.goff[g], g1 = a.goff[g + 1];
+  const int nmem = (int)(g1 - g0);
   const int64_t side = (int64_t)1 << a.l_c;
-  for (int t = threadIdx.x; t < ne; t += blockDim.x) {
-    const int64_t slot = a.p_src[e0 + t];
-    const int64_t S = a.dense_ids[slot];
-    s_slot[t] = slot;
+  for (int i = threadIdx.x; i < NREL; i += blockDim.x) s_mask[i] = 0;
+  if (threadIdx.x < NSIB) gt_out[g * NSIB + threadIdx.x] = -1;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int m = warp; m < nmem; m += blockDim.x >> 5) {
+    const int64_t i = g0 + m;
+    const int64_t T = a.psi_ids[i];
+    int c = 0;
+    int64_t base[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      int64_t o = a.coords[T * D + k] - (a.coords[S * D + k] + (int64_t)a.p_v[(e0 + t) * D + k] * side);
-      s_o[t][k] = (int)o + 1;  // index into phase rows (-1, 0, 1)
+      const int64_t ct = a.coords[T * D + k];
+      c |= (int)(ct & 1) << k;
+      base[k] = ct & ~(int64_t)1;
+    }
+    const int64_t e0 = a.p_off[i], e1 = a.p_off[i + 1];
+    for (int64_t t = e0 + lane; t < e1; t += 32) {
+      const int64_t slot = a.p_src[t];
+      const int64_t S = a.dense_ids[slot];
+      int idx = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int64_t rel = a.coords[S * D + k] + (int64_t)a.p_v[t * D + k] * side - base[k];
+        idx |= (int)(rel + 1) << (2 * k);
+      }
+      s_slot[idx] = slot;
+      atomicOr(&s_mask[idx], 1u << c);
     }
   }
   __syncthreads();
-  const int n_f = a.n_f;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.NF;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int m[D];
-    int64_t rem = e;
+  // the psi row of each child position (written after the -1 fill above)
+  for (int m = threadIdx.x; m < nmem; m += blockDim.x) {
+    const int64_t T = a.psi_ids[g0 + m];
+    int c = 0;
 #pragma unroll
-    for (int k = D - 1; k >= 0; --k) {
-      m[k] = (int)(rem % n_f);
-      rem /= n_f;
-    }
-    double2 acc = make_double2(0.0, 0.0);
-    for (int t = 0; t < ne; ++t) {
-      double2 p = a.phase[s_o[t][0] * n_f + m[0]];
+    for (int k = 0; k < D; ++k) c |= (int)(a.coords[T * D + k] & 1) << k;
+    gt_out[g * NSIB + c] = g0 + m - a.i0;
+  }
+  if (threadIdx.x == 0) {
+    int nu = 0;
+    for (int idx = 0; idx < NREL; ++idx)
+      if (s_mask[idx]) {
+        gt_slot[g * NREL + nu] = s_slot[idx];
+        gt_code[g * NREL + nu] = s_mask[idx] | ((unsigned)idx << 8);
+        ++nu;
+      }
+    gt_nu[g] = nu;
+  }
+}
+
+// One CTA per (group, chunk of GATHER_CHUNK modes), GATHER_MPT modes per thread.
+template <int D>
+__global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel(
+    GatherArgs a, const int64_t* __restrict__ gt_slot, const unsigned* __restrict__ gt_code,
+    const int* __restrict__ gt_nu, const int64_t* __restrict__ gt_out) {
+  constexpr int NSIB = 1 << D;
+  constexpr int NREL = 1 << (2 * D);
+  __shared__ int64_t u_slot[NREL];
+  __shared__ unsigned u_code[NREL];
+  const int64_t g = blockIdx.y;
+  const int nu = gt_nu[g];
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    u_slot[u] = gt_slot[g * NREL + u];
+    u_code[u] = gt_code[g * NREL + u];
+  }
+  int64_t outr[NSIB];
 #pragma unroll
-      for (int k = 1; k < D; ++k) p = cmul(p, a.phase[s_o[t][k] * n_f + m[k]]);
-      double2 f = a.phi[(size_t)s_slot[t] * a.NF + e];
-      acc.x += p.x * f.x - p.y * f.y;
-      acc.y += p.x * f.y + p.y * f.x;
+  for (int c = 0; c < NSIB; ++c) outr[c] = gt_out[g * NSIB + c];
+  __syncthreads();
+  const unsigned n_f = (unsigned)a.n_f;
+  const unsigned NF = (unsigned)a.NF;
+#pragma unroll 1
+  for (int j = 0; j < GATHER_MPT; ++j) {
+    const unsigned e = (unsigned)blockIdx.x * GATHER_CHUNK + j * GATHER_THREADS + threadIdx.x;
+    if (e >= NF) return;
+    double2 P[D];
+    {
+      unsigned rem = e;
+#pragma unroll
+      for (int k = D - 1; k >= 0; --k) {
+        const unsigned mk = rem % n_f;
+        rem /= n_f;
+        P[k] = a.phase[2 * n_f + mk];  // shift +1 row
+      }
     }
-    a.psi[(size_t)blockIdx.y * a.NF + e] = acc;
+    double2 acc[NSIB];
+#pragma unroll
+    for (int c = 0; c < NSIB; ++c) acc[c] = make_double2(0.0, 0.0);
+#pragma unroll GATHER_UNROLL
+    for (int u = 0; u < nu; ++u) {
+      const unsigned code = u_code[u];
+      const double2 f = a.phi[(size_t)u_slot[u] * NF + e];
+      // per axis: factor for child bit 0 (o = -rel) and child bit 1 (o = 1 - rel)
+      double2 F[D][2];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int rel = (int)((code >> (8 + 2 * k)) & 3) - 1;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int o = b - rel;  // -1, 0, 1 where used
+          F[k][b] = o == 0 ? make_double2(1.0, 0.0)
+                           : (o > 0 ? P[k] : make_double2(P[k].x, -P[k].y));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NSIB; ++c) {
+        if (code & (1u << c)) {
+          double2 ph = F[0][c & 1];
+#pragma unroll
+          for (int k = 1; k < D; ++k) ph = cmul(ph, F[k][(c >> k) & 1]);
+          acc[c].x += ph.x * f.x - ph.y * f.y;
+          acc[c].y += ph.x * f.y + ph.y * f.x;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NSIB; ++c)
+      if (outr[c] >= 0) a.psi[(size_t)outr[c] * NF + e] = acc[c];
   }
 }
 
@@ -584,6 +707,27 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
     }
   P.phase.alloc(ph.size(), st);
   P.phase.from_host(ph.data(), ph.size());
+  // targets per psi box and the parent of each psi box, fetched once (one sync, while the
+  // stream is idle after the lists)
+  const int64_t n = T.n_psi;
+  P.h_cnt.assign(n, 0);
+  P.h_goff.assign(1, 0);
+  if (n > 0) {
+    DBuf<int64_t> m(2 * n, st);
+    psi_meta_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get(), n, T.tgt_count.get(),
+                                                      T.parent.get(), m.get());
+    FGT_LAUNCHED();
+    std::vector<int64_t> h(2 * n);
+    m.to_host(h.data(), 2 * n);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    std::copy(h.begin(), h.begin() + n, P.h_cnt.begin());
+    const int64_t nsib = (int64_t)1 << P.d;
+    for (int64_t i = 1; i < n; ++i) {
+      const int64_t p = h[n + i];
+      if (p < 0 || p != h[n + i - 1] || i - P.h_goff.back() >= nsib) P.h_goff.push_back(i);
+    }
+    P.h_goff.push_back(n);
+  }
 }
 
 template <int D>
@@ -708,11 +852,36 @@ void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   ga.n_f = P.n_f;
   ga.l_c = T.l_c;
   FGT_REQUIRE(hi - lo <= 65535, FGT_ERANGE, "psi batch too large");
-  dim3 grid(grid_for(P.NF, 256, 256), (unsigned)(hi - lo));
+  // sibling groups of this batch (clamped to [lo, hi))
+  std::vector<int64_t> goff;
+  {
+    const auto& G = P.h_goff;
+    size_t g = std::upper_bound(G.begin(), G.end(), lo) - G.begin() - 1;
+    goff.push_back(lo);
+    for (++g; g < G.size() && G[g] < hi; ++g) goff.push_back(G[g]);
+    goff.push_back(hi);
+  }
+  DBuf<int64_t> goff_d(goff.size(), st);
+  goff_d.from_host(goff.data(), goff.size());
+  ga.goff = goff_d.get();
+  const int64_t n_groups = (int64_t)goff.size() - 1;
+  FGT_REQUIRE(n_groups <= 65535, FGT_ERANGE, "too many sibling groups");
+  const int nrel = 1 << (2 * T.d), nsib = 1 << T.d;
+  DBuf<int64_t> gt_slot(n_groups * nrel, st), gt_out(n_groups * nsib, st);
+  DBuf<unsigned> gt_code(n_groups * nrel, st);
+  DBuf<int> gt_nu(n_groups, st);
+  dim3 grid((unsigned)((P.NF + GATHER_CHUNK - 1) / GATHER_CHUNK), (unsigned)n_groups);
   P.k_gather.begin(st);
-  if (T.d == 1) gather_kernel<1><<<grid, 256, 0, st>>>(ga);
-  else if (T.d == 2) gather_kernel<2><<<grid, 256, 0, st>>>(ga);
-  else gather_kernel<3><<<grid, 256, 0, st>>>(ga);
+#define FGT_GATHER_D(DD)                                                                      \
+  group_table_kernel<DD><<<(unsigned)n_groups, 64, 0, st>>>(ga, gt_slot.get(), gt_code.get(), \
+                                                             gt_nu.get(), gt_out.get());      \
+  FGT_LAUNCHED();                                                                             \
+  gather_kernel<DD><<<grid, GATHER_THREADS, 0, st>>>(ga, gt_slot.get(), gt_code.get(),        \
+                                                     gt_nu.get(), gt_out.get());
+  if (T.d == 1) { FGT_GATHER_D(1) }
+  else if (T.d == 2) { FGT_GATHER_D(2) }
+  else { FGT_GATHER_D(3) }
+#undef FGT_GATHER_D
   FGT_LAUNCHED();
   P.k_gather.end(st);
 }
@@ -721,15 +890,10 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   if (hi == lo) return;
   cudaStream_t st = T.st;
   std::vector<int64_t> direct_list, spread_list;
-  std::vector<int64_t> h_cnt(hi - lo);
+  const int64_t* h_cnt_all = P.h_cnt.data() + lo;
   {
     const int64_t n = hi - lo;
-    DBuf<int64_t> c(n, st);
-    gather_counts_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get() + lo, n, T.tgt_count.get(), c.get());
-    FGT_LAUNCHED();
-    std::vector<int64_t>& h = h_cnt;
-    c.to_host(h.data(), n);
-    FGT_CUDA(cudaStreamSynchronize(st));
+    const int64_t* h = h_cnt_all;
     for (int64_t i = 0; i < n; ++i) {
       P.n_tgt_psi += h[i];
       if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) {
@@ -751,7 +915,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   std::vector<int64_t> work_box;
   std::vector<int> work_p0;
   for (int64_t ii : direct_list) {
-    const int64_t n = h_cnt[ii - lo];
+    const int64_t n = h_cnt_all[ii - lo];
     for (int64_t p0 = 0; p0 < n; p0 += EVAL_TB) {
       work_box.push_back(ii);
       work_p0.push_back((int)p0);

@@ -20,6 +20,9 @@ struct PwDev {
   KClock k_form, k_gather, k_eval, k_direct;
   int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
   int64_t n_src_spread = 0, n_tgt_spread = 0;
+  // host copies fetched once after the lists: targets per psi box and sibling groups
+  // (runs of psi boxes with a common parent, offsets into psi_ids)
+  std::vector<int64_t> h_cnt, h_goff;
 };
 
 struct NufftPlan;
