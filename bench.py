@@ -154,13 +154,19 @@ HBM_PEAK_GBS = 6555.5  # MEASURED_PEAKS.json hbm_gbs (copy test)
 
 def box_dft_cmacs(d, G, n_f):
     """Complex MACs of the separable grid<->mode transform of one box (real x complex
-    counted as half)."""
-    g, n = float(G), float(n_f)
+    counted as half) onto the stored half spectrum (d >= 2: h = n_f/2 + 1 axis-0 planes,
+    axis 0 contracted first; k_nufft.cu)."""
+    g, n, h = float(G), float(n_f), float(n_f // 2 + 1)
     if d == 1:
         return n * g
     if d == 2:
-        return 0.5 * g * g * n + n * n * g
-    return 0.5 * g ** 3 * n + g * g * n * n + n ** 3 * g
+        return 0.5 * g * g * n + h * n * g
+    return 0.5 * g ** 3 * h + h * g * g * n + h * n * g * n
+
+
+def stored_modes(d, n_f):
+    """Modes stored per expansion: the Hermitian half spectrum for d >= 2 (k_pw.cuh)."""
+    return n_f ** d if d == 1 else (n_f // 2 + 1) * n_f ** (d - 1)
 
 
 def kernel_rooflines(phases, fp64_peak_tf, d=3):
@@ -168,10 +174,13 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
     time, averaged over the timed steps.  Exact tensor-factored sums: 8 N_F flops per
     point (one complex MAC per mode).  NUFFT path: per point 2 W^d (spread/interp FMA)
     + d W c_exp (c_exp = 20 flops per kernel exp), per box 8 x the separable-DFT complex
-    MACs.  Gather: 16 B per mode read per P entry + written per psi box (streamed)."""
+    MACs.  Gather: 16 B per mode read per P entry + written per psi box (streamed).  N_F
+    counts the stored (half-spectrum) modes: the work the algorithm needs for real
+    charges, not the full n_f^d grid."""
     ph = phases[-1]
-    NF, w, G = ph["n_modes"], ph["nufft_w"], ph["nufft_G"]
-    n_f = round(NF ** (1.0 / d))
+    w, G = ph["nufft_w"], ph["nufft_G"]
+    n_f = round(ph["n_modes"] ** (1.0 / d))
+    NF = stored_modes(d, n_f)
     exact_src = ph["n_src_dense"] - ph["n_src_spread"]
     exact_tgt = ph["n_tgt_psi"] - ph["n_tgt_spread"]
     per_pt = 2.0 * w ** d + d * w * 20.0

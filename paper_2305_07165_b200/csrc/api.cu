@@ -206,7 +206,7 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     pw_form(P, T, &NP);
     t.form_ms = tm.lap();
     // psi is produced and consumed in batches of bounded size (<= ~4 GB)
-    const int64_t per = P.NF * 16;
+    const int64_t per = P.NH * 16;
     const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)4 << 30) / per));
     for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
       const int64_t hi = std::min(T.n_psi, lo + batch);

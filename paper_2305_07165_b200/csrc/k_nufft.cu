@@ -530,6 +530,24 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.Ee.from_host(Ee.data(), Ee.size());
   N.EeT.alloc(EeT.size(), st);
   N.EeT.from_host(EeT.data(), EeT.size());
+  // half-spectrum axis-0 matrices (d >= 2): rows / columns of the stored planes, the eval
+  // side weighted by the Hermitian pair factor
+  const int nh = n_f / 2 + 1;
+  std::vector<double> EfH(2 * nh * G), EeH(2 * nh * G);
+  for (int s = 0; s < nh; ++s) {
+    const int mi = half_plane_mi(s, n_f, true);
+    const double ws = half_plane_w(s, n_f, true);
+    for (int g = 0; g < G; ++g) {
+      EfH[2 * (s * G + g)] = Ef[2 * (mi * G + g)];
+      EfH[2 * (s * G + g) + 1] = Ef[2 * (mi * G + g) + 1];
+      EeH[2 * (g * nh + s)] = ws * Ee[2 * (g * n_f + mi)];
+      EeH[2 * (g * nh + s) + 1] = ws * Ee[2 * (g * n_f + mi) + 1];
+    }
+  }
+  N.EfH.alloc(EfH.size(), st);
+  N.EfH.from_host(EfH.data(), EfH.size());
+  N.EeH.alloc(EeH.size(), st);
+  N.EeH.from_host(EeH.data(), EeH.size());
   FGT_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
 }
 
@@ -554,7 +572,9 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   FGT_CUDA(cudaStreamSynchronize(st));
   FGT_REQUIRE(G < 256 && G <= 64, FGT_ERANGE, "spreading grid too large (G > 64)");
   // batches bounded by ~1.5 GB of grid + stage buffers + per-point weights
-  const int64_t per_box = GD * 8 + (D >= 2 ? plane * n_f * 16 : 0) + (D == 3 ? (int64_t)G * n_f * n_f * 16 : 0);
+  const int nh = P.nh;
+  const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)G * n_f * 16 : 0) +
+                          (D == 3 ? (int64_t)nh * plane * 16 + (int64_t)nh * n_f * G * 16 : 0);
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
   const int CH = D == 2 ? 4096 : 2048;  // points per job
   // grid cells written by one job: a plane (d = 3), the whole grid (d = 2), a cell (d = 1)
@@ -682,25 +702,26 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     scratch.release();
     wts.release();
     // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
+    // (d >= 2: only the nh stored axis-0 planes of the half spectrum, axis 0 contracted
+    // first so the later stages run on nh planes)
     double* phi = P.phi.get();
-    const int64_t NF = P.NF;
+    const int64_t NH = P.NH;
     if (D == 1) {
-      bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid.get(), 1, G, phi, 1, NF, n_f, 1, G, (int)nbat, sl_d.get()), st);
+      bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid.get(), 1, G, phi, 1, NH, n_f, 1, G, (int)nbat, sl_d.get()), st);
     } else if (D == 2) {
       DBuf<double> t1(2 * nbat * G * n_f, st);
       // T1[g1][m2] = sum_g2 grid[g1][g2] EfT[g2][m2]
       bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
-      // phi[m1][m2] = sum_g1 Ef[m1][g1] T1[g1][m2]
-      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NF, n_f, n_f, G, (int)nbat, sl_d.get()), st);
+      // phi[s][m2] = sum_g1 EfH[s][g1] T1[g1][m2]
+      bgemm<true, true, false>(gemm(N.EfH.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NH, nh, n_f, G, (int)nbat, sl_d.get()), st);
     } else {
-      DBuf<double> t1(2 * nbat * plane * n_f, st), t2(2 * nbat * G * n_f * n_f, st);
-      // T1[(g1 g2)][m3] = sum_g3 grid[(g1 g2)][g3] EfT[g3][m3]
-      bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, plane * n_f, (int)plane, n_f, G, (int)nbat), st);
-      // T2[g1][m2][m3] = sum_g2 Ef[m2][g2] T1[g1][g2][m3]      (batch = box x g1)
-      FGT_REQUIRE(nbat * G <= 65535, FGT_ERANGE, "GEMM batch too large");
-      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, t2.get(), n_f, (int64_t)n_f * n_f, n_f, n_f, G, (int)(nbat * G)), st);
-      // phi[m1][(m2 m3)] = sum_g1 Ef[m1][g1] T2[g1][(m2 m3)]
-      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, t2.get(), (int64_t)n_f * n_f, (int64_t)G * n_f * n_f, phi, (int64_t)n_f * n_f, NF, n_f, n_f * n_f, G, (int)nbat, sl_d.get()), st);
+      DBuf<double> x(2 * nbat * nh * plane, st), y(2 * nbat * nh * n_f * G, st);
+      // X[s][(g2 g3)] = sum_g1 EfH[s][g1] grid[g1][(g2 g3)]
+      bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid.get(), plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
+      // Y[s][m2][g3] = sum_g2 Ef[m2][g2] X[s][g2][g3]      (batch = box x s)
+      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, x.get(), G, (int64_t)G * G, y.get(), G, (int64_t)n_f * G, n_f, G, G, nbat * nh), st);
+      // phi[(s m2)][m3] = sum_g3 Y[(s m2)][g3] EfT[g3][m3]
+      bgemm<true, true, false>(gemm(y.get(), G, (int64_t)nh * n_f * G, N.EfT.get(), n_f, 0, phi, n_f, NH, nh * n_f, n_f, G, (int)nbat, sl_d.get()), st);
     }
     b0 += nbat;
   }
@@ -712,8 +733,10 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   if (idx.empty()) return;
   cudaStream_t st = T.st;
   const int G = N.G, n_f = N.n_f;
-  const int64_t GD = ipow(G, D), plane = GD / G, NF = P.NF;
-  const int64_t per_box = GD * 8 + (D >= 2 ? (int64_t)G * ipow(n_f, D - 1) * 16 : 0) + (D == 3 ? plane * n_f * 16 : 0);
+  const int64_t GD = ipow(G, D), plane = GD / G, NH = P.NH;
+  const int nh = P.nh;
+  const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)G * n_f * 16 : 0) +
+                          (D == 3 ? (int64_t)nh * n_f * G * 16 + (int64_t)nh * plane * 16 : 0);
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
   for (size_t b0 = 0; b0 < idx.size(); b0 += nb_max) {
     const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)idx.size() - b0);
@@ -723,22 +746,21 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     const double* psi = P.psi_view();  // first stage reads psi[list[b]] through bidx
     if (D == 1) {
       // grid[g] = Re sum_m Ee[g][m] psi[m]
-      bgemm<true, true, true>(gemm(N.Ee.get(), n_f, 0, psi, 1, NF, grid.get(), 1, GD, G, 1, n_f, (int)nbat, nullptr, li.get()), st);
+      bgemm<true, true, true>(gemm(N.Ee.get(), n_f, 0, psi, 1, NH, grid.get(), 1, GD, G, 1, n_f, (int)nbat, nullptr, li.get()), st);
     } else if (D == 2) {
       DBuf<double> v1(2 * nbat * G * n_f, st);
-      // V1[g1][m2] = sum_m1 Ee[g1][m1] psi[m1][m2]
-      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, psi, n_f, NF, v1.get(), n_f, (int64_t)G * n_f, G, n_f, n_f, (int)nbat, nullptr, li.get()), st);
+      // V1[g1][m2] = sum_s EeH[g1][s] psi[s][m2]   (pair weights in EeH)
+      bgemm<true, true, false>(gemm(N.EeH.get(), nh, 0, psi, n_f, NH, v1.get(), n_f, (int64_t)G * n_f, G, n_f, nh, (int)nbat, nullptr, li.get()), st);
       // grid[g1][g2] = Re sum_m2 V1[g1][m2] EeT[m2][g2]
       bgemm<true, true, true>(gemm(v1.get(), n_f, (int64_t)G * n_f, N.EeT.get(), G, 0, grid.get(), G, GD, G, G, n_f, (int)nbat), st);
     } else {
-      DBuf<double> v1(2 * nbat * G * n_f * n_f, st), v2(2 * nbat * plane * n_f, st);
-      // V1[g1][(m2 m3)] = sum_m1 Ee[g1][m1] psi[m1][(m2 m3)]
-      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, psi, (int64_t)n_f * n_f, NF, v1.get(), (int64_t)n_f * n_f, (int64_t)G * n_f * n_f, G, n_f * n_f, n_f, (int)nbat, nullptr, li.get()), st);
-      // V2[g1][g2][m3] = sum_m2 Ee[g2][m2] V1[g1][m2][m3]     (batch = box x g1)
-      FGT_REQUIRE(nbat * G <= 65535, FGT_ERANGE, "GEMM batch too large");
-      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, v1.get(), n_f, (int64_t)n_f * n_f, v2.get(), n_f, (int64_t)G * n_f, G, n_f, n_f, (int)(nbat * G)), st);
-      // grid[(g1 g2)][g3] = Re sum_m3 V2[(g1 g2)][m3] EeT[m3][g3]
-      bgemm<true, true, true>(gemm(v2.get(), n_f, plane * n_f, N.EeT.get(), G, 0, grid.get(), G, GD, (int)plane, G, n_f, (int)nbat), st);
+      DBuf<double> v(2 * nbat * nh * n_f * G, st), wv(2 * nbat * nh * plane, st);
+      // V[(s m2)][g3] = sum_m3 psi[(s m2)][m3] EeT[m3][g3]
+      bgemm<true, true, false>(gemm(psi, n_f, NH, N.EeT.get(), G, 0, v.get(), G, (int64_t)nh * n_f * G, nh * n_f, G, n_f, (int)nbat, nullptr, nullptr, li.get()), st);
+      // W[s][g2][g3] = sum_m2 Ee[g2][m2] V[s][m2][g3]      (batch = box x s)
+      bgemm<true, true, false>(gemm(N.Ee.get(), n_f, 0, v.get(), G, (int64_t)n_f * G, wv.get(), G, (int64_t)G * G, G, G, n_f, nbat * nh), st);
+      // grid[g1][(g2 g3)] = Re sum_s EeH[g1][s] W[s][(g2 g3)]   (pair weights in EeH)
+      bgemm<true, true, true>(gemm(N.EeH.get(), nh, 0, wv.get(), plane, (int64_t)nh * plane, grid.get(), plane, GD, G, (int)plane, nh, (int)nbat), st);
     }
     InterpArgs ia;
     ia.tgt = T.tgt_sorted.get();

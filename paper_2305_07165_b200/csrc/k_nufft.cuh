@@ -17,6 +17,8 @@ struct NufftPlan {
   std::vector<double> fh;   // (n_f)
   DBuf<double> Ef, EfT;     // form: (n_f, G) and (G, n_f) complex  w1d[m]/fh[m] e^{-i m g Delta}
   DBuf<double> Ee, EeT;     // eval: (G, n_f) and (n_f, G) complex        e^{+i m g Delta}/fh[m]
+  DBuf<double> EfH;         // (nh, G): rows of Ef for the stored axis-0 planes (half spectrum)
+  DBuf<double> EeH;         // (G, nh): columns of Ee for the stored planes x pair weight
 };
 
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);

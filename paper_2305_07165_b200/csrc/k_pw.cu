@@ -32,14 +32,16 @@ int nufft_mode() {
 
 namespace {
 // complex-MAC equivalents of the separable grid <-> mode transform of one box
+// (half spectrum for d >= 2: nh = n_f/2 + 1 planes along axis 0)
 double box_dft_cost(int D, int G, int n_f) {
-  const double g = G, n = n_f;
+  const double g = G, n = n_f, h = n_f / 2 + 1;
   if (D == 1) return n * g;
-  if (D == 2) return 0.5 * g * g * n + n * n * g;
-  return 0.5 * g * g * g * n + g * g * n * n + n * n * n * g;
+  if (D == 2) return 0.5 * g * g * n + h * n * g;
+  return 0.5 * g * g * g * h + h * g * g * n + h * n * g * n;
 }
 // true if the box-local NUFFT beats the exact sums for a box with npts points
 bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double tap_cost) {
+  // NF: stored modes per expansion
   if (!N) return false;
   const int mode = nufft_mode();
   if (mode == 1) return false;
@@ -110,7 +112,8 @@ struct FormArgs {
   double2* phi;
   double2* scratch;
   const double* w1d;
-  int n_f, R, MG, KS;
+  int n_f, R, MG, KS;  // R: stored rows (RH)
+  int half;
   double sc;
 };
 
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
   for (int mt = 0; mt < MT; ++mt) {
     int r = row0 + mt * 8 + (lane >> 2);
     rv[mt] = r < a.R;
-    ra[mt] = D == 3 ? r / n_f : r;
+    ra[mt] = half_plane_mi(D == 3 ? r / n_f : r, n_f, a.half);
     rb[mt] = D == 3 ? r % n_f : 0;
   }
 
@@ -238,8 +241,8 @@ __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
     const int r = row0 + mt * 8 + (lane >> 2);
     if (r >= a.R) continue;
     double wr = 1.0;
-    if (D == 2) wr = a.w1d[r];
-    if (D == 3) wr = a.w1d[r / n_f] * a.w1d[r % n_f];
+    if (D == 2) wr = a.w1d[half_plane_mi(r, n_f, a.half)];
+    if (D == 3) wr = a.w1d[half_plane_mi(r / n_f, n_f, a.half)] * a.w1d[r % n_f];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(256, 1) form_kernel(FormArgs a) {
 // sum the K-split partials of multi-unit boxes (fixed order: deterministic)
 template <int D>
 __global__ void form_reduce_kernel(const double2* __restrict__ scratch, const int4* __restrict__ red,
-                                   int64_t NF, int n_f, const double* __restrict__ w1d,
+                                   int64_t NF, int n_f, int half, const double* __restrict__ w1d,
                                    double2* __restrict__ phi) {
   const int4 rj = red[blockIdx.y];  // (slot, first scratch, count, -)
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NF;
@@ -275,8 +278,9 @@ __global__ void form_reduce_kernel(const double2* __restrict__ scratch, const in
     int64_t rem = e;
     double w = 1.0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      w *= w1d[rem % n_f];
+    for (int k = D - 1; k >= 0; --k) {
+      const int idx = k == 0 ? half_plane_mi((int)rem, n_f, half) : (int)(rem % n_f);
+      w *= w1d[idx];
       rem /= n_f;
     }
     phi[(size_t)rj.x * NF + e] = make_double2(s.x * w, s.y * w);
@@ -312,8 +316,8 @@ struct GatherArgs {
   const double2* phi;
   double2* psi;   // batch-local output
   const int64_t* goff;  // sibling groups: psi index ranges
-  int64_t NF, i0; // first psi index of the batch
-  int n_f, l_c;
+  int64_t NF, i0; // NF: stored modes; i0: first psi index of the batch
+  int n_f, l_c, half;
 };
 
 #ifndef FGT_GATHER_MPT
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
       unsigned rem = e;
 #pragma unroll
       for (int k = D - 1; k >= 0; --k) {
-        const unsigned mk = rem % n_f;
+        const unsigned mk = k == 0 ? (unsigned)half_plane_mi((int)rem, (int)n_f, a.half) : rem % n_f;
         rem /= n_f;
         P[k] = a.phase[2 * n_f + mk];  // shift +1 row
       }
@@ -484,7 +488,7 @@ struct EvalArgs {
   const int* pstart;      // blockIdx.x -> first target of this 32-target pass
   const double2* psi;
   double* u;
-  int n_f, R, ksteps;
+  int n_f, R, ksteps, half;  // R: stored rows (RH)
   double sc;
 };
 
@@ -496,7 +500,7 @@ constexpr int EVAL_MT = 4;
 // actually used, fixed at compile time so the last (partial) pass issues no idle DMMAs.
 template <int D, int NT, int MTP>
 __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, const double2* __restrict__ psi,
-                                          double* __restrict__ s_u, int R, int n_f, int ksteps) {
+                                          double* __restrict__ s_u, int R, int n_f, int ksteps, bool half) {
   constexpr int TB = EVAL_TB, NFP = NT * 8, RS = NFP + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
@@ -535,9 +539,17 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
         const int r = nt * 8 + 2 * (lane & 3) + i2;
         if (r >= R) continue;
         double2 f = make_double2(1.0, 0.0);
-        if (D == 2) f = etab[(0 * TB + j) * RS + r];
-        if (D == 3) f = cmul(etab[(0 * TB + j) * RS + r / n_f], etab[(1 * TB + j) * RS + r % n_f]);
-        part[mt] += acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y;
+        double wp = 1.0;
+        if (D == 2) {
+          f = etab[(0 * TB + j) * RS + half_plane_mi(r, n_f, half)];
+          wp = half_plane_w(r, n_f, half);
+        }
+        if (D == 3) {
+          const int s = r / n_f;
+          f = cmul(etab[(0 * TB + j) * RS + half_plane_mi(s, n_f, half)], etab[(1 * TB + j) * RS + r % n_f]);
+          wp = half_plane_w(s, n_f, half);
+        }
+        part[mt] += wp * (acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y);
       }
     }
   }
@@ -576,10 +588,10 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
     build_etab<D>(etab, TB, NFP, RS, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
     __syncthreads();
     switch ((cnt + 7) >> 3) {
-      case 1: eval_pass<D, NT, 1>(etab, psi, s_u, R, n_f, a.ksteps); break;
-      case 2: eval_pass<D, NT, 2>(etab, psi, s_u, R, n_f, a.ksteps); break;
-      case 3: eval_pass<D, NT, 3>(etab, psi, s_u, R, n_f, a.ksteps); break;
-      default: eval_pass<D, NT, 4>(etab, psi, s_u, R, n_f, a.ksteps); break;
+      case 1: eval_pass<D, NT, 1>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
+      case 2: eval_pass<D, NT, 2>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
+      case 3: eval_pass<D, NT, 3>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
+      default: eval_pass<D, NT, 4>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
     }
     __syncthreads();
     // deterministic cross-warp sum in a fixed order
@@ -692,6 +704,10 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   P.R = 1;
   for (int k = 0; k < P.d - 1; ++k) P.R *= P.n_f;
   P.NF = P.R * P.n_f;
+  P.half = P.d >= 2;
+  P.nh = P.half ? P.n_f / 2 + 1 : P.n_f;
+  P.RH = P.half ? P.R / P.n_f * P.nh : P.R;
+  P.NH = P.RH * P.n_f;
   P.sc = pw.h / std::sqrt(pw.delta);
   P.side_lc = T.root_side;
   for (int l = 0; l < T.l_c; ++l) P.side_lc *= 0.5;
@@ -734,7 +750,7 @@ template <int D>
 static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   cudaStream_t st = T.st;
   const int64_t nd = T.n_dense;
-  P.phi.alloc((size_t)nd * P.NF * 2, st);
+  P.phi.alloc((size_t)nd * P.NH * 2, st);
   if (nd == 0) return;
   P.phi.zero();
   // per-box source counts -> work units of at most KU points (split-K for big boxes)
@@ -752,7 +768,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
     int64_t n = cnt[s];
     if (n == 0) continue;
     if (!T.dense_need.empty() && !T.dense_need[s]) continue;
-    if (prefer_nufft(N, D, P.NF, n, 3.0)) {
+    if (prefer_nufft(N, D, P.NH, n, 3.0)) {
       spread_slots.push_back(s);
       P.n_src_spread += n;
       continue;
@@ -779,11 +795,11 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   }
   DBuf<int4> units_d(units.size(), st);
   units_d.from_host(units.data(), units.size());
-  DBuf<double> scratch((size_t)nscratch * P.NF * 2, st);
+  DBuf<double> scratch((size_t)nscratch * P.NH * 2, st);
 
   const int n_f = P.n_f;
   const int NT = (n_f + 7) / 8;
-  const int mtiles = (int)((P.R + 7) / 8);
+  const int mtiles = (int)((P.RH + 7) / 8);
   const int groups = (mtiles + FORM_MT - 1) / FORM_MT;
   int MG, KS, nrowblk;
   if (groups >= 8) { MG = 8; KS = 1; nrowblk = (groups + 7) / 8; }
@@ -799,7 +815,8 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   fa.scratch = reinterpret_cast<double2*>(scratch.get());
   fa.w1d = P.w1d.get();
   fa.n_f = n_f;
-  fa.R = (int)P.R;
+  fa.R = (int)P.RH;
+  fa.half = P.half;
   fa.MG = MG;
   fa.KS = KS;
   fa.sc = P.sc;
@@ -818,9 +835,9 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   if (!reds.empty()) {
     DBuf<int4> reds_d(reds.size(), st);
     reds_d.from_host(reds.data(), reds.size());
-    dim3 grid(grid_for(P.NF, 256, 64), (unsigned)reds.size());
+    dim3 grid(grid_for(P.NH, 256, 64), (unsigned)reds.size());
     form_reduce_kernel<D><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(scratch.get()), reds_d.get(),
-                                                P.NF, n_f, P.w1d.get(), reinterpret_cast<double2*>(P.phi.get()));
+                                                P.NH, n_f, (int)P.half, P.w1d.get(), reinterpret_cast<double2*>(P.phi.get()));
     FGT_LAUNCHED();
   }
 }
@@ -833,7 +850,7 @@ void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N) {
 
 void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   cudaStream_t st = T.st;
-  if (P.psi.size() < (size_t)(hi - lo) * P.NF * 2) P.psi.alloc((size_t)(hi - lo) * P.NF * 2, st);
+  if (P.psi.size() < (size_t)(hi - lo) * P.NH * 2) P.psi.alloc((size_t)(hi - lo) * P.NH * 2, st);
   P.psi_lo = lo;
   P.psi_hi = hi;
   if (hi == lo) return;
@@ -847,7 +864,8 @@ void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   ga.phase = reinterpret_cast<const double2*>(P.phase.get());
   ga.phi = reinterpret_cast<const double2*>(P.phi.get());
   ga.psi = reinterpret_cast<double2*>(P.psi.get());
-  ga.NF = P.NF;
+  ga.NF = P.NH;
+  ga.half = P.half;
   ga.i0 = lo;
   ga.n_f = P.n_f;
   ga.l_c = T.l_c;
@@ -870,7 +888,7 @@ void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   DBuf<int64_t> gt_slot(n_groups * nrel, st), gt_out(n_groups * nsib, st);
   DBuf<unsigned> gt_code(n_groups * nrel, st);
   DBuf<int> gt_nu(n_groups, st);
-  dim3 grid((unsigned)((P.NF + GATHER_CHUNK - 1) / GATHER_CHUNK), (unsigned)n_groups);
+  dim3 grid((unsigned)((P.NH + GATHER_CHUNK - 1) / GATHER_CHUNK), (unsigned)n_groups);
   P.k_gather.begin(st);
 #define FGT_GATHER_D(DD)                                                                      \
   group_table_kernel<DD><<<(unsigned)n_groups, 64, 0, st>>>(ga, gt_slot.get(), gt_code.get(), \
@@ -896,7 +914,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
     const int64_t* h = h_cnt_all;
     for (int64_t i = 0; i < n; ++i) {
       P.n_tgt_psi += h[i];
-      if (prefer_nufft(N, T.d, P.NF, h[i], 2.0)) {
+      if (prefer_nufft(N, T.d, P.NH, h[i], 2.0)) {
         spread_list.push_back(lo + i);
         P.n_tgt_spread += h[i];
       } else {
@@ -937,7 +955,8 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   ea.psi = reinterpret_cast<const double2*>(P.psi_view());
   ea.u = u_sorted;
   ea.n_f = P.n_f;
-  ea.R = (int)P.R;
+  ea.R = (int)P.RH;
+  ea.half = P.half;
   ea.ksteps = (P.n_f + 3) / 4;
   ea.sc = P.sc;
   const int NT = (P.n_f + 7) / 8;

@@ -4,19 +4,36 @@
 namespace fgt {
 
 // Plane-wave data of one discrete FGT evaluation.
+// Half spectrum.  The charges are real, so every expansion is Hermitian:
+// phi[-m] = conj(phi[m]) (the weights are even in m) and the same holds for psi (the
+// translation phases are conj-symmetric).  For d >= 2 only nh = n_f/2 + 1 planes along
+// axis 0 are stored: plane s holds m_0 = s for s < n_f/2 and m_0 = -n_f/2 for s = n_f/2
+// (the one plane without a partner); the potential Re sum_m psi_m e^{ik.x} then weighs
+// plane s by 1 (m_0 = 0 or -n_f/2) or 2 (the pair +-m_0).  Exact in exact arithmetic.
+__host__ __device__ inline int half_plane_mi(int s, int n_f, bool half) {
+  return half ? (s + n_f / 2) % n_f : s;
+}
+__host__ __device__ inline double half_plane_w(int s, int n_f, bool half) {
+  return (!half || s == 0 || s == n_f / 2) ? 1.0 : 2.0;
+}
+
 struct PwDev {
   int d = 0, n_f = 0;
+  bool half = false;   // half-spectrum storage (d >= 2)
+  int nh = 0;          // stored axis-0 planes
   int64_t R = 0;       // rows n_f^(d-1)
   int64_t NF = 0;      // n_f^d modes
+  int64_t RH = 0;      // stored rows nh * n_f^(d-2) (d >= 2), else R
+  int64_t NH = 0;      // stored modes per expansion: RH * n_f
   double sc = 0;       // coordinate scale h / sqrt(delta)
   double side_lc = 0;  // cutoff box side
   DBuf<double> w1d;    // (n_f) pre-multiplied 1-D weights (planewave.py:33-70)
   DBuf<double> phase;  // (3, n_f) complex: exp(+i m sc o side_lc), o = -1, 0, 1
-  DBuf<double> phi;    // (n_dense, R, n_f) complex outgoing expansions
-  DBuf<double> psi;    // (psi_hi - psi_lo, R, n_f) complex incoming expansions (one batch)
+  DBuf<double> phi;    // (n_dense, RH, n_f) complex outgoing expansions
+  DBuf<double> psi;    // (psi_hi - psi_lo, RH, n_f) complex incoming expansions (one batch)
   int64_t psi_lo = 0, psi_hi = 0;
-  // base pointer such that psi_view() + 2 * i * NF addresses psi box i of the batch
-  double* psi_view() const { return psi.get() - 2 * psi_lo * NF; }
+  // base pointer such that psi_view() + 2 * i * NH addresses psi box i of the batch
+  double* psi_view() const { return psi.get() - 2 * psi_lo * NH; }
   KClock k_form, k_gather, k_eval, k_direct;
   int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
   int64_t n_src_spread = 0, n_tgt_spread = 0;
