@@ -238,7 +238,7 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.n_src_dense = P.n_src_dense;
   t.n_tgt_psi = P.n_tgt_psi;
   t.n_p_entries = T.n_p;
-  t.n_direct_pairs = T.n_direct_pairs;
+  t.n_direct_pairs = direct_pairs(T);
   t.n_modes = P.NF;
   t.n_spread_boxes = P.n_spread_boxes;
   t.n_src_spread = P.n_src_spread;
@@ -446,7 +446,7 @@ int fgt_tree_lists(fgt_tree* t, fgt_list_info* info) {
       info->n_p_entries = t->T.n_p;
       info->n_d_entries = t->T.n_d;
       info->n_psi_boxes = t->T.n_psi;
-      info->n_direct_pairs = t->T.n_direct_pairs;
+      info->n_direct_pairs = direct_pairs(t->T);
     }
   });
 }

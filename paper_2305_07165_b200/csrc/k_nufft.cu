@@ -548,7 +548,8 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.EfH.from_host(EfH.data(), EfH.size());
   N.EeH.alloc(EeH.size(), st);
   N.EeH.from_host(EeH.data(), EeH.size());
-  FGT_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+  // (pageable host -> device async copies are staged before they return: the host
+  // vectors may go out of scope without a stream sync)
 }
 
 namespace {
@@ -565,11 +566,8 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   const int G = N.G, n_f = N.n_f, w = N.w;
   const int64_t GD = ipow(G, D);
   const int64_t plane = GD / G;
-  // per-slot source counts
-  std::vector<int64_t> dense(T.n_dense), scount(T.nb);
-  T.dense_ids.to_host(dense.data(), T.n_dense);
-  T.src_count.to_host(scount.data(), T.nb);
-  FGT_CUDA(cudaStreamSynchronize(st));
+  // per-slot source counts (fetched once in pw_setup)
+  const std::vector<int64_t>& scount = P.h_src;
   FGT_REQUIRE(G < 256 && G <= 64, FGT_ERANGE, "spreading grid too large (G > 64)");
   // batches bounded by ~1.5 GB of grid + stage buffers + per-point weights
   const int nh = P.nh;
@@ -586,7 +584,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     int64_t nbat = 0, npts = 0;
     std::vector<int64_t> boff(1, 0);
     while (b0 + nbat < slots.size() && nbat < nb_max) {
-      const int64_t n = scount[dense[slots[b0 + nbat]]];
+      const int64_t n = scount[slots[b0 + nbat]];
       if (nbat > 0 && npts + n > (int64_t)4 << 20) break;
       npts += n;
       boff.push_back(npts);

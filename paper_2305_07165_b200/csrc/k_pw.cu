@@ -725,18 +725,29 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   P.phase.from_host(ph.data(), ph.size());
   // targets per psi box and the parent of each psi box, fetched once (one sync, while the
   // stream is idle after the lists)
-  const int64_t n = T.n_psi;
+  // (and the source count of every P-box slot, for the form's path choice)
+  const int64_t n = T.n_psi, nd = T.n_dense;
   P.h_cnt.assign(n, 0);
   P.h_goff.assign(1, 0);
-  if (n > 0) {
-    DBuf<int64_t> m(2 * n, st);
-    psi_meta_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get(), n, T.tgt_count.get(),
-                                                      T.parent.get(), m.get());
-    FGT_LAUNCHED();
-    std::vector<int64_t> h(2 * n);
-    m.to_host(h.data(), 2 * n);
+  P.h_src.assign(nd, 0);
+  std::vector<int64_t> h(2 * n + nd);
+  if (n + nd > 0) {
+    DBuf<int64_t> m(2 * n + nd, st);
+    if (n > 0) {
+      psi_meta_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get(), n, T.tgt_count.get(),
+                                                        T.parent.get(), m.get());
+      FGT_LAUNCHED();
+    }
+    if (nd > 0) {
+      gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), m.get() + 2 * n);
+      FGT_LAUNCHED();
+    }
+    m.to_host(h.data(), h.size());
     FGT_CUDA(cudaStreamSynchronize(st));
     std::copy(h.begin(), h.begin() + n, P.h_cnt.begin());
+    std::copy(h.begin() + 2 * n, h.end(), P.h_src.begin());
+  }
+  if (n > 0) {
     const int64_t nsib = (int64_t)1 << P.d;
     for (int64_t i = 1; i < n; ++i) {
       const int64_t p = h[n + i];
@@ -754,12 +765,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   if (nd == 0) return;
   P.phi.zero();
   // per-box source counts -> work units of at most KU points (split-K for big boxes)
-  DBuf<int64_t> cnt_d(nd, st);
-  gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), cnt_d.get());
-  FGT_LAUNCHED();
-  std::vector<int64_t> cnt(nd);
-  cnt_d.to_host(cnt.data(), nd);
-  FGT_CUDA(cudaStreamSynchronize(st));
+  const std::vector<int64_t>& cnt = P.h_src;
   const int KU = 2048;
   std::vector<int4> units, reds;
   std::vector<int64_t> spread_slots;

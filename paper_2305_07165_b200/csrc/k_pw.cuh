@@ -40,6 +40,7 @@ struct PwDev {
   // host copies fetched once after the lists: targets per psi box and sibling groups
   // (runs of psi boxes with a common parent, offsets into psi_ids)
   std::vector<int64_t> h_cnt, h_goff;
+  std::vector<int64_t> h_src;  // sources per P-box slot
 };
 
 struct NufftPlan;

@@ -217,6 +217,36 @@ __global__ void make_children_kernel(const uint64_t* __restrict__ parents, int64
   }
 }
 
+// Device-count variants for the level loop: the frontier size lives on the device, the
+// launch covers a host-side capacity and entries past the count are flagged 0 / skipped.
+__global__ void count_flag_dev_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
+                                      int64_t cap, const uint64_t* __restrict__ pkey, int64_t npts, int d,
+                                      int l_c, int64_t n_s, uint8_t* __restrict__ flag) {
+  const int64_t n = n_dev ? (*n_dev << d) : 1;  // children of the boxes split one level up
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t f = 0;
+    if (i < n) {
+      uint64_t k = keys[i];
+      int sh = d * (l_c - key_level(k));
+      uint64_t c = key_code(k);
+      f = (prefix_hi(pkey, npts, c, sh) - prefix_lo(pkey, npts, c, sh)) > n_s ? 1 : 0;
+    }
+    flag[i] = f;
+  }
+}
+
+__global__ void make_children_dev_kernel(const uint64_t* __restrict__ parents, const int64_t* __restrict__ k_dev,
+                                         int64_t cap, int d, uint64_t* __restrict__ out) {
+  const int nc = 1 << d;
+  const int64_t n = *k_dev * nc;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap * nc;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t p = parents[i / nc];
+    out[i] = box_key(key_level(p) + 1, (key_code(p) << d) | (uint64_t)(i % nc));
+  }
+}
+
 __global__ void leaf_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int d,
                                  uint8_t* __restrict__ leaf) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
@@ -391,6 +421,14 @@ __global__ void dense_slot_kernel(const int64_t* __restrict__ ids, int64_t n, in
     slot[ids[i]] = i;
 }
 
+__global__ void dense_slot_dev_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
+                                      int64_t cap, int64_t* __restrict__ slot) {
+  const int64_t n = *n_dev;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap;
+       i += (int64_t)gridDim.x * blockDim.x)
+    slot[ids[i]] = i;
+}
+
 __global__ void fill_i64_kernel(int64_t* a, int64_t n, int64_t v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -548,30 +586,45 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   // ---- level-synchronous refinement (tree.py:493-502).  The frontier of level l is a
   // sorted key array; the children of its split boxes (consecutive codes) form the next
   // sorted frontier, so the level-major box array is their concatenation (no re-sort).
+  // Frontier sizes stay on the device (capacities bound the launches: the boxes split at
+  // one level are disjoint and hold > n_s points each), so the whole descent costs one
+  // host round trip instead of one per level.
   BoxSet B;
   {
     std::vector<DBuf<uint64_t>> levels;
-    std::vector<int64_t> lsize;
+    std::vector<int64_t> cap;
     levels.emplace_back(1, st);
     const uint64_t k0 = box_key(0, 0);
     levels.back().from_host(&k0, 1);
-    lsize.push_back(1);
+    cap.push_back(1);
+    DBuf<int64_t> nsel(std::max(l_c, 1), st);  // boxes split at level l
+    const int64_t split_cap = np / (T.n_s + 1);
     for (int l = 0; l < l_c; ++l) {
-      const int64_t fn = lsize.back();
+      const int64_t fn = cap.back();
+      const int64_t kc = std::min<int64_t>(fn, split_cap);
+      if (kc == 0) break;
       DBuf<uint8_t> flag(fn, st);
-      count_flag_kernel<<<grid_for(fn, 256), 256, 0, st>>>(levels.back().get(), 0, fn, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
+      count_flag_dev_kernel<<<grid_for(fn, 256), 256, 0, st>>>(levels.back().get(), l ? nsel.get() + (l - 1) : nullptr,
+                                                               fn, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
       FGT_LAUNCHED();
       DBuf<uint64_t> sel(fn, st);
-      DBuf<int64_t> nsel(1, st);
       size_t bytes = 0;
-      FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, levels.back().get(), flag.get(), sel.get(), nsel.get(), (int)fn, st));
-      FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, levels.back().get(), flag.get(), sel.get(), nsel.get(), (int)fn, st));
+      FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, levels.back().get(), flag.get(), sel.get(), nsel.get() + l, (int)fn, st));
+      FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, levels.back().get(), flag.get(), sel.get(), nsel.get() + l, (int)fn, st));
       count_launch();
-      const int64_t k = read_scalar(nsel.get(), st);
-      if (k == 0) break;
-      levels.emplace_back(k << D, st);
-      make_children_kernel<<<grid_for(k << D, 256), 256, 0, st>>>(sel.get(), k, D, levels.back().get());
+      levels.emplace_back(kc << D, st);
+      make_children_dev_kernel<<<grid_for(kc << D, 256), 256, 0, st>>>(sel.get(), nsel.get() + l, kc, D, levels.back().get());
       FGT_LAUNCHED();
+      cap.push_back(kc << D);
+    }
+    std::vector<int64_t> hsel(cap.size() - 1);
+    if (!hsel.empty()) {
+      nsel.to_host(hsel.data(), hsel.size());
+      FGT_CUDA(cudaStreamSynchronize(st));
+    }
+    std::vector<int64_t> lsize(1, 1);
+    for (int64_t k : hsel) {
+      if (k == 0) break;
       lsize.push_back(k << D);
     }
     int64_t tot = 0;
@@ -606,11 +659,11 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   // ---- finalise boxes
   const int64_t nb = B.n;
   T.nb = nb;
-  T.level_off = level_offsets(B, l_c + 1, st);  // l_c+2 entries
+  // level offsets (l_c + 2), dense-box count, leaf count: one host round trip at the end
+  DBuf<int64_t> fin(l_c + 4, st);
+  level_offsets_kernel<<<1, 64, 0, st>>>(B.keys.get(), B.n, l_c + 1, fin.get());
+  FGT_LAUNCHED();
   T.bkey = std::move(B.keys);
-  T.n_levels = 0;
-  for (int l = 0; l <= l_c; ++l)
-    if (T.level_off[l + 1] > T.level_off[l]) T.n_levels = l + 1;
 
   DBuf<int64_t> srcpre(np + 1, st);
   {
@@ -670,31 +723,34 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     DBuf<uint8_t> flag(nb, st);
     dense_flag_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.level.get(), T.is_leaf.get(), T.n_points.get(), nb, l_c, T.n_s, flag.get());
     FGT_LAUNCHED();
-    DBuf<int64_t> iota(nb, st), sel(nb, st), nsel(1, st);
+    DBuf<int64_t> iota(nb, st), sel(nb, st);
+    int64_t* nsel = fin.get() + l_c + 2;
     iota_kernel<<<grid_for(nb, 256), 256, 0, st>>>(iota.get(), nb);
     FGT_LAUNCHED();
     size_t bytes = 0;
-    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), sel.get(), nsel.get(), (int)nb, st));
-    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), sel.get(), nsel.get(), (int)nb, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), sel.get(), nsel, (int)nb, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), sel.get(), nsel, (int)nb, st));
     count_launch();
-    T.n_dense = read_scalar(nsel.get(), st);
-    T.dense_ids.alloc(T.n_dense, st);
-    if (T.n_dense)
-      FGT_CUDA(cudaMemcpyAsync(T.dense_ids.get(), sel.get(), T.n_dense * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     T.dense_slot.alloc(nb, st);
     fill_i64_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.dense_slot.get(), nb, -1);
     FGT_LAUNCHED();
-    if (T.n_dense) {
-      dense_slot_kernel<<<grid_for(T.n_dense, 256), 256, 0, st>>>(T.dense_ids.get(), T.n_dense, T.dense_slot.get());
-      FGT_LAUNCHED();
-    }
+    dense_slot_dev_kernel<<<grid_for(nb, 256), 256, 0, st>>>(sel.get(), nsel, nb, T.dense_slot.get());
+    FGT_LAUNCHED();
+    T.dense_ids = std::move(sel);  // capacity nb, first n_dense entries used
     // leaf count
-    DBuf<int64_t> nl(1, st);
     size_t b2 = 0;
-    FGT_CUDA(cub::DeviceReduce::Sum(nullptr, b2, T.is_leaf.get(), nl.get(), (int)nb, st));
-    FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), nl.get(), (int)nb, st));
+    FGT_CUDA(cub::DeviceReduce::Sum(nullptr, b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
+    FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     count_launch();
-    T.n_leaves = read_scalar(nl.get(), st);
+    std::vector<int64_t> h(l_c + 4);
+    fin.to_host(h.data(), h.size());
+    FGT_CUDA(cudaStreamSynchronize(st));
+    T.level_off.assign(h.begin(), h.begin() + l_c + 2);
+    T.n_dense = h[l_c + 2];
+    T.n_leaves = h[l_c + 3];
+    T.n_levels = 0;
+    for (int l = 0; l <= l_c; ++l)
+      if (T.level_off[l + 1] > T.level_off[l]) T.n_levels = l + 1;
   }
 }
 
@@ -802,13 +858,14 @@ constexpr int list_cap() { return D == 1 ? 4 : (D == 2 ? 16 : 64); }  // <= 4^d 
 // leaf's fixed slots [i*CAP, (i+1)*CAP), plus their counts.
 template <int D>
 __global__ void __launch_bounds__(128) lists_kernel(
-    const int64_t* __restrict__ tleaves, int64_t ntl, const uint64_t* __restrict__ keys, int64_t nb,
+    const int64_t* __restrict__ tleaves, const int64_t* __restrict__ ntl_dev, const uint64_t* __restrict__ keys, int64_t nb,
     const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
     const int64_t* __restrict__ children, const int64_t* __restrict__ scount,
     const int64_t* __restrict__ dense_slot, int periodic, int64_t* __restrict__ pcnt,
     int64_t* __restrict__ dcnt, int64_t* __restrict__ fix_id, int32_t* __restrict__ fix_v) {
   constexpr int CAP = list_cap<D>();
   NbrEntry<D> ent[CAP];
+  const int64_t ntl = *ntl_dev;  // launch covers a capacity
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntl;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t T = tleaves[i];
@@ -892,46 +949,62 @@ static void build_lists_impl(TreeDev& T) {
   cudaStream_t st = T.st;
   CubTmp tmp;
   const int64_t nb = T.nb;
+  // Sizes stay on the device until one host round trip (target leaves, P/D entry totals,
+  // psi boxes); launches before it cover the capacity n_leaves.
+  const int64_t cap = T.n_leaves;
+  DBuf<int64_t> cnt(4, st);  // ntl, n_p, n_d, n_psi
   // target leaves (leaves with targets), canonical order
   DBuf<uint8_t> flag(nb, st);
   target_leaf_flag_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.is_leaf.get(), T.tgt_count.get(), nb, flag.get());
   FGT_LAUNCHED();
-  DBuf<int64_t> iota(nb, st), tl(nb, st), ntl_d(1, st);
+  DBuf<int64_t> iota(nb, st), tl(nb, st);
   iota_kernel<<<grid_for(nb, 256), 256, 0, st>>>(iota.get(), nb);
   FGT_LAUNCHED();
   size_t bytes = 0;
-  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), tl.get(), ntl_d.get(), (int)nb, st));
-  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), tl.get(), ntl_d.get(), (int)nb, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, iota.get(), flag.get(), tl.get(), cnt.get(), (int)nb, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), tl.get(), cnt.get(), (int)nb, st));
   count_launch();
-  const int64_t ntl = read_scalar(ntl_d.get(), st);
-  T.n_dtgt = ntl;
 
-  DBuf<int64_t> pcnt(ntl + 1, st), dcnt(ntl + 1, st), poff(ntl + 1, st), doff(ntl + 1, st);
+  DBuf<int64_t> pcnt(cap + 1, st), dcnt(cap + 1, st), poff(cap + 1, st), doff(cap + 1, st);
   pcnt.zero();
   dcnt.zero();
-  DBuf<unsigned long long> pairs(1, st);
-  pairs.zero();
+  T.pairs_dev.alloc(1, st);
+  T.pairs_dev.zero();
   constexpr int CAP = list_cap<D>();
-  DBuf<int64_t> fix_id(ntl * CAP, st);
-  DBuf<int32_t> fix_v(ntl * CAP * D, st);
-  if (ntl > 0) {
-    lists_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
-        tl.get(), ntl, T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
+  DBuf<int64_t> fix_id(cap * CAP, st);
+  DBuf<int32_t> fix_v(cap * CAP * D, st);
+  if (cap > 0) {
+    lists_kernel<D><<<grid_for(cap, 128), 128, 0, st>>>(
+        tl.get(), cnt.get(), T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
         T.src_count.get(), T.dense_slot.get(), T.periodic, pcnt.get(), dcnt.get(), fix_id.get(),
         fix_v.get());
     FGT_LAUNCHED();
   }
   bytes = 0;
-  FGT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, pcnt.get(), poff.get(), (int)(ntl + 1), st));
-  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, pcnt.get(), poff.get(), (int)(ntl + 1), st));
-  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, dcnt.get(), doff.get(), (int)(ntl + 1), st));
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, pcnt.get(), poff.get(), (int)(cap + 1), st));
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, pcnt.get(), poff.get(), (int)(cap + 1), st));
+  FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes, st), bytes, dcnt.get(), doff.get(), (int)(cap + 1), st));
   count_launch(2);
-  int64_t tot[2];
-  FGT_CUDA(cudaMemcpyAsync(&tot[0], poff.get() + ntl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FGT_CUDA(cudaMemcpyAsync(&tot[1], doff.get() + ntl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FGT_CUDA(cudaMemcpyAsync(cnt.get() + 1, poff.get() + cap, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  FGT_CUDA(cudaMemcpyAsync(cnt.get() + 2, doff.get() + cap, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  // psi boxes: target leaves with P entries -> compact CSR (entries past ntl have pcnt 0)
+  DBuf<uint8_t> f2(cap + 1, st);
+  nonzero_flag_kernel<<<grid_for(cap, 256), 256, 0, st>>>(pcnt.get(), cap, f2.get());
+  FGT_LAUNCHED();
+  DBuf<int64_t> sel(cap + 1, st), seloff(cap + 1, st);
+  bytes = 0;
+  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, tl.get(), f2.get(), sel.get(), cnt.get() + 3, (int)cap, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, tl.get(), f2.get(), sel.get(), cnt.get() + 3, (int)cap, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), cnt.get() + 3, (int)cap, st));
+  count_launch(2);
+  int64_t h[4];
+  cnt.to_host(h, 4);
   FGT_CUDA(cudaStreamSynchronize(st));
-  T.n_p = tot[0];
-  T.n_d = tot[1];
+  const int64_t ntl = h[0];
+  T.n_dtgt = ntl;
+  T.n_p = h[1];
+  T.n_d = h[2];
+  T.n_psi = h[3];
   T.p_src.alloc(T.n_p, st);
   T.p_v.alloc(T.n_p * D, st);
   T.p_tgt.alloc(T.n_p, st);
@@ -942,41 +1015,31 @@ static void build_lists_impl(TreeDev& T) {
     lists_compact_kernel<D><<<grid_for(ntl, 128), 128, 0, st>>>(
         tl.get(), ntl, pcnt.get(), dcnt.get(), poff.get(), doff.get(), fix_id.get(), fix_v.get(),
         T.src_count.get(), T.tgt_count.get(), T.p_src.get(), T.p_v.get(), T.p_tgt.get(),
-        T.d_src.get(), T.d_v.get(), T.d_tgt.get(), pairs.get());
+        T.d_src.get(), T.d_v.get(), T.d_tgt.get(), reinterpret_cast<unsigned long long*>(T.pairs_dev.get()));
     FGT_LAUNCHED();
   }
   fix_id.release();
   fix_v.release();
-  // direct CSR over all target leaves
+  // direct CSR over all target leaves (d_off[ntl] = n_d: the counts past ntl are 0)
   T.d_tgt_ids = std::move(tl);
   T.d_off = std::move(doff);
-  // psi boxes: target leaves with P entries -> compact CSR
-  {
-    DBuf<uint8_t> f2(ntl + 1, st);
-    nonzero_flag_kernel<<<grid_for(ntl, 256), 256, 0, st>>>(pcnt.get(), ntl, f2.get());
-    FGT_LAUNCHED();
-    DBuf<int64_t> sel(ntl + 1, st), nsel(1, st), seloff(ntl + 1, st);
-    bytes = 0;
-    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, T.d_tgt_ids.get(), f2.get(), sel.get(), nsel.get(), (int)ntl, st));
-    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, T.d_tgt_ids.get(), f2.get(), sel.get(), nsel.get(), (int)ntl, st));
-    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), nsel.get(), (int)ntl, st));
-    count_launch(2);
-    // one round trip for the psi count and the direct-pair statistic
-    int64_t h2[2];
-    FGT_CUDA(cudaMemcpyAsync(&h2[0], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    FGT_CUDA(cudaMemcpyAsync(&h2[1], pairs.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    FGT_CUDA(cudaStreamSynchronize(st));
-    T.n_psi = h2[0];
-    T.n_direct_pairs = h2[1];
-    T.psi_ids.alloc(T.n_psi, st);
-    T.p_off.alloc(T.n_psi + 1, st);
-    if (T.n_psi) {
-      FGT_CUDA(cudaMemcpyAsync(T.psi_ids.get(), sel.get(), T.n_psi * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-      FGT_CUDA(cudaMemcpyAsync(T.p_off.get(), seloff.get(), T.n_psi * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    }
-    FGT_CUDA(cudaMemcpyAsync(T.p_off.get() + T.n_psi, &T.n_p, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  }
+  T.psi_ids = std::move(sel);
+  T.p_off = std::move(seloff);
+  FGT_CUDA(cudaMemcpyAsync(T.p_off.get() + T.n_psi, cnt.get() + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  T.n_direct_pairs = -1;  // read lazily (direct_pairs)
   T.lists_built = true;
+}
+
+int64_t direct_pairs(TreeDev& T) {
+  if (T.n_direct_pairs < 0) {
+    int64_t v = 0;
+    if (T.pairs_dev.size()) {
+      T.pairs_dev.to_host(&v, 1);
+      FGT_CUDA(cudaStreamSynchronize(T.st));
+    }
+    T.n_direct_pairs = v;
+  }
+  return T.n_direct_pairs;
 }
 
 void build_lists(TreeDev& T) {

@@ -32,7 +32,8 @@ struct TreeDev {
 
   // lists (target-centric), built by build_lists()
   bool lists_built = false;
-  int64_t n_p = 0, n_d = 0, n_psi = 0, n_direct_pairs = 0;
+  int64_t n_p = 0, n_d = 0, n_psi = 0, n_direct_pairs = 0;  // n_direct_pairs < 0: on device
+  DBuf<int64_t> pairs_dev;  // direct pair statistic (unsigned long long counter)
   DBuf<int64_t> p_off;   // (n_psi+1) CSR over psi boxes
   DBuf<int64_t> psi_ids; // (n_psi) target box ids with P entries
   DBuf<int64_t> p_src;   // (n_p) dense slot of S
@@ -59,5 +60,7 @@ void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, in
 void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt);
 // Target-centric P/D lists.
 void build_lists(TreeDev& T);
+// direct-pair statistic of the lists (one device read, cached)
+int64_t direct_pairs(TreeDev& T);
 
 }  // namespace fgt
