@@ -14,6 +14,8 @@
 //   3. evaluation runs the transposed chain and interpolates with the same kernel.
 // Partial grids of K-split boxes are summed in a fixed order (deterministic).
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include <cub/cub.cuh>
 
@@ -125,15 +127,25 @@ __global__ void __launch_bounds__(256) spread_taps_kernel(WeightArgs a) {
   }
 }
 
-// key = (box, a_0, ..., a_{d-1}), 8 bits per tap index: a plane job is one key range and
-// consecutive points share rows and columns, so a 4-point DMMA group touches few tiles
+// interleave two 8-bit values (x in the odd bits)
+__device__ __forceinline__ uint64_t morton2_8(unsigned x, unsigned y) {
+  uint64_t r = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) r |= (uint64_t)(((x >> b) & 1u) << (2 * b + 1)) | (uint64_t)(((y >> b) & 1u) << (2 * b));
+  return r;
+}
+
+// key = (box, a_0, Morton(a_1, a_2)) for d = 3, (box, Morton(a_0, a_1)) for d = 2 (16 bits
+// for the last two taps), (box, a_0) for d = 1: a plane job is one key range (a_0 major) and
+// consecutive points are spatially compact, so a 4-point DMMA group touches few tiles
 template <int D>
 __global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __restrict__ ai, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = key[i];
-#pragma unroll
-    for (int a = 0; a < D; ++a) k = (k << 8) | (uint64_t)ai[i * D + a];
+    if (D == 1) k = (k << 8) | (uint64_t)ai[i];
+    if (D == 2) k = (k << 16) | morton2_8((unsigned)ai[i * 2], (unsigned)ai[i * 2 + 1]);
+    if (D == 3) k = (((k << 8) | (uint64_t)ai[i * 3]) << 16) | morton2_8((unsigned)ai[i * 3 + 1], (unsigned)ai[i * 3 + 2]);
     key[i] = k;
   }
 }
@@ -288,33 +300,31 @@ __global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
       const bool valid = j < cnt;
       const double cj = valid ? s_c[j] : 0.0;
       const int a1 = valid ? s_a1[j] : 0, a2 = valid ? s_a2[j] : 0;
-      // rows / columns the group touches (warp-uniform)
-      int rlo = 1 << 20, rhi = -1, clo = 1 << 20, chi = -1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (4 * g + k < cnt) {
-          rlo = min(rlo, s_a1[4 * g + k]);
-          rhi = max(rhi, s_a1[4 * g + k] + w - 1);
-          clo = min(clo, s_a2[4 * g + k]);
-          chi = max(chi, s_a2[4 * g + k] + w - 1);
-        }
-      }
+      // rows / columns the group touches (warp-uniform: reductions over its <= 4 points)
+      const int rlo = __reduce_min_sync(0xffffffffu, valid ? a1 : 1 << 20);
+      const int rhi = __reduce_max_sync(0xffffffffu, valid ? a1 + w - 1 : -1);
+      const int clo = __reduce_min_sync(0xffffffffu, valid ? a2 : 1 << 20);
+      const int chi = __reduce_max_sync(0xffffffffu, valid ? a2 + w - 1 : -1);
       const int bl = rlo >> 3, bh = rhi >> 3, tl = clo >> 3, th = chi >> 3;
-      double A[NB], B[NB];
+      // fragments only for the touched tiles (uniform branches skip the rest)
+      double B[NB];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int d = 8 * b + (lane >> 2) - a1;
-        A[b] = (valid && (unsigned)d < (unsigned)w) ? cj * w1[j * TILE_RS + d] : 0.0;
-        const int e = 8 * b + (lane >> 2) - a2;
-        B[b] = (valid && (unsigned)e < (unsigned)w) ? w2[j * TILE_RS + e] : 0.0;
+      for (int t = 0; t < NB; ++t) {
+        B[t] = 0.0;
+        if (t >= tl && t <= th) {
+          const int e = 8 * t + (lane >> 2) - a2;
+          if (valid && (unsigned)e < (unsigned)w) B[t] = w2[j * TILE_RS + e];
+        }
       }
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         if (b < bl || b > bh) continue;
+        const int d = 8 * b + (lane >> 2) - a1;
+        const double A = (valid && (unsigned)d < (unsigned)w) ? cj * w1[j * TILE_RS + d] : 0.0;
 #pragma unroll
         for (int t = 0; t < NB; ++t) {
           if (t < tl || t > th) continue;
-          dmma2(acc[b][t][0], acc[b][t][1], A[b], B[t]);
+          dmma2(acc[b][t][0], acc[b][t][1], A, B[t]);
         }
       }
     }
