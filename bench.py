@@ -211,6 +211,40 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
     return out
 
 
+# kernels (ncu names) that make up each CUDA-event phase of kernel_rooflines
+PHASE_KERNELS = {
+    "form": ("spread_tile_kernel", "sort_records_kernel", "spread_taps_kernel", "spread_keys_kernel",
+             "form_kernel", "form_reduce_kernel", "plane_reduce_kernel", "bgemm_kernel",
+             "job_ranges_kernel", "DeviceRadixSort"),
+    "eval": ("eval_kernel", "interp_kernel"),
+    "gather": ("gather_kernel", "group_table_kernel"),
+}
+
+
+def phase_traffic(kernel_label):
+    """DRAM bytes (read + write) per step of the kernels of a phase, from the newest
+    committed `ncu --set full` summary of the same workload (profiles/r*_ncu_kernels.json,
+    tools/ncu_summary.py); None if there is none."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_kernels.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        rep = json.load(f)
+    if not isinstance(rep, dict) or "kernels" not in rep:
+        return None
+    phase = kernel_label.split(" ")[0].split("_")[0]
+    pats = PHASE_KERNELS.get(phase)
+    if not pats:
+        return None
+    tot = 0.0
+    for k in rep["kernels"]:
+        if any(p in k["kernel"] for p in pats):
+            tot += k.get("dram__bytes_read.sum [GB]", 0.0) + k.get("dram__bytes_write.sum [GB]", 0.0)
+    return {"bytes": tot * 1e9 / rep.get("steps", 1), "source": os.path.basename(files[-1]),
+            "kernels": list(pats)}
+
+
 # ------------------------------------------------------------------ distributed helpers
 def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,11 +373,7 @@ def run_ours(args, world, rank, local):
     _lib.check(lib.fgt_bench_fp64_peak(1, ctypes.byref(peak)))
     kr = kernel_rooflines(phases, peak.value)
     dom = max(kr, key=lambda k: k["kernel_ms"])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "kernel_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(dom["kernel"])
+    traffic = phase_traffic(dom["kernel"])
 
     res = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
@@ -356,7 +386,9 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": (N + M) / e2e_sec, "unit": "points/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_sec * 1e3},
         "roofline": {**{k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac")},
-                     "traffic": traffic, "kernel": dom["kernel"], "kernel_ms": dom["kernel_ms"],
+                     "traffic": traffic["bytes"] if traffic else None,
+                     "traffic_unit": "bytes per step (dram read + write, ncu --set full)",
+                     "traffic_source": traffic, "kernel": dom["kernel"], "kernel_ms": dom["kernel_ms"],
                      "alg_per_launch": dom["alg"], "accounting": dom["accounting"],
                      "peak_source": dom["peak_source"]},
         "kernels": kr,
