@@ -38,6 +38,30 @@ struct OwnedStream {
   }
 };
 
+// Phase boundaries as events on the stream, read once at the end (no host stall between
+// phases).
+struct PhaseMarks {
+  std::vector<cudaEvent_t> ev;
+  cudaStream_t st;
+  explicit PhaseMarks(cudaStream_t s) : st(s) { mark(); }
+  void mark() {
+    cudaEvent_t e;
+    FGT_CUDA(cudaEventCreate(&e));
+    FGT_CUDA(cudaEventRecord(e, st));
+    ev.push_back(e);
+  }
+  // elapsed ms between marks i and i + 1
+  double ms(size_t i) const {
+    FGT_CUDA(cudaEventSynchronize(ev[i + 1]));
+    float v = 0;
+    FGT_CUDA(cudaEventElapsedTime(&v, ev[i], ev[i + 1]));
+    return v;
+  }
+  ~PhaseMarks() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
 struct Timer {
   cudaEvent_t a, b;
   cudaStream_t st;
@@ -178,13 +202,15 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
                             double* u, cudaStream_t st, fgt_phase_times* times) {
   FGT_REQUIRE(tp.dim == pw.dim, FGT_EINVAL, "tree/plane-wave dim mismatch");
   const int64_t l0 = g_launches;
-  Timer tm(st);
+  PhaseMarks pm(st);  // marks: 0 start, 1 tree, 2 lists, 3 form, 4 gather+eval, 5 direct
+  trace_mark(st, "start");
   fgt_phase_times t;
   std::memset(&t, 0, sizeof(t));
   TreeDev T;
   build_tree(T, src, ns, tgt, nt, tp, st);
   gather_sorted_points(T, src, q, tgt);
-  t.tree_ms = tm.lap();
+  pm.mark();
+  trace_mark(st, "tree");
   build_lists(T);
   if (tp.part_size > 1) {
     FGT_REQUIRE(tp.part_rank >= 0 && tp.part_rank < tp.part_size, FGT_EINVAL, "bad part_rank");
@@ -192,40 +218,53 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     for (int k = 0; k < pw.dim; ++k) NF *= pw.n_f;
     restrict_to_share(T, tp.part_rank, tp.part_size, NF);
   }
-  t.lists_ms = tm.lap();
+  pm.mark();
+  trace_mark(st, "lists");
   DBuf<double> us(nt, st);
   us.zero();
   PwDev P;
-  NufftPlan NP;
+  const NufftPlan* NPp = nullptr;
   if (T.n_dense > 0) {
     pw_setup(P, T, pw);
     // box-local NUFFT plan at tolerance eps/10; eps = 3 exp(-D0^2)
     const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
     const double X = 0.5 * P.side_lc * P.sc * (1.0 + 1e-12);
-    nufft_plan(NP, pw.n_f, tol, X, pw.weights_1d, st);
-    pw_form(P, T, &NP);
-    t.form_ms = tm.lap();
+    trace_mark(st, "setup");
+    NPp = &nufft_plan_cached(pw.n_f, tol, X, pw.weights_1d, st);
+    trace_mark(st, "nufft_plan");
+    pw_form(P, T, NPp);
+    pm.mark();
+    trace_mark(st, "form");
     // psi is produced and consumed in batches of bounded size (<= ~4 GB)
     const int64_t per = P.NH * 16;
     const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)4 << 30) / per));
     for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
       const int64_t hi = std::min(T.n_psi, lo + batch);
       pw_gather(P, T, lo, hi);
-      pw_eval(P, T, us.get(), &NP, lo, hi);
+      pw_eval(P, T, us.get(), NPp, lo, hi);
     }
     P.phi.release();
     P.psi.release();
-    const double ge = tm.lap();
-    t.gather_ms = P.k_gather.ms();
-    t.eval_ms = ge - t.gather_ms;
+  } else {
+    pm.mark();  // empty form phase
   }
+  pm.mark();
+  trace_mark(st, "gather+eval");
   const double D0 = tp.D0;
   direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get(), &P.k_direct);
   if (nt > 0) {
     scatter_kernel<<<grid_for(nt, 256), 256, 0, st>>>(us.get(), T.tgt_perm.get(), nt, u);
     FGT_LAUNCHED();
   }
-  t.direct_ms = tm.lap();
+  pm.mark();
+  trace_mark(st, "direct");
+  t.tree_ms = pm.ms(0);
+  t.lists_ms = pm.ms(1);
+  t.form_ms = pm.ms(2);
+  t.gather_ms = P.k_gather.ms();
+  t.eval_ms = pm.ms(3) - t.gather_ms;
+  t.direct_ms = pm.ms(4);
+  trace_dump();
   t.total_ms = t.tree_ms + t.lists_ms + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
   t.launches = g_launches - l0;
   t.k_form_ms = P.k_form.ms();
@@ -244,8 +283,8 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.n_src_spread = P.n_src_spread;
   t.n_spread_psi = P.n_spread_psi;
   t.n_tgt_spread = P.n_tgt_spread;
-  t.nufft_w = NP.w;
-  t.nufft_G = NP.G;
+  t.nufft_w = NPp ? NPp->w : 0;
+  t.nufft_G = NPp ? NPp->G : 0;
   if (times) *times = t;
 }
 

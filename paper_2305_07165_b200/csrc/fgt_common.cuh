@@ -1,5 +1,7 @@
 // Shared helpers for libfgtcuda (sm_100a).
 #pragma once
+#include <cstdlib>
+#include <chrono>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
@@ -136,6 +138,51 @@ struct KClock {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
 };
+
+// Timeline tracing (FGT_TRACE=1): trace_mark records a CUDA event and the host clock;
+// trace_dump prints, per mark, the device and host times since the first mark (device
+// time that jumps while the host time advances = the GPU waited on the host).
+struct TraceMark {
+  const char* label;
+  cudaEvent_t ev;
+  double host_ms;
+};
+inline std::vector<TraceMark>& trace_marks() {
+  static std::vector<TraceMark> m;
+  return m;
+}
+inline bool trace_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("FGT_TRACE");
+    on = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return on == 1;
+}
+inline void trace_mark(cudaStream_t st, const char* label) {
+  if (!trace_on()) return;
+  TraceMark m;
+  m.label = label;
+  cudaEventCreate(&m.ev);
+  cudaEventRecord(m.ev, st);
+  m.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  trace_marks().push_back(m);
+}
+inline void trace_dump() {
+  if (!trace_on() || trace_marks().empty()) return;
+  auto& m = trace_marks();
+  cudaEventSynchronize(m.back().ev);
+  double prev = 0.0;
+  std::fprintf(stderr, "%-28s %9s %9s %9s\n", "mark", "gpu_ms", "d_gpu", "host_ms");
+  for (auto& x : m) {
+    float g = 0.f;
+    cudaEventElapsedTime(&g, m[0].ev, x.ev);
+    std::fprintf(stderr, "%-28s %9.3f %9.3f %9.3f\n", x.label, g, g - prev, x.host_ms - m[0].host_ms);
+    prev = g;
+  }
+  for (auto& x : m) cudaEventDestroy(x.ev);
+  m.clear();
+}
 
 inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 64) {
   int64_t g = (n + block - 1) / block;

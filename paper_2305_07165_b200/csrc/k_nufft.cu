@@ -14,6 +14,9 @@
 //   3. evaluation runs the transposed chain and interpolates with the same kernel.
 // Partial grids of K-split boxes are summed in a fixed order (deterministic).
 #include <cmath>
+#include <string>
+#include <mutex>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 
@@ -230,11 +233,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-constexpr int TILE_BUF = 32 * TILE_RS;                  // doubles per staged batch
+#ifndef FGT_TILE_PTS
+#define FGT_TILE_PTS 32
+#endif
+constexpr int TILE_PTS = FGT_TILE_PTS;                  // points per staged batch (<= 32)
+constexpr int TILE_BUF = TILE_PTS * TILE_RS;            // doubles per staged batch
 constexpr size_t TILE_SMEM = 4 * (2 * TILE_BUF * sizeof(double) + 32 * (sizeof(double) + 2 * sizeof(int)));
 
 template <int D, int NB>
-__global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
+#ifndef FGT_TILE_MINB
+#define FGT_TILE_MINB 2
+#endif
+__global__ void __launch_bounds__(128, FGT_TILE_MINB) spread_tile_kernel(PlaneArgs a) {
   extern __shared__ double tsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* wbuf = tsm + (size_t)warp * 2 * TILE_BUF;             // 2 staged batches
@@ -252,11 +262,11 @@ __global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
 #pragma unroll
     for (int t = 0; t < NB; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
   const int jend = jb.y + jb.z;
-  const int nbatch = (jb.z + 31) / 32;
+  const int nbatch = (jb.z + TILE_PTS - 1) / TILE_PTS;
   // lane layout of one staged weight row: w1 -> [0, 16), w2 -> [TILE_W2, TILE_W2 + 16)
   const int dst_off = lane < 16 ? lane : TILE_W2 + lane - 16;
   auto issue = [&](int bi) {
-    const int base = jb.y + 32 * bi, cnt = min(32, jend - base);
+    const int base = jb.y + TILE_PTS * bi, cnt = min(TILE_PTS, jend - base);
     double* dst = wbuf + (bi & 1) * TILE_BUF;
     const double* src = a.rw + (int64_t)base * 32 + lane;
     for (int it = 0; it < cnt; ++it) cp_async8(dst + it * TILE_RS + dst_off, src + it * 32);
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
   double nc = 0.0;
   int na1 = 0, na2 = 0;
   auto fetch = [&](int bi) {
-    const int base = jb.y + 32 * bi, cnt = min(32, jend - base);
+    const int base = jb.y + TILE_PTS * bi, cnt = min(TILE_PTS, jend - base);
     if (lane < cnt) {
       const int64_t j = base + lane;
       const int4 r = *reinterpret_cast<const int4*>(a.ra + 4 * j);
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(128, 2) spread_tile_kernel(PlaneArgs a) {
   issue(0);
   fetch(0);
   for (int bi = 0; bi < nbatch; ++bi) {
-    const int cnt = min(32, jend - (jb.y + 32 * bi));
+    const int cnt = min(TILE_PTS, jend - (jb.y + TILE_PTS * bi));
     __syncwarp();
     s_c[lane] = nc;
     s_a1[lane] = na1;
@@ -488,6 +498,27 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wq) {
 
 }  // namespace
 
+const NufftPlan& nufft_plan_cached(int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
+  // key: every input bit that shapes the plan, plus the device
+  int dev = 0;
+  FGT_CUDA(cudaGetDevice(&dev));
+  std::string key(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  key.append(reinterpret_cast<const char*>(&n_f), sizeof(n_f));
+  key.append(reinterpret_cast<const char*>(&tol), sizeof(tol));
+  key.append(reinterpret_cast<const char*>(&X), sizeof(X));
+  if (w1d) key.append(reinterpret_cast<const char*>(w1d), sizeof(double) * n_f);
+  static std::mutex mu;
+  static auto* cache = new std::map<std::string, NufftPlan*>();  // process lifetime
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache->find(key);
+  if (it != cache->end()) return *it->second;
+  auto* p = new NufftPlan();
+  nufft_plan(*p, n_f, tol, X, w1d, st);
+  FGT_CUDA(cudaStreamSynchronize(st));  // usable from any stream from now on
+  (*cache)[key] = p;
+  return *p;
+}
+
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
   N.n_f = n_f;
   N.tol = tol;
@@ -628,8 +659,10 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     wa.w = w;
     wa.gmin = N.gmin;
     wa.G = G;
+    trace_mark(st, "form:alloc");
     spread_taps_kernel<D><<<grid_for(npts * D, 256), 256, 0, st>>>(wa);
     FGT_LAUNCHED();
+    trace_mark(st, "form:taps");
     spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
@@ -641,8 +674,10 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
     FGT_LAUNCHED();
     std::vector<int> hr(2 * njob);
+    trace_mark(st, "form:taps+sort");
     range.to_host(hr.data(), hr.size());
     FGT_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "form:ranges(sync)");
     std::vector<int4> jobs, reds;
     int nscr = 0;
     for (int64_t jid = 0; jid < njob; ++jid) {

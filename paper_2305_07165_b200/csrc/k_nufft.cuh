@@ -22,6 +22,9 @@ struct NufftPlan {
 };
 
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
+// Process-lifetime cache of plans keyed by (device, n_f, tol, X, weights): the host-side
+// quadrature and the six small matrix uploads happen once per parameter set.
+const NufftPlan& nufft_plan_cached(int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
 
 // phi[slot] for the listed P-box slots, by spreading + separable DFT (DMMA GEMMs).
 void nufft_form(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots);

@@ -742,8 +742,10 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
       gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), m.get() + 2 * n);
       FGT_LAUNCHED();
     }
+    trace_mark(st, "setup:meta");
     m.to_host(h.data(), h.size());
     FGT_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "setup:meta(sync)");
     std::copy(h.begin(), h.begin() + n, P.h_cnt.begin());
     std::copy(h.begin() + 2 * n, h.end(), P.h_src.begin());
   }
@@ -795,6 +797,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   P.n_spread_boxes = (int64_t)spread_slots.size();
   P.k_form.begin(st);
   if (!spread_slots.empty()) nufft_form(*N, P, T, spread_slots);
+  trace_mark(st, "form:nufft");
   if (units.empty()) {
     P.k_form.end(st);
     return;
@@ -929,6 +932,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
     }
   }
   P.n_spread_psi += (int64_t)spread_list.size();
+  trace_mark(st, "gather");
   P.k_eval.begin(st);
   if (!spread_list.empty()) nufft_eval(*N, P, T, spread_list, u_sorted);
   if (direct_list.empty()) {

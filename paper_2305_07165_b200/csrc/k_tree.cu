@@ -247,6 +247,16 @@ __global__ void make_children_dev_kernel(const uint64_t* __restrict__ parents, c
   }
 }
 
+// merge of two sorted arrays with no common element: each element's rank in the other
+__global__ void merge_unique_kernel(const uint64_t* __restrict__ a, int64_t na, const uint64_t* __restrict__ b,
+                                    int64_t nb, uint64_t* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < na + nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < na) out[t + lower_bound_dev(b, nb, a[t])] = a[t];
+    else out[t - na + lower_bound_dev(a, na, b[t - na])] = b[t - na];
+  }
+}
+
 __global__ void leaf_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int d,
                                  uint8_t* __restrict__ leaf) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
@@ -262,30 +272,32 @@ template <int D>
 __global__ void balance_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb,
                                     const uint8_t* __restrict__ leaf, int periodic,
                                     uint8_t* __restrict__ split, int* __restrict__ any) {
+  // one thread per (box, neighbour offset): the covering searches are latency chains, so
+  // spread them over 3^d x more threads
   constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nb * NOFF;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = it / NOFF;
+    const int t = (int)(it - i * NOFF);
     if (!leaf[i]) continue;
     uint64_t key = keys[i];
     int l = key_level(key);
     if (l < 2) continue;
+    int o[D];
+    offset_of<D>(t, o);
+    bool self = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) self &= (o[k] == 0);
+    if (self) continue;
     int64_t g[D];
     morton_decode(key_code(key), D, l, g);
-    for (int t = 0; t < NOFF; ++t) {
-      int o[D];
-      offset_of<D>(t, o);
-      bool self = true;
-#pragma unroll
-      for (int k = 0; k < D; ++k) self &= (o[k] == 0);
-      if (self) continue;
-      int64_t n[D];
-      int v[D];
-      if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
-      int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
-      if (j >= 0 && leaf[j] && l - key_level(keys[j]) >= 2) {
-        split[j] = 1;
-        *any = 1;
-      }
+    int64_t n[D];
+    int v[D];
+    if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
+    int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
+    if (j >= 0 && leaf[j] && l - key_level(keys[j]) >= 2) {
+      split[j] = 1;
+      *any = 1;
     }
   }
 }
@@ -298,32 +310,33 @@ __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t 
                                      const uint64_t* __restrict__ pkey, int64_t npts, int l_c,
                                      int64_t n_s, int periodic, uint8_t* __restrict__ split,
                                      int* __restrict__ any) {
+  // one thread per (box, neighbour offset), as balance_flag_kernel
   constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
-  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < (hi - lo) * NOFF;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = lo + it / NOFF;
+    const int t = (int)(it % NOFF);
     if (!leaf[i]) continue;
     uint64_t key = keys[i];
     if (key_level(key) != l_c) continue;
+    int o[D];
+    offset_of<D>(t, o);
+    bool self = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) self &= (o[k] == 0);
+    if (self) continue;
     uint64_t c = key_code(key);
     int64_t cnt = prefix_hi(pkey, npts, c, 0) - prefix_lo(pkey, npts, c, 0);
     if (cnt <= n_s) continue;
     int64_t g[D];
     morton_decode(c, D, l_c, g);
-    for (int t = 0; t < NOFF; ++t) {
-      int o[D];
-      offset_of<D>(t, o);
-      bool self = true;
-#pragma unroll
-      for (int k = 0; k < D; ++k) self &= (o[k] == 0);
-      if (self) continue;
-      int64_t n[D];
-      int v[D];
-      if (!neighbor_cell<D>(g, o, l_c, periodic, n, v)) continue;
-      int64_t j = find_covering_dev(keys, nb, D, l_c, morton_encode(n, D, l_c));
-      if (j >= 0 && leaf[j] && key_level(keys[j]) == l_c - 1) {
-        split[j] = 1;
-        *any = 1;
-      }
+    int64_t n[D];
+    int v[D];
+    if (!neighbor_cell<D>(g, o, l_c, periodic, n, v)) continue;
+    int64_t j = find_covering_dev(keys, nb, D, l_c, morton_encode(n, D, l_c));
+    if (j >= 0 && leaf[j] && key_level(keys[j]) == l_c - 1) {
+      split[j] = 1;
+      *any = 1;
     }
   }
 }
@@ -458,14 +471,6 @@ struct BoxSet {
   int64_t n = 0;
 };
 
-void sort_keys(BoxSet& B, CubTmp& tmp, cudaStream_t st) {
-  DBuf<uint64_t> out(B.n, st);
-  size_t bytes = 0;
-  FGT_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, B.keys.get(), out.get(), (int)B.n, 0, 64, st));
-  FGT_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(bytes, st), bytes, B.keys.get(), out.get(), (int)B.n, 0, 64, st));
-  count_launch();
-  B.keys = std::move(out);
-}
 
 // Split the boxes flagged in `flag` (aligned with keys[lo, lo+n)): append their 2^d
 // children and re-sort.  Returns the number of boxes split.
@@ -481,13 +486,14 @@ int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int
   int64_t k = read_scalar(nsel.get(), st);
   if (k == 0) return 0;
   const int64_t nc = (int64_t)k << d;
-  DBuf<uint64_t> grown(B.n + nc, st);
-  FGT_CUDA(cudaMemcpyAsync(grown.get(), B.keys.get(), B.n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
-  make_children_kernel<<<grid_for(nc, 256), 256, 0, st>>>(sel.get(), k, d, grown.get() + B.n);
+  // the children of the (sorted, stably selected) flagged leaves are sorted and new: merge
+  DBuf<uint64_t> kids(nc, st), grown(B.n + nc, st);
+  make_children_kernel<<<grid_for(nc, 256), 256, 0, st>>>(sel.get(), k, d, kids.get());
+  FGT_LAUNCHED();
+  merge_unique_kernel<<<grid_for(B.n + nc, 256), 256, 0, st>>>(B.keys.get(), B.n, kids.get(), nc, grown.get());
   FGT_LAUNCHED();
   B.keys = std::move(grown);
   B.n += nc;
-  sort_keys(B, tmp, st);
   return k;
 }
 
@@ -510,7 +516,7 @@ void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st) {
     split.zero();
     leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
     FGT_LAUNCHED();
-    balance_flag_kernel<D><<<grid_for(B.n, 128), 128, 0, st>>>(B.keys.get(), B.n, leaf.get(), periodic,
+    balance_flag_kernel<D><<<grid_for(B.n * 27, 128), 128, 0, st>>>(B.keys.get(), B.n, leaf.get(), periodic,
                                                                  split.get(), any.get());
     FGT_LAUNCHED();
     if (split_flagged(B, 0, B.n, split.get(), D, tmp, st) == 0) return;
@@ -540,6 +546,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   } else {
     double lo[3], hi[3];
     device_bbox(src, ns, tgt, nt, D, lo, hi, st);
+    trace_mark(st, "tree:bbox(sync)");
     double spread = 0.0;
     for (int k = 0; k < D; ++k) {
       T.root_center[k] = 0.5 * (lo[k] + hi[k]);
@@ -618,10 +625,12 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       cap.push_back(kc << D);
     }
     std::vector<int64_t> hsel(cap.size() - 1);
+    trace_mark(st, "tree:descent");
     if (!hsel.empty()) {
       nsel.to_host(hsel.data(), hsel.size());
       FGT_CUDA(cudaStreamSynchronize(st));
     }
+    trace_mark(st, "tree:descent(sync)");
     std::vector<int64_t> lsize(1, 1);
     for (int64_t k : hsel) {
       if (k == 0) break;
@@ -640,6 +649,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
 
   // ---- balance + dense-cutoff-leaf fix to the joint fixpoint (tree.py:504-523)
   balance_rounds<D>(B, tp.periodic, tmp, st);
+  trace_mark(st, "tree:balance");
   if (l_c >= 1) {
     DBuf<int> any(1, st);
     for (int round = 0; round < 4096; ++round) {
@@ -647,7 +657,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       split.zero();
       leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
       FGT_LAUNCHED();
-      densefix_flag_kernel<D><<<grid_for(B.n, 128), 128, 0, st>>>(
+      densefix_flag_kernel<D><<<grid_for(B.n * 27, 128), 128, 0, st>>>(
           B.keys.get(), B.n, 0, B.n, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
           split.get(), any.get());
       FGT_LAUNCHED();
@@ -657,6 +667,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   }
 
   // ---- finalise boxes
+  trace_mark(st, "tree:densefix");
   const int64_t nb = B.n;
   T.nb = nb;
   // level offsets (l_c + 2), dense-box count, leaf count: one host round trip at the end
@@ -743,8 +754,10 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     count_launch();
     std::vector<int64_t> h(l_c + 4);
+    trace_mark(st, "tree:finalize");
     fin.to_host(h.data(), h.size());
     FGT_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "tree:finalize(sync)");
     T.level_off.assign(h.begin(), h.begin() + l_c + 2);
     T.n_dense = h[l_c + 2];
     T.n_leaves = h[l_c + 3];
@@ -794,86 +807,70 @@ namespace {
 // covering leaf (colleague or coarse) or, when the colleague is subdivided, its
 // children touching T (fine neighbours; leaves by balance).  Deduplicated on (S, v).
 template <int D>
-struct NbrEntry {
-  int64_t box;
-  int v[D];
-};
-
-template <int D>
-__device__ int enumerate_neighbors(const uint64_t* __restrict__ keys, int64_t nb,
-                                   const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
-                                   const int64_t* __restrict__ children, int64_t T, int periodic,
-                                   NbrEntry<D>* out) {
-  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
-  constexpr int NC = 1 << D;
-  uint64_t key = keys[T];
-  int l = key_level(key);
-  int64_t g[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) g[k] = coords[T * D + k];
-  int cnt = 0;
-  auto push = [&](int64_t b, const int* v) {
-    for (int e = 0; e < cnt; ++e) {
-      bool same = out[e].box == b;
-#pragma unroll
-      for (int k = 0; k < D; ++k) same &= out[e].v[k] == v[k];
-      if (same) return;
-    }
-    out[cnt].box = b;
-#pragma unroll
-    for (int k = 0; k < D; ++k) out[cnt].v[k] = v[k];
-    ++cnt;
-  };
-  for (int t = 0; t < NOFF; ++t) {
-    int o[D];
-    offset_of<D>(t, o);
-    int64_t n[D];
-    int v[D];
-    if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
-    int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
-    if (j < 0) continue;
-    if (leaf[j]) {
-      push(j, v);
-    } else {
-      const int64_t side = (int64_t)1 << l;
-      for (int c = 0; c < NC; ++c) {
-        int64_t ch = children[j * NC + c];
-        bool touch = true;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          int64_t gc = coords[ch * D + k] + 2 * (int64_t)v[k] * side;
-          touch &= (gc >= 2 * g[k] - 1) && (gc <= 2 * g[k] + 2);
-        }
-        if (touch) push(ch, v);
-      }
-    }
-  }
-  return cnt;
-}
-
-template <int D>
 constexpr int list_cap() { return D == 1 ? 4 : (D == 2 ? 16 : 64); }  // <= 4^d entries per leaf
 
 // One enumeration per target leaf: P entries (dense slot) then D entries (box) into the
 // leaf's fixed slots [i*CAP, (i+1)*CAP), plus their counts.
+// Neighbour resolution, one thread per (target leaf, offset): the box covering the
+// neighbour cell (-1 if none / outside) and the packed image shift.  The covering searches
+// are latency chains, so they get 3^d x the threads of the per-leaf enumeration.
+template <int D>
+__global__ void __launch_bounds__(128) lists_resolve_kernel(
+    const int64_t* __restrict__ tleaves, const int64_t* __restrict__ ntl_dev, const uint64_t* __restrict__ keys,
+    int64_t nb, const int64_t* __restrict__ coords, int periodic, int32_t* __restrict__ cov_j,
+    int32_t* __restrict__ cov_v) {
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  const int64_t ntl = *ntl_dev;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < ntl * NOFF;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = it / NOFF;
+    const int t = (int)(it - i * NOFF);
+    const int64_t T = tleaves[i];
+    const int l = key_level(keys[T]);
+    int64_t g[D], n[D];
+    int o[D], v[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = coords[T * D + k];
+    offset_of<D>(t, o);
+    int32_t j = -1, pv = 0;
+    if (neighbor_cell<D>(g, o, l, periodic, n, v)) {
+      j = (int32_t)find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
+#pragma unroll
+      for (int k = 0; k < D; ++k) pv |= (v[k] + 1) << (2 * k);
+    }
+    cov_j[it] = j;
+    cov_v[it] = pv;
+  }
+}
+
+// One enumeration per target leaf over its resolved neighbours (the reference order: offsets
+// in order, a non-leaf neighbour's touching children in child order; a coarse leaf covering
+// several neighbour cells once, at its first offset): P entries (dense slot) from the front
+// of the leaf's fixed slots [i*CAP, (i+1)*CAP), D entries (box) from the back, plus counts.
 template <int D>
 __global__ void __launch_bounds__(128) lists_kernel(
-    const int64_t* __restrict__ tleaves, const int64_t* __restrict__ ntl_dev, const uint64_t* __restrict__ keys, int64_t nb,
+    const int64_t* __restrict__ tleaves, const int64_t* __restrict__ ntl_dev,
     const uint8_t* __restrict__ leaf, const int64_t* __restrict__ coords,
     const int64_t* __restrict__ children, const int64_t* __restrict__ scount,
-    const int64_t* __restrict__ dense_slot, int periodic, int64_t* __restrict__ pcnt,
+    const int64_t* __restrict__ dense_slot, const uint64_t* __restrict__ keys,
+    const int32_t* __restrict__ cov_j, const int32_t* __restrict__ cov_v, int64_t* __restrict__ pcnt,
     int64_t* __restrict__ dcnt, int64_t* __restrict__ fix_id, int32_t* __restrict__ fix_v) {
   constexpr int CAP = list_cap<D>();
-  NbrEntry<D> ent[CAP];
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  constexpr int NC = 1 << D;
   const int64_t ntl = *ntl_dev;  // launch covers a capacity
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntl;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t T = tleaves[i];
-    const int cnt = enumerate_neighbors<D>(keys, nb, leaf, coords, children, T, periodic, ent);
+    const int l = key_level(keys[T]);
+    const int64_t side = (int64_t)1 << l;
+    int64_t g[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = coords[T * D + k];
+    const int32_t* cj = cov_j + i * NOFF;
+    const int32_t* cv = cov_v + i * NOFF;
     int np_ = 0, nd_ = 0;
-    // P entries from the front of the slot range, D entries from the back
-    for (int e = 0; e < cnt; ++e) {
-      const int64_t S = ent[e].box;
+    auto emit = [&](int64_t S, int pv) {
       const int64_t slot = dense_slot[S];
       int at;
       if (slot >= 0) {
@@ -883,10 +880,32 @@ __global__ void __launch_bounds__(128) lists_kernel(
         at = CAP - 1 - nd_++;
         fix_id[i * CAP + at] = S;
       } else {
-        continue;
+        return;
       }
 #pragma unroll
-      for (int k = 0; k < D; ++k) fix_v[(i * CAP + at) * D + k] = ent[e].v[k];
+      for (int k = 0; k < D; ++k) fix_v[(i * CAP + at) * D + k] = ((pv >> (2 * k)) & 3) - 1;
+    };
+    for (int t = 0; t < NOFF; ++t) {
+      const int32_t j = cj[t];
+      if (j < 0) continue;
+      const int pv = cv[t];
+      if (leaf[j]) {
+        // a coarse leaf covering several neighbour cells is listed once (first offset)
+        bool seen = false;
+        for (int u = 0; u < t; ++u) seen |= (cj[u] == j && cv[u] == pv);
+        if (!seen) emit(j, pv);
+      } else {
+        for (int c = 0; c < NC; ++c) {
+          const int64_t ch = children[(int64_t)j * NC + c];
+          bool touch = true;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const int64_t gc = coords[ch * D + k] + 2 * (int64_t)(((pv >> (2 * k)) & 3) - 1) * side;
+            touch &= (gc >= 2 * g[k] - 1) && (gc <= 2 * g[k] + 2);
+          }
+          if (touch) emit(ch, pv);
+        }
+      }
     }
     pcnt[i] = np_;
     dcnt[i] = nd_;
@@ -974,9 +993,14 @@ static void build_lists_impl(TreeDev& T) {
   DBuf<int64_t> fix_id(cap * CAP, st);
   DBuf<int32_t> fix_v(cap * CAP * D, st);
   if (cap > 0) {
+    constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+    DBuf<int32_t> cov_j(cap * NOFF, st), cov_v(cap * NOFF, st);
+    lists_resolve_kernel<D><<<grid_for(cap * NOFF, 128), 128, 0, st>>>(
+        tl.get(), cnt.get(), T.bkey.get(), nb, T.coords.get(), T.periodic, cov_j.get(), cov_v.get());
+    FGT_LAUNCHED();
     lists_kernel<D><<<grid_for(cap, 128), 128, 0, st>>>(
-        tl.get(), cnt.get(), T.bkey.get(), nb, T.is_leaf.get(), T.coords.get(), T.children.get(),
-        T.src_count.get(), T.dense_slot.get(), T.periodic, pcnt.get(), dcnt.get(), fix_id.get(),
+        tl.get(), cnt.get(), T.is_leaf.get(), T.coords.get(), T.children.get(), T.src_count.get(),
+        T.dense_slot.get(), T.bkey.get(), cov_j.get(), cov_v.get(), pcnt.get(), dcnt.get(), fix_id.get(),
         fix_v.get());
     FGT_LAUNCHED();
   }
@@ -998,8 +1022,10 @@ static void build_lists_impl(TreeDev& T) {
   FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), cnt.get() + 3, (int)cap, st));
   count_launch(2);
   int64_t h[4];
+  trace_mark(st, "lists:enum");
   cnt.to_host(h, 4);
   FGT_CUDA(cudaStreamSynchronize(st));
+  trace_mark(st, "lists:enum(sync)");
   const int64_t ntl = h[0];
   T.n_dtgt = ntl;
   T.n_p = h[1];
