@@ -669,6 +669,18 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     int bits = 8 * D;
     while (((int64_t)1 << (bits - 8 * D)) < nbat) ++bits;
     sort_pairs_key(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
+    // records first: the GPU builds them while the host waits for the job ranges
+    DBuf<double> rw, rq, rw0;
+    DBuf<int> ra;
+    if (D >= 2) {
+      rw.alloc(npts * 32, st);
+      rq.alloc(npts, st);
+      ra.alloc(npts * 4, st);
+      if (D == 3) rw0.alloc(npts * 16, st);
+      sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
+          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, rw.get(), rq.get(), ra.get(), rw0.get());
+      FGT_LAUNCHED();
+    }
     const int64_t njob = D == 2 ? nbat : nbat * G;
     DBuf<int> range(2 * njob, st);
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
@@ -694,17 +706,6 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     jobs_d.from_host(jobs.data(), jobs.size());
     if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
     DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * job_cells, st);
-    DBuf<double> rw, rq, rw0;
-    DBuf<int> ra;
-    if (D >= 2) {
-      rw.alloc(npts * 32, st);
-      rq.alloc(npts, st);
-      ra.alloc(npts * 4, st);
-      if (D == 3) rw0.alloc(npts * 16, st);
-      sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
-          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, rw.get(), rq.get(), ra.get(), rw0.get());
-      FGT_LAUNCHED();
-    }
     PlaneArgs pa;
     pa.rw = rw.get();
     pa.rq = rq.get();
