@@ -240,6 +240,45 @@ constexpr int TILE_PTS = FGT_TILE_PTS;                  // points per staged bat
 constexpr int TILE_BUF = TILE_PTS * TILE_RS;            // doubles per staged batch
 constexpr size_t TILE_SMEM = 4 * (2 * TILE_BUF * sizeof(double) + 32 * (sizeof(double) + 2 * sizeof(int)));
 
+// rank-4 update of the 3x3 tile window at (BL, TL) (tile kernel, see below)
+template <int NB, int BL, int TL>
+__device__ __forceinline__ void tile_window(double (&acc)[NB][NB][2], const double* __restrict__ w1,
+                                            const double* __restrict__ w2, int jr, double cj, int a1,
+                                            int a2, bool valid, int w, int lane) {
+  double A[3], B[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int d = 8 * (BL + i) + (lane >> 2) - a1;
+    A[i] = (valid && (unsigned)d < (unsigned)w) ? cj * w1[jr + d] : 0.0;
+    const int e = 8 * (TL + i) + (lane >> 2) - a2;
+    B[i] = (valid && (unsigned)e < (unsigned)w) ? w2[jr + e] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dmma2(acc[BL + i][TL + k][0], acc[BL + i][TL + k][1], A[i], B[k]);
+}
+
+template <int NB>
+__device__ __forceinline__ void window_dispatch(int widx, double (&acc)[NB][NB][2], const double* w1,
+                                                const double* w2, int jr, double cj, int a1, int a2,
+                                                bool valid, int w, int lane) {
+  constexpr int NW = NB - 2;
+  switch (widx) {
+#define FGT_WIN(K)                                                                        \
+  case K:                                                                                 \
+    if constexpr ((K) < NW * NW) tile_window<NB, (K) / NW, (K) % NW>(acc, w1, w2, jr, cj, a1, a2, valid, w, lane); \
+    break;
+    FGT_WIN(0) FGT_WIN(1) FGT_WIN(2) FGT_WIN(3) FGT_WIN(4) FGT_WIN(5) FGT_WIN(6) FGT_WIN(7)
+    FGT_WIN(8) FGT_WIN(9) FGT_WIN(10) FGT_WIN(11) FGT_WIN(12) FGT_WIN(13) FGT_WIN(14) FGT_WIN(15)
+    FGT_WIN(16) FGT_WIN(17) FGT_WIN(18) FGT_WIN(19) FGT_WIN(20) FGT_WIN(21) FGT_WIN(22) FGT_WIN(23)
+    FGT_WIN(24) FGT_WIN(25) FGT_WIN(26) FGT_WIN(27) FGT_WIN(28) FGT_WIN(29) FGT_WIN(30) FGT_WIN(31)
+    FGT_WIN(32) FGT_WIN(33) FGT_WIN(34) FGT_WIN(35)
+#undef FGT_WIN
+    default: break;
+  }
+}
+
 template <int D, int NB>
 #ifndef FGT_TILE_MINB
 #define FGT_TILE_MINB 2
@@ -316,7 +355,16 @@ __global__ void __launch_bounds__(128, FGT_TILE_MINB) spread_tile_kernel(PlaneAr
       const int clo = __reduce_min_sync(0xffffffffu, valid ? a2 : 1 << 20);
       const int chi = __reduce_max_sync(0xffffffffu, valid ? a2 + w - 1 : -1);
       const int bl = rlo >> 3, bh = rhi >> 3, tl = clo >> 3, th = chi >> 3;
-      // fragments only for the touched tiles (uniform branches skip the rest)
+      if constexpr (NB >= 3) {
+        // a 3x3-tile window covers every 4-point group (span <= 11 + 7 + spread): one
+        // straight-line block of 9 unpredicated DMMAs per window position
+        if (bh - bl <= 2 && th - tl <= 2) {
+          const int wb = min(bl, NB - 3), wt = min(tl, NB - 3);
+          window_dispatch<NB>(wb * (NB - 2) + wt, acc, w1, w2, j * TILE_RS, cj, a1, a2, valid, w, lane);
+          continue;
+        }
+      }
+      // wide groups: fragments only for the touched tiles (uniform branches skip the rest)
       double B[NB];
 #pragma unroll
       for (int t = 0; t < NB; ++t) {
