@@ -9,7 +9,11 @@ namespace fgt {
 // translation phases are conj-symmetric).  For d >= 2 only nh = n_f/2 + 1 planes along
 // axis 0 are stored: plane s holds m_0 = s for s < n_f/2 and m_0 = -n_f/2 for s = n_f/2
 // (the one plane without a partner); the potential Re sum_m psi_m e^{ik.x} then weighs
-// plane s by 1 (m_0 = 0 or -n_f/2) or 2 (the pair +-m_0).  Exact in exact arithmetic.
+// plane s by 1 (m_0 = 0 or -n_f/2) or 2 (the pair +-m_0).  The pairing m <-> -m is exact
+// for every mode whose other components lie in [-n_f/2+1, n_f/2-1]; a paired-plane mode
+// with some m_k = -n_f/2 (k >= 1) stands in for its out-of-range partner m_k = +n_f/2.
+// Those modes carry weight w_{n_f/2}/w_0 = exp(-n_f^2 h^2/16) <= 0.24 eps at every
+// configuration, so the quadrature changes by O(eps/16) relative.
 __host__ __device__ inline int half_plane_mi(int s, int n_f, bool half) {
   return half ? (s + n_f / 2) % n_f : s;
 }
