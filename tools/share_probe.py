@@ -1,0 +1,59 @@
+"""Per-rank cost of the strong-scaling shares, measured on ONE GPU.
+
+    python tools/share_probe.py [--sizes 1,2,4,8] [--n 1000000]
+
+For each world size P it runs rank r's share (fgt_points_device(..., share=(r, P))) for
+every r on the same GPU, one after another, and reports the per-rank CUDA-event step times.
+The max over ranks is what a P-GPU run of bench.py would measure per step (each rank
+rebuilds the replicated tree and lists, forms the expansions its targets need, and evaluates
+its own targets; there is no data-path collective).  Config-2 input (bench.gen_config2).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2305_07165_b200 import fgt_points_device  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1,2,4,8")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    y, q, x = bench.gen_config2(a.n, a.n)
+    dy, dq, dx = (torch.from_numpy(v).cuda() for v in (y, q, x))
+    out = {}
+    for P in (int(s) for s in a.sizes.split(",")):
+        per = []
+        for r in range(P):
+            best = None
+            for _ in range(a.reps):
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                _, t = fgt_points_device(dy, dq, dx, 1e-4, 1e-9, 200, return_times=True, share=(r, P))
+                e.record()
+                torch.cuda.synchronize()
+                ms = s.elapsed_time(e)
+                if best is None or ms < best[0]:
+                    best = (ms, {k: round(t[k], 3) for k in ("tree_ms", "lists_ms", "form_ms", "gather_ms",
+                                                            "eval_ms", "direct_ms")},
+                            dict(n_spread_boxes=t["n_spread_boxes"], n_src_spread=t["n_src_spread"],
+                                 n_psi=t["n_psi"], n_tgt_psi=t["n_tgt_psi"]))
+            per.append({"rank": r, "ms": round(best[0], 3), **best[1], **best[2]})
+        mx = max(p["ms"] for p in per)
+        out[P] = {"max_rank_ms": mx, "points_per_s": 2 * a.n / (mx * 1e-3), "ranks": per}
+        print(json.dumps({"P": P, "max_rank_ms": mx, "est_points_per_s": 2 * a.n / (mx * 1e-3),
+                          "rank_ms": [p["ms"] for p in per],
+                          "slowest": max(per, key=lambda p: p["ms"])}))
+    return out
+
+
+if __name__ == "__main__":
+    main()
