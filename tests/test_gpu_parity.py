@@ -268,3 +268,67 @@ def test_shares_sum_to_full(cuda, size):
     nz = sum((p != 0).astype(int) for p in parts)
     assert nz.max() <= 1
     assert np.array_equal(sum(parts), full)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_no_sources_or_no_targets(cuda):
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(21)
+    x = r.uniform(-0.5, 0.5, (300, 2))
+    u = fgt_points(np.zeros((0, 2)), np.zeros(0), x, 1e-3, 1e-6, 10)
+    assert u.shape == (300,) and np.all(u == 0)
+    y = r.uniform(-0.5, 0.5, (300, 2))
+    u = fgt_points(y, r.uniform(-1, 1, 300), np.zeros((0, 2)), 1e-3, 1e-6, 10)
+    assert u.shape == (0,)
+
+
+def test_coincident_sources(cuda):
+    """All sources at one point (zero-extent bounding box of the sources)."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(22)
+    y = np.tile([[0.1, -0.2, 0.3]], (3000, 1))
+    q = r.uniform(-1, 1, 3000)
+    x = np.vstack([y[:1], r.uniform(-0.2, 0.4, (500, 3))])
+    u = fgt_points(y, q, x, 1e-3, 1e-9, 50)
+    ex = q.sum() * np.exp(-((x - y[0]) ** 2).sum(1) / 1e-3)
+    assert rel(u, ex) <= 10 * 1e-9
+
+
+def test_grid_aligned_points_tree_exact(cuda):
+    """Coordinates on dyadic grid lines (box boundaries at every level): the Morton
+    assignment of boundary points must match the reference's arithmetic exactly."""
+    r = np.random.default_rng(23)
+    for periodic in (False, True):
+        y = r.integers(-32, 32, (3000, 2)) / 64.0
+        x = r.integers(-32, 32, (2000, 2)) / 64.0
+        a, la, tg = gpu_canonical(y, x, 20, 1e-4, 1e-6, periodic)
+        b, lb, to = oracle_canonical(y, x, 20, 1e-4, 1e-6, periodic)
+        assert la == lb and tg.root_side == to.root_side
+        assert a == b
+
+
+@pytest.mark.parametrize("n_s", [1, 100000])
+def test_extreme_leaf_capacity(cuda, n_s):
+    """n_s = 1 (deepest trees, every occupied l_c leaf dense) and n_s >= N (no dense box:
+    everything through the direct near field)."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(24)
+    y = clustered(r, 3000, 2)
+    x = r.uniform(-0.5, 0.5, (2000, 2))
+    q = r.standard_normal(3000)
+    u = fgt_points(y, q, x, 1e-4, 1e-8, n_s)
+    ex = ofgt.direct_oracle(y, q, x, 1e-4, "free")
+    assert rel(u, ex) <= 10 * 1e-8
+
+
+def test_disjoint_sources_and_targets(cuda):
+    """Targets far from every source: empty P- and D-lists for most target leaves."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(25)
+    y = r.uniform(-0.5, -0.3, (4000, 3))
+    x = np.vstack([r.uniform(0.3, 0.5, (2000, 3)), r.uniform(-0.5, -0.3, (200, 3))])
+    q = r.uniform(-1, 1, 4000)
+    u = fgt_points(y, q, x, 1e-4, 1e-9, 40)
+    ex = ofgt.direct_oracle(y, q, x, 1e-4, "free")
+    assert np.all(u[:2000] == 0)
+    assert rel(u, ex) <= 10 * 1e-9
