@@ -101,7 +101,10 @@ typedef struct fgt_pw_params {
 /* Tree construction controls (build_point_tree, tree.py:442-527). */
 typedef struct fgt_tree_params {
   int32_t dim;
-  int32_t periodic;     /* 0 free space, 1 unit cell [-1/2,1/2)^d */
+  int32_t periodic;     /* 0 free space, 1 unit cell [-1/2,1/2)^d with one image layer
+                           (l_c >= 2), 2 root Fourier-series regime (l_c <= 1,
+                           PAPER.md:1449-1453): the unit cell is the single box, n_s is
+                           ignored, no image neighbours, no near field */
   int64_t n_s;          /* split boxes with more than n_s sources+targets */
   double D0;            /* cutoff factor (as above) */
   double delta;

@@ -178,6 +178,46 @@ def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free", 
     return a.potentials()
 
 
+def fgt_points_periodic_root(sources, charges, targets, delta, epsilon):
+    """Periodic transform in the root Fourier-series regime (cutoff level <= 1):
+    PAPER.md:1449-1453 ("the plane-wave expansion of the periodic Gaussian G_p on the
+    entire box B ... can be used directly"), series PAPER.md:363-383 with n_p
+    and coefficients of planewave.periodic_params (planewave.py:148-155):
+
+        u_i = Re sum_{n in [-n_p, n_p]^d} prod_k c(n_k) e^{2 pi i n.x_i} sum_j q_j e^{-2 pi i n.y_j}
+
+    computed as dense separable DFTs (small problems only)."""
+    src = np.atleast_2d(np.asarray(sources, dtype=float))
+    tgt = np.atleast_2d(np.asarray(targets, dtype=float))
+    q = np.asarray(charges, dtype=float)
+    d = tgt.shape[1] if tgt.size else src.shape[1]
+    eps = clamp_eps(epsilon)
+    n_p = int(np.ceil(np.sqrt(np.log(1.0 / eps)) / (np.pi * np.sqrt(delta))))
+    n = np.arange(-n_p, n_p + 1)
+    c = np.sqrt(np.pi * delta) * np.exp(-(np.pi * np.sqrt(delta) * n) ** 2)
+    # outgoing: phi[n_0, .., n_{d-1}] = prod_k c(n_k) sum_j q_j prod_k e^{-2 pi i n_k y_jk}
+    E = [np.exp(-2j * np.pi * np.multiply.outer(src[:, k], n)) for k in range(d)]
+    if d == 1:
+        phi = q @ E[0]
+    elif d == 2:
+        phi = np.einsum("j,ja,jb->ab", q, E[0], E[1])
+    else:
+        phi = np.einsum("j,ja,jb,jc->abc", q, E[0], E[1], E[2])
+    for k in range(d):
+        shape = [1] * d
+        shape[k] = -1
+        phi = phi * c.reshape(shape)
+    # evaluation at the targets
+    F = [np.exp(2j * np.pi * np.multiply.outer(tgt[:, k], n)) for k in range(d)]
+    if d == 1:
+        u = F[0] @ phi
+    elif d == 2:
+        u = np.einsum("ia,ib,ab->i", F[0], F[1], phi)
+    else:
+        u = np.einsum("ia,ib,ic,abc->i", F[0], F[1], F[2], phi)
+    return u.real
+
+
 def direct_oracle(sources, charges, targets, delta, boundary="free"):
     """Exact O(NM) sums; periodic via per-axis periodic kernels."""
     src = np.atleast_2d(np.asarray(sources, dtype=float))

@@ -43,6 +43,7 @@ double box_dft_cost(int D, int G, int n_f) {
 bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double tap_cost) {
   // NF: stored modes per expansion
   if (!N) return false;
+  if (N->G > 64) return false;  // beyond the spreading kernels' grid (wide root series)
   const int mode = nufft_mode();
   if (mode == 1) return false;
   if (mode == 2) return npts > 0;
@@ -696,7 +697,9 @@ void launch_eval(const EvalArgs& ea, int64_t n_psi, cudaStream_t st) {
 
 void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   FGT_REQUIRE(pw.dim == T.d, FGT_EINVAL, "plane-wave dim != tree dim");
-  FGT_REQUIRE(pw.n_f >= 2 && pw.n_f % 2 == 0, FGT_EINVAL, "n_f must be even and >= 2");
+  // n_f even: the quadrature's modes -n_f/2 .. n_f/2-1; odd: the periodic root series
+  // -n_p .. n_p (n_f = 2 n_p + 1)
+  FGT_REQUIRE(pw.n_f >= 2, FGT_EINVAL, "n_f must be >= 2");
   FGT_REQUIRE(pw.n_f <= 64, FGT_ERANGE, "n_f > 64 not supported by the plane-wave kernels");
   cudaStream_t st = T.st;
   P.d = T.d;

@@ -18,7 +18,9 @@ __host__ __device__ inline int half_plane_mi(int s, int n_f, bool half) {
   return half ? (s + n_f / 2) % n_f : s;
 }
 __host__ __device__ inline double half_plane_w(int s, int n_f, bool half) {
-  return (!half || s == 0 || s == n_f / 2) ? 1.0 : 2.0;
+  // odd n_f (symmetric modes -n_f/2 .. n_f/2, the periodic root series): only m_0 = 0 is
+  // unpaired
+  return (!half || s == 0 || ((n_f & 1) == 0 && s == n_f / 2)) ? 1.0 : 2.0;
 }
 
 struct PwDev {

@@ -535,11 +535,18 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   T.n_s = tp.n_s;
   T.periodic = tp.periodic;
   FGT_REQUIRE(T.ntot > 0, FGT_EINVAL, "need at least one source or target");
-  FGT_REQUIRE(tp.n_s >= 1, FGT_EINVAL, "n_s must be >= 1");
+  FGT_REQUIRE(tp.n_s >= 1 || tp.periodic == 2, FGT_EINVAL, "n_s must be >= 1");
+  FGT_REQUIRE(tp.periodic >= 0 && tp.periodic <= 2, FGT_EINVAL, "periodic must be 0, 1 or 2");
   FGT_REQUIRE(T.ntot < ((int64_t)1 << 31), FGT_ERANGE, "more than 2^31 points");
 
   // ---- root and cutoff level (tree.py:458-472, cutoff_level :207-233)
-  if (tp.periodic) {
+  if (tp.periodic == 2) {
+    // root Fourier-series regime: the unit cell is the only box
+    for (int k = 0; k < D; ++k) T.root_center[k] = 0.0;
+    T.root_side = 1.0;
+    T.l_c = 0;
+    T.periodic = 0;  // the series carries every image: no image neighbours
+  } else if (tp.periodic) {
     for (int k = 0; k < D; ++k) T.root_center[k] = 0.0;
     T.root_side = 1.0;
     T.l_c = tp.l_c_periodic;

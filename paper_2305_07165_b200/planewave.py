@@ -103,3 +103,26 @@ def cutoff_level(delta, epsilon, L0=1.0, kind="density"):
         s = L0 / 2 ** l_c
         return l_c, max(2.0 * s / np.sqrt(delta), D0)
     raise ValueError(f"unknown tree kind {kind!r}")
+
+
+@dataclass(frozen=True)
+class PeriodicSeries:
+    """Truncated Fourier series of the periodic Gaussian on the unit cell:
+    G_p(x) ~= sum_{|n| <= n_p} coeffs[n + n_p] exp(2 pi i n x), coeffs = sqrt(pi delta)
+    exp(-(pi sqrt(delta) n)^2), n_p = ceil(sqrt(log(1/eps)) / (pi sqrt(delta)))
+    (planewave.periodic_params, /root/reference/pkg/src/fgt/planewave.py:148-155)."""
+
+    epsilon: float
+    delta: float
+    n_p: int
+    coeffs: np.ndarray = field(repr=False)
+
+
+def periodic_params(epsilon, delta):
+    if epsilon <= 0 or delta <= 0:
+        raise ValueError("epsilon and delta must be positive")
+    n_p = int(np.ceil(np.sqrt(np.log(1.0 / epsilon)) / (np.pi * np.sqrt(delta))))
+    n = np.arange(-n_p, n_p + 1)
+    c = np.sqrt(np.pi * delta) * np.exp(-(np.pi * np.sqrt(delta) * n) ** 2)
+    return PeriodicSeries(float(epsilon), float(delta), n_p, c)
+

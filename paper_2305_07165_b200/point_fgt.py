@@ -17,7 +17,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, pw_params
+from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_factor, periodic_params, pw_params
 from .tree import tree_params
 
 
@@ -33,19 +33,29 @@ class FgtParams:
         if not 0 <= rank < size:
             raise ValueError(f"bad share {share!r}")
         self.tp.part_rank, self.tp.part_size = int(rank), int(size)
-        if periodic and not (delta < PERIODIC_IMAGE_DELTA and self.l_c_periodic >= 2):
-            raise ValueError(
-                "periodic transform implemented for the image regime (delta < 1/36, "
-                "cutoff level >= 2); the root Fourier-series regime is not supported")
-        # NUFFT/plane-wave rule for the cutoff boxes
-        self.pwq = pw_params(float(epsilon), delta, R=self.R, dim=dim)
-        self._w = np.ascontiguousarray(self.pwq.weights_1d, dtype=np.float64)
         pw = _lib.FgtPwParams()
         pw.dim = dim
-        pw.n_f = self.pwq.n_f
         pw.delta = float(delta)
-        pw.D0 = float(self.pwq.D0)
-        pw.h = float(self.pwq.h)
+        self.root_series = bool(periodic) and not (delta < PERIODIC_IMAGE_DELTA and self.l_c_periodic >= 2)
+        if self.root_series:
+            # l_c <= 1: the periodic Gaussian's Fourier
+            # series on the root, k_n = 2 pi n, |n| <= n_p, weights sqrt(pi delta)
+            # exp(-(pi sqrt(delta) n)^2).  One box (the unit cell) holds every point; its
+            # outgoing expansion is its incoming one; no near field.
+            self.series = periodic_params(eps, delta)
+            self.tp.periodic = 2
+            self.tp.n_s = 0
+            self._w = np.ascontiguousarray(self.series.coeffs, dtype=np.float64)
+            pw.n_f = 2 * self.series.n_p + 1
+            pw.D0 = float(cutoff_factor(eps))
+            pw.h = float(2.0 * np.pi * np.sqrt(delta))  # k = h n / sqrt(delta) = 2 pi n
+        else:
+            # NUFFT/plane-wave rule for the cutoff boxes
+            self.pwq = pw_params(float(epsilon), delta, R=self.R, dim=dim)
+            self._w = np.ascontiguousarray(self.pwq.weights_1d, dtype=np.float64)
+            pw.n_f = self.pwq.n_f
+            pw.D0 = float(self.pwq.D0)
+            pw.h = float(self.pwq.h)
         pw.weights_1d = self._w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         self.pw = pw
 

@@ -90,13 +90,15 @@ class PointPartition:
 
 
 def tree_params(dim, n_s, delta, epsilon, periodic):
-    """Fill the C tree parameters; returns (FgtTreeParams, l_c_periodic, R_periodic)."""
+    """Fill the C tree parameters; returns (FgtTreeParams, l_c_periodic, R_periodic).
+
+    periodic = 2 selects the root Fourier-series regime (one box: the unit cell)."""
     if n_s < 1:
         raise ValueError("n_s must be >= 1")
     D0 = cutoff_factor(clamp_tolerance(epsilon))
     tp = _lib.FgtTreeParams()
     tp.dim = dim
-    tp.periodic = 1 if periodic else 0
+    tp.periodic = int(periodic)
     tp.n_s = int(n_s)
     tp.D0 = float(D0)
     tp.delta = float(delta)
