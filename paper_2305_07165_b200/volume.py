@@ -15,11 +15,13 @@ SURVEY.md §3(D) verified against quadrature.
 
 import ctypes
 
+from types import SimpleNamespace
+
 import numpy as np
 from scipy.special import spherical_jn
 
 from . import _lib
-from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_level, pw_params
+from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_level, periodic_params, pw_params
 from .tree import Tree
 
 MAX_LEVEL = 30
@@ -253,9 +255,18 @@ class BoxPlan:
         self.dim, self.k = d, k
         eps = clamp_tolerance(epsilon)
         self.l_c, R = cutoff_level(delta, eps, tree.root_side, kind="density")
-        if periodic and not (delta < PERIODIC_IMAGE_DELTA and self.l_c >= 2):
-            raise ValueError("periodic box FGT implemented for delta < 1/36 and l_c >= 2")
-        self.pw = pw_params(float(epsilon), delta, R=R, dim=d)
+        # periodic with cutoff level <= 1: the root Fourier-series regime
+        # -- the unit cell is the one plane-wave box, k_n = 2 pi n, |n| <= n_p, weights
+        # sqrt(pi delta) exp(-(pi sqrt(delta) n)^2), every leaf merges into it, no near field
+        self.root_series = bool(periodic) and not (delta < PERIODIC_IMAGE_DELTA and self.l_c >= 2)
+        if self.root_series:
+            ser = periodic_params(eps, delta)
+            self.l_c = 0
+            self.pw = SimpleNamespace(n_f=2 * ser.n_p + 1, h=2.0 * np.pi * np.sqrt(delta),
+                                      weights_1d=ser.coeffs)
+            periodic = False  # the series carries every image
+        else:
+            self.pw = pw_params(float(epsilon), delta, R=R, dim=d)
         n_f = self.n_f = self.pw.n_f
         basis = self.basis = LegendreBasis(k)
         nb = tree.n_boxes
@@ -301,7 +312,7 @@ class BoxPlan:
             lst = [(key[kk], v) for n, v in neighbour_cells(b)
                    if (kk := (l_c,) + tuple(int(x) for x in n)) in key]
             coll[b] = lst
-            f[b] = any(not tree.is_leaf[S] for S, _ in lst)
+            f[b] = any(not tree.is_leaf[S] for S, _ in lst) or self.root_series
         pw_slot = np.full(nb, -1, np.int64)
         pw_slot[f] = np.arange(int(f.sum()))
         self.n_pw = int(f.sum())
@@ -349,7 +360,7 @@ class BoxPlan:
                 continue
             ents = []
             for S, v in lst:
-                if f[S] and not (tree.is_leaf[T] and tree.is_leaf[S]):
+                if f[S] and (self.root_series or not (tree.is_leaf[T] and tree.is_leaf[S])):
                     o = tree.coords[T] - tree.coords[S] - v * 2 ** l_c  # in {-1, 0, 1}
                     ents.append((S, [int(x) + 1 for x in o]))
             n_gpairs += len(ents)
@@ -389,7 +400,7 @@ class BoxPlan:
 
         # ---- direct: touching leaf pairs with both leaves at level <= l_c (D-list)
         pairs = []
-        for T in leaves[tree.level[leaves] <= l_c]:
+        for T in (leaves[tree.level[leaves] <= l_c] if not self.root_series else []):
             lt = int(tree.level[T])
             seen = set()
             for n, v in neighbour_cells(T):

@@ -96,3 +96,37 @@ def test_box_fgt_device_path(cuda):
     torch.cuda.synchronize()
     ud = ud.cpu().numpy()
     assert all(np.array_equal(ud[i], u[int(b)]) for i, b in enumerate(leaves))
+
+
+@pytest.mark.parametrize("d,delta,eps,n", [(1, 0.05, 1e-10, 3), (2, 0.03, 1e-9, 2), (2, 0.02, 1e-12, 1),
+                                           (3, 0.1, 1e-7, 1)])
+def test_box_fgt_periodic_root_series(cuda, d, delta, eps, n):
+    """Root Fourier-series regime (cutoff level <= 1): eigenfunctions
+    sigma_n -> (pi delta)^{d/2} exp(-d pi^2 delta n^2) sigma_n, and a constant density on a
+    single-leaf tree -> (pi delta)^{d/2} sigma."""
+    from paper_2305_07165_b200 import volume as pv
+    k = 10 if d < 3 else 8
+
+    def sig(p):
+        out = np.sin(2 * np.pi * n * p[..., 0])
+        for ax in range(1, d):
+            out = out * np.cos(2 * np.pi * n * p[..., ax])
+        return out
+    tree, vals, _ = pv.build_density_tree(sig, d, k, 1e-11 if d < 3 else 1e-8, periodic=True)
+    plan = pv.BoxPlan(tree, delta, eps, k, True)
+    assert plan.root_series and plan.l_c == 0 and plan.d_tgt.size == 0
+    u = pv.fgt_box(tree, vals, delta, eps, boundary="periodic", plan=plan)
+    fac = (np.pi * delta) ** (d / 2) * np.exp(-d * np.pi ** 2 * delta * n * n)
+    num = den = 0.0
+    for b, ub in u.items():
+        ex = fac * sig(pv.leaf_grid(tree, b, pv.LegendreBasis(k)))
+        num += np.sum((ub - ex) ** 2)
+        den += np.sum(ex ** 2)
+    assert np.sqrt(num / den) <= 10 * eps
+    # constant density: the root stays a single leaf
+    tree, vals, _ = pv.build_density_tree(lambda p: np.full(p.shape[:-1], 2.5), d, k, 1e-12, periodic=True)
+    assert tree.n_boxes == 1
+    u = pv.fgt_box(tree, vals, delta, eps, boundary="periodic")
+    ex = 2.5 * (np.pi * delta) ** (d / 2)
+    for ub in u.values():
+        assert np.max(np.abs(ub - ex)) <= 10 * eps * ex
