@@ -235,9 +235,10 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     pw_form(P, T, NPp);
     pm.mark();
     trace_mark(st, "form");
-    // psi is produced and consumed in batches of bounded size (<= ~4 GB)
+    // psi is produced and consumed in batches of bounded size (<= ~1 GB: one reusable
+    // buffer; larger pool allocations stall the host for tens of ms)
     const int64_t per = P.NH * 16;
-    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)4 << 30) / per));
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
     for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
       const int64_t hi = std::min(T.n_psi, lo + batch);
       pw_gather(P, T, lo, hi);

@@ -108,6 +108,37 @@ struct DBuf {
   }
 };
 
+// Grow-only device buffer for batch loops: one pool allocation serves every batch that
+// fits (re-allocating per batch lets the stream-ordered pool fragment and grow, and pool
+// growth blocks the host for milliseconds while the GPU idles).
+template <class T>
+struct BufView {  // a DBuf-like view of the first n elements of a GrowBuf
+  T* p;
+  size_t n;
+  cudaStream_t s;
+  T* get() const { return p; }
+  size_t size() const { return n; }
+  void from_host(const T* h, size_t count) {
+    if (count) FGT_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void to_host(T* h, size_t count) const {
+    if (count) FGT_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero() {
+    if (n) FGT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+template <class T>
+struct GrowBuf {
+  DBuf<T> b;
+  T* get(size_t count, cudaStream_t st) {
+    if (b.size() < count) b.alloc(count + count / 4, st);
+    return b.get();
+  }
+  BufView<T> view(size_t count, cudaStream_t st) { return BufView<T>{get(count, st), count, st}; }
+};
+
 // CUDA-event pair bracketing one kernel launch (device time of that kernel alone).
 // Several begin/end intervals may be recorded; ms() returns their sum.
 struct KClock {

@@ -667,6 +667,12 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   // grid cells written by one job: a plane (d = 3), the whole grid (d = 2), a cell (d = 1)
   const int64_t job_cells = D == 3 ? plane : (D == 2 ? GD : 1);
   CubTmpBuf tmp;
+  // per-batch work buffers, allocated once for the largest batch (GrowBuf)
+  GrowBuf<int64_t> g_sl, g_boff, g_iota, g_perm;
+  GrowBuf<double> g_wts, g_tt, g_qb, g_rw, g_rq, g_rw0, g_grid, g_scratch, g_t1, g_t2;
+  GrowBuf<int> g_ai, g_ra, g_range;
+  GrowBuf<uint64_t> g_key, g_skey;
+  GrowBuf<int4> g_jobs, g_reds;
   size_t b0 = 0;
   while (b0 < slots.size()) {
     // grow the batch up to nb_max boxes and ~4M points
@@ -679,13 +685,18 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       boff.push_back(npts);
       ++nbat;
     }
-    DBuf<int64_t> sl_d(nbat, st), boff_d(nbat + 1, st);
+    auto sl_d = g_sl.view(nbat, st);
+    auto boff_d = g_boff.view(nbat + 1, st);
     sl_d.from_host(slots.data() + b0, nbat);
     boff_d.from_host(boff.data(), nbat + 1);
-    DBuf<double> wts(D == 1 ? npts * MAXW : 0, st), tt(npts * D, st), qb(npts, st);
-    DBuf<int> ai(npts * D, st);
-    DBuf<uint64_t> key(npts, st), skey(npts, st);
-    DBuf<int64_t> iota(npts, st), perm(npts, st);
+    auto wts = g_wts.view(D == 1 ? npts * MAXW : 0, st);
+    auto tt = g_tt.view(npts * D, st);
+    auto qb = g_qb.view(npts, st);
+    auto ai = g_ai.view(npts * D, st);
+    auto key = g_key.view(npts, st);
+    auto skey = g_skey.view(npts, st);
+    auto iota = g_iota.view(npts, st);
+    auto perm = g_perm.view(npts, st);
     WeightArgs wa;
     wa.src = T.src_sorted.get();
     wa.q = T.q_sorted.get();
@@ -718,19 +729,19 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     while (((int64_t)1 << (bits - 8 * D)) < nbat) ++bits;
     sort_pairs_key(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
     // records first: the GPU builds them while the host waits for the job ranges
-    DBuf<double> rw, rq, rw0;
-    DBuf<int> ra;
+    BufView<double> rw{nullptr, 0, st}, rq{nullptr, 0, st}, rw0{nullptr, 0, st};
+    BufView<int> ra{nullptr, 0, st};
     if (D >= 2) {
-      rw.alloc(npts * 32, st);
-      rq.alloc(npts, st);
-      ra.alloc(npts * 4, st);
-      if (D == 3) rw0.alloc(npts * 16, st);
+      rw = g_rw.view(npts * 32, st);
+      rq = g_rq.view(npts, st);
+      ra = g_ra.view(npts * 4, st);
+      if (D == 3) rw0 = g_rw0.view(npts * 16, st);
       sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
           perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, rw.get(), rq.get(), ra.get(), rw0.get());
       FGT_LAUNCHED();
     }
     const int64_t njob = D == 2 ? nbat : nbat * G;
-    DBuf<int> range(2 * njob, st);
+    auto range = g_range.view(2 * njob, st);
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
     FGT_LAUNCHED();
     std::vector<int> hr(2 * njob);
@@ -750,10 +761,12 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
         for (int c = 0; c < nc; ++c) jobs.push_back(make_int4((int)jid, lo + c * CH, std::min(CH, n - c * CH), nscr++));
       }
     }
-    DBuf<int4> jobs_d(jobs.size(), st), reds_d(reds.size(), st);
+    auto jobs_d = g_jobs.view(jobs.size(), st);
+    auto reds_d = g_reds.view(reds.size(), st);
     jobs_d.from_host(jobs.data(), jobs.size());
     if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
-    DBuf<double> grid(nbat * GD, st), scratch((int64_t)nscr * job_cells, st);
+    auto grid = g_grid.view(nbat * GD, st);
+    auto scratch = g_scratch.view((int64_t)nscr * job_cells, st);
     PlaneArgs pa;
     pa.rw = rw.get();
     pa.rq = rq.get();
@@ -791,8 +804,6 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
           scratch.get(), reds_d.get(), job_cells, 0, grid.get());
       FGT_LAUNCHED();
     }
-    scratch.release();
-    wts.release();
     // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
     // (d >= 2: only the nh stored axis-0 planes of the half spectrum, axis 0 contracted
     // first so the later stages run on nh planes)
@@ -801,13 +812,14 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     if (D == 1) {
       bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid.get(), 1, G, phi, 1, NH, n_f, 1, G, (int)nbat, sl_d.get()), st);
     } else if (D == 2) {
-      DBuf<double> t1(2 * nbat * G * n_f, st);
+      auto t1 = g_t1.view(2 * nbat * G * n_f, st);
       // T1[g1][m2] = sum_g2 grid[g1][g2] EfT[g2][m2]
       bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
       // phi[s][m2] = sum_g1 EfH[s][g1] T1[g1][m2]
       bgemm<true, true, false>(gemm(N.EfH.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NH, nh, n_f, G, (int)nbat, sl_d.get()), st);
     } else {
-      DBuf<double> x(2 * nbat * nh * plane, st), y(2 * nbat * nh * n_f * G, st);
+      auto x = g_t1.view(2 * nbat * nh * plane, st);
+      auto y = g_t2.view(2 * nbat * nh * n_f * G, st);
       // X[s][(g2 g3)] = sum_g1 EfH[s][g1] grid[g1][(g2 g3)]
       bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid.get(), plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
       // Y[s][m2][g3] = sum_g2 Ef[m2][g2] X[s][g2][g3]      (batch = box x s)
@@ -830,23 +842,26 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)G * n_f * 16 : 0) +
                           (D == 3 ? (int64_t)nh * n_f * G * 16 + (int64_t)nh * plane * 16 : 0);
   const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
+  GrowBuf<int64_t> g_li;
+  GrowBuf<double> g_grid, g_v1, g_v2;
   for (size_t b0 = 0; b0 < idx.size(); b0 += nb_max) {
     const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)idx.size() - b0);
-    DBuf<int64_t> li(nbat, st);
+    auto li = g_li.view(nbat, st);
     li.from_host(idx.data() + b0, nbat);
-    DBuf<double> grid(nbat * GD, st);
+    auto grid = g_grid.view(nbat * GD, st);
     const double* psi = P.psi_view();  // first stage reads psi[list[b]] through bidx
     if (D == 1) {
       // grid[g] = Re sum_m Ee[g][m] psi[m]
       bgemm<true, true, true>(gemm(N.Ee.get(), n_f, 0, psi, 1, NH, grid.get(), 1, GD, G, 1, n_f, (int)nbat, nullptr, li.get()), st);
     } else if (D == 2) {
-      DBuf<double> v1(2 * nbat * G * n_f, st);
+      auto v1 = g_v1.view(2 * nbat * G * n_f, st);
       // V1[g1][m2] = sum_s EeH[g1][s] psi[s][m2]   (pair weights in EeH)
       bgemm<true, true, false>(gemm(N.EeH.get(), nh, 0, psi, n_f, NH, v1.get(), n_f, (int64_t)G * n_f, G, n_f, nh, (int)nbat, nullptr, li.get()), st);
       // grid[g1][g2] = Re sum_m2 V1[g1][m2] EeT[m2][g2]
       bgemm<true, true, true>(gemm(v1.get(), n_f, (int64_t)G * n_f, N.EeT.get(), G, 0, grid.get(), G, GD, G, G, n_f, (int)nbat), st);
     } else {
-      DBuf<double> v(2 * nbat * nh * n_f * G, st), wv(2 * nbat * nh * plane, st);
+      auto v = g_v1.view(2 * nbat * nh * n_f * G, st);
+      auto wv = g_v2.view(2 * nbat * nh * plane, st);
       // V[(s m2)][g3] = sum_m3 psi[(s m2)][m3] EeT[m3][g3]
       bgemm<true, true, false>(gemm(psi, n_f, NH, N.EeT.get(), G, 0, v.get(), G, (int64_t)nh * n_f * G, nh * n_f, G, n_f, (int)nbat, nullptr, nullptr, li.get()), st);
       // W[s][g2][g3] = sum_m2 Ee[g2][m2] V[s][m2][g3]      (batch = box x s)
