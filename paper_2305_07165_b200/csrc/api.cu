@@ -1,6 +1,7 @@
 // extern "C" surface of libfgtcuda.so (declared in include/fgt_cuda.h).
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <memory>
 
 #include "k_kernels.cuh"
@@ -25,6 +26,81 @@ void ensure_pool_retained() {
   done_dev = dev;
 }
 void count_launch(int n) { g_launches += n; }
+
+namespace {
+struct BigBlock {
+  void* p;
+  size_t bytes;
+  int dev;
+  bool busy;
+  cudaStream_t last;
+  cudaEvent_t ev;
+};
+std::mutex& big_mu() {
+  static std::mutex m;
+  return m;
+}
+std::vector<BigBlock>& big_blocks() {
+  static auto* v = new std::vector<BigBlock>();  // process lifetime
+  return *v;
+}
+}  // namespace
+
+void* big_alloc(size_t bytes, cudaStream_t st) {
+  const size_t rounded = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+  int dev = 0;
+  FGT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(big_mu());
+  auto& v = big_blocks();
+  // best fit among idle blocks of this device no larger than 2x the request
+  BigBlock* best = nullptr;
+  for (auto& b : v)
+    if (!b.busy && b.dev == dev && b.bytes >= rounded && b.bytes <= 2 * rounded &&
+        (!best || b.bytes < best->bytes))
+      best = &b;
+  if (best) {
+    best->busy = true;
+    if (best->last != st) FGT_CUDA(cudaStreamWaitEvent(st, best->ev, 0));
+    return best->p;
+  }
+  BigBlock b;
+  b.bytes = rounded;
+  b.dev = dev;
+  b.busy = true;
+  b.last = st;
+  cudaError_t e = cudaMalloc(&b.p, rounded);
+  if (e != cudaSuccess) {
+    // release idle cached blocks of this device and retry once
+    cudaGetLastError();
+    FGT_CUDA(cudaDeviceSynchronize());
+    for (auto it = v.begin(); it != v.end();) {
+      if (!it->busy && it->dev == dev) {
+        cudaFree(it->p);
+        cudaEventDestroy(it->ev);
+        it = v.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    e = cudaMalloc(&b.p, rounded);
+    if (e == cudaErrorMemoryAllocation) throw Error(FGT_ENOMEM, "device allocation failed");
+    FGT_CUDA(e);
+  }
+  FGT_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+  v.push_back(b);
+  return b.p;
+}
+
+void big_free(void* p, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(big_mu());
+  for (auto& b : big_blocks())
+    if (b.p == p) {
+      cudaEventRecord(b.ev, st);
+      b.last = st;
+      b.busy = false;
+      return;
+    }
+}
 
 // RAII stream for host-pointer entry points
 struct OwnedStream {

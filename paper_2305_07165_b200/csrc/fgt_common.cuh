@@ -65,6 +65,15 @@ int guarded(F&& f) {
 // synchronisation, so multi-GB scratch would be unmapped/remapped on each call).
 void ensure_pool_retained();
 
+// Large buffers (>= BIG_BYTES) bypass the stream-ordered pool: carving multi-GB blocks
+// out of a fragmented pool makes the driver remap physical pages, which blocks the host
+// for 100s of ms while the GPU idles.  A process-lifetime cache of cudaMalloc'd blocks
+// serves them instead: a freed block records an event on its stream and a later user on
+// another stream waits on it, so reuse keeps stream order (api.cu).
+constexpr size_t BIG_BYTES = size_t(64) << 20;
+void* big_alloc(size_t bytes, cudaStream_t st);
+void big_free(void* p, cudaStream_t st);
+
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered device allocation (cudaMallocAsync pool): frees are ordered after
 // the work already queued on the stream, so scratch never needs a device sync.
@@ -75,27 +84,38 @@ struct DBuf {
   cudaStream_t s = nullptr;
   DBuf() = default;
   DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  bool big = false;
   void alloc(size_t count, cudaStream_t st) {
     release();
     ensure_pool_retained();
     s = st;
     n = count;
-    if (count) FGT_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    big = count * sizeof(T) >= BIG_BYTES;
+    if (big) p = static_cast<T*>(big_alloc(count * sizeof(T), st));
+    else if (count) FGT_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
   }
   void zero() {
     if (n) FGT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+      if (big) big_free(p, s);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     n = 0;
+    big = false;
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), big(o.big) { o.p = nullptr; o.n = 0; o.big = false; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s; big = o.big;
+      o.p = nullptr; o.n = 0; o.big = false;
+    }
     return *this;
   }
   T* get() const { return p; }
@@ -213,6 +233,17 @@ inline void trace_dump() {
   }
   for (auto& x : m) cudaEventDestroy(x.ev);
   m.clear();
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t rc = 0, rh = 0, uc = 0, uh = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &rc);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &rh);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &uc);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &uh);
+    std::fprintf(stderr, "pool reserved %.2f GB (high %.2f), used %.2f GB (high %.2f)\n", rc / 1e9, rh / 1e9,
+                 uc / 1e9, uh / 1e9);
+  }
 }
 
 inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 64) {

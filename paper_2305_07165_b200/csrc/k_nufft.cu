@@ -658,11 +658,11 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   // per-slot source counts (fetched once in pw_setup)
   const std::vector<int64_t>& scount = P.h_src;
   FGT_REQUIRE(G < 256 && G <= 64, FGT_ERANGE, "spreading grid too large (G > 64)");
-  // batches bounded by ~1.5 GB of grid + stage buffers + per-point weights
+  // batches bounded by ~6 GB of grid + stage buffers and 16M points (~350 B each)
   const int nh = P.nh;
   const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)G * n_f * 16 : 0) +
                           (D == 3 ? (int64_t)nh * plane * 16 + (int64_t)nh * n_f * G * 16 : 0);
-  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(1 << 20, ((int64_t)6 << 30) / per_box));
   const int CH = D == 2 ? 4096 : 2048;  // points per job
   // grid cells written by one job: a plane (d = 3), the whole grid (d = 2), a cell (d = 1)
   const int64_t job_cells = D == 3 ? plane : (D == 2 ? GD : 1);
@@ -680,7 +680,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     std::vector<int64_t> boff(1, 0);
     while (b0 + nbat < slots.size() && nbat < nb_max) {
       const int64_t n = scount[slots[b0 + nbat]];
-      if (nbat > 0 && npts + n > (int64_t)4 << 20) break;
+      if (nbat > 0 && npts + n > (int64_t)16 << 20) break;
       npts += n;
       boff.push_back(npts);
       ++nbat;
@@ -841,7 +841,7 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   const int nh = P.nh;
   const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)G * n_f * 16 : 0) +
                           (D == 3 ? (int64_t)nh * n_f * G * 16 + (int64_t)nh * plane * 16 : 0);
-  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(65535 / G, (int64_t)1536 * 1024 * 1024 / per_box));
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(1 << 20, ((int64_t)6 << 30) / per_box));
   GrowBuf<int64_t> g_li;
   GrowBuf<double> g_grid, g_v1, g_v2;
   for (size_t b0 = 0; b0 < idx.size(); b0 += nb_max) {
