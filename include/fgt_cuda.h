@@ -195,6 +195,27 @@ int fgt_points_dev(const double* src, int64_t ns, const double* charges,
                    const double* tgt, int64_t nt, const fgt_tree_params* tp,
                    const fgt_pw_params* pw, double* u, void* stream,
                    fgt_phase_times* times);
+/* The same transform split at the multi-GPU exchange point (one process per GPU,
+ * tp->part_rank / part_size set).  begin: tree, lists, this rank's cost-balanced share
+ * of the target leaves, and the outgoing expansions of the P-boxes this rank OWNS (the
+ * ones whose leaf lies in its range).  The one-box halo -- expansions owned by other
+ * ranks that this rank's P-lists use -- is then exchanged: exchange_counts gives, per
+ * peer, the slots to send and to receive (slot_doubles doubles each); pack writes this
+ * rank's send slots, peer by peer, into a device buffer laid out for an all-to-all;
+ * unpack scatters the received buffer (same peer order) into place.  finish: translation,
+ * evaluation, near field; u (nt) gets this rank's targets (0 elsewhere).  All calls run on
+ * the stream given to begin.  With part_size = 1 there is nothing to exchange. */
+typedef struct fgt_points_run fgt_points_run;
+int fgt_points_begin(const double* src, int64_t ns, const double* charges, const double* tgt,
+                     int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, void* stream,
+                     fgt_points_run** out);
+int fgt_points_exchange_counts(const fgt_points_run* r, int64_t* send_slots, int64_t* recv_slots,
+                               int64_t* slot_doubles);
+int fgt_points_pack(fgt_points_run* r, double* send_buf);
+int fgt_points_unpack(fgt_points_run* r, const double* recv_buf);
+int fgt_points_finish(fgt_points_run* r, double* u, fgt_phase_times* times);
+void fgt_points_run_free(fgt_points_run* r);
+
 /* Same with HOST pointers; the H2D of inputs and D2H of u are inside the call. */
 int fgt_points(const double* src, int64_t ns, const double* charges, const double* tgt,
                int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, double* u,

@@ -111,6 +111,13 @@ SIGNATURES = {
     "fgt_tree_copy_lists": (_I, [_P] + [_P] * 6),
     "fgt_points_dev": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
                             ctypes.POINTER(FgtPwParams), _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_points_begin": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
+                              ctypes.POINTER(FgtPwParams), _P, ctypes.POINTER(_P)]),
+    "fgt_points_exchange_counts": (_I, [_P, _P, _P, ctypes.POINTER(_I64)]),
+    "fgt_points_pack": (_I, [_P, _P]),
+    "fgt_points_unpack": (_I, [_P, _P]),
+    "fgt_points_finish": (_I, [_P, _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_points_run_free": (None, [_P]),
     "fgt_points": (_I, [_P, _I64, _P, _P, _I64, ctypes.POINTER(FgtTreeParams),
                         ctypes.POINTER(FgtPwParams), _P, ctypes.POINTER(FgtPhaseTimes)]),
     "fgt_bench_fp64_peak": (_I, [_I, ctypes.POINTER(_D)]),

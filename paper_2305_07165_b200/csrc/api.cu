@@ -1,4 +1,5 @@
 // extern "C" surface of libfgtcuda.so (declared in include/fgt_cuda.h).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -170,14 +171,17 @@ __global__ void scatter_kernel(const double* __restrict__ us, const int64_t* __r
 __global__ void leaf_direct_cost_kernel(const int64_t* __restrict__ tl, int64_t n,
                                         const int64_t* __restrict__ d_off, const int64_t* __restrict__ d_src,
                                         const int64_t* __restrict__ scount, const int64_t* __restrict__ tcount,
-                                        double* __restrict__ nt_out, double* __restrict__ pairs_out) {
+                                        const int64_t* __restrict__ dense_slot, double* __restrict__ nt_out,
+                                        double* __restrict__ pairs_out, double* __restrict__ form_out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0;
     for (int64_t e = d_off[i]; e < d_off[i + 1]; ++e) s += (double)scount[d_src[e]];
-    double t = (double)tcount[tl[i]];
+    const int64_t T = tl[i];
+    double t = (double)tcount[T];
     nt_out[i] = t;
     pairs_out[i] = t * s;
+    form_out[i] = dense_slot[T] >= 0 ? (double)scount[T] : 0.0;  // sources of a P-box leaf
   }
 }
 
@@ -197,53 +201,127 @@ std::vector<int64_t> partition_bounds(const std::vector<double>& cost, int parts
   return b;
 }
 
-// Restrict the target-side work of T to this rank's cost-balanced contiguous range of
-// target leaves (canonical = Morton order at each level).  P-boxes needed by the
-// range's P-lists are flagged in T.dense_need (their expansions are recomputed on
-// every rank that needs them: a one-box halo, no exchange).
-static void restrict_to_share(TreeDev& T, int rank, int size, int64_t NF) {
+// Multi-GPU shares (one process per GPU).  Every rank builds the same tree and lists,
+// then keeps a cost-balanced contiguous range of target leaves (canonical = Morton order
+// at each level).  P-box expansions either get recomputed by every rank that needs them
+// (exchange = false: a one-box halo of extra form work, no communication) or are formed
+// only by their owner -- the rank whose leaf range holds the box -- and the one-box halo
+// is exchanged (exchange = true: ExchangePlan, then an all-to-all of the packed slots).
+struct ExchangePlan {
+  int rank = 0, world = 1;
+  std::vector<int64_t> send_off, recv_off;  // (world + 1) slot offsets per peer
+  DBuf<int64_t> send_slots, recv_slots;     // dense slots, concatenated in peer order
+};
+
+__global__ void pack_slots_kernel(const double2* __restrict__ phi, const int64_t* __restrict__ slots,
+                                  int64_t n, int64_t NH, double2* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * NH;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / NH, e = i - k * NH;
+    out[i] = phi[slots[k] * NH + e];
+  }
+}
+
+__global__ void unpack_slots_kernel(double2* __restrict__ phi, const int64_t* __restrict__ slots,
+                                    int64_t n, int64_t NH, const double2* __restrict__ in) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * NH;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / NH, e = i - k * NH;
+    phi[slots[k] * NH + e] = in[i];
+  }
+}
+
+static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool exchange, ExchangePlan* X) {
   cudaStream_t st = T.st;
   const int64_t n = T.n_dtgt;
-  std::vector<double> nt(n), pairs(n);
-  std::vector<int64_t> tl(n), doff(n + 1), psi(T.n_psi), poff(T.n_psi + 1);
+  std::vector<double> nt(n), pairs(n), fsrc(n);
+  std::vector<int64_t> tl(n), psi(T.n_psi), poff(T.n_psi + 1), psrc(T.n_p), dense(T.n_dense);
   if (n > 0) {
-    DBuf<double> ntd(n, st), prd(n, st);
+    DBuf<double> ntd(n, st), prd(n, st), fsd(n, st);
     leaf_direct_cost_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.d_tgt_ids.get(), n, T.d_off.get(), T.d_src.get(),
-                                                              T.src_count.get(), T.tgt_count.get(), ntd.get(), prd.get());
+                                                              T.src_count.get(), T.tgt_count.get(),
+                                                              T.dense_slot.get(), ntd.get(), prd.get(), fsd.get());
     FGT_LAUNCHED();
     ntd.to_host(nt.data(), n);
     prd.to_host(pairs.data(), n);
+    fsd.to_host(fsrc.data(), n);
     T.d_tgt_ids.to_host(tl.data(), n);
   }
-  T.d_off.to_host(doff.data(), n + 1);
   T.psi_ids.to_host(psi.data(), T.n_psi);
   T.p_off.to_host(poff.data(), T.n_psi + 1);
+  T.p_src.to_host(psrc.data(), T.n_p);
+  T.dense_ids.to_host(dense.data(), T.n_dense);
   FGT_CUDA(cudaStreamSynchronize(st));
-  // cost in flop-equivalents: eval 8 N_F per target, gather ~100 N_F per P entry
-  // (HBM-bound, ridge ~6 flop/B x 16 B), direct ~40 per pair
+  // cost in ns, calibrated on the B200 kernels (profiles/r01f_*): eval 8 N_H flops per
+  // target at ~21 TFLOP/s, gather ~2.4 ps per stored mode per P entry, direct ~10 ps per
+  // pair; with the exchange, a P-box's form (~2.4 ns per source at w = 11, ~w^3) is
+  // charged to the leaf position that owns it
+  const double form_ns = exchange ? 2.4 * std::pow(w / 11.0, 3) : 0.0;
   std::vector<double> cost(n);
   std::vector<int64_t> psi_of(n, -1);
   for (int64_t i = 0, j = 0; i < n; ++i) {
     while (j < T.n_psi && psi[j] < tl[i]) ++j;
-    double c = 40.0 * pairs[i];
+    double c = 0.01 * pairs[i] + form_ns * fsrc[i];
     if (j < T.n_psi && psi[j] == tl[i]) {
       psi_of[i] = j;
-      c += 8.0 * NF * nt[i] + 100.0 * NF * (double)(poff[j + 1] - poff[j]);
+      c += 8.0 * NH * nt[i] / 21e3 + 2.4e-3 * NH * (double)(poff[j + 1] - poff[j]);
     }
     cost[i] = c;
   }
   std::vector<int64_t> b = partition_bounds(cost, size);
+  auto first_psi = [&](int64_t i) {
+    for (; i < n; ++i)
+      if (psi_of[i] >= 0) return psi_of[i];
+    return T.n_psi;
+  };
+  std::vector<int64_t> pb(size + 1);  // psi index range of every rank
+  for (int r = 0; r <= size; ++r) pb[r] = first_psi(b[r]);
   const int64_t lo = b[rank], hi = b[rank + 1];
-  // psi index range covered by target leaves [lo, hi)
-  int64_t plo = 0, phi = 0;
-  {
-    auto first_psi = [&](int64_t i) {
-      for (; i < n; ++i)
-        if (psi_of[i] >= 0) return psi_of[i];
-      return T.n_psi;
-    };
-    plo = first_psi(lo);
-    phi = first_psi(hi);
+  const int64_t plo = pb[rank], phi = pb[rank + 1];
+  // slots needed by every rank (from the replicated lists)
+  auto needs = [&](int r) {
+    std::vector<int64_t> v(psrc.begin() + poff[pb[r]], psrc.begin() + poff[pb[r + 1]]);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    return v;
+  };
+  T.dense_need.assign(T.n_dense, 0);
+  const std::vector<int64_t> mine = needs(rank);
+  if (!exchange) {
+    for (int64_t s : mine) T.dense_need[s] = 1;
+  } else {
+    // owner of a slot: the rank whose target-leaf range holds the box's position
+    std::vector<int> owner(T.n_dense);
+    for (int64_t s = 0; s < T.n_dense; ++s) {
+      const int64_t pos = std::lower_bound(tl.begin(), tl.end(), dense[s]) - tl.begin();
+      int r = (int)(std::upper_bound(b.begin(), b.end(), pos) - b.begin()) - 1;
+      owner[s] = std::max(0, std::min(size - 1, r));
+    }
+    X->rank = rank;
+    X->world = size;
+    X->send_off.assign(size + 1, 0);
+    X->recv_off.assign(size + 1, 0);
+    std::vector<int64_t> send, recv;
+    for (int r = 0; r < size; ++r) {
+      if (r != rank) {
+        for (int64_t s : needs(r))
+          if (owner[s] == rank) {
+            send.push_back(s);
+            T.dense_need[s] = 1;
+          }
+        for (int64_t s : mine)
+          if (owner[s] == r) recv.push_back(s);
+      } else {
+        for (int64_t s : mine)
+          if (owner[s] == rank) T.dense_need[s] = 1;
+      }
+      X->send_off[r + 1] = (int64_t)send.size();
+      X->recv_off[r + 1] = (int64_t)recv.size();
+    }
+    X->send_slots.alloc(send.size(), st);
+    X->send_slots.from_host(send.data(), send.size());
+    X->recv_slots.alloc(recv.size(), st);
+    X->recv_slots.from_host(recv.data(), recv.size());
   }
   // restrict direct CSR (absolute offsets stay valid)
   {
@@ -254,16 +332,8 @@ static void restrict_to_share(TreeDev& T, int rank, int size, int64_t NF) {
     T.d_off = std::move(off);
     T.n_dtgt = hi - lo;
   }
-  // restrict psi boxes and flag the P-boxes they need
-  T.dense_need.assign(T.n_dense, 0);
+  // restrict psi boxes
   {
-    const int64_t e0 = poff[plo], e1 = poff[phi];
-    std::vector<int64_t> slots(e1 - e0);
-    if (e1 > e0) {
-      FGT_CUDA(cudaMemcpyAsync(slots.data(), T.p_src.get() + e0, (e1 - e0) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      FGT_CUDA(cudaStreamSynchronize(st));
-    }
-    for (int64_t s : slots) T.dense_need[s] = 1;
     DBuf<int64_t> ids(phi - plo, st), off(phi - plo + 1, st);
     if (phi > plo) FGT_CUDA(cudaMemcpyAsync(ids.get(), T.psi_ids.get() + plo, (phi - plo) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     FGT_CUDA(cudaMemcpyAsync(off.get(), T.p_off.get() + plo, (phi - plo + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
@@ -273,44 +343,72 @@ static void restrict_to_share(TreeDev& T, int rank, int size, int64_t NF) {
   }
 }
 
-static void points_pipeline(const double* src, int64_t ns, const double* q, const double* tgt,
-                            int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw,
-                            double* u, cudaStream_t st, fgt_phase_times* times) {
-  FGT_REQUIRE(tp.dim == pw.dim, FGT_EINVAL, "tree/plane-wave dim mismatch");
-  const int64_t l0 = g_launches;
-  PhaseMarks pm(st);  // marks: 0 start, 1 tree, 2 lists, 3 form, 4 gather+eval, 5 direct
-  trace_mark(st, "start");
-  fgt_phase_times t;
-  std::memset(&t, 0, sizeof(t));
+// One transform split at the exchange point: begin = tree, lists, share, own expansions;
+// finish = translation, evaluation, near field, scatter.
+struct PointsRun {
+  cudaStream_t st = nullptr;
   TreeDev T;
+  PwDev P;
+  const NufftPlan* NP = nullptr;
+  DBuf<double> us;
+  fgt_tree_params tp;
+  fgt_pw_params pw;
+  std::vector<double> w1d;
+  ExchangePlan X;
+  std::unique_ptr<PhaseMarks> pm;
+  int64_t l0 = 0, nt = 0;
+};
+
+static void points_begin(PointsRun& R, const double* src, int64_t ns, const double* q, const double* tgt,
+                         int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw, cudaStream_t st,
+                         bool exchange) {
+  FGT_REQUIRE(tp.dim == pw.dim, FGT_EINVAL, "tree/plane-wave dim mismatch");
+  R.st = st;
+  R.tp = tp;
+  R.pw = pw;
+  R.w1d.assign(pw.weights_1d, pw.weights_1d + pw.n_f);
+  R.pw.weights_1d = R.w1d.data();
+  R.nt = nt;
+  R.l0 = g_launches;
+  R.pm.reset(new PhaseMarks(st));  // marks: 0 start, 1 tree, 2 lists, 3 form, 4 gather+eval, 5 direct
+  trace_mark(st, "start");
+  TreeDev& T = R.T;
   build_tree(T, src, ns, tgt, nt, tp, st);
   gather_sorted_points(T, src, q, tgt);
-  pm.mark();
+  R.pm->mark();
   trace_mark(st, "tree");
   build_lists(T);
+  // stored modes (half spectrum for d >= 2) and the NUFFT width the plan will use
+  int64_t NH = pw.dim >= 2 ? pw.n_f / 2 + 1 : pw.n_f;
+  for (int k = 1; k < pw.dim; ++k) NH *= pw.n_f;
+  const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
+  const int w = std::max(2, std::min((int)std::ceil(std::log10(1.0 / tol) - 1e-9) + 1, 16));
   if (tp.part_size > 1) {
     FGT_REQUIRE(tp.part_rank >= 0 && tp.part_rank < tp.part_size, FGT_EINVAL, "bad part_rank");
-    int64_t NF = 1;
-    for (int k = 0; k < pw.dim; ++k) NF *= pw.n_f;
-    restrict_to_share(T, tp.part_rank, tp.part_size, NF);
+    plan_share(T, tp.part_rank, tp.part_size, NH, w, exchange, &R.X);
   }
-  pm.mark();
+  R.pm->mark();
   trace_mark(st, "lists");
-  DBuf<double> us(nt, st);
-  us.zero();
-  PwDev P;
-  const NufftPlan* NPp = nullptr;
+  R.us.alloc(nt, st);
+  R.us.zero();
   if (T.n_dense > 0) {
-    pw_setup(P, T, pw);
-    // box-local NUFFT plan at tolerance eps/10 (SPEC.md:433); eps = 3 exp(-D0^2)
-    const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
-    const double X = 0.5 * P.side_lc * P.sc * (1.0 + 1e-12);
+    pw_setup(R.P, T, R.pw);
     trace_mark(st, "setup");
-    NPp = &nufft_plan_cached(pw.n_f, tol, X, pw.weights_1d, st);
+    // box-local NUFFT plan at tolerance eps/10 (SPEC.md:433); eps = 3 exp(-D0^2)
+    const double X = 0.5 * R.P.side_lc * R.P.sc * (1.0 + 1e-12);
+    R.NP = &nufft_plan_cached(pw.n_f, tol, X, R.w1d.data(), st);
     trace_mark(st, "nufft_plan");
-    pw_form(P, T, NPp);
-    pm.mark();
-    trace_mark(st, "form");
+    pw_form(R.P, T, R.NP);
+  }
+  R.pm->mark();
+  trace_mark(st, "form");
+}
+
+static void points_finish(PointsRun& R, double* u, fgt_phase_times* times) {
+  cudaStream_t st = R.st;
+  TreeDev& T = R.T;
+  PwDev& P = R.P;
+  if (T.n_dense > 0) {
     // psi is produced and consumed in batches of bounded size (<= ~1 GB: one reusable
     // buffer; larger pool allocations stall the host for tens of ms)
     const int64_t per = P.NH * 16;
@@ -318,23 +416,24 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
     for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
       const int64_t hi = std::min(T.n_psi, lo + batch);
       pw_gather(P, T, lo, hi);
-      pw_eval(P, T, us.get(), NPp, lo, hi);
+      pw_eval(P, T, R.us.get(), R.NP, lo, hi);
     }
     P.phi.release();
     P.psi.release();
-  } else {
-    pm.mark();  // empty form phase
   }
-  pm.mark();
+  R.pm->mark();
   trace_mark(st, "gather+eval");
-  const double D0 = tp.D0;
-  direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, us.get(), &P.k_direct);
-  if (nt > 0) {
-    scatter_kernel<<<grid_for(nt, 256), 256, 0, st>>>(us.get(), T.tgt_perm.get(), nt, u);
+  const double D0 = R.tp.D0;
+  direct_lists(T, 1.0 / R.tp.delta, D0 * D0 * R.tp.delta, R.us.get(), &P.k_direct);
+  if (R.nt > 0) {
+    scatter_kernel<<<grid_for(R.nt, 256), 256, 0, st>>>(R.us.get(), T.tgt_perm.get(), R.nt, u);
     FGT_LAUNCHED();
   }
-  pm.mark();
+  R.pm->mark();
   trace_mark(st, "direct");
+  fgt_phase_times t;
+  std::memset(&t, 0, sizeof(t));
+  PhaseMarks& pm = *R.pm;
   t.tree_ms = pm.ms(0);
   t.lists_ms = pm.ms(1);
   t.form_ms = pm.ms(2);
@@ -343,7 +442,7 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.direct_ms = pm.ms(4);
   trace_dump();
   t.total_ms = t.tree_ms + t.lists_ms + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
-  t.launches = g_launches - l0;
+  t.launches = g_launches - R.l0;
   t.k_form_ms = P.k_form.ms();
   t.k_gather_ms = P.k_gather.ms();
   t.k_eval_ms = P.k_eval.ms();
@@ -360,9 +459,17 @@ static void points_pipeline(const double* src, int64_t ns, const double* q, cons
   t.n_src_spread = P.n_src_spread;
   t.n_spread_psi = P.n_spread_psi;
   t.n_tgt_spread = P.n_tgt_spread;
-  t.nufft_w = NPp ? NPp->w : 0;
-  t.nufft_G = NPp ? NPp->G : 0;
+  t.nufft_w = R.NP ? R.NP->w : 0;
+  t.nufft_G = R.NP ? R.NP->G : 0;
   if (times) *times = t;
+}
+
+static void points_pipeline(const double* src, int64_t ns, const double* q, const double* tgt,
+                            int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw,
+                            double* u, cudaStream_t st, fgt_phase_times* times) {
+  PointsRun R;
+  points_begin(R, src, ns, q, tgt, nt, tp, pw, st, false);
+  points_finish(R, u, times);
 }
 
 // ---------------------------------------------------------------- microbenchmarks
@@ -607,6 +714,74 @@ int fgt_points_dev(const double* src, int64_t ns, const double* charges, const d
     FGT_REQUIRE(tp && pw, FGT_EINVAL, "null parameters");
     points_pipeline(src, ns, charges, tgt, nt, *tp, *pw, u, (cudaStream_t)stream, times);
   });
+}
+
+struct fgt_points_run {
+  PointsRun R;
+};
+
+int fgt_points_begin(const double* src, int64_t ns, const double* charges, const double* tgt,
+                     int64_t nt, const fgt_tree_params* tp, const fgt_pw_params* pw, void* stream,
+                     fgt_points_run** out) {
+  return guarded([&] {
+    FGT_REQUIRE(tp && pw && out, FGT_EINVAL, "null argument");
+    auto r = std::make_unique<fgt_points_run>();
+    points_begin(r->R, src, ns, charges, tgt, nt, *tp, *pw, (cudaStream_t)stream, true);
+    *out = r.release();
+  });
+}
+
+int fgt_points_exchange_counts(const fgt_points_run* r, int64_t* send_slots, int64_t* recv_slots,
+                               int64_t* slot_doubles) {
+  return guarded([&] {
+    FGT_REQUIRE(r, FGT_EINVAL, "null run");
+    const ExchangePlan& X = r->R.X;
+    for (int p = 0; p < X.world; ++p) {
+      if (send_slots) send_slots[p] = X.send_off.empty() ? 0 : X.send_off[p + 1] - X.send_off[p];
+      if (recv_slots) recv_slots[p] = X.recv_off.empty() ? 0 : X.recv_off[p + 1] - X.recv_off[p];
+    }
+    if (slot_doubles) *slot_doubles = 2 * r->R.P.NH;
+  });
+}
+
+int fgt_points_pack(fgt_points_run* r, double* send_buf) {
+  return guarded([&] {
+    FGT_REQUIRE(r, FGT_EINVAL, "null run");
+    PointsRun& R = r->R;
+    const int64_t n = R.X.send_slots.size();
+    if (n == 0) return;
+    pack_slots_kernel<<<grid_for(n * R.P.NH, 256), 256, 0, R.st>>>(
+        reinterpret_cast<const double2*>(R.P.phi.get()), R.X.send_slots.get(), n, R.P.NH,
+        reinterpret_cast<double2*>(send_buf));
+    FGT_LAUNCHED();
+  });
+}
+
+int fgt_points_unpack(fgt_points_run* r, const double* recv_buf) {
+  return guarded([&] {
+    FGT_REQUIRE(r, FGT_EINVAL, "null run");
+    PointsRun& R = r->R;
+    const int64_t n = R.X.recv_slots.size();
+    if (n == 0) return;
+    unpack_slots_kernel<<<grid_for(n * R.P.NH, 256), 256, 0, R.st>>>(
+        reinterpret_cast<double2*>(R.P.phi.get()), R.X.recv_slots.get(), n, R.P.NH,
+        reinterpret_cast<const double2*>(recv_buf));
+    FGT_LAUNCHED();
+  });
+}
+
+int fgt_points_finish(fgt_points_run* r, double* u, fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(r, FGT_EINVAL, "null run");
+    points_finish(r->R, u, times);
+  });
+}
+
+void fgt_points_run_free(fgt_points_run* r) {
+  if (r) {
+    cudaStreamSynchronize(r->R.st);
+    delete r;
+  }
 }
 
 int fgt_points(const double* src, int64_t ns, const double* charges, const double* tgt, int64_t nt,

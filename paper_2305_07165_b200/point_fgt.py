@@ -125,3 +125,84 @@ def fgt_points_device(sources, charges, targets, delta, epsilon, n_s, boundary="
                                           nt, ctypes.byref(prm.tp), ctypes.byref(prm.pw),
                                           vp(out), ctypes.c_void_p(stream), ctypes.byref(times)))
     return (out, times.as_dict()) if return_times else out
+
+
+class TorchExchange:
+    """Halo exchange of outgoing expansions over torch.distributed (NCCL over NVLink):
+    one all-to-all of the packed slots (SURVEY.md section 8(e) exchange 1)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def __call__(self, send, recv, send_counts, recv_counts, slot):
+        import torch.distributed as dist
+        dist.all_to_all_single(recv, send, [int(c) * slot for c in recv_counts],
+                               [int(c) * slot for c in send_counts], group=self.group)
+
+
+def fgt_points_exchange_begin(sources, charges, targets, delta, epsilon, n_s, boundary="free",
+                              share=(0, 1)):
+    """Phase 1 of a multi-GPU transform with the expansion halo exchanged instead of
+    recomputed: returns a PointsRun (tree, lists, this rank's owned expansions formed)."""
+    import torch
+    periodic = _boundary(boundary)
+    for name, t in (("sources", sources), ("charges", charges), ("targets", targets)):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CUDA float64 tensor")
+    dim = sources.shape[1] if sources.dim() == 2 else targets.shape[1]
+    prm = FgtParams(dim, delta, epsilon, n_s, periodic, share)
+    return PointsRun(prm, sources, charges, targets)
+
+
+class PointsRun:
+    """An fgt_points_run handle: begin -> (pack / exchange / unpack) -> finish."""
+
+    def __init__(self, prm, sources, charges, targets):
+        import torch
+        self.prm = prm
+        self.world = prm.tp.part_size
+        self.nt = targets.shape[0]
+        self.device = targets.device
+        self.stream = torch.cuda.current_stream().cuda_stream
+        h = ctypes.c_void_p()
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.load().fgt_points_begin(vp(sources), sources.shape[0], vp(charges), vp(targets),
+                                                self.nt, ctypes.byref(prm.tp), ctypes.byref(prm.pw),
+                                                ctypes.c_void_p(self.stream), ctypes.byref(h)))
+        self._h = h
+        self._keep = (sources, charges, targets)
+        sc = (ctypes.c_int64 * self.world)()
+        rc = (ctypes.c_int64 * self.world)()
+        slot = ctypes.c_int64()
+        _lib.check(_lib.load().fgt_points_exchange_counts(h, sc, rc, ctypes.byref(slot)))
+        self.send_counts, self.recv_counts, self.slot = list(sc), list(rc), slot.value
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _lib.load().fgt_points_run_free(h)
+
+    def pack(self):
+        import torch
+        buf = torch.empty(sum(self.send_counts) * self.slot, dtype=torch.float64, device=self.device)
+        _lib.check(_lib.load().fgt_points_pack(self._h, ctypes.c_void_p(buf.data_ptr())))
+        return buf
+
+    def unpack(self, buf):
+        _lib.check(_lib.load().fgt_points_unpack(self._h, ctypes.c_void_p(buf.data_ptr())))
+
+    def exchange(self, exchanger):
+        import torch
+        send = self.pack()
+        recv = torch.empty(sum(self.recv_counts) * self.slot, dtype=torch.float64, device=self.device)
+        exchanger(send, recv, self.send_counts, self.recv_counts, self.slot)
+        self.unpack(recv)
+
+    def finish(self, out=None, return_times=False):
+        import torch
+        if out is None:
+            out = torch.empty(self.nt, dtype=torch.float64, device=self.device)
+        times = _lib.FgtPhaseTimes()
+        _lib.check(_lib.load().fgt_points_finish(self._h, ctypes.c_void_p(out.data_ptr()), ctypes.byref(times)))
+        return (out, times.as_dict()) if return_times else out
+

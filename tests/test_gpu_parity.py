@@ -332,3 +332,48 @@ def test_disjoint_sources_and_targets(cuda):
     ex = ofgt.direct_oracle(y, q, x, 1e-4, "free")
     assert np.all(u[:2000] == 0)
     assert rel(u, ex) <= 10 * 1e-9
+
+
+def _emulated_exchange(runs):
+    """The all-to-all of TorchExchange, done with device copies between the runs of one
+    process: rank r receives, peer by peer, the block every peer q packed for r."""
+    import torch
+    sends = [r.pack() for r in runs]
+    for r, run in enumerate(runs):
+        parts = []
+        for q, rq in enumerate(runs):
+            assert rq.send_counts[r] == run.recv_counts[q]
+            off = sum(rq.send_counts[:r]) * rq.slot
+            parts.append(sends[q][off:off + rq.send_counts[r] * rq.slot])
+        recv = torch.cat(parts) if parts else torch.empty(0, dtype=torch.float64, device="cuda")
+        run.unpack(recv)
+
+
+@pytest.mark.parametrize("size", [2, 3, 5])
+@pytest.mark.parametrize("case", ["clust3d", "periodic2d"])
+def test_exchange_shares_sum_to_full(cuda, size, case):
+    """Owner-formed expansions + halo exchange (the multi-GPU path), ranks run one after
+    another on one GPU with the all-to-all emulated by device copies: the shares are
+    disjoint and sum bitwise to the single-GPU transform; each expansion is formed once."""
+    import torch
+    from paper_2305_07165_b200 import fgt_points_device
+    from paper_2305_07165_b200.point_fgt import fgt_points_exchange_begin
+    r = np.random.default_rng(12)
+    if case == "clust3d":
+        y, x, args = clustered(r, 20000, 3), r.uniform(-0.5, 0.5, (20000, 3)), (1e-4, 1e-9, 100, "free")
+    else:
+        y, x, args = r.uniform(-0.5, 0.5, (30000, 2)), r.uniform(-0.5, 0.5, (30000, 2)), (1e-4, 1e-8, 60, "periodic")
+    q = r.standard_normal(y.shape[0])
+    dy, dq, dx = (torch.from_numpy(a).cuda() for a in (y, q, x))
+    full = fgt_points_device(dy, dq, dx, *args)
+    runs = [fgt_points_exchange_begin(dy, dq, dx, *args, share=(k, size)) for k in range(size)]
+    _emulated_exchange(runs)
+    outs = [run.finish(return_times=True) for run in runs]
+    parts = torch.stack([o[0] for o in outs])
+    assert int(((parts != 0).sum(0)).max()) <= 1
+    assert torch.equal(parts.sum(0), full)
+    # every P-box expansion is formed by exactly one rank (the per-box path choice is the
+    # same as in the full run, so the NUFFT-formed boxes and sources add up exactly)
+    _, tf = fgt_points_device(dy, dq, dx, *args, return_times=True)
+    assert sum(o[1]["n_spread_boxes"] for o in outs) == tf["n_spread_boxes"]
+    assert sum(o[1]["n_src_spread"] for o in outs) == tf["n_src_spread"]

@@ -155,3 +155,47 @@ def test_two_rank_shares_gloo():
     for rank, tiled, err in res:
         assert tiled, f"rank {rank}: targets not covered exactly once"
         assert err < 1e-13, err
+
+
+def _exchange_worker(rank, world, port, q):
+    """One gloo rank of the expansion-halo all-to-all (TorchExchange) on CPU tensors: the
+    counts matrix is known to every rank (as the replicated lists make it on the GPU), the
+    payload encodes (source rank, destination rank, slot)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_07165_b200.point_fgt import TorchExchange
+        slot = 3
+        C = [[0 if a == b else (a + 2 * b) % 4 for b in range(world)] for a in range(world)]  # C[src][dst]
+        send_counts, recv_counts = C[rank], [C[p][rank] for p in range(world)]
+        send = torch.cat([torch.tensor([[rank * 100 + dst * 10 + k] * slot for k in range(C[rank][dst])],
+                                       dtype=torch.float64).reshape(-1) for dst in range(world)])
+        recv = torch.empty(sum(recv_counts) * slot, dtype=torch.float64)
+        TorchExchange()(send, recv, send_counts, recv_counts, slot)
+        want = torch.cat([torch.tensor([[src * 100 + rank * 10 + k] * slot for k in range(C[src][rank])],
+                                       dtype=torch.float64).reshape(-1) for src in range(world)])
+        q.put((rank, bool(torch.equal(recv, want))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_exchange_all_to_all_gloo():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok in res:
+        assert ok, f"rank {rank}: halo blocks out of place"

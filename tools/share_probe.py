@@ -14,6 +14,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -25,10 +26,13 @@ def main():
     ap.add_argument("--sizes", default="1,2,4,8")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mode", choices=["recompute", "exchange"], default="exchange")
     a = ap.parse_args()
     y, q, x = bench.gen_config2(a.n, a.n)
     dy, dq, dx = (torch.from_numpy(v).cuda() for v in (y, q, x))
     out = {}
+    if a.mode == "exchange":
+        return exchange_probe(a, dy, dq, dx)
     for P in (int(s) for s in a.sizes.split(",")):
         per = []
         for r in range(P):
@@ -53,6 +57,45 @@ def main():
                           "rank_ms": [p["ms"] for p in per],
                           "slowest": max(per, key=lambda p: p["ms"])}))
     return out
+
+
+def exchange_probe(a, dy, dq, dx):
+    """Owner-formed expansions + halo all-to-all: per rank, time begin (tree, lists, own
+    expansions, pack) and finish (unpack, translation, evaluation, near field) with CUDA
+    events; the all-to-all itself is emulated by device copies and reported as bytes (the
+    NVLink time is bytes / ~400 GB/s per direction, NCCL all-to-all over NVSwitch)."""
+    from paper_2305_07165_b200.point_fgt import fgt_points_exchange_begin
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
+    from test_gpu_parity import _emulated_exchange
+    for P in (int(s) for s in a.sizes.split(",")):
+        best = None
+        for _ in range(a.reps):
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(P)]
+            runs = []
+            for r in range(P):
+                ev[r][0].record()
+                run = fgt_points_exchange_begin(dy, dq, dx, 1e-4, 1e-9, 200, share=(r, P))
+                ev[r][1].record()
+                runs.append(run)
+            _emulated_exchange(runs)
+            times = []
+            for r, run in enumerate(runs):
+                ev[r][2].record()
+                _, t = run.finish(return_times=True)
+                ev[r][3].record()
+                times.append(t)
+            torch.cuda.synchronize()
+            ms = [ev[r][0].elapsed_time(ev[r][1]) + ev[r][2].elapsed_time(ev[r][3]) for r in range(P)]
+            xbytes = [sum(run.recv_counts) * run.slot * 8 for run in runs]
+            if best is None or max(ms) < best[0]:
+                best = (max(ms), ms, xbytes, times)
+        mx, ms, xbytes, times = best
+        slow = int(np.argmax(ms))
+        print(json.dumps({"P": P, "mode": "exchange", "max_rank_ms": round(mx, 3),
+                          "est_points_per_s": 2 * a.n / (mx * 1e-3), "rank_ms": [round(m, 3) for m in ms],
+                          "halo_recv_MB": [round(b / 1e6, 1) for b in xbytes],
+                          "slowest": {k: round(times[slow][k], 3) for k in ("tree_ms", "lists_ms", "form_ms",
+                                                                            "gather_ms", "eval_ms", "direct_ms")}}))
 
 
 if __name__ == "__main__":
