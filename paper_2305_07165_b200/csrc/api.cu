@@ -234,24 +234,40 @@ __global__ void unpack_slots_kernel(double2* __restrict__ phi, const int64_t* __
 static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool exchange, ExchangePlan* X) {
   cudaStream_t st = T.st;
   const int64_t n = T.n_dtgt;
-  std::vector<double> nt(n), pairs(n), fsrc(n);
-  std::vector<int64_t> tl(n), psi(T.n_psi), poff(T.n_psi + 1), psrc(T.n_p), dense(T.n_dense);
+  // everything the host needs, staged contiguously on the device: one D2H, one sync
+  const int64_t np_ = T.n_p, nps = T.n_psi, nd = T.n_dense;
+  const int64_t o_nt = 0, o_pr = n, o_fs = 2 * n, o_tl = 3 * n, o_psi = 4 * n, o_poff = o_psi + nps,
+                o_psrc = o_poff + nps + 1, o_dense = o_psrc + np_, tot = o_dense + nd;
+  DBuf<int64_t> stage(tot, st);
   if (n > 0) {
-    DBuf<double> ntd(n, st), prd(n, st), fsd(n, st);
+    double* sd = reinterpret_cast<double*>(stage.get());
     leaf_direct_cost_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.d_tgt_ids.get(), n, T.d_off.get(), T.d_src.get(),
                                                               T.src_count.get(), T.tgt_count.get(),
-                                                              T.dense_slot.get(), ntd.get(), prd.get(), fsd.get());
+                                                              T.dense_slot.get(), sd + o_nt, sd + o_pr, sd + o_fs);
     FGT_LAUNCHED();
-    ntd.to_host(nt.data(), n);
-    prd.to_host(pairs.data(), n);
-    fsd.to_host(fsrc.data(), n);
-    T.d_tgt_ids.to_host(tl.data(), n);
   }
-  T.psi_ids.to_host(psi.data(), T.n_psi);
-  T.p_off.to_host(poff.data(), T.n_psi + 1);
-  T.p_src.to_host(psrc.data(), T.n_p);
-  T.dense_ids.to_host(dense.data(), T.n_dense);
+  auto d2d = [&](int64_t off, const int64_t* srcp, int64_t cnt) {
+    if (cnt > 0) FGT_CUDA(cudaMemcpyAsync(stage.get() + off, srcp, cnt * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  };
+  d2d(o_tl, T.d_tgt_ids.get(), n);
+  d2d(o_psi, T.psi_ids.get(), nps);
+  d2d(o_poff, T.p_off.get(), nps + 1);
+  d2d(o_psrc, T.p_src.get(), np_);
+  d2d(o_dense, T.dense_ids.get(), nd);
+  std::vector<int64_t> h(tot);
+  trace_mark(st, "share:stage");
+  stage.to_host(h.data(), tot);
   FGT_CUDA(cudaStreamSynchronize(st));
+  trace_mark(st, "share:d2h(sync)");
+  auto dv = [&](int64_t off, int64_t cnt) {
+    std::vector<double> v(cnt);
+    if (cnt) std::memcpy(v.data(), h.data() + off, cnt * sizeof(double));
+    return v;
+  };
+  const std::vector<double> nt = dv(o_nt, n), pairs = dv(o_pr, n), fsrc = dv(o_fs, n);
+  const std::vector<int64_t> tl(h.begin() + o_tl, h.begin() + o_tl + n), psi(h.begin() + o_psi, h.begin() + o_psi + nps),
+      poff(h.begin() + o_poff, h.begin() + o_poff + nps + 1), psrc(h.begin() + o_psrc, h.begin() + o_psrc + np_),
+      dense(h.begin() + o_dense, h.begin() + o_dense + nd);
   // cost in ns, calibrated on the B200 kernels (profiles/r01f_*): eval 8 N_H flops per
   // target at ~21 TFLOP/s, gather ~2.4 ps per stored mode per P entry, direct ~10 ps per
   // pair; with the exchange, a P-box's form (~2.4 ns per source at w = 11, ~w^3) is
@@ -323,6 +339,7 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
     X->recv_slots.alloc(recv.size(), st);
     X->recv_slots.from_host(recv.data(), recv.size());
   }
+  trace_mark(st, "share:plans");
   // restrict direct CSR (absolute offsets stay valid)
   {
     DBuf<int64_t> ids(hi - lo, st), off(hi - lo + 1, st);
