@@ -501,7 +501,8 @@ constexpr int EVAL_MT = 4;
 // actually used, fixed at compile time so the last (partial) pass issues no idle DMMAs.
 template <int D, int NT, int MTP>
 __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, const double2* __restrict__ psi,
-                                          double* __restrict__ s_u, int R, int n_f, int ksteps, bool half) {
+                                          double* __restrict__ s_u, const int* __restrict__ rinfo, int R,
+                                          int n_f, int ksteps) {
   constexpr int TB = EVAL_TB, NFP = NT * 8, RS = NFP + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
@@ -510,47 +511,47 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
 #pragma unroll
   for (int mt = 0; mt < MTP; ++mt) part[mt] = 0.0;
   for (int nt = warp; nt < ntiles; nt += nwarps) {
-    double acc[MTP][4];
+    // four independent real accumulators per m-tile (re.re, re.im, im.im, im.re): the 4
+    // DMMAs of a complex MAC never wait on each other
+    double acc[MTP][4][2];
 #pragma unroll
     for (int mt = 0; mt < MTP; ++mt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[mt][e] = 0.0;
+      for (int e = 0; e < 4; ++e) acc[mt][e][0] = acc[mt][e][1] = 0.0;
     const int rb = nt * 8 + (lane >> 2);
+    const bool rv = rb < R;
+    const double2* prow = psi + (size_t)(rv ? rb : 0) * n_f;
     for (int kk = 0; kk < ksteps; ++kk) {
       const int c = kk * 4 + (lane & 3);
       double2 B = make_double2(0.0, 0.0);
-      if (rb < R && c < n_f) B = psi[(size_t)rb * n_f + c];
+      if (rv && c < n_f) B = prow[c];
       double2 A[MTP];
 #pragma unroll
       for (int mt = 0; mt < MTP; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
 #pragma unroll
-      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][0], acc[mt][1], A[mt].x, B.x);
-#pragma unroll
-      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].x, B.y);
-#pragma unroll
-      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][0], acc[mt][1], -A[mt].y, B.y);
-#pragma unroll
-      for (int mt = 0; mt < MTP; ++mt) dmma(acc[mt][2], acc[mt][3], A[mt].y, B.x);
+      for (int mt = 0; mt < MTP; ++mt) {
+        dmma(acc[mt][0][0], acc[mt][0][1], A[mt].x, B.x);
+        dmma(acc[mt][1][0], acc[mt][1][1], A[mt].x, B.y);
+        dmma(acc[mt][2][0], acc[mt][2][1], A[mt].y, B.y);
+        dmma(acc[mt][3][0], acc[mt][3][1], A[mt].y, B.x);
+      }
     }
+    // epilogue: per output row its axis-0/1 mode indices and pair weight from rinfo
 #pragma unroll
-    for (int mt = 0; mt < MTP; ++mt) {
-      const int j = mt * 8 + (lane >> 2);
+    for (int i2 = 0; i2 < 2; ++i2) {
+      const int r = nt * 8 + 2 * (lane & 3) + i2;
+      if (r >= R) continue;
+      const int info = rinfo[r];
+      const int i0 = info & 255, i1 = (info >> 8) & 255;
+      const double wp = (info >> 16) ? 2.0 : 1.0;
 #pragma unroll
-      for (int i2 = 0; i2 < 2; ++i2) {
-        const int r = nt * 8 + 2 * (lane & 3) + i2;
-        if (r >= R) continue;
+      for (int mt = 0; mt < MTP; ++mt) {
+        const int j = mt * 8 + (lane >> 2);
         double2 f = make_double2(1.0, 0.0);
-        double wp = 1.0;
-        if (D == 2) {
-          f = etab[(0 * TB + j) * RS + half_plane_mi(r, n_f, half)];
-          wp = half_plane_w(r, n_f, half);
-        }
-        if (D == 3) {
-          const int s = r / n_f;
-          f = cmul(etab[(0 * TB + j) * RS + half_plane_mi(s, n_f, half)], etab[(1 * TB + j) * RS + r % n_f]);
-          wp = half_plane_w(s, n_f, half);
-        }
-        part[mt] += wp * (acc[mt][i2] * f.x - acc[mt][2 + i2] * f.y);
+        if (D == 2) f = etab[(0 * TB + j) * RS + i0];
+        if (D == 3) f = cmul(etab[(0 * TB + j) * RS + i0], etab[(1 * TB + j) * RS + i1]);
+        const double re = acc[mt][0][i2] - acc[mt][2][i2], im = acc[mt][1][i2] + acc[mt][3][i2];
+        part[mt] += wp * (re * f.x - im * f.y);
       }
     }
   }
@@ -570,6 +571,13 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
   static_assert(EVAL_MT == 4, "eval passes are dispatched for 1..4 m-tiles");
   double2* etab = sm;
   double* s_u = reinterpret_cast<double*>(etab + D * TB * RS);
+  int* rinfo = reinterpret_cast<int*>(s_u + 8 * TB);
+  // per stored row: axis-0 mode index (half spectrum), axis-1 index, pair-weight flag
+  for (int r = threadIdx.x; r < a.R; r += blockDim.x) {
+    const int s = D == 3 ? r / a.n_f : r;
+    const int i1 = D == 3 ? r % a.n_f : 0;
+    rinfo[r] = half_plane_mi(s, a.n_f, a.half) | (i1 << 8) | ((half_plane_w(s, a.n_f, a.half) > 1.5) << 16);
+  }
   // one CTA per 32-target pass of a psi box (work items listed box by box, so the
   // passes of one box run together and share psi through L2)
   const int64_t i = a.list[blockIdx.x];
@@ -589,10 +597,10 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
     build_etab<D>(etab, TB, NFP, RS, a.tgt, t0 + p0, cnt, ctr, a.sc, +1.0, n_f);
     __syncthreads();
     switch ((cnt + 7) >> 3) {
-      case 1: eval_pass<D, NT, 1>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
-      case 2: eval_pass<D, NT, 2>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
-      case 3: eval_pass<D, NT, 3>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
-      default: eval_pass<D, NT, 4>(etab, psi, s_u, R, n_f, a.ksteps, a.half); break;
+      case 1: eval_pass<D, NT, 1>(etab, psi, s_u, rinfo, R, n_f, a.ksteps); break;
+      case 2: eval_pass<D, NT, 2>(etab, psi, s_u, rinfo, R, n_f, a.ksteps); break;
+      case 3: eval_pass<D, NT, 3>(etab, psi, s_u, rinfo, R, n_f, a.ksteps); break;
+      default: eval_pass<D, NT, 4>(etab, psi, s_u, rinfo, R, n_f, a.ksteps); break;
     }
     __syncthreads();
     // deterministic cross-warp sum in a fixed order
@@ -685,7 +693,8 @@ void launch_form(PwDev& P, TreeDev& T, const FormArgs& fa, int nrowblk, int nuni
 
 template <int D, int NT>
 void launch_eval(const EvalArgs& ea, int64_t n_psi, cudaStream_t st) {
-  size_t smem = (size_t)D * EVAL_TB * (NT * 8 + 4) * sizeof(double2) + 8 * EVAL_TB * sizeof(double);
+  size_t smem = (size_t)D * EVAL_TB * (NT * 8 + 4) * sizeof(double2) + 8 * EVAL_TB * sizeof(double) +
+                (size_t)ea.R * sizeof(int);
   FGT_CUDA(cudaFuncSetAttribute(eval_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   eval_kernel<D, NT><<<(unsigned)n_psi, 256, smem, st>>>(ea);
   FGT_LAUNCHED();
