@@ -648,7 +648,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     B.keys.alloc(tot, st);
     B.n = tot;
     int64_t off = 0;
-    for (size_t l = 0; l < levels.size(); ++l) {
+    for (size_t l = 0; l < lsize.size(); ++l) {  // levels past the first empty one stay unused
       FGT_CUDA(cudaMemcpyAsync(B.keys.get() + off, levels[l].get(), lsize[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
       off += lsize[l];
     }

@@ -377,3 +377,41 @@ def test_exchange_shares_sum_to_full(cuda, size, case):
     _, tf = fgt_points_device(dy, dq, dx, *args, return_times=True)
     assert sum(o[1]["n_spread_boxes"] for o in outs) == tf["n_spread_boxes"]
     assert sum(o[1]["n_src_spread"] for o in outs) == tf["n_src_spread"]
+
+
+def _sweep_cases(n_cases=24, seed=2024):
+    r = np.random.default_rng(seed)
+    out = []
+    for k in range(n_cases):
+        d = int(r.integers(1, 4))
+        periodic = bool(r.integers(0, 2)) and d >= 2
+        eps = float(10.0 ** -r.integers(3, 13))
+        # periodic image regime needs delta < 1/36 and l_c >= 2; larger delta -> root series
+        delta = float(10.0 ** r.uniform(-5.5, -1.3))
+        n = int(r.integers(200, 6000))
+        n_s = int(r.integers(1, 300))
+        dist = ["uniform", "clustered", "shell"][int(r.integers(0, 3 if d == 3 else 2))]
+        out.append((f"s{k}", d, n, delta, eps, n_s, "periodic" if periodic else "free", dist))
+    return out
+
+
+SWEEP = _sweep_cases()
+
+
+@pytest.mark.parametrize("case", SWEEP, ids=[c[0] for c in SWEEP])
+def test_random_parameter_sweep(cuda, case):
+    """Seeded random (d, n, delta, eps, s, boundary, distribution) against the exact
+    direct sum (and the oracle Alg 2 where it runs in seconds): <= 10 eps."""
+    from paper_2305_07165_b200 import fgt_points
+    name, d, n, delta, eps, n_s, boundary, dist = case
+    r = np.random.default_rng(int(name[1:]) + 77)
+    y = make_points(r, dist, n, d)
+    x = r.uniform(-0.5, 0.5, (max(200, n // 2), d))
+    q = r.uniform(-1, 1, n)
+    u = fgt_points(y, q, x, delta, eps, n_s, boundary)
+    ex = ofgt.direct_oracle(y, q, x, delta, boundary)
+    tol = 10 * max(eps, 1e-14)
+    if np.linalg.norm(ex) > eps * np.linalg.norm(q):
+        assert rel(u, ex) <= tol
+    else:  # the field is below the truncation level everywhere: absolute criterion
+        assert np.linalg.norm(u - ex) <= tol * np.linalg.norm(q)
