@@ -415,3 +415,23 @@ def test_random_parameter_sweep(cuda, case):
         assert rel(u, ex) <= tol
     else:  # the field is below the truncation level everywhere: absolute criterion
         assert np.linalg.norm(u - ex) <= tol * np.linalg.norm(q)
+
+
+TREE_SWEEP = [(c[0], c[1], min(c[2], 2500), c[3], c[4], c[5], c[6] == "periodic", c[7]) for c in _sweep_cases(20, 99)]
+
+
+@pytest.mark.parametrize("case", TREE_SWEEP, ids=[c[0] for c in TREE_SWEEP])
+def test_random_tree_sweep_bit_exact(cuda, case):
+    """Seeded random trees (d, n, delta, eps, s, boundary, distribution): the GPU tree is
+    bit-identical to the oracle's restatement of the reference builder."""
+    from paper_2305_07165_b200.planewave import PERIODIC_IMAGE_DELTA
+    name, d, n, delta, eps, n_s, periodic, dist = case
+    if periodic and delta >= PERIODIC_IMAGE_DELTA:
+        pytest.skip("root Fourier-series regime: a single box")
+    r = np.random.default_rng(int(name[1:]) + 500)
+    y = make_points(r, dist, n, d)
+    x = r.uniform(-0.5, 0.5, (n // 2 + 1, d))
+    a, la, tg = gpu_canonical(y, x, n_s, delta, eps, periodic)
+    b, lb, to = oracle_canonical(y, x, n_s, delta, eps, periodic)
+    assert la == lb and tg.root_side == to.root_side
+    assert a == b
