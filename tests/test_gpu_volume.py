@@ -130,3 +130,41 @@ def test_box_fgt_periodic_root_series(cuda, d, delta, eps, n):
     ex = 2.5 * (np.pi * delta) ** (d / 2)
     for ub in u.values():
         assert np.max(np.abs(ub - ex)) <= 10 * eps * ex
+
+
+def _vol_cases(n=8, seed=7):
+    r = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        d = int(r.integers(1, 4))
+        k = int(r.integers(4, 13 if d < 3 else 9))
+        delta = float(10.0 ** r.uniform(-3.5, -1.5))
+        eps = float(10.0 ** -r.integers(4, 11 if d < 3 else 8))
+        out.append((f"v{i}", d, k, delta, eps, int(r.integers(1, 4))))
+    return out
+
+
+VSWEEP = _vol_cases()
+
+
+@pytest.mark.parametrize("case", VSWEEP, ids=[c[0] for c in VSWEEP])
+def test_box_fgt_random_sweep(cuda, case):
+    """Seeded random (d, k, delta, eps, Gaussian mixture): density tree bit-exact vs the
+    oracle, GPU transform vs the oracle Alg 4 (<= 1e-10 relative) and vs the closed-form
+    Gaussian convolution (<= 10 eps)."""
+    from paper_2305_07165_b200 import volume as pv
+    name, d, k, delta, eps, ng = case
+    r = np.random.default_rng(int(name[1:]) + 31)
+    C = r.uniform(-0.3, 0.3, (ng, d))
+    W = r.uniform(0.03, 0.15, ng)
+    A = r.uniform(0.5, 1.5, ng)
+    dens = lambda p: sum(a * np.exp(-np.sum((p - c) ** 2, axis=-1) / w ** 2)  # noqa: E731
+                         for c, w, a in zip(C, W, A))
+    tree, vals, _ = pv.build_density_tree(dens, d, k, max(eps * 0.1, 1e-12))
+    to = ov.density_tree(dens, d, k, max(eps * 0.1, 1e-12))
+    assert np.array_equal(to.level, tree.level) and np.array_equal(to.coords, tree.coords)
+    u = pv.fgt_box(tree, vals, delta, eps)
+    ref = ov.fgt_box(to, delta, eps)
+    assert rel_err(u, ref) < 1e-10
+    exact = {b: ov.gaussian_box_convolution(to.leaf_points(b), delta, C, W, A) for b in ref}
+    assert rel_err(u, exact) <= 10 * eps
