@@ -453,6 +453,45 @@ struct InterpArgs {
   int w, gmin, G;
 };
 
+// d = 2 interpolation with the kernel width W a compile-time constant (taps and weights in
+// registers) and the box's G x G grid staged in shared memory: one CTA per psi box, one
+// thread per target.
+template <int W>
+__global__ void __launch_bounds__(256) interp2_kernel(InterpArgs a) {
+  extern __shared__ double s_grid[];
+  const int64_t li = blockIdx.x;
+  const int64_t T = a.psi_ids[a.list[li]];
+  const int64_t t0 = a.tgt_start[T];
+  const int nt = (int)a.tgt_count[T];
+  const int G = a.G;
+  const double* grid = a.grid + li * (int64_t)G * G;
+  for (int i = threadIdx.x; i < G * G; i += blockDim.x) s_grid[i] = grid[i];
+  __syncthreads();
+  const double c0 = a.center[T * 2], c1 = a.center[T * 2 + 1];
+  const double s = a.sc * a.inv_delta, half = 0.5 * W, inv_half = 2.0 / W;
+  for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+    const double t_0 = (a.tgt[(t0 + j) * 2] - c0) * s, t_1 = (a.tgt[(t0 + j) * 2 + 1] - c1) * s;
+    const double a0 = ceil(t_0 - half), a1 = ceil(t_1 - half);
+    const int i0 = max(0, min((int)a0 - a.gmin, G - W)), i1 = max(0, min((int)a1 - a.gmin, G - W));
+    double w0[W], w1[W];
+#pragma unroll
+    for (int o = 0; o < W; ++o) {
+      w0[o] = es_kernel((a0 + o - t_0) * inv_half, a.beta);
+      w1[o] = es_kernel((a1 + o - t_1) * inv_half, a.beta);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int o0 = 0; o0 < W; ++o0) {
+      const double* row = s_grid + (i0 + o0) * G + i1;
+      double part = 0.0;
+#pragma unroll
+      for (int o1 = 0; o1 < W; ++o1) part += w1[o1] * row[o1];
+      acc += w0[o0] * part;
+    }
+    a.u[t0 + j] += acc;
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
   __shared__ double s_w[8][D][MAXW];
@@ -884,7 +923,22 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     ia.w = N.w;
     ia.gmin = N.gmin;
     ia.G = G;
-    interp_kernel<D><<<(unsigned)nbat, 256, 0, st>>>(ia);
+    if (D == 2) {
+      const size_t smem = (size_t)G * G * sizeof(double);
+      switch (N.w) {
+#define FGT_I2(WV)                                                                                  \
+  case WV:                                                                                          \
+    FGT_CUDA(cudaFuncSetAttribute(interp2_kernel<WV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    interp2_kernel<WV><<<(unsigned)nbat, 256, smem, st>>>(ia);                                      \
+    break;
+        FGT_I2(2) FGT_I2(3) FGT_I2(4) FGT_I2(5) FGT_I2(6) FGT_I2(7) FGT_I2(8) FGT_I2(9)
+        FGT_I2(10) FGT_I2(11) FGT_I2(12) FGT_I2(13) FGT_I2(14) FGT_I2(15) FGT_I2(16)
+#undef FGT_I2
+        default: throw Error(FGT_ERANGE, "kernel width out of range");
+      }
+    } else {
+      interp_kernel<D><<<(unsigned)nbat, 256, 0, st>>>(ia);
+    }
     FGT_LAUNCHED();
   }
 }
