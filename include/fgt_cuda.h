@@ -271,6 +271,24 @@ int fgt_box_dev(const fgt_box_plan* plan, const double* values, double* u, void*
 int fgt_box(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times);
 
 /* Microbenchmarks used for the roofline denominators (FP64 pipes). */
+/* interp_at (section 4.2 "simply use polynomial interpolation"):
+ * evaluate the piecewise Legendre expansion of a box-FGT output at arbitrary points.
+ * The tree is given by its leaves (host arrays); coeffs (n_leaves, k^dim) are the Legendre
+ * coefficients of each leaf's k^dim grid values (LegendreBasis.val_to_pol per axis).  A
+ * point is located by the deepest leaf containing it (periodic: wrapped into the cell). */
+typedef struct fgt_interp_tree {
+  int32_t dim, k, periodic, pad;
+  int64_t n_leaves;
+  const int32_t* level;   /* (n_leaves) */
+  const int64_t* coords;  /* (n_leaves, dim), integer box coordinates at the box's level */
+  const double* coeffs;   /* (n_leaves, k^dim) */
+  double root_low[3];
+  double root_side;
+} fgt_interp_tree;
+int fgt_box_interp(const fgt_interp_tree* t, const double* x, int64_t n, double* out);
+int fgt_box_interp_dev(const fgt_interp_tree* t, const double* x, int64_t n, double* out,
+                       void* stream);
+
 int fgt_bench_fp64_peak(int use_dmma, double* tflops);
 
 #ifdef __cplusplus

@@ -91,7 +91,19 @@ _I64 = ctypes.c_int64
 _I = ctypes.c_int
 
 # name -> (restype, argtypes); also the list the CPU test checks against the header.
+class FgtInterpTree(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("k", ctypes.c_int32), ("periodic", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("n_leaves", ctypes.c_int64),
+                ("level", ctypes.POINTER(ctypes.c_int32)), ("coords", ctypes.POINTER(ctypes.c_int64)),
+                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("root_low", ctypes.c_double * 3),
+                ("root_side", ctypes.c_double)]
+
+
 SIGNATURES = {
+    "fgt_box_interp": (ctypes.c_int, [ctypes.POINTER(FgtInterpTree), ctypes.c_void_p, ctypes.c_int64,
+                                      ctypes.c_void_p]),
+    "fgt_box_interp_dev": (ctypes.c_int, [ctypes.POINTER(FgtInterpTree), ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
     "fgt_last_error": (ctypes.c_char_p, []),
     "fgt_version": (ctypes.c_char_p, []),
     "fgt_launch_count": (_I64, []),

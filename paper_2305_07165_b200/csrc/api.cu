@@ -839,6 +839,25 @@ int fgt_box_dev(const fgt_box_plan* plan, const double* values, double* u, void*
   });
 }
 
+int fgt_box_interp_dev(const fgt_interp_tree* t, const double* x, int64_t n, double* out, void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(t, FGT_EINVAL, "null tree");
+    box_interp(*t, x, n, out, (cudaStream_t)stream);
+  });
+}
+
+int fgt_box_interp(const fgt_interp_tree* t, const double* x, int64_t n, double* out) {
+  return guarded([&] {
+    FGT_REQUIRE(t, FGT_EINVAL, "null tree");
+    OwnedStream os;
+    DBuf<double> dx(n * t->dim, os.s), dout(n, os.s);
+    dx.from_host(x, n * t->dim);
+    box_interp(*t, dx.get(), n, dout.get(), os.s);
+    dout.to_host(out, n);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+  });
+}
+
 int fgt_box(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times) {
   return guarded([&] {
     FGT_REQUIRE(plan, FGT_EINVAL, "null plan");

@@ -67,5 +67,7 @@ void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted,
 // Continuous (box) FGT executor (k_volume.cu).
 void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
              fgt_phase_times* times);
+// interp_at of a box-FGT output (k_volume.cu)
+void box_interp(const fgt_interp_tree& t, const double* x, int64_t n, double* out, cudaStream_t st);
 
 }  // namespace fgt

@@ -330,4 +330,164 @@ void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream
   else throw Error(FGT_EINVAL, "dim must be 1, 2, or 3");
 }
 
+
+// ---------------------------------------------------------------- interp_at
+namespace {
+constexpr int IMAXK = 24;
+
+struct InterpTreeDev {
+  const uint64_t* keys;   // sorted leaf keys
+  const int64_t* slots;   // coefficient row of each sorted key
+  const double* coeffs;
+  int64_t n_leaves;
+  int dim, k, periodic, max_level;
+  double low[3], side;
+};
+
+// deepest leaf containing x; its centre and half side
+template <int D>
+__device__ int64_t locate_leaf(const InterpTreeDev& t, double* x, double* ctr, double* half) {
+  if (t.periodic)
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] -= floor((x[c] - t.low[c]) / t.side) * t.side;
+  for (int l = t.max_level; l >= 0; --l) {
+    const int64_t n = (int64_t)1 << l;
+    const double sl = t.side / (double)n;
+    int64_t g[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      int64_t v = (int64_t)floor((x[c] - t.low[c]) / sl);
+      g[c] = v < 0 ? 0 : (v >= n ? n - 1 : v);
+    }
+    const uint64_t key = box_key(l, morton_encode(g, D, l));
+    const int64_t i = find_dev(t.keys, t.n_leaves, key);
+    if (i >= 0) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) ctr[c] = t.low[c] + ((double)g[c] + 0.5) * sl;
+      *half = 0.5 * sl;
+      return t.slots[i];
+    }
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void legendre_row(double t, int k, double* P) {
+  P[0] = 1.0;
+  if (k > 1) P[1] = t;
+  for (int n = 1; n + 1 < k; ++n) P[n + 1] = ((2 * n + 1) * t * P[n] - n * P[n - 1]) / (n + 1);
+}
+
+// d = 1, 2: one thread per point
+template <int D>
+__global__ void interp_at_kernel(InterpTreeDev t, const double* __restrict__ xs, int64_t n,
+                                 double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double x[D], ctr[D], half;
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = xs[i * D + c];
+    const int64_t s = locate_leaf<D>(t, x, ctr, &half);
+    if (s < 0) {
+      out[i] = NAN;
+      continue;
+    }
+    const int k = t.k;
+    double P0[IMAXK], P1[IMAXK];
+    legendre_row((x[0] - ctr[0]) / half, k, P0);
+    const double* C = t.coeffs + s * (D == 2 ? k * k : k);
+    double acc = 0.0;
+    if (D == 1) {
+      for (int a = 0; a < k; ++a) acc += C[a] * P0[a];
+    } else {
+      legendre_row((x[1] - ctr[1]) / half, k, P1);
+      for (int a = 0; a < k; ++a) {
+        double r = 0.0;
+        for (int b = 0; b < k; ++b) r += C[a * k + b] * P1[b];
+        acc += P0[a] * r;
+      }
+    }
+    out[i] = acc;
+  }
+}
+
+// d = 3: one warp per point, lanes over the (b, c) pairs of each a-slice
+__global__ void __launch_bounds__(256) interp_at3_kernel(InterpTreeDev t, const double* __restrict__ xs,
+                                                         int64_t n, double* __restrict__ out) {
+  __shared__ double s_P[8][3][IMAXK];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += (int64_t)gridDim.x * 8) {
+    double x[3], ctr[3], half;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[c] = xs[i * 3 + c];
+    const int64_t s = locate_leaf<3>(t, x, ctr, &half);
+    const int k = t.k;
+    if (s >= 0 && lane < 3) legendre_row((x[lane] - ctr[lane]) / half, k, s_P[warp][lane]);
+    __syncwarp();
+    double acc = 0.0;
+    if (s >= 0) {
+      const double* C = t.coeffs + s * (int64_t)k * k * k;
+      for (int a = 0; a < k; ++a) {
+        double r = 0.0;
+        for (int bc = lane; bc < k * k; bc += 32) {
+          const int b = bc / k, c = bc - b * k;
+          r += C[(a * k + b) * k + c] * s_P[warp][1][b] * s_P[warp][2][c];
+        }
+        acc += s_P[warp][0][a] * r;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) out[i] = s >= 0 ? acc : NAN;
+    __syncwarp();
+  }
+}
+}  // namespace
+
+void box_interp(const fgt_interp_tree& tr, const double* x, int64_t n, double* out, cudaStream_t st) {
+  const int d = tr.dim, k = tr.k;
+  FGT_REQUIRE(d >= 1 && d <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+  FGT_REQUIRE(k >= 2 && k <= IMAXK, FGT_ERANGE, "polynomial order outside [2, 24]");
+  FGT_REQUIRE(tr.n_leaves >= 1 && tr.level && tr.coords && tr.coeffs, FGT_EINVAL, "empty tree");
+  int64_t kd = 1;
+  for (int c = 0; c < d; ++c) kd *= k;
+  // leaf keys (level, Morton code) sorted on the host; coefficients stay in leaf order
+  std::vector<std::pair<uint64_t, int64_t>> kv(tr.n_leaves);
+  int max_level = 0;
+  for (int64_t i = 0; i < tr.n_leaves; ++i) {
+    const int l = tr.level[i];
+    FGT_REQUIRE(l >= 0 && d * l <= 57, FGT_ERANGE, "leaf level out of range");
+    max_level = std::max(max_level, l);
+    kv[i] = {box_key(l, morton_encode(tr.coords + i * d, d, l)), i};
+  }
+  std::sort(kv.begin(), kv.end());
+  std::vector<uint64_t> hk(tr.n_leaves);
+  std::vector<int64_t> hs(tr.n_leaves);
+  for (int64_t i = 0; i < tr.n_leaves; ++i) {
+    hk[i] = kv[i].first;
+    hs[i] = kv[i].second;
+  }
+  DBuf<uint64_t> keys(tr.n_leaves, st);
+  DBuf<int64_t> slots(tr.n_leaves, st);
+  DBuf<double> coeffs(tr.n_leaves * kd, st);
+  keys.from_host(hk.data(), hk.size());
+  slots.from_host(hs.data(), hs.size());
+  coeffs.from_host(tr.coeffs, tr.n_leaves * kd);
+  InterpTreeDev t;
+  t.keys = keys.get();
+  t.slots = slots.get();
+  t.coeffs = coeffs.get();
+  t.n_leaves = tr.n_leaves;
+  t.dim = d;
+  t.k = k;
+  t.periodic = tr.periodic;
+  t.max_level = max_level;
+  for (int c = 0; c < 3; ++c) t.low[c] = tr.root_low[c];
+  t.side = tr.root_side;
+  if (n == 0) return;
+  if (d == 1) interp_at_kernel<1><<<grid_for(n, 256), 256, 0, st>>>(t, x, n, out);
+  else if (d == 2) interp_at_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(t, x, n, out);
+  else interp_at3_kernel<<<grid_for(n, 8, 148 * 64), 256, 0, st>>>(t, x, n, out);
+  FGT_LAUNCHED();
+  FGT_CUDA(cudaStreamSynchronize(st));  // host-side tables go out of scope
+}
 }  // namespace fgt

@@ -506,3 +506,36 @@ def fgt_box_device(plan, values_dev, out_dev=None, return_times=False):
                                        ctypes.c_void_p(out_dev.data_ptr()), ctypes.c_void_p(stream),
                                        ctypes.byref(t)))
     return (out_dev, t.as_dict()) if return_times else out_dev
+
+
+def interp_at(tree, potentials, targets):
+    """Values of a box-FGT output at arbitrary points (per-target leaf
+    lookup + tensor Legendre evaluation of the leaf's coefficient tensor; PAPER.md section
+    4.2 "simply use polynomial interpolation").  potentials: {leaf: (k,)*d grid values}
+    as returned by fgt_box; targets (n, d) inside the root box (wrapped if periodic).
+    Runs on the GPU (fgt_box_interp); out-of-domain points give nan."""
+    d = tree.dim
+    leaves = np.nonzero(tree.is_leaf)[0]
+    k = np.asarray(potentials[int(leaves[0])]).shape[0]
+    V = np.stack([np.asarray(potentials[int(b)], float).reshape((k,) * d) for b in leaves])
+    basis = LegendreBasis(k)
+    C = V
+    for ax in range(d):  # values -> Legendre coefficients, axis by axis, all leaves at once
+        C = np.moveaxis(np.tensordot(basis.val_to_pol, C, axes=([1], [ax + 1])), 0, ax + 1)
+    C = np.ascontiguousarray(C.reshape(len(leaves), -1))
+    lev = np.ascontiguousarray(tree.level[leaves], dtype=np.int32)
+    crd = np.ascontiguousarray(tree.coords[leaves], dtype=np.int64)
+    x = np.ascontiguousarray(np.atleast_2d(np.asarray(targets, dtype=np.float64)).reshape(-1, d))
+    t = _lib.FgtInterpTree()
+    t.dim, t.k, t.periodic, t.n_leaves = d, k, int(bool(tree.periodic)), len(leaves)
+    t.level = lev.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    t.coords = crd.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    t.coeffs = C.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    low = np.zeros(3)
+    low[:d] = tree.root_low
+    t.root_low = (ctypes.c_double * 3)(*low)
+    t.root_side = float(tree.root_side)
+    out = np.empty(x.shape[0])
+    _lib.check(_lib.load().fgt_box_interp(ctypes.byref(t), _lib.ptr(x), x.shape[0], _lib.ptr(out)))
+    return out
+

@@ -168,3 +168,32 @@ def test_box_fgt_random_sweep(cuda, case):
     assert rel_err(u, ref) < 1e-10
     exact = {b: ov.gaussian_box_convolution(to.leaf_points(b), delta, C, W, A) for b in ref}
     assert rel_err(u, exact) <= 10 * eps
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_interp_at(cuda, d):
+    """interp_at: exact for polynomials of degree < k, the stored value
+    at a grid node, and the transform's closed form at random points."""
+    from paper_2305_07165_b200 import volume as pv
+    k = 8
+    dens, C, W, A = gaussians(d)
+    tree, vals, _ = pv.build_density_tree(dens, d, k, 1e-9)
+    leaves = np.nonzero(tree.is_leaf)[0]
+    basis = pv.LegendreBasis(k)
+    r = np.random.default_rng(40 + d)
+    # (1) a polynomial of degree k-1 per axis is reproduced to roundoff
+    poly = lambda p: np.prod(1.0 + 0.3 * p + 0.2 * p ** 3 - 0.1 * p ** (k - 1), axis=-1)  # noqa: E731
+    pots = {int(b): poly(pv.leaf_grid(tree, b, basis)) for b in leaves}
+    x = r.uniform(-0.5, 0.5, (5000, d))
+    assert np.max(np.abs(pv.interp_at(tree, pots, x) - poly(x))) < 1e-12
+    # (2) grid nodes of a leaf give the stored values
+    b = int(leaves[len(leaves) // 2])
+    g = pv.leaf_grid(tree, b, basis).reshape(-1, d)
+    assert np.max(np.abs(pv.interp_at(tree, pots, g) - pots[b].reshape(-1))) < 1e-12
+    # (3) the transform at random points vs the closed-form Gaussian convolution
+    delta, eps = 1e-3, 1e-9
+    u = pv.fgt_box(tree, vals, delta, eps)
+    ui = pv.interp_at(tree, u, x)
+    from oracle import volume as ov
+    ex = ov.gaussian_box_convolution(x, delta, C, W, A)
+    assert np.linalg.norm(ui - ex) / np.linalg.norm(ex) < 1e-7
