@@ -539,3 +539,62 @@ def interp_at(tree, potentials, targets):
     _lib.check(_lib.load().fgt_box_interp(ctypes.byref(t), _lib.ptr(x), x.shape[0], _lib.ptr(out)))
     return out
 
+
+
+def coarsen_output(tree, potentials, epsilon):
+    """Alg 6: bottom-up, a non-leaf box whose
+    children are all leaves gets the potential at its own k^d grid by evaluating whichever
+    child holds each node; if that grid's Legendre tail error (Eq. funerr, tail_error) is
+    <= epsilon the children are deleted and the box becomes a leaf.  Returns (tree,
+    potentials) with boxes renumbered (level-restriction is not re-imposed)."""
+    d = tree.dim
+    k = np.asarray(next(iter(potentials.values()))).shape[0]
+    basis = LegendreBasis(k)
+    pots = {int(b): np.asarray(v, float).reshape((k,) * d) for b, v in potentials.items()}
+    is_leaf = tree.is_leaf.copy()
+    alive = np.ones(tree.n_boxes, bool)
+    nc = 1 << d
+    bits = np.array([[(c >> a) & 1 for a in range(d)] for c in range(nc)])
+    for lev in range(int(tree.level.max()) - 1, -1, -1):
+        for b in np.nonzero((tree.level == lev) & ~is_leaf & alive)[0]:
+            ch = tree.children[b]
+            if not all(is_leaf[c] for c in ch):
+                continue
+            # parent nodes -> containing child (node > 0 along an axis -> upper child) and
+            # that child's local coordinate 2 x - (+-1)
+            g = np.stack(np.meshgrid(*([basis.nodes] * d), indexing="ij"), -1).reshape(-1, d)
+            up = (g > 0).astype(int)
+            loc = 2.0 * g - np.where(up == 1, 1.0, -1.0)
+            vals = np.empty(g.shape[0])
+            for c in range(nc):
+                sel = np.all(up == bits[c], axis=1)
+                if not sel.any():
+                    continue
+                child = int(ch[c])
+                coef = apply_per_axis(basis.val_to_pol, pots[child], d)
+                P = [legendre_values(k - 1, loc[sel, a]) for a in range(d)]  # (k, m)
+                if d == 1:
+                    vals[sel] = coef @ P[0]
+                elif d == 2:
+                    vals[sel] = np.einsum("ab,am,bm->m", coef, P[0], P[1])
+                else:
+                    vals[sel] = np.einsum("abc,am,bm,cm->m", coef, P[0], P[1], P[2])
+            V = vals.reshape((k,) * d)
+            if tail_error(apply_per_axis(basis.val_to_pol, V, d)) <= epsilon:
+                pots[int(b)] = V
+                is_leaf[b] = True
+                for c in ch:
+                    alive[c] = False
+                    pots.pop(int(c), None)
+    # renumber the surviving boxes (creation order kept)
+    keep = np.nonzero(alive)[0]
+    new_id = np.full(tree.n_boxes, -1, np.int64)
+    new_id[keep] = np.arange(keep.size)
+    children = tree.children[keep].copy()
+    children[is_leaf[keep]] = -1
+    children = np.where(children >= 0, new_id[np.maximum(children, 0)], -1)
+    parent = np.where(tree.parent[keep] >= 0, new_id[np.maximum(tree.parent[keep], 0)], -1)
+    out = Tree(dim=d, root_center=tree.root_center, root_side=tree.root_side, periodic=tree.periodic,
+               level=tree.level[keep].copy(), parent=parent, children=children,
+               coords=tree.coords[keep].copy(), is_leaf=is_leaf[keep].copy())
+    return out, {int(new_id[b]): v for b, v in pots.items() if alive[b] and is_leaf[b]}

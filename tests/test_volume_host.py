@@ -65,3 +65,26 @@ def test_box_plan_lists_match_oracle(periodic):
     assert got == want
     # every direct pair references 11-offset tables of the source level only
     assert plan.d_tab.size > 0 and plan.d_tab.max() < plan.dtab.shape[0]
+
+
+def test_coarsen_output_alg6():
+    """Alg 6: an over-refined smooth potential collapses toward the root
+    and the kept leaves still hold the function to ~epsilon; a constant collapses fully."""
+    from paper_2305_07165_b200 import volume as pv
+    d, k = 2, 8
+    tree, vals, _ = pv.build_density_tree(lambda p: np.exp(-np.sum(p ** 2, axis=-1) / 0.01), d, k, 1e-10)
+    basis = pv.LegendreBasis(k)
+    f = lambda p: np.prod(np.cos(2 * p), axis=-1)  # noqa: E731
+    pots = {int(b): f(pv.leaf_grid(tree, b, basis)) for b in np.nonzero(tree.is_leaf)[0]}
+    t2, p2 = pv.coarsen_output(tree, pots, 1e-9)
+    assert t2.n_boxes < tree.n_boxes and set(p2) == set(np.nonzero(t2.is_leaf)[0].tolist())
+    assert max(np.max(np.abs(v - f(pv.leaf_grid(t2, b, basis)))) for b, v in p2.items()) < 1e-8
+    # renumbered tree is consistent: parents/children point at live boxes of the right level
+    for b in range(t2.n_boxes):
+        if t2.parent[b] >= 0:
+            assert t2.level[t2.parent[b]] == t2.level[b] - 1
+        for c in t2.children[b]:
+            assert (c < 0) == bool(t2.is_leaf[b])
+    const = {int(b): np.full((k,) * d, 3.0) for b in np.nonzero(tree.is_leaf)[0]}
+    t3, p3 = pv.coarsen_output(tree, const, 1e-12)
+    assert t3.n_boxes == 1 and np.allclose(p3[0], 3.0)
