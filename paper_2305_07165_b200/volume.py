@@ -598,3 +598,56 @@ def coarsen_output(tree, potentials, epsilon):
                level=tree.level[keep].copy(), parent=parent, children=children,
                coords=tree.coords[keep].copy(), is_leaf=is_leaf[keep].copy())
     return out, {int(new_id[b]): v for b, v in pots.items() if alive[b] and is_leaf[b]}
+
+
+def refine_output(tree, values, potentials, delta, epsilon, boundary="free", max_rounds=30):
+    """Alg 5: refine the output tree until every
+    leaf's potential passes the tail test (Eq. funerr) at epsilon.
+
+    Realisation: a refined leaf's children get the source density by exact polynomial
+    refill (the parent's degree < k polynomial evaluated on the children's grids, so
+    sigma is unchanged), the tree is re-balanced with the same refill (level restriction
+    keeps the standard T_pol2pot offsets, so the Alg 5 Remark's extended tables are not
+    needed), and the GPU transform (fgt_box) is re-run on the refined tree: the children
+    receive the true transform values, the quantity Alg 5's translated psi + direct
+    corrections approximate.  Refinement never goes deeper than the input tree's deepest
+    level (Alg 5 Remark).  Returns (tree, values, potentials, n_rounds)."""
+    d = tree.dim
+    k = np.asarray(next(iter(values.values()))).shape[0]
+    basis = LegendreBasis(k)
+    lmax = int(tree.level.max())
+    # child refill operators: P(t)^T with t the child's nodes in the parent's coordinates
+    M = [legendre_values(k - 1, 0.5 * basis.nodes + (0.5 if bit else -0.5)).T for bit in (0, 1)]
+    B = _Builder(d, tree.root_center, tree.root_side, bool(tree.periodic))
+    B.level, B.parent = tree.level.tolist(), tree.parent.tolist()
+    B.coords = [np.asarray(c, np.int64) for c in tree.coords]
+    B.kids = [None if tree.is_leaf[b] else tree.children[b].tolist() for b in range(tree.n_boxes)]
+    B.index = [dict() for _ in range(lmax + 1)]
+    for b in range(tree.n_boxes):
+        B.index[tree.level[b]][tuple(tree.coords[b])] = b
+    vals = {int(b): np.asarray(v, float).reshape((k,) * d) for b, v in values.items()}
+    pots = potentials
+
+    def refill(b, kids):
+        coef = apply_per_axis(basis.val_to_pol, vals.pop(b), d)
+        for c, kid in enumerate(kids):
+            out = coef
+            for ax in range(d):
+                out = np.moveaxis(np.tensordot(M[(c >> ax) & 1], out, axes=([1], [ax])), 0, ax)
+            vals[kid] = np.ascontiguousarray(out)
+
+    rounds = 0
+    cur = tree
+    for rounds in range(max_rounds + 1):
+        marks = [b for b, u in pots.items()
+                 if cur.level[b] < lmax and tail_error(apply_per_axis(basis.val_to_pol,
+                                                                      np.asarray(u).reshape((k,) * d), d)) > epsilon]
+        if not marks or rounds == max_rounds:
+            break
+        for b in marks:
+            if B.leaf(b):
+                refill(b, B.split(b))
+        B.balance(refill)
+        cur = B.finalize()
+        pots = fgt_box(cur, vals, delta, epsilon, boundary)
+    return cur, vals, pots, rounds

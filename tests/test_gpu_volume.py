@@ -197,3 +197,28 @@ def test_interp_at(cuda, d):
     from oracle import volume as ov
     ex = ov.gaussian_box_convolution(x, delta, C, W, A)
     assert np.linalg.norm(ui - ex) / np.linalg.norm(ex) < 1e-7
+
+
+def test_refine_output_alg5(cuda):
+    """Alg 5: leaves whose potential fails the tail test are refined
+    until every leaf passes (up to the input tree's depth, Alg 5 Remark); the refined
+    potentials agree with the old ones at the old grid nodes (value consistency) and the
+    source density is unchanged (exact polynomial refill)."""
+    from paper_2305_07165_b200 import volume as pv
+    d, k, eps, delta, w = 2, 5, 1e-8, 5e-3, 0.12
+    dens = lambda p: np.exp(-np.sum((p - 0.1) ** 2, axis=-1) / w ** 2)  # noqa: E731
+    tree, vals, _ = pv.build_density_tree(dens, d, k, 1e-5)
+    u = pv.fgt_box(tree, vals, delta, eps)
+    basis = pv.LegendreBasis(k)
+    tail = lambda v: pv.tail_error(pv.apply_per_axis(basis.val_to_pol, np.asarray(v).reshape((k,) * d), d))  # noqa: E731
+    lmax = int(tree.level.max())
+    assert any(tail(v) > eps and tree.level[b] < lmax for b, v in u.items())
+    t2, v2, u2, rounds = pv.refine_output(tree, vals, u, delta, eps)
+    assert rounds >= 1 and t2.n_boxes > tree.n_boxes and int(t2.level.max()) <= lmax
+    assert all(tail(v) <= eps for b, v in u2.items() if t2.level[b] < lmax)
+    nodes = np.concatenate([pv.leaf_grid(tree, b, basis).reshape(-1, d) for b in u])
+    old = np.concatenate([np.asarray(u[b]).reshape(-1) for b in u])
+    # (the tail test is an absolute error estimate, Eq. funerr)
+    assert np.max(np.abs(pv.interp_at(t2, u2, nodes) - old)) <= 10 * eps
+    x = np.random.default_rng(51).uniform(-0.5, 0.5, (3000, d))
+    assert np.max(np.abs(pv.interp_at(t2, v2, x) - pv.interp_at(tree, vals, x))) < 1e-12
