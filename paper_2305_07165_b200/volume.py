@@ -277,45 +277,54 @@ class BoxPlan:
         self.leaves = leaves
         leaf_slot = np.full(nb, -1, np.int64)
         leaf_slot[leaves] = np.arange(leaves.size)
-        key = {(int(tree.level[b]),) + tuple(int(c) for c in tree.coords[b]): b for b in range(nb)}
+        # plain-Python views of the tree (per-element numpy indexing dominated this plan)
+        lev = tree.level.tolist()
+        crd = [tuple(c) for c in tree.coords.tolist()]
+        isleaf = tree.is_leaf.tolist()
+        kids = tree.children.tolist()
+        key = {(lev[b],) + crd[b]: b for b in range(nb)}
+        self._plan_views = (lev, crd, isleaf, kids, key)
         km = (np.arange(n_f) - n_f // 2) * self.pw.h / np.sqrt(delta)
         side = tree.root_side / 2.0 ** np.arange(self.n_levels)
-        offs = np.stack(np.meshgrid(*([np.arange(-1, 2)] * d), indexing="ij"), -1).reshape(-1, d)
+        offs = [tuple(o) for o in
+                np.stack(np.meshgrid(*([np.arange(-1, 2)] * d), indexing="ij"), -1).reshape(-1, d).tolist()]
+        zero = (0,) * d
 
         def covering(l, cell):
-            c = np.asarray(cell)
+            c = cell
             for lv in range(l, -1, -1):
-                b = key.get((lv,) + tuple(int(x) for x in c))
+                b = key.get((lv,) + c)
                 if b is not None:
                     return b
-                c = c >> 1
+                c = tuple(x >> 1 for x in c)
             raise RuntimeError("no covering box")
 
         def neighbour_cells(b, with_self=True):
-            l = int(tree.level[b])
-            n_side = 2 ** l
+            n_side = 1 << lev[b]
+            g = crd[b]
             for o in offs:
-                if not with_self and not o.any():
+                if not with_self and o == zero:
                     continue
-                n = tree.coords[b] + o
+                n = tuple(gi + oi for gi, oi in zip(g, o))
                 if periodic:
-                    v = n // n_side
-                    yield n - v * n_side, v
-                elif not (np.any(n < 0) or np.any(n >= n_side)):
-                    yield n, np.zeros(d, np.int64)
+                    v = tuple(x // n_side for x in n)
+                    yield tuple(x - vi * n_side for x, vi in zip(n, v)), v
+                elif all(0 <= x < n_side for x in n):
+                    yield n, zero
 
         # f flags (Definition fflagdef): level > l_c, or level l_c with a subdivided colleague
         f = tree.level > l_c
         coll = {}
-        for b in np.nonzero(tree.level == l_c)[0]:
+        for b in np.nonzero(tree.level == l_c)[0].tolist():
             # colleagues that exist at l_c (a coarser covering leaf interacts directly)
-            lst = [(key[kk], v) for n, v in neighbour_cells(b)
-                   if (kk := (l_c,) + tuple(int(x) for x in n)) in key]
+            lst = [(key[kk], v) for n, v in neighbour_cells(b) if (kk := (l_c,) + n) in key]
             coll[b] = lst
-            f[b] = any(not tree.is_leaf[S] for S, _ in lst) or self.root_series
+            f[b] = any(not isleaf[S] for S, _ in lst) or self.root_series
         pw_slot = np.full(nb, -1, np.int64)
         pw_slot[f] = np.arange(int(f.sum()))
         self.n_pw = int(f.sum())
+        fl = f.tolist()
+        slot = pw_slot.tolist()
 
         # ---- phase rows: out2in (3) at l_c, then c2p (2) and p2c (2) per child level
         rows = [np.exp(1j * km * o * side[l_c]) for o in (-1, 0, 1)]
@@ -334,10 +343,10 @@ class BoxPlan:
         dst, dst_acc, dst_off, ent_src, ent_rows = [], [], [0], [], []
 
         def add_dst(t, entries, acc=0):
-            dst.append(pw_slot[t])
+            dst.append(slot[t])
             dst_acc.append(acc)
-            for s, r in entries:
-                ent_src.append(pw_slot[s])
+            for s_, r in entries:
+                ent_src.append(slot[s_])
                 ent_rows.append(r)
             dst_off.append(len(ent_src))
 
@@ -346,32 +355,31 @@ class BoxPlan:
                 stage_off.append(len(dst))
                 stage_kind.append(kind)
 
+        def child_rows(b, c, table, l1):
+            return [table[(l1, ci - 2 * bi)] for ci, bi in zip(crd[c], crd[b])]
+
         for l in range(lmax - 1, l_c - 1, -1):
-            for b in np.nonzero((tree.level == l) & ~tree.is_leaf)[0]:
-                ents = []
-                for c in tree.children[b]:
-                    bits = tree.coords[c] - 2 * tree.coords[b]
-                    ents.append((c, [c2p_row[(l + 1, int(x))] for x in bits]))
-                add_dst(b, ents)
+            for b in np.nonzero((tree.level == l) & ~tree.is_leaf)[0].tolist():
+                add_dst(b, [(c, child_rows(b, c, c2p_row, l + 1)) for c in kids[b]])
             end_stage(0)
         n_gpairs = 0
+        side_c = 1 << l_c
         for T, lst in coll.items():
-            if not f[T]:
+            if not fl[T]:
                 continue
             ents = []
             for S, v in lst:
-                if f[S] and (self.root_series or not (tree.is_leaf[T] and tree.is_leaf[S])):
-                    o = tree.coords[T] - tree.coords[S] - v * 2 ** l_c  # in {-1, 0, 1}
-                    ents.append((S, [int(x) + 1 for x in o]))
+                if fl[S] and (self.root_series or not (isleaf[T] and isleaf[S])):
+                    # o = coords_T - coords_S - v 2^l_c, in {-1, 0, 1}
+                    ents.append((S, [t - s_ - vi * side_c + 1 for t, s_, vi in zip(crd[T], crd[S], v)]))
             n_gpairs += len(ents)
             add_dst(T, ents)
         end_stage(1)
         self.n_gather_pairs = n_gpairs
         for l in range(l_c, lmax):
-            for b in np.nonzero((tree.level == l) & ~tree.is_leaf & f)[0]:
-                for c in tree.children[b]:
-                    bits = tree.coords[c] - 2 * tree.coords[b]
-                    add_dst(c, [(b, [p2c_row[(l + 1, int(x))] for x in bits])])
+            for b in np.nonzero((tree.level == l) & ~tree.is_leaf & f)[0].tolist():
+                for c in kids[b]:
+                    add_dst(c, [(b, child_rows(b, c, p2c_row, l + 1))])
             end_stage(2)
         self.stage_off = np.array(stage_off, np.int64)
         self.stage_kind = np.array(stage_kind, np.int64)
@@ -400,23 +408,27 @@ class BoxPlan:
 
         # ---- direct: touching leaf pairs with both leaves at level <= l_c (D-list)
         pairs = []
-        for T in (leaves[tree.level[leaves] <= l_c] if not self.root_series else []):
-            lt = int(tree.level[T])
+        for T in (leaves[tree.level[leaves] <= l_c].tolist() if not self.root_series else []):
+            lt = lev[T]
+            side_t = 1 << lt
+            gT = crd[T]
             seen = set()
             for n, v in neighbour_cells(T):
                 S = covering(lt, n)
-                cands = [S] if tree.is_leaf[S] else [
-                    c for c in tree.children[S]
-                    if np.all(tree.coords[c] + 2 * v * 2 ** lt >= 2 * tree.coords[T] - 1)
-                    and np.all(tree.coords[c] + 2 * v * 2 ** lt <= 2 * tree.coords[T] + 2)]
+                if isleaf[S]:
+                    cands = [S]
+                else:
+                    cands = [c for c in kids[S]
+                             if all(2 * gt - 1 <= gc + 2 * vi * side_t <= 2 * gt + 2
+                                    for gc, vi, gt in zip(crd[c], v, gT))]
                 for S2 in cands:
-                    kk = (int(S2),) + tuple(int(x) for x in v)
-                    if kk in seen or not tree.is_leaf[S2] or tree.level[S2] > l_c:
+                    kk = (S2,) + v
+                    if kk in seen or not isleaf[S2] or lev[S2] > l_c:
                         continue
                     seen.add(kk)
                     pairs.append((T, S2, v))
         ctr = tree.centers()
-        used_levels = sorted({int(tree.level[S]) for _, S, _ in pairs})
+        used_levels = sorted({lev[S] for _, S, _ in pairs})
         tab_id = {}
         tabs = []
         for l in used_levels:
@@ -428,17 +440,18 @@ class BoxPlan:
                 tabs.append(((L / 2.0) * Jm.T) @ basis.val_to_pol)
         self.dtab = np.ascontiguousarray(np.array(tabs, np.float64).reshape(-1, k, k))
         look = {(o, r): j for j, (o, r) in enumerate(OFFSETS)}
+        ctr_l = ctr.tolist()
+        side_l = side.tolist()
+        rs = float(tree.root_side)
         d_t, d_s, d_tab = [], [], []
         for T, S, v in sorted(pairs, key=lambda p: leaf_slot[p[0]]):
-            ls = int(tree.level[S])
-            Ls, Lt = side[ls], side[int(tree.level[T])]
-            ids = []
-            for ax in range(d):
-                o = (ctr[T][ax] - ctr[S][ax] - v[ax] * tree.root_side) / Ls
-                ids.append(tab_id[(ls, look[(float(o), float(Lt / Ls))])])
-            d_t.append(leaf_slot[T])
-            d_s.append(leaf_slot[S])
-            d_tab.append(ids)
+            ls = lev[S]
+            Ls, Lt = side_l[ls], side_l[lev[T]]
+            ratio = Lt / Ls
+            cT, cS = ctr_l[T], ctr_l[S]
+            d_tab.append([tab_id[(ls, look[((cT[ax] - cS[ax] - v[ax] * rs) / Ls, ratio)])] for ax in range(d)])
+            d_t.append(int(leaf_slot[T]))
+            d_s.append(int(leaf_slot[S]))
         self.d_tgt = np.array(d_t, np.int64)
         self.d_src = np.array(d_s, np.int64)
         self.d_tab = np.array(d_tab, np.int64).reshape(-1, d)
