@@ -439,6 +439,11 @@ def run_volume_leg(args, flush):
     from paper_2305_07165_b200 import volume as pv
     from tools.prof_volume import build
     tree, vals, plan, t_tree, t_plan = build()
+    from tools.prof_volume import config4_density_torch
+    t0 = time.perf_counter()
+    tree_g, _, _ = pv.build_density_tree(config4_density_torch(), 3, 16, 1e-10, device="cuda")
+    t_tree_gpu = time.perf_counter() - t0
+    same_tree = bool(np.array_equal(tree_g.level, tree.level) and np.array_equal(tree_g.coords, tree.coords))
     leaves, V = pv._stack_values(tree, vals, 16)
     dv = torch.from_numpy(V).cuda()
     out = torch.empty_like(dv)
@@ -489,6 +494,7 @@ def run_volume_leg(args, flush):
                                 "includes": "H2D + GPU + D2H (BoxPlan built once per tree)"},
             "cpu_baseline": cpu,
             "host_density_tree_s": t_tree, "host_plan_s": t_plan,
+            "density_tree_gpu_sigma_s": t_tree_gpu, "density_tree_gpu_sigma_same_tree": same_tree,
             "phases_ms": {k: ph[k] for k in ("form_ms", "gather_ms", "eval_ms", "direct_ms")},
             "checksum": float(sum(np.sum(v) for v in u.values()))}
 

@@ -144,20 +144,32 @@ class _Builder:
             c = c >> 1
         raise RuntimeError("no covering box")
 
+    def _cover_t(self, l, c):
+        for lv in range(min(l, len(self.index) - 1), -1, -1):
+            b = self.index[lv].get(c)
+            if b is not None:
+                return b
+            c = tuple(x >> 1 for x in c)
+        raise RuntimeError("no covering box")
+
     def balance(self, on_split):
+        # same LIFO sweep as the reference builder, on plain-Python tuples
+        offs = [tuple(int(x) for x in o) for o in self.offs]
         stack = [b for b in range(len(self.level)) if self.leaf(b)]
         while stack:
             b = stack.pop()
             if not self.leaf(b) or self.level[b] < 2:
                 continue
-            l, n_side, again = self.level[b], 2 ** self.level[b], False
-            for o in self.offs:
-                n = self.coords[b] + o
+            l, again = self.level[b], False
+            n_side = 1 << l
+            g = tuple(self.coords[b].tolist())
+            for o in offs:
+                n = tuple(gi + oi for gi, oi in zip(g, o))
                 if self.periodic:
-                    n = n - (n // n_side) * n_side
-                elif np.any(n < 0) or np.any(n >= n_side):
+                    n = tuple(x - (x // n_side) * n_side for x in n)
+                elif not all(0 <= x < n_side for x in n):
                     continue
-                nb = self.covering(l, n)
+                nb = self._cover_t(l, n)
                 if self.leaf(nb) and l - self.level[nb] >= 2:
                     kids = self.split(nb)
                     on_split(nb, kids)
@@ -187,8 +199,12 @@ def leaf_grid(tree, box, basis):
 
 
 def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL,
-                       refill="evaluate", root_center=None, root_side=1.0):
-    """Resolve sigma on a level-restricted tree (Alg 3); returns (tree, values, coeffs)."""
+                       refill="evaluate", root_center=None, root_side=1.0, device=None):
+    """Resolve sigma on a level-restricted tree (Alg 3); returns (tree, values, coeffs).
+
+    device="cuda": sigma is a torch function, evaluated on the GPU on each level's batch of
+    grid nodes (one call per refinement level and one for the balance refill); the tree
+    decisions (tail test, balance) stay on the host."""
     if refill != "evaluate":
         # the reference's interpolation refill evaluates at local*0.5 (tree.py:665) and is
         # wrong by O(1); only re-evaluation is supported
@@ -202,13 +218,29 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
     for _ in range(dim - 1):
         wt = np.multiply.outer(wt, basis.weights)
 
-    def sample(b):
+    def nodes_of(b):
         c = B.center(b)
         s = B.rs / 2 ** B.level[b]
         axes = [c[i] + 0.5 * s * basis.nodes for i in range(dim)]
-        v = np.asarray(density(np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1)), float)
-        values[b] = v
-        coeffs[b] = apply_per_axis(basis.val_to_pol, v, dim)
+        return np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1)
+
+    def sample_many(boxes):
+        # one density call for a whole batch of boxes (sigma acts pointwise, so the values
+        # equal per-box calls); coefficients per box as the reference computes them
+        if not boxes:
+            return
+        pts = np.stack([nodes_of(b) for b in boxes])
+        if device is None:
+            vs = np.asarray(density(pts), float)
+        else:
+            import torch
+            vs = density(torch.from_numpy(pts).to(device)).double().cpu().numpy()
+        for b, v in zip(boxes, vs):
+            values[b] = v
+            coeffs[b] = apply_per_axis(basis.val_to_pol, v, dim)
+
+    def sample(b):
+        sample_many([b])
 
     def sigma_norm():
         tot = 0.0
@@ -229,10 +261,12 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
             raise RuntimeError(f"density not resolved at maximum refinement level {l_max}")
         frontier = []
         for b in split:
-            for c in B.split(b):
-                sample(c)
-                frontier.append(c)
-    B.balance(lambda parent, kids: [sample(c) for c in kids])
+            frontier.extend(B.split(b))
+        sample_many(frontier)
+    # balance decisions use only geometry: sample the boxes it creates in one batch
+    created = []
+    B.balance(lambda parent, kids: created.extend(kids))
+    sample_many(created)
     tree = B.finalize()
     leaves = np.nonzero(tree.is_leaf)[0]
     return tree, {b: values[b] for b in leaves}, {b: coeffs[b] for b in leaves}

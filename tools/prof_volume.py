@@ -17,6 +17,21 @@ def config4_density():
                          for ci, ai, wi in zip(c, a, w))
 
 
+def config4_density_torch():
+    """The same density as a torch function (GPU evaluation in build_density_tree)."""
+    import torch
+    r = np.random.default_rng(0)
+    c = torch.from_numpy(r.uniform(-0.3, 0.3, (5, 3)))
+    a = r.uniform(0.5, 1.5, 5)
+    w = np.geomspace(0.01, 0.1, 5)
+
+    def f(p):
+        cc = c.to(p.device)
+        return sum(float(ai) * torch.exp(-torch.sum((p - cc[i]) ** 2, dim=-1) / float(wi) ** 2)
+                   for i, (ai, wi) in enumerate(zip(a, w)))
+    return f
+
+
 def build(k=16, eps_tree=1e-10, delta=1e-4, eps=1e-10):
     from paper_2305_07165_b200 import volume as pv
     t0 = time.perf_counter()
