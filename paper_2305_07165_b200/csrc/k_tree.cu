@@ -193,20 +193,6 @@ __device__ __forceinline__ void offset_of(int t, int* o) {
   }
 }
 
-__global__ void count_flag_kernel(const uint64_t* __restrict__ keys, int64_t lo, int64_t hi,
-                                  const uint64_t* __restrict__ pkey, int64_t npts, int d, int l_c,
-                                  int64_t n_s, uint8_t* __restrict__ flag) {
-  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[i];
-    int l = key_level(k);
-    int sh = d * (l_c - l);
-    uint64_t c = key_code(k);
-    int64_t cnt = prefix_hi(pkey, npts, c, sh) - prefix_lo(pkey, npts, c, sh);
-    flag[i - lo] = cnt > n_s ? 1 : 0;
-  }
-}
-
 __global__ void make_children_kernel(const uint64_t* __restrict__ parents, int64_t np, int d,
                                      uint64_t* __restrict__ out) {
   const int nc = 1 << d;
@@ -428,12 +414,6 @@ __global__ void dense_flag_kernel(const int32_t* __restrict__ level, const uint8
     flag[b] = (leaf[b] && level[b] == l_c && npoints[b] > n_s) ? 1 : 0;
 }
 
-__global__ void dense_slot_kernel(const int64_t* __restrict__ ids, int64_t n, int64_t* __restrict__ slot) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    slot[ids[i]] = i;
-}
-
 __global__ void dense_slot_dev_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
                                       int64_t cap, int64_t* __restrict__ slot) {
   const int64_t n = *n_dev;
@@ -495,16 +475,6 @@ int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int
   B.keys = std::move(grown);
   B.n += nc;
   return k;
-}
-
-std::vector<int64_t> level_offsets(const BoxSet& B, int nlev, cudaStream_t st) {
-  DBuf<int64_t> off(nlev + 1, st);
-  level_offsets_kernel<<<1, 64, 0, st>>>(B.keys.get(), B.n, nlev, off.get());
-  FGT_LAUNCHED();
-  std::vector<int64_t> h(nlev + 1);
-  off.to_host(h.data(), nlev + 1);
-  FGT_CUDA(cudaStreamSynchronize(st));
-  return h;
 }
 
 // One host round trip per round: the count of selected boxes doubles as "changed".
