@@ -102,6 +102,104 @@ __global__ void pair_reduce_kernel(const double* __restrict__ Y, const int64_t* 
   }
 }
 
+// Fused 3-D direct near field: one CTA per target leaf walks its (sorted) D-pairs; per
+// pair the source leaf's k^3 values and the three k x k tables sit in shared memory and
+// Y = (D0 (x) D1 (x) D2) V is formed by three DMMA contractions (V -> X1 -> X2 -> Y) with
+// no global intermediates; Y accumulates in registers across the target's pairs (fixed
+// pair order: deterministic) and is added to u once.  KP = k padded to a multiple of 8.
+template <int KP, int NW>
+__global__ void __launch_bounds__(32 * NW) direct3_kernel(const double* __restrict__ values, const double* __restrict__ dtab,
+                                                      const int64_t* __restrict__ toff, const int64_t* __restrict__ tleaf,
+                                                      const int64_t* __restrict__ src, const int64_t* __restrict__ tab,
+                                                      int k, double* __restrict__ u) {
+  // padded row stride: KP + 4 = 4 mod 16 doubles, so the 16 lanes of a half-warp fragment
+  // load (4 rows x 4 columns, either orientation) hit 16 distinct double-bank pairs
+  constexpr int RS = KP + 4;
+  constexpr int NT1 = KP * KP / 8 * (KP / 8);  // C tiles per stage
+  constexpr int TPW = NT1 / NW;         // tiles per warp
+  extern __shared__ double dsm[];
+  double* Vb = dsm;                     // (KP*KP) x RS : V, later X2
+  double* X1 = Vb + KP * KP * RS;       // (KP*KP) x RS
+  double* Tb = X1 + KP * KP * RS;       // 3 x KP x RS : D0, D1, D2
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x;
+  const int64_t p0 = toff[t], p1 = toff[t + 1];
+  const int64_t kd = (int64_t)k * k * k;
+  double acc[TPW][2];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int r8 = lane >> 2, c4 = lane & 3;
+  for (int64_t p = p0; p < p1; ++p) {
+    __syncthreads();  // previous pair's buffers are free
+    const double* vs = values + src[p] * kd;
+    for (int i = threadIdx.x; i < KP * KP * KP; i += blockDim.x) {
+      const int a = i / (KP * KP), b = (i / KP) % KP, c = i % KP;
+      Vb[(a * KP + b) * RS + c] = (a < k && b < k && c < k) ? vs[((int64_t)a * k + b) * k + c] : 0.0;
+    }
+    for (int i = threadIdx.x; i < 3 * KP * KP; i += blockDim.x) {
+      const int ax = i / (KP * KP), n = (i / KP) % KP, a = i % KP;
+      const double* tb = dtab + tab[p * 3 + ax] * (int64_t)k * k;
+      Tb[(ax * KP + n) * RS + a] = (n < k && a < k) ? tb[n * k + a] : 0.0;
+    }
+    __syncthreads();
+    // stage 1: X1[(a b)][n3] = sum_c V[(a b)][c] D2[n3][c]
+    for (int tt = warp; tt < NT1; tt += NW) {
+      const int mt = tt / (KP / 8), nt = tt % (KP / 8);
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KP; kk += 4) {
+        const double A = Vb[(mt * 8 + r8) * RS + kk + c4];
+        const double B = Tb[(2 * KP + nt * 8 + r8) * RS + kk + c4];
+        dmma2(c0, c1, A, B);
+      }
+      X1[(mt * 8 + r8) * RS + nt * 8 + 2 * c4] = c0;
+      X1[(mt * 8 + r8) * RS + nt * 8 + 2 * c4 + 1] = c1;
+    }
+    __syncthreads();
+    // stage 2: X2[(a n2)][n3] = sum_b D1[n2][b] X1[(a b)][n3]   (into Vb)
+    for (int tt = warp; tt < NT1; tt += NW) {
+      const int a = tt / ((KP / 8) * (KP / 8)), rem = tt % ((KP / 8) * (KP / 8));
+      const int mt = rem / (KP / 8), nt = rem % (KP / 8);
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KP; kk += 4) {
+        const double A = Tb[(KP + mt * 8 + r8) * RS + kk + c4];
+        const double B = X1[(a * KP + kk + c4) * RS + nt * 8 + r8];
+        dmma2(c0, c1, A, B);
+      }
+      Vb[(a * KP + mt * 8 + r8) * RS + nt * 8 + 2 * c4] = c0;
+      Vb[(a * KP + mt * 8 + r8) * RS + nt * 8 + 2 * c4 + 1] = c1;
+    }
+    __syncthreads();
+    // stage 3: Y[n1][(n2 n3)] += sum_a D0[n1][a] X2[(a n2)][n3]   (registers)
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int tt = warp + NW * i;
+      const int mt = tt / (KP * KP / 8), nt = tt % (KP * KP / 8);
+      const int col = nt * 8 + r8, n2 = col / KP, n3 = col % KP;
+#pragma unroll
+      for (int kk = 0; kk < KP; kk += 4) {
+        const double A = Tb[(mt * 8 + r8) * RS + kk + c4];
+        const double B = Vb[((kk + c4) * KP + n2) * RS + n3];
+        dmma2(acc[i][0], acc[i][1], A, B);
+      }
+    }
+  }
+  // u[T] += Y  (fragment: row n1 = 8 mt + lane/4, cols 8 nt + 2 (lane%4) + {0, 1})
+  double* ut = u + tleaf[t] * kd;
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) {
+    const int tt = warp + NW * i;
+    const int mt = tt / (KP * KP / 8), nt = tt % (KP * KP / 8);
+    const int n1 = mt * 8 + r8;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int col = nt * 8 + 2 * c4 + j, n2 = col / KP, n3 = col % KP;
+      if (n1 < k && n2 < k && n3 < k) ut[((int64_t)n1 * k + n2) * k + n3] += acc[i][j];
+    }
+  }
+}
+
 template <class T>
 DBuf<T> upload(const T* h, int64_t n, cudaStream_t st) {
   DBuf<T> d(n, st);
@@ -263,6 +361,20 @@ void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStrea
     toff.push_back(np);
     DBuf<int64_t> src = upload(pl.d_src, np, st), tab = upload(pl.d_tab, np * D, st);
     DBuf<int64_t> toff_d = upload(toff.data(), (int64_t)toff.size(), st), tleaf_d = upload(tleaf.data(), (int64_t)tleaf.size(), st);
+    if (D == 3 && k <= 16) {
+      // fused: tables and intermediates in shared memory, accumulation in registers
+      const int KP = k <= 8 ? 8 : 16;
+      const size_t smem = (size_t)(2 * KP * KP * (KP + 4) + 3 * KP * (KP + 4)) * sizeof(double);
+      const unsigned nt = (unsigned)tleaf.size();
+      if (KP == 8) {
+        FGT_CUDA(cudaFuncSetAttribute(direct3_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        direct3_kernel<8, 4><<<nt, 128, smem, st>>>(values, dtab.get(), toff_d.get(), tleaf_d.get(), src.get(), tab.get(), k, u);
+      } else {
+        FGT_CUDA(cudaFuncSetAttribute(direct3_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        direct3_kernel<16, 8><<<nt, 256, smem, st>>>(values, dtab.get(), toff_d.get(), tleaf_d.get(), src.get(), tab.get(), k, u);
+      }
+      FGT_LAUNCHED();
+    } else {
     const int64_t chunk = std::max<int64_t>(1, (int64_t)(512ll << 20) / (KD * 8 * 2));
     DBuf<double> Y(np * KD, st);
     for (int64_t p0 = 0; p0 < np; p0 += chunk) {
@@ -302,6 +414,7 @@ void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStrea
       pair_reduce_kernel<<<dim3(grid_for(KD, 256, 16), (unsigned)n), 256, 0, st>>>(
           Y.get(), toff_d.get() + t0, tleaf_d.get() + t0, KD, u);
       FGT_LAUNCHED();
+    }
     }
   }
   c_direct.end(st);
