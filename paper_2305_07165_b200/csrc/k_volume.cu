@@ -56,11 +56,10 @@ __global__ void __launch_bounds__(256) shift_kernel(ShiftArgs a) {
   __syncthreads();
   const bool acc_in = a.dst_acc[t] != 0;
   double2* out = a.out + a.dst[t] * a.NF;
-  const int n_f = a.n_f;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.NF;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const unsigned n_f = (unsigned)a.n_f, NF = (unsigned)a.NF;  // n_f^d < 2^32
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < NF; e += gridDim.x * blockDim.x) {
     int m[D];
-    int64_t rem = e;
+    unsigned rem = e;
 #pragma unroll
     for (int k = D - 1; k >= 0; --k) {
       m[k] = (int)(rem % n_f);
