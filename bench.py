@@ -174,7 +174,7 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
     time, averaged over the timed steps.  Exact tensor-factored sums: 8 N_F flops per
     point (one complex MAC per mode).  NUFFT path: per point 2 W^d (spread/interp FMA)
     + d W c_exp (c_exp = 20 flops per kernel exp), per box 8 x the separable-DFT complex
-    MACs.  Gather: 16 B per mode read per P entry + written per psi box (streamed).  N_F
+    MACs.  Gather: 16 B per mode per P-box read + per psi box written (compulsory).  N_F
     counts the stored (half-spectrum) modes: the work the algorithm needs for real
     charges, not the full n_f^d grid."""
     ph = phases[-1]
@@ -187,7 +187,10 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
     dft = 8.0 * box_dft_cmacs(d, G, n_f)
     f_form = 8.0 * NF * exact_src + per_pt * ph["n_src_spread"] + dft * ph["n_spread_boxes"]
     f_eval = 8.0 * NF * exact_tgt + per_pt * ph["n_tgt_spread"] + dft * ph["n_spread_psi"]
-    b_gather = 16.0 * NF * (ph["n_p_entries"] + ph["n_psi"])
+    # compulsory bytes: every phi read once, every psi written once; the
+    # per-P-entry streamed count (16 N_F per entry) exceeds what the sibling-group kernel
+    # actually moves, so it is not used as the roofline numerator
+    b_gather = 16.0 * NF * (ph["n_dense"] + ph["n_psi"])
     mean = lambda k: float(np.mean([p[k] for p in phases]))  # noqa: E731
     src = "FP64 DMMA microbenchmark on this GPU (fgt_bench_fp64_peak; not in MEASURED_PEAKS.json)"
     out = []
@@ -206,7 +209,7 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
             ach = alg / (ms * 1e-3) / 1e9
             out.append({"kernel": name, "bound": "hbm", "achieved": ach, "peak": HBM_PEAK_GBS,
                         "unit": "GB/s", "frac": ach / HBM_PEAK_GBS, "kernel_ms": ms, "alg": alg,
-                        "accounting": "streamed bytes per launch (phi per P entry + psi)",
+                        "accounting": "compulsory bytes per launch (each phi read once, each psi written once)",
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
     return out
 
