@@ -288,6 +288,51 @@ __global__ void balance_flag_kernel(const uint64_t* __restrict__ keys, int64_t n
   }
 }
 
+// Incremental balance round: the fine-side check of balance_flag_kernel for a list of
+// candidate boxes (by key), one thread per (candidate, offset); candidates that forced a
+// split are marked active (their neighbourhood changed: re-checked next round).
+template <int D>
+__global__ void balance_cand_kernel(const uint64_t* __restrict__ keys, int64_t nb,
+                                    const uint64_t* __restrict__ cand, int64_t ncand, int periodic,
+                                    uint8_t* __restrict__ split, uint8_t* __restrict__ active) {
+  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < ncand * NOFF;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = it / NOFF;
+    const int t = (int)(it - i * NOFF);
+    const uint64_t key = cand[i];
+    const int l = key_level(key);
+    if (l < 2) continue;
+    int o[D];
+    offset_of<D>(t, o);
+    bool self = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) self &= (o[k] == 0);
+    if (self) continue;
+    // only leaves force splits
+    if (find_dev(keys, nb, box_key(l + 1, key_code(key) << D)) >= 0) continue;
+    int64_t g[D];
+    morton_decode(key_code(key), D, l, g);
+    int64_t n[D];
+    int v[D];
+    if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
+    const int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
+    if (j < 0) continue;
+    const uint64_t kj = keys[j];
+    if (l - key_level(kj) >= 2 && find_dev(keys, nb, box_key(key_level(kj) + 1, key_code(kj) << D)) < 0) {
+      split[j] = 1;
+      active[i] = 1;
+    }
+  }
+}
+
+__global__ void concat_keys_kernel(const uint64_t* __restrict__ a, int64_t na, const uint64_t* __restrict__ b,
+                                   int64_t nb, uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < na ? a[i] : b[i - na];
+}
+
 // dense-cutoff-leaf fix (tree.py:506-523): a level-l_c leaf with > n_s points forces
 // the split of every leaf neighbour at level l_c-1.
 template <int D>
@@ -455,7 +500,7 @@ struct BoxSet {
 // Split the boxes flagged in `flag` (aligned with keys[lo, lo+n)): append their 2^d
 // children and re-sort.  Returns the number of boxes split.
 int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int d, CubTmp& tmp,
-                      cudaStream_t st) {
+                      cudaStream_t st, DBuf<uint64_t>* kids_out = nullptr) {
   if (n == 0) return 0;
   DBuf<uint64_t> sel(n, st);
   DBuf<int64_t> nsel(1, st);
@@ -474,22 +519,53 @@ int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int
   FGT_LAUNCHED();
   B.keys = std::move(grown);
   B.n += nc;
+  if (kids_out) *kids_out = std::move(kids);
   return k;
 }
 
-// One host round trip per round: the count of selected boxes doubles as "changed".
+// 2:1 balance to its fixpoint.  Round 1 checks every candidate; later rounds only the
+// boxes whose neighbourhood changed: the children just created and the leaves that forced
+// a split (a violation needs a fine leaf next to a coarse one, so any new one involves a
+// new box or a leaf whose covering neighbour was just split).  One host round trip per
+// round (the split count doubles as "changed").  cand == nullptr: all boxes.
 template <int D>
-void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st) {
-  DBuf<int> any(1, st);
+void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st, const DBuf<uint64_t>* first = nullptr) {
+  DBuf<uint64_t> cand;
+  int64_t ncand;
+  if (first) {
+    ncand = first->size();
+    cand.alloc(ncand, st);
+    if (ncand) FGT_CUDA(cudaMemcpyAsync(cand.get(), first->get(), ncand * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  } else {
+    ncand = B.n;
+    cand.alloc(ncand, st);
+    FGT_CUDA(cudaMemcpyAsync(cand.get(), B.keys.get(), ncand * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  }
   for (int round = 0; round < 4096; ++round) {
-    DBuf<uint8_t> leaf(B.n, st), split(B.n, st);
+    if (ncand == 0) return;
+    DBuf<uint8_t> split(B.n, st), active(ncand, st);
     split.zero();
-    leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
+    active.zero();
+    balance_cand_kernel<D><<<grid_for(ncand * 27, 128), 128, 0, st>>>(B.keys.get(), B.n, cand.get(), ncand,
+                                                                      periodic, split.get(), active.get());
     FGT_LAUNCHED();
-    balance_flag_kernel<D><<<grid_for(B.n * 27, 128), 128, 0, st>>>(B.keys.get(), B.n, leaf.get(), periodic,
-                                                                 split.get(), any.get());
+    // active candidates, selected before the key array grows
+    DBuf<uint64_t> act(ncand, st);
+    DBuf<int64_t> nact(1, st);
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, cand.get(), active.get(), act.get(), nact.get(), (int)ncand, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, cand.get(), active.get(), act.get(), nact.get(), (int)ncand, st));
+    count_launch();
+    DBuf<uint64_t> kids;
+    const int64_t k = split_flagged(B, 0, B.n, split.get(), D, tmp, st, &kids);
+    if (k == 0) return;
+    const int64_t na = read_scalar(nact.get(), st);
+    const int64_t nk = kids.size();
+    DBuf<uint64_t> next(nk + na, st);
+    concat_keys_kernel<<<grid_for(nk + na, 256), 256, 0, st>>>(kids.get(), nk, act.get(), na, next.get());
     FGT_LAUNCHED();
-    if (split_flagged(B, 0, B.n, split.get(), D, tmp, st) == 0) return;
+    cand = std::move(next);
+    ncand = nk + na;
   }
   throw Error(FGT_ECUDA, "tree balance did not converge");
 }
@@ -638,8 +714,9 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
           B.keys.get(), B.n, 0, B.n, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
           split.get(), any.get());
       FGT_LAUNCHED();
-      if (split_flagged(B, 0, B.n, split.get(), D, tmp, st) == 0) break;
-      balance_rounds<D>(B, tp.periodic, tmp, st);
+      DBuf<uint64_t> kids;
+      if (split_flagged(B, 0, B.n, split.get(), D, tmp, st, &kids) == 0) break;
+      balance_rounds<D>(B, tp.periodic, tmp, st, &kids);
     }
   }
 
