@@ -252,43 +252,8 @@ __global__ void leaf_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, 
   }
 }
 
-// 2:1 balance round (tree.py:378-403): a leaf b at level l >= 2 forces the split of any
-// leaf neighbour covering at level <= l-2.
-template <int D>
-__global__ void balance_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb,
-                                    const uint8_t* __restrict__ leaf, int periodic,
-                                    uint8_t* __restrict__ split, int* __restrict__ any) {
-  // one thread per (box, neighbour offset): the covering searches are latency chains, so
-  // spread them over 3^d x more threads
-  constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nb * NOFF;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = it / NOFF;
-    const int t = (int)(it - i * NOFF);
-    if (!leaf[i]) continue;
-    uint64_t key = keys[i];
-    int l = key_level(key);
-    if (l < 2) continue;
-    int o[D];
-    offset_of<D>(t, o);
-    bool self = true;
-#pragma unroll
-    for (int k = 0; k < D; ++k) self &= (o[k] == 0);
-    if (self) continue;
-    int64_t g[D];
-    morton_decode(key_code(key), D, l, g);
-    int64_t n[D];
-    int v[D];
-    if (!neighbor_cell<D>(g, o, l, periodic, n, v)) continue;
-    int64_t j = find_covering_dev(keys, nb, D, l, morton_encode(n, D, l));
-    if (j >= 0 && leaf[j] && l - key_level(keys[j]) >= 2) {
-      split[j] = 1;
-      *any = 1;
-    }
-  }
-}
-
-// Incremental balance round: the fine-side check of balance_flag_kernel for a list of
+// Incremental 2:1 balance round (tree.py:378-403): a leaf b at level l >= 2 forces the
+// split of any leaf neighbour covering at level <= l-2.  Checked for a list of
 // candidate boxes (by key), one thread per (candidate, offset); candidates that forced a
 // split are marked active (their neighbourhood changed: re-checked next round).
 template <int D>
@@ -341,7 +306,7 @@ __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t 
                                      const uint64_t* __restrict__ pkey, int64_t npts, int l_c,
                                      int64_t n_s, int periodic, uint8_t* __restrict__ split,
                                      int* __restrict__ any) {
-  // one thread per (box, neighbour offset), as balance_flag_kernel
+  // one thread per (box, neighbour offset), as balance_cand_kernel
   constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < (hi - lo) * NOFF;
        it += (int64_t)gridDim.x * blockDim.x) {
@@ -427,14 +392,31 @@ __global__ void source_flag_kernel(const int64_t* __restrict__ pidx, int64_t npt
 
 // leaf of every point (the deepest box containing its l_c cell), scattered to the
 // original (combined) index, so a stable sort by leaf keeps ascending indices
-template <int D>
-__global__ void point_leaf_kernel(const uint64_t* __restrict__ keys, int64_t nb,
-                                  const uint64_t* __restrict__ pkey, const int64_t* __restrict__ pidx,
-                                  int64_t npts, int l_c, int64_t* __restrict__ leaf_of) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npts;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    leaf_of[pidx[i]] = find_covering_dev(keys, nb, D, l_c, pkey[i]);
+// Leaves are contiguous ranges of the Morton-sorted points: each non-empty leaf marks its
+// first point (two binary searches per leaf instead of one covering search per point);
+// a fill-forward scan then gives every sorted point its leaf.
+__global__ void leaf_first_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ is_leaf,
+                                  int64_t nb, const uint64_t* __restrict__ pkey, int64_t npts, int d, int l_c,
+                                  int64_t* __restrict__ mark) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    if (!is_leaf[b]) continue;
+    const uint64_t k = keys[b];
+    const int sh = d * (l_c - key_level(k));
+    const int64_t s = prefix_lo(pkey, npts, key_code(k), sh);
+    if (s < npts && s < prefix_hi(pkey, npts, key_code(k), sh)) mark[s] = b;
   }
+}
+
+struct FillForward {
+  __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return b >= 0 ? b : a; }
+};
+
+__global__ void leaf_scatter_kernel(const int64_t* __restrict__ filled, const int64_t* __restrict__ pidx,
+                                    int64_t npts, int64_t* __restrict__ leaf_of) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npts;
+       i += (int64_t)gridDim.x * blockDim.x)
+    leaf_of[pidx[i]] = filled[i];
 }
 
 __global__ void iota_kernel(int64_t* a, int64_t n) {
@@ -758,8 +740,20 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   // ---- per-point leaves, stable sorts -> src_perm / tgt_perm (tree.py:533-564)
   {
     DBuf<int64_t> leaf_of(np, st);
-    point_leaf_kernel<D><<<grid_for(np, 256), 256, 0, st>>>(T.bkey.get(), nb, T.pkey.get(), T.pidx.get(), np, l_c, leaf_of.get());
-    FGT_LAUNCHED();
+    {
+      DBuf<int64_t> mark(np, st), filled(np, st);
+      fill_i64_kernel<<<grid_for(np, 256), 256, 0, st>>>(mark.get(), np, -1);
+      FGT_LAUNCHED();
+      leaf_first_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, T.pkey.get(), np, D,
+                                                         l_c, mark.get());
+      FGT_LAUNCHED();
+      size_t bytes = 0;
+      FGT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.get(), filled.get(), FillForward(), (int)np, st));
+      FGT_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(bytes, st), bytes, mark.get(), filled.get(), FillForward(), (int)np, st));
+      count_launch();
+      leaf_scatter_kernel<<<grid_for(np, 256), 256, 0, st>>>(filled.get(), T.pidx.get(), np, leaf_of.get());
+      FGT_LAUNCHED();
+    }
     const int bits = bits_for(nb);
     for (int which = 0; which < 2; ++which) {
       int64_t n = which ? nt : ns;
