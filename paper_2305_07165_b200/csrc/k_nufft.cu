@@ -180,27 +180,61 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
 // weights], rq (n) charge, ra (n, 4) first taps (a_0, a_1, a_2), rw0 (n, 16) axis-0 weights
 // (d = 3 plane factor).  One gather after the sort makes every job's staging a contiguous,
 // coalesced copy instead of a perm -> index -> weights pointer chase.
+// Block = 32 sorted points; warp a evaluates axis a (lane = point).  Interior taps by the
+// plan's Horner polynomials (16 independent accumulators), the two edge taps -- where the
+// kernel has its square-root branch point -- exactly; then each warp writes its 32 x 16
+// weights through shared memory as 128-byte rows.
+constexpr int REC_PTS = 32;
+constexpr int HC_MAX = 25;  // max polynomial degree + 1
 template <int D>
-__global__ void sort_records_kernel(const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ tt,
-                                    const int* __restrict__ ai, const double* __restrict__ qb, int w,
-                                    double beta, double* __restrict__ rw, double* __restrict__ rq,
-                                    int* __restrict__ ra, double* __restrict__ rw0) {
-  const int RA = D == 3 ? 1 : 0, CA = D == 3 ? 2 : 1;
+__global__ void __launch_bounds__(D * 32) sort_records_kernel(
+    const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ tt, const int* __restrict__ ai,
+    const double* __restrict__ qb, int w, double beta, const double* __restrict__ hc, int K,
+    double* __restrict__ rw, double* __restrict__ rq, int* __restrict__ ra, double* __restrict__ rw0) {
+  __shared__ double s_c[HC_MAX * 16];
+  __shared__ double s_w[D][REC_PTS][17];
+  for (int i = threadIdx.x; i < (K + 1) * 16; i += blockDim.x) s_c[i] = hc[i];
+  __syncthreads();
+  const int ax = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * REC_PTS, j = j0 + lane;
   const double half = 0.5 * w, inv_half = 2.0 / w;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 32;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = t >> 5;
-    const int o = (int)(t & 31);
+  if (j < n) {
     const int64_t i = perm[j];
-    const int ax = o < 16 ? RA : CA, tap = o & 15;
     const double x = tt[i * D + ax];
-    rw[t] = tap < w ? es_kernel((ceil(x - half) + tap - x) * inv_half, beta) : 0.0;
-    if (D == 3 && o < 16) {
-      const double x0 = tt[i * D];
-      rw0[j * 16 + o] = o < w ? es_kernel((ceil(x0 - half) + o - x0) * inv_half, beta) : 0.0;
+    const double a0 = ceil(x - half);
+    const double y = 2.0 * ((a0 - x) + half) - 1.0;
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = s_c[K * 16 + t];
+    for (int p = K - 1; p >= 0; --p) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) acc[t] = fma(acc[t], y, s_c[p * 16 + t]);
     }
-    if (o < 4) ra[j * 4 + o] = o < D ? ai[i * D + o] : 0;
-    if (o == 0) rq[j] = qb[i];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      double v = acc[t];
+      if (t == 0 || t == w - 1) v = es_kernel((a0 + t - x) * inv_half, beta);
+      s_w[ax][lane][t] = t < w ? v : 0.0;
+    }
+    if (ax == 0) {
+      rq[j] = qb[i];
+      int4 a;
+      a.x = ai[i * D];
+      a.y = D > 1 ? ai[i * D + 1] : 0;
+      a.z = D > 2 ? ai[i * D + 2] : 0;
+      a.w = 0;
+      reinterpret_cast<int4*>(ra)[j] = a;
+    }
+  }
+  __syncwarp();
+  // d = 3: axis 0 -> rw0, axis 1 -> rw rows, axis 2 -> rw columns; d = 2: axes 0, 1 -> rw
+  double* dst;
+  int stride, off;
+  if (D == 3 && ax == 0) { dst = rw0; stride = 16; off = 0; }
+  else { dst = rw; stride = 32; off = (ax == D - 1) ? 16 : 0; }
+  for (int e = lane; e < REC_PTS * 16; e += 32) {
+    const int pt = e >> 4, t = e & 15;
+    if (j0 + pt < n) dst[(j0 + pt) * stride + off + t] = s_w[ax][pt][t];
   }
 }
 
@@ -606,6 +640,64 @@ const NufftPlan& nufft_plan_cached(int n_f, double tol, double X, const double* 
   return *p;
 }
 
+// Piecewise-polynomial ES kernel (the Horner scheme FINUFFT uses for its spreader): a point
+// whose first tap sits f in [0, 1) cells right of x - w/2 gives tap t the weight
+// es((2 (f + t) - w) / w).  Per interior tap, Chebyshev interpolation in y = 2f - 1 at
+// degree K, converted to monomials in long double; K grows until the worst interior-tap
+// error on a fine grid is <= max(tol / 1000, 2e-14) (or the best K <= 24 is kept).  The
+// edge taps t = 0, w-1 hold the kernel's square-root branch point (z = -+1) and are always
+// evaluated exactly.  Output hc[p * 16 + t], p = 0..K.
+static void es_fit(int w, double beta, double tol, std::vector<double>& hc, int& K_out) {
+  const double target = std::max(1e-3 * tol, 2e-14);
+  double best_err = 1e300;
+  std::vector<double> best;
+  int best_k = 0;
+  for (int K = 8; K < HC_MAX; ++K) {
+    std::vector<double> c((K + 1) * 16, 0.0);
+    for (int t = 1; t + 1 < w; ++t) {
+      std::vector<long double> a(K + 1, 0.0L);
+      for (int k = 0; k <= K; ++k) {
+        long double s = 0;
+        for (int j = 0; j <= K; ++j) {
+          const long double th = M_PIl * (j + 0.5L) / (K + 1);
+          const double y = (double)cosl(th);
+          s += (long double)es_kernel((2.0 * (0.5 * (y + 1.0) + t) - w) / w, beta) * cosl(k * th);
+        }
+        a[k] = 2.0L * s / (K + 1);
+      }
+      a[0] *= 0.5L;
+      // sum_k a_k T_k(y) in monomials: T_{k+1} = 2 y T_k - T_{k-1}
+      std::vector<long double> tm1(K + 1, 0.0L), tk(K + 1, 0.0L), mono(K + 1, 0.0L);
+      tm1[0] = 1.0L;
+      if (K >= 1) tk[1] = 1.0L;
+      for (int p = 0; p <= K; ++p) mono[p] += a[0] * tm1[p];
+      for (int k = 1; k <= K; ++k) {
+        for (int p = 0; p <= K; ++p) mono[p] += a[k] * tk[p];
+        std::vector<long double> nx(K + 1, 0.0L);
+        for (int p = 0; p <= K; ++p) {
+          if (p + 1 <= K) nx[p + 1] += 2.0L * tk[p];
+          nx[p] -= tm1[p];
+        }
+        tm1.swap(tk);
+        tk.swap(nx);
+      }
+      for (int p = 0; p <= K; ++p) c[p * 16 + t] = (double)mono[p];
+    }
+    double err = 0.0;
+    for (int t = 1; t + 1 < w; ++t)
+      for (int q = 0; q <= 2000; ++q) {
+        const double f = q / 2000.0, y = 2.0 * f - 1.0;
+        double v = c[K * 16 + t];
+        for (int p = K - 1; p >= 0; --p) v = std::fma(v, y, c[p * 16 + t]);
+        err = std::max(err, std::fabs(v - es_kernel((2.0 * (f + t) - w) / w, beta)));
+      }
+    if (err < best_err) { best_err = err; best = c; best_k = K; }
+    if (err <= target) break;
+  }
+  hc = best;
+  K_out = best_k;
+}
+
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
   N.n_f = n_f;
   N.tol = tol;
@@ -676,6 +768,10 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.EfH.from_host(EfH.data(), EfH.size());
   N.EeH.alloc(EeH.size(), st);
   N.EeH.from_host(EeH.data(), EeH.size());
+  std::vector<double> hc;
+  es_fit(N.w, N.beta, tol, hc, N.hdeg);
+  N.hc.alloc(hc.size(), st);
+  N.hc.from_host(hc.data(), hc.size());
   // (pageable host -> device async copies are staged before they return: the host
   // vectors may go out of scope without a stream sync)
 }
@@ -775,8 +871,9 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       rq = g_rq.view(npts, st);
       ra = g_ra.view(npts * 4, st);
       if (D == 3) rw0 = g_rw0.view(npts * 16, st);
-      sort_records_kernel<D><<<grid_for(npts * 32, 256), 256, 0, st>>>(
-          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, rw.get(), rq.get(), ra.get(), rw0.get());
+      sort_records_kernel<D><<<(unsigned)((npts + REC_PTS - 1) / REC_PTS), D * 32, 0, st>>>(
+          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, N.hc.get(), N.hdeg, rw.get(), rq.get(),
+          ra.get(), rw0.get());
       FGT_LAUNCHED();
     }
     const int64_t njob = D == 2 ? nbat : nbat * G;

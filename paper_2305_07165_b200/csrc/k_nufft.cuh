@@ -19,6 +19,10 @@ struct NufftPlan {
   DBuf<double> Ee, EeT;     // eval: (G, n_f) and (n_f, G) complex        e^{+i m g Delta}/fh[m]
   DBuf<double> EfH;         // (nh, G): rows of Ef for the stored axis-0 planes (half spectrum)
   DBuf<double> EeH;         // (G, nh): columns of Ee for the stored planes x pair weight
+  // piecewise-polynomial kernel weights (interior taps): hc[p * 16 + t] is the degree-p
+  // coefficient of tap t in y = 2f - 1, f in [0, 1) the first tap's offset (see es_fit)
+  int hdeg = 0;
+  DBuf<double> hc;
 };
 
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);

@@ -10,3 +10,8 @@ for i in range(6):
     u, t = fgt_points(hy, hq, hx, 1e-4, 1e-9, 200, return_times=True)
     dt = time.perf_counter() - t0
     print(f"wall {dt*1e3:.2f} ms  h2d {t['h2d_ms']:.2f} total {t['total_ms']:.2f} d2h {t['d2h_ms']:.2f} form {t['form_ms']:.2f} tree {t['tree_ms']:.2f}")
+from paper_2305_07165_b200.point_fgt import FgtParams
+for i in range(3):
+    t0 = time.perf_counter()
+    FgtParams(3, 1e-4, 1e-9, 200, False, (0, 1))
+    print(f"params {1e3*(time.perf_counter()-t0):.3f} ms")
