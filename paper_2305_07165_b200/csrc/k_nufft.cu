@@ -13,6 +13,7 @@
 //      only n_f of the 2 n_f modes are ever needed);
 //   3. evaluation runs the transposed chain and interpolates with the same kernel.
 // Partial grids of K-split boxes are summed in a fixed order (deterministic).
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <mutex>
@@ -141,29 +142,47 @@ __device__ __forceinline__ uint64_t morton2_8(unsigned x, unsigned y) {
 // key = (box, a_0, Morton(a_1, a_2)) for d = 3, (box, Morton(a_0, a_1)) for d = 2 (16 bits
 // for the last two taps), (box, a_0) for d = 1: a plane job is one key range (a_0 major) and
 // consecutive points are spatially compact, so a 4-point DMMA group touches few tiles
+// d = 3 row class of a first tap: 8-row blocks cut at a = 0 and a = 1 - w (mod 8), so the
+// taps [a, a + w) touch row block b exactly for the classes [cls(8b - w + 1), cls(8b + 7)]
+__host__ __device__ __forceinline__ int row_class(int a, int w) {
+  const int r = ((1 - w) % 8 + 8) % 8;
+  return 2 * (a >> 3) + ((a & 7) >= r ? 1 : 0);
+}
+
+// d = 3 key (box, row class of a_1, a_0, a_2): a pencil's row range is one key range
 template <int D>
-__global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __restrict__ ai, int64_t n) {
+__global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __restrict__ ai, int64_t n, int w) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = key[i];
     if (D == 1) k = (k << 8) | (uint64_t)ai[i];
     if (D == 2) k = (k << 16) | morton2_8((unsigned)ai[i * 2], (unsigned)ai[i * 2 + 1]);
-    if (D == 3) k = (((k << 8) | (uint64_t)ai[i * 3]) << 16) | morton2_8((unsigned)ai[i * 3 + 1], (unsigned)ai[i * 3 + 2]);
+    if (D == 3)
+      k = (k << 24) | ((uint64_t)row_class(ai[i * 3 + 1], w) << 16) | ((uint64_t)ai[i * 3] << 8) |
+          (uint64_t)ai[i * 3 + 2];
     key[i] = k;
   }
 }
 
-// job ranges in the sorted keys: d = 3 per (box, plane), d = 1 per (box, cell), d = 2 per box
+// job ranges in the sorted keys: d = 3 per (box, row block), d = 1 per (box, cell), d = 2
+// per box
 template <int D>
 __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts, int64_t nbat, int G,
                                   int w, int* __restrict__ range) {
-  const int64_t njob = D == 2 ? nbat : nbat * G;
+  const int NB = (G + 7) / 8;
+  const int64_t njob = D == 2 ? nbat : (D == 3 ? nbat * NB : nbat * G);
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < njob;
        t += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k0, k1;
     if (D == 2) {
       k0 = (uint64_t)t << 16;
       k1 = (uint64_t)(t + 1) << 16;
+    } else if (D == 3) {
+      const uint64_t bx = (uint64_t)(t / NB);
+      const int b = (int)(t % NB);
+      const int clo = row_class(max(0, 8 * b - w + 1), w), chi = row_class(8 * b + 7, w);
+      k0 = (bx << 24) | ((uint64_t)clo << 16);
+      k1 = (bx << 24) | ((uint64_t)(chi + 1) << 16);
     } else {
       const uint64_t b = (uint64_t)(t / G), p = (uint64_t)(t % G);
       const uint64_t plo = (uint64_t)max(0, (int)p - w + 1);
@@ -176,10 +195,11 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
   }
 }
 
-// Sorted point records for the tile kernel: rw (n, 32) = [row-axis weights | column-axis
-// weights], rq (n) charge, ra (n, 4) first taps (a_0, a_1, a_2), rw0 (n, 16) axis-0 weights
-// (d = 3 plane factor).  One gather after the sort makes every job's staging a contiguous,
-// coalesced copy instead of a perm -> index -> weights pointer chase.
+// Sorted point records for the spreading kernels, one gather after the sort so every job's
+// staging is a contiguous, coalesced copy instead of a perm -> index -> weights chase:
+//   d = 2: rw (n, 32) = [axis-0 weights | axis-1 weights], rq (n) charge;
+//   d = 3: rw (n, 48) = [q x axis-1 weights | axis-2 weights | axis-0 weights];
+// ra (n, 4) = first taps (a_0, a_1, a_2).
 // Block = 32 sorted points; warp a evaluates axis a (lane = point).  Interior taps by the
 // plan's Horner polynomials (16 independent accumulators), the two edge taps -- where the
 // kernel has its square-root branch point -- exactly; then each warp writes its 32 x 16
@@ -211,13 +231,14 @@ __global__ void __launch_bounds__(D * 32) sort_records_kernel(
       for (int t = 0; t < 16; ++t) acc[t] = fma(acc[t], y, s_c[p * 16 + t]);
     }
 #pragma unroll
+    const double cq = (D == 3 && ax == 1) ? qb[i] : 1.0;  // d = 3: charge folded into w1
     for (int t = 0; t < 16; ++t) {
       double v = acc[t];
       if (t == 0 || t == w - 1) v = es_kernel((a0 + t - x) * inv_half, beta);
-      s_w[ax][lane][t] = t < w ? v : 0.0;
+      s_w[ax][lane][t] = t < w ? v * cq : 0.0;
     }
     if (ax == 0) {
-      rq[j] = qb[i];
+      if (D != 3) rq[j] = qb[i];
       int4 a;
       a.x = ai[i * D];
       a.y = D > 1 ? ai[i * D + 1] : 0;
@@ -227,11 +248,12 @@ __global__ void __launch_bounds__(D * 32) sort_records_kernel(
     }
   }
   __syncwarp();
-  // d = 3: axis 0 -> rw0, axis 1 -> rw rows, axis 2 -> rw columns; d = 2: axes 0, 1 -> rw
-  double* dst;
+  // d = 3: rw (n, 48) = [q w1 | w2 | w0] (pencil kernel); d = 2: rw (n, 32) = [w0 | w1]
+  double* dst = rw;
   int stride, off;
-  if (D == 3 && ax == 0) { dst = rw0; stride = 16; off = 0; }
-  else { dst = rw; stride = 32; off = (ax == D - 1) ? 16 : 0; }
+  if (D == 3) { stride = 48; off = ax == 1 ? 0 : (ax == 2 ? 16 : 32); }
+  else { stride = 32; off = (ax == D - 1) ? 16 : 0; }
+  (void)rw0;
   for (int e = lane; e < REC_PTS * 16; e += 32) {
     const int pt = e >> 4, t = e & 15;
     if (j0 + pt < n) dst[(j0 + pt) * stride + off + t] = s_w[ax][pt][t];
@@ -437,6 +459,220 @@ __global__ void __launch_bounds__(128, FGT_TILE_MINB) spread_tile_kernel(PlaneAr
         if (r < G && c < G) out[(int64_t)r * G + c] = acc[b][t][i2];
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------- d = 3 pencil spreading
+// A pencil is the 8 x 8 x PH block of grid cells (rows 8b + [0, 8), columns 8t + [0, 8),
+// planes h PH + [0, PH)); one warp keeps it as PH DMMA accumulator tiles in registers.
+// Points are sorted by (box, row class, a_0, a_2), where the row classes cut every 8 rows
+// at a = 0 and a = 1 - w (mod 8): the points whose row taps [a_1, a_1 + w) touch block b
+// are then ONE contiguous key range per (box, b) (a "row job", split at 1024 points).
+// Work item = (row job, pencil (t, h)); warps are persistent and take items from a global
+// counter (largest row jobs first), so no warp waits on another.  Per item the warp scans
+// the range 32 points at a time, keeps (ballot) the points whose column and axis-0 taps
+// touch its pencil and stages one row per kept point by cp.async (double-buffered): the
+// 8 row weights q w1[8b + r - a_1], the 8 column weights w2[8t + c - a_2] (zero-filled
+// outside the taps), a zero band, the 16 axis-0 weights.  A group of 4 kept points then
+// issues one rank-4 DMMA per plane,
+//   C_p += (q w1[rows] w0[p - a_0]) (x) w2[cols],
+// as a straight-line block of NPL planes chosen by a jump table on the group's first
+// plane; planes past a point's taps read the zero band / zero padding of its staged row,
+// so the plane loop is one shared load, one multiply and one DMMA per plane.
+constexpr int PEN_PH = 24;    // planes per pencil part (2 PEN_PH accumulator doubles per lane)
+constexpr int PEN_RS = 40;    // staged row: A 8 | B 8 | zeros 8 | w0 16
+constexpr int PEN_W0 = 24;    // offset of w0 in a staged row
+constexpr int PEN_WARPS = 2;  // warps per CTA (each independent)
+constexpr int PEN_BUF = 32 * PEN_RS;
+// per warp: 2 staged row buffers, 2 x 32 a_0, 32 (j, a_1, a_2) metas
+constexpr size_t PEN_WSMEM = 2 * PEN_BUF * sizeof(double) + 64 * sizeof(int) + 32 * sizeof(int4);
+constexpr size_t PEN_SMEM = PEN_WARPS * PEN_WSMEM;
+
+struct PencilArgs {
+  const int4* jobs;  // row jobs: (box * NB + b, first sorted point, count, scratch base or -1)
+  int nitems;        // row jobs x per
+  int* counter;      // work-item counter (zeroed before the launch)
+  const double* rw;  // sorted records (n, 48) [q w1 | w2 | w0]
+  const int* ra;     // (n, 4) first taps (a_0, a_1, a_2, -)
+  double* grid;      // (nbat, G^3)
+  double* scratch;   // (nscr, PEN_PH * 64) partial pencils
+  int w, G, NB, nparts, PH, per;
+};
+
+__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
+
+// planes [s, s + NPL) of the part, s = S - 15 >= 1 - w, clipped to [0, PEN_PH) at compile
+// time; the lane's axis-0 weight at plane s + q is w0row[q] (zero outside its taps)
+template <int NPL, int S>
+__device__ __forceinline__ void pencil_planes(double (&acc)[PEN_PH][2], const double* __restrict__ w0row,
+                                              double A, double B) {
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int pl = S - 15 + q;
+    if (pl >= 0 && pl < PEN_PH) dmma2(acc[pl][0], acc[pl][1], A * w0row[q], B);
+  }
+}
+
+template <int NPL>
+__device__ __forceinline__ void pencil_dispatch(int S, double (&acc)[PEN_PH][2], const double* w0row, double A,
+                                                double B) {
+  switch (S) {
+#define FGT_PL(K) \
+  case K: pencil_planes<NPL, K>(acc, w0row, A, B); break;
+    FGT_PL(0) FGT_PL(1) FGT_PL(2) FGT_PL(3) FGT_PL(4) FGT_PL(5) FGT_PL(6) FGT_PL(7)
+    FGT_PL(8) FGT_PL(9) FGT_PL(10) FGT_PL(11) FGT_PL(12) FGT_PL(13) FGT_PL(14) FGT_PL(15)
+    FGT_PL(16) FGT_PL(17) FGT_PL(18) FGT_PL(19) FGT_PL(20) FGT_PL(21) FGT_PL(22) FGT_PL(23)
+    FGT_PL(24) FGT_PL(25) FGT_PL(26) FGT_PL(27) FGT_PL(28) FGT_PL(29) FGT_PL(30) FGT_PL(31)
+    FGT_PL(32) FGT_PL(33) FGT_PL(34) FGT_PL(35) FGT_PL(36) FGT_PL(37) FGT_PL(38)
+#undef FGT_PL
+    default: break;
+  }
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(PEN_WARPS * 32) spread_pencil_kernel(PencilArgs a) {
+  extern __shared__ double psm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* wsm = reinterpret_cast<char*>(psm) + warp * PEN_WSMEM;
+  double* stg = reinterpret_cast<double*>(wsm);
+  int* s_a0 = reinterpret_cast<int*>(stg + 2 * PEN_BUF);
+  int4* s_meta = reinterpret_cast<int4*>(s_a0 + 64);
+  const int NB = a.NB, G = a.G, w = a.w;
+  // zero band of every staged row (never written by the staging)
+  for (int e = lane; e < 2 * 32 * 8; e += 32) stg[(e >> 3) * PEN_RS + 16 + (e & 7)] = 0.0;
+  const int4* ra4 = reinterpret_cast<const int4*>(a.ra);
+  // staging lane roles: lanes 0-7 row weights, 8-15 column weights, 16-31 axis-0 weights
+  const int st_dst = lane < 16 ? lane : lane + 8;
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(a.counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= a.nitems) break;
+    const int4 jb = a.jobs[item / a.per];
+    const int th = item - (item / a.per) * a.per;  // t * nparts + h
+    const int t = th / a.nparts, h = th - t * a.nparts;
+    const int box = jb.x / NB, b = jb.x - box * NB;
+    const int P0 = h * a.PH, PHc = min(a.PH, G - P0);
+    const int c_lo = 8 * t - w + 1, c_hi = 8 * t + 7;
+    const int p_lo = P0 - w + 1, p_hi = P0 + PHc - 1;
+    const int st_base = lane < 8 ? 8 * b + lane : 8 * t + lane - 8;
+    double acc[PEN_PH][2];
+#pragma unroll
+    for (int i = 0; i < PEN_PH; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const int nchunk = (jb.z + 31) >> 5;
+    auto load_ra = [&](int c) {
+      int4 r = make_int4(0, 0, -1000, 0);
+      if (32 * c + lane < jb.z) r = ra4[jb.y + 32 * c + lane];
+      return r;
+    };
+    // keep the chunk's points that touch the pencil; stage their rows into buffer buf
+    auto stage = [&](int c, int4 r, int buf) {
+      const bool ok = r.z >= c_lo && r.z <= c_hi && r.x >= p_lo && r.x <= p_hi;
+      const unsigned mask = __ballot_sync(0xffffffffu, ok);
+      const int nok = __popc(mask);
+      if (ok) {
+        const int pos = __popc(mask & ((1u << lane) - 1u));
+        s_meta[pos] = make_int4(jb.y + 32 * c + lane, r.y, r.z, 0);
+        s_a0[buf * 32 + pos] = r.x;
+      }
+      __syncwarp();
+      double* dst = stg + buf * PEN_BUF + st_dst;
+      for (int i = 0; i < nok; ++i) {
+        const int4 m = s_meta[i];
+        const int ix = st_base - (lane < 8 ? m.y : m.z);
+        const bool v = lane >= 16 || (unsigned)ix < 16u;
+        const int off = lane < 8 ? ix : (lane < 16 ? 16 + ix : 16 + lane);
+        cp_async8_zfill(dst + i * PEN_RS, a.rw + (int64_t)m.x * 48 + (v ? off : 0), v);
+      }
+      cp_async_commit();
+      __syncwarp();
+      return nok;
+    };
+    int nok_cur = 0;
+    int4 r_next = make_int4(0, 0, -1000, 0);
+    if (nchunk > 0) {
+      nok_cur = stage(0, load_ra(0), 0);
+      if (nchunk > 1) r_next = load_ra(1);
+    }
+    for (int c = 0; c < nchunk; ++c) {
+      int nok_next = 0;
+      if (c + 1 < nchunk) {
+        nok_next = stage(c + 1, r_next, (c + 1) & 1);
+        if (c + 2 < nchunk) r_next = load_ra(c + 2);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const int buf = c & 1;
+      const double* sb = stg + buf * PEN_BUF;
+      for (int g = 0; 4 * g < nok_cur; ++g) {
+        const int i = 4 * g + (lane & 3);
+        const bool valid = i < nok_cur;
+        const double* row = sb + (valid ? i : 0) * PEN_RS;
+        const double A = valid ? row[lane >> 2] : 0.0;
+        const double B = valid ? row[8 + (lane >> 2)] : 0.0;
+        const int a0i = valid ? s_a0[buf * 32 + i] : (1 << 20);
+        bool pend = valid;
+        while (true) {
+          const int m = __reduce_min_sync(0xffffffffu, pend ? a0i : (1 << 20));
+          if (m == (1 << 20)) break;
+          const bool sel = pend && a0i <= m + NPL - w;
+          // the lane's axis-0 weights from plane m on: m - a0i in [w - NPL, 0] for a
+          // selected lane (the zero band before its taps, zero padding after)
+          const double* w0row = row + PEN_W0 + (sel ? m - a0i : 0);
+          pencil_dispatch<NPL>(m - P0 + 15, acc, w0row, sel ? A : 0.0, B);
+          pend = pend && !sel;
+        }
+      }
+      __syncwarp();
+      nok_cur = nok_next;
+    }
+    // write the pencil: lane holds rows 8b + lane/4, columns 8t + 2 (lane % 4) + {0, 1}
+    const int r = lane >> 2, cc = 2 * (lane & 3);
+    if (jb.w < 0) {
+      double* out = a.grid + (int64_t)box * G * G * G;
+      const int gr = 8 * b + r, gc = 8 * t + cc;
+#pragma unroll
+      for (int pl = 0; pl < PEN_PH; ++pl) {
+        if (pl < PHc && gr < G) {
+          double* o = out + ((int64_t)(P0 + pl) * G + gr) * G + gc;
+          if (gc < G) o[0] = acc[pl][0];
+          if (gc + 1 < G) o[1] = acc[pl][1];
+        }
+      }
+    } else {
+      double* o = a.scratch + ((int64_t)jb.w + th) * (PEN_PH * 64) + r * 8 + cc;
+#pragma unroll
+      for (int pl = 0; pl < PEN_PH; ++pl) {
+        o[pl * 64] = acc[pl][0];
+        o[pl * 64 + 1] = acc[pl][1];
+      }
+    }
+  }
+}
+
+// partial pencils of K-split (box, b) ranges: red = (box * NB + b, first scratch, chunks, -);
+// chunk k's pencil (t, h) is scratch[first + k * NB * nparts + t * nparts + h]; summed in
+// chunk order (deterministic) and scattered into the grid
+__global__ void pencil_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red, int NB,
+                                     int nparts, int PH, int G, double* __restrict__ grid) {
+  const int4 rd = red[blockIdx.y];
+  const int th = blockIdx.z, t = th / nparts, h = th - t * nparts;
+  const int box = rd.x / NB, b = rd.x - box * NB;
+  const int P0 = h * PH, PHc = min(PH, G - P0);
+  const int64_t stride = (int64_t)NB * nparts * PEN_PH * 64;
+  for (int e = threadIdx.x; e < PEN_PH * 64; e += blockDim.x) {
+    const int pl = e >> 6, r = (e >> 3) & 7, c = e & 7;
+    const int gr = 8 * b + r, gc = 8 * t + c;
+    if (pl >= PHc || gr >= G || gc >= G) continue;
+    const double* src = scratch + ((int64_t)rd.y + th) * (PEN_PH * 64) + e;
+    double s = 0.0;
+    for (int k = 0; k < rd.z; ++k) s += src[k * stride];
+    grid[(int64_t)box * G * G * G + ((int64_t)(P0 + pl) * G + gr) * G + gc] = s;
   }
 }
 
@@ -783,6 +1019,37 @@ int64_t ipow(int64_t b, int e) {
   return r;
 }
 
+// grid -> modes for a batch of spread grids (see nufft_form_impl)
+template <int D>
+void form_modes(const NufftPlan& N, PwDev& P, const double* grid, const int64_t* sl, int64_t nbat,
+                GrowBuf<double>& g_t1, GrowBuf<double>& g_t2, cudaStream_t st) {
+  const int G = N.G, n_f = N.n_f, nh = P.nh;
+  const int64_t GD = ipow(G, D), plane = GD / G;
+  // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
+  // (d >= 2: only the nh stored axis-0 planes of the half spectrum, axis 0 contracted
+  // first so the later stages run on nh planes)
+  double* phi = P.phi.get();
+  const int64_t NH = P.NH;
+  if (D == 1) {
+    bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid, 1, G, phi, 1, NH, n_f, 1, G, (int)nbat, sl), st);
+  } else if (D == 2) {
+    auto t1 = g_t1.view(2 * nbat * G * n_f, st);
+    // T1[g1][m2] = sum_g2 grid[g1][g2] EfT[g2][m2]
+    bgemm<false, true, false>(gemm(grid, G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
+    // phi[s][m2] = sum_g1 EfH[s][g1] T1[g1][m2]
+    bgemm<true, true, false>(gemm(N.EfH.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NH, nh, n_f, G, (int)nbat, sl), st);
+  } else {
+    auto x = g_t1.view(2 * nbat * nh * plane, st);
+    auto y = g_t2.view(2 * nbat * nh * n_f * G, st);
+    // X[s][(g2 g3)] = sum_g1 EfH[s][g1] grid[g1][(g2 g3)]
+    bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid, plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
+    // Y[s][m2][g3] = sum_g2 Ef[m2][g2] X[s][g2][g3]      (batch = box x s)
+    bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, x.get(), G, (int64_t)G * G, y.get(), G, (int64_t)n_f * G, n_f, G, G, nbat * nh), st);
+    // phi[(s m2)][m3] = sum_g3 Y[(s m2)][g3] EfT[g3][m3]
+    bgemm<true, true, false>(gemm(y.get(), G, (int64_t)nh * n_f * G, N.EfT.get(), n_f, 0, phi, n_f, NH, nh * n_f, n_f, G, (int)nbat, sl), st);
+  }
+}
+
 template <int D>
 void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots) {
   if (slots.empty()) return;
@@ -808,6 +1075,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   GrowBuf<int> g_ai, g_ra, g_range;
   GrowBuf<uint64_t> g_key, g_skey;
   GrowBuf<int4> g_jobs, g_reds;
+  GrowBuf<int> g_counter;
   size_t b0 = 0;
   while (b0 < slots.size()) {
     // grow the batch up to nb_max boxes and ~4M points
@@ -857,7 +1125,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     spread_taps_kernel<D><<<grid_for(npts * D, 256), 256, 0, st>>>(wa);
     FGT_LAUNCHED();
     trace_mark(st, "form:taps");
-    spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts);
+    spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts, w);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
     int bits = 8 * D;
@@ -867,16 +1135,16 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     BufView<double> rw{nullptr, 0, st}, rq{nullptr, 0, st}, rw0{nullptr, 0, st};
     BufView<int> ra{nullptr, 0, st};
     if (D >= 2) {
-      rw = g_rw.view(npts * 32, st);
-      rq = g_rq.view(npts, st);
+      rw = g_rw.view(npts * (D == 3 ? 48 : 32), st);
+      if (D != 3) rq = g_rq.view(npts, st);
       ra = g_ra.view(npts * 4, st);
-      if (D == 3) rw0 = g_rw0.view(npts * 16, st);
       sort_records_kernel<D><<<(unsigned)((npts + REC_PTS - 1) / REC_PTS), D * 32, 0, st>>>(
           perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, N.hc.get(), N.hdeg, rw.get(), rq.get(),
           ra.get(), rw0.get());
       FGT_LAUNCHED();
     }
-    const int64_t njob = D == 2 ? nbat : nbat * G;
+    const int NBP = (G + 7) / 8;  // d = 3: pencil row / column blocks
+    const int64_t njob = D == 2 ? nbat : (D == 3 ? nbat * NBP : nbat * G);
     auto range = g_range.view(2 * njob, st);
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
     FGT_LAUNCHED();
@@ -887,6 +1155,76 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     trace_mark(st, "form:ranges(sync)");
     std::vector<int4> jobs, reds;
     int nscr = 0;
+    if constexpr (D == 3) {
+      // pencil jobs: one per (box, b, chunk of <= PCH scanned points), x NB columns x parts
+      const int nparts = (G + PEN_PH - 1) / PEN_PH, PH = (G + nparts - 1) / nparts;
+      const int per = NBP * nparts, PCH = 1024;
+      for (int64_t jid = 0; jid < njob; ++jid) {
+        const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
+        if (n <= PCH) {
+          jobs.push_back(make_int4((int)jid, lo, n, -1));
+        } else {
+          const int nc = (n + PCH - 1) / PCH;
+          reds.push_back(make_int4((int)jid, nscr, nc, 0));
+          for (int c = 0; c < nc; ++c) {
+            jobs.push_back(make_int4((int)jid, lo + c * PCH, std::min(PCH, n - c * PCH), nscr));
+            nscr += per;
+          }
+        }
+      }
+      // largest row jobs first (the persistent warps take items in order)
+      std::stable_sort(jobs.begin(), jobs.end(), [](const int4& x, const int4& y) { return x.z > y.z; });
+      auto jobs_d = g_jobs.view(jobs.size(), st);
+      auto reds_d = g_reds.view(reds.size(), st);
+      jobs_d.from_host(jobs.data(), jobs.size());
+      if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
+      auto grid = g_grid.view(nbat * GD, st);
+      auto scratch = g_scratch.view((int64_t)nscr * PEN_PH * 64, st);
+      auto counter = g_counter.view(1, st);
+      FGT_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(int), st));
+      PencilArgs pa;
+      pa.jobs = jobs_d.get();
+      pa.nitems = (int)jobs.size() * per;
+      pa.counter = counter.get();
+      pa.rw = rw.get();
+      pa.ra = ra.get();
+      pa.grid = grid.get();
+      pa.scratch = scratch.get();
+      pa.w = w;
+      pa.G = G;
+      pa.NB = NBP;
+      pa.nparts = nparts;
+      pa.PH = PH;
+      pa.per = per;
+      // persistent CTAs: as many as fit on the device at once
+      static int nsm = 0;
+      if (!nsm) FGT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+      // planes per dispatch: the w taps plus room for the group's a_0 spread
+#define FGT_PEN(NPL)                                                                                         \
+  {                                                                                                          \
+    FGT_CUDA(cudaFuncSetAttribute(spread_pencil_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PEN_SMEM)); \
+    int per_sm = 0;                                                                                          \
+    FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
+    const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm),       \
+                                                        ((int64_t)pa.nitems + PEN_WARPS - 1) / PEN_WARPS));           \
+    spread_pencil_kernel<NPL><<<nblk, PEN_WARPS * 32, PEN_SMEM, st>>>(pa);                                   \
+  }
+      if (!jobs.empty()) {
+        if (w <= 5) FGT_PEN(8)
+        else if (w <= 9) FGT_PEN(12)
+        else FGT_PEN(16)
+        FGT_LAUNCHED();
+      }
+#undef FGT_PEN
+      if (!reds.empty()) {
+        pencil_reduce_kernel<<<dim3(1, (unsigned)reds.size(), (unsigned)per), 256, 0, st>>>(
+            scratch.get(), reds_d.get(), NBP, nparts, PH, G, grid.get());
+        FGT_LAUNCHED();
+      }
+      form_modes<D>(N, P, grid.get(), sl_d.get(), nbat, g_t1, g_t2, st);
+      b0 += nbat;
+      continue;
+    }
     for (int64_t jid = 0; jid < njob; ++jid) {
       const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
       if (n <= CH) {
@@ -940,29 +1278,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
           scratch.get(), reds_d.get(), job_cells, 0, grid.get());
       FGT_LAUNCHED();
     }
-    // grid -> modes: separable GEMMs on the FP64 tensor cores, straight into phi[slot]
-    // (d >= 2: only the nh stored axis-0 planes of the half spectrum, axis 0 contracted
-    // first so the later stages run on nh planes)
-    double* phi = P.phi.get();
-    const int64_t NH = P.NH;
-    if (D == 1) {
-      bgemm<true, false, false>(gemm(N.Ef.get(), G, 0, grid.get(), 1, G, phi, 1, NH, n_f, 1, G, (int)nbat, sl_d.get()), st);
-    } else if (D == 2) {
-      auto t1 = g_t1.view(2 * nbat * G * n_f, st);
-      // T1[g1][m2] = sum_g2 grid[g1][g2] EfT[g2][m2]
-      bgemm<false, true, false>(gemm(grid.get(), G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
-      // phi[s][m2] = sum_g1 EfH[s][g1] T1[g1][m2]
-      bgemm<true, true, false>(gemm(N.EfH.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NH, nh, n_f, G, (int)nbat, sl_d.get()), st);
-    } else {
-      auto x = g_t1.view(2 * nbat * nh * plane, st);
-      auto y = g_t2.view(2 * nbat * nh * n_f * G, st);
-      // X[s][(g2 g3)] = sum_g1 EfH[s][g1] grid[g1][(g2 g3)]
-      bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid.get(), plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
-      // Y[s][m2][g3] = sum_g2 Ef[m2][g2] X[s][g2][g3]      (batch = box x s)
-      bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, x.get(), G, (int64_t)G * G, y.get(), G, (int64_t)n_f * G, n_f, G, G, nbat * nh), st);
-      // phi[(s m2)][m3] = sum_g3 Y[(s m2)][g3] EfT[g3][m3]
-      bgemm<true, true, false>(gemm(y.get(), G, (int64_t)nh * n_f * G, N.EfT.get(), n_f, 0, phi, n_f, NH, nh * n_f, n_f, G, (int)nbat, sl_d.get()), st);
-    }
+    form_modes<D>(N, P, grid.get(), sl_d.get(), nbat, g_t1, g_t2, st);
     b0 += nbat;
   }
 }
