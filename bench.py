@@ -216,7 +216,7 @@ def kernel_rooflines(phases, fp64_peak_tf, d=3):
 
 # kernels (ncu names) that make up each CUDA-event phase of kernel_rooflines
 PHASE_KERNELS = {
-    "form": ("spread_tile_kernel", "sort_records_kernel", "spread_taps_kernel", "spread_keys_kernel",
+    "form": ("spread_pencil_kernel", "pencil_reduce_kernel", "spread_tile_kernel", "sort_records_kernel", "spread_taps_kernel", "spread_keys_kernel",
              "form_kernel", "form_reduce_kernel", "plane_reduce_kernel", "bgemm_kernel",
              "job_ranges_kernel", "DeviceRadixSort"),
     "eval": ("eval_kernel", "interp_kernel"),

@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(128, FGT_TILE_MINB) spread_tile_kernel(PlaneAr
 // planes h PH + [0, PH)); one warp keeps it as PH DMMA accumulator tiles in registers.
 // Points are sorted by (box, row class, a_0, a_2), where the row classes cut every 8 rows
 // at a = 0 and a = 1 - w (mod 8): the points whose row taps [a_1, a_1 + w) touch block b
-// are then ONE contiguous key range per (box, b) (a "row job", split at 1024 points).
+// are then ONE contiguous key range per (box, b) (a "row job", split at 4096 points).
 // Work item = (row job, pencil (t, h)); warps are persistent and take items from a global
 // counter (largest row jobs first), so no warp waits on another.  Per item the warp scans
 // the range 32 points at a time, keeps (ballot) the points whose column and axis-0 taps
@@ -509,10 +509,16 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bo
 template <int NPL, int S>
 __device__ __forceinline__ void pencil_planes(double (&acc)[PEN_PH][2], const double* __restrict__ w0row,
                                               double A, double B) {
+  double wq[NPL];  // all loads first: the DMUL -> DMMA chains then issue back to back
 #pragma unroll
   for (int q = 0; q < NPL; ++q) {
     const int pl = S - 15 + q;
-    if (pl >= 0 && pl < PEN_PH) dmma2(acc[pl][0], acc[pl][1], A * w0row[q], B);
+    if (pl >= 0 && pl < PEN_PH) wq[q] = w0row[q];
+  }
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int pl = S - 15 + q;
+    if (pl >= 0 && pl < PEN_PH) dmma2(acc[pl][0], acc[pl][1], A * wq[q], B);
   }
 }
 
@@ -533,7 +539,7 @@ __device__ __forceinline__ void pencil_dispatch(int S, double (&acc)[PEN_PH][2],
 }
 
 template <int NPL>
-__global__ void __launch_bounds__(PEN_WARPS * 32) spread_pencil_kernel(PencilArgs a) {
+__global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(PencilArgs a) {
   extern __shared__ double psm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   char* wsm = reinterpret_cast<char*>(psm) + warp * PEN_WSMEM;
@@ -1158,7 +1164,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     if constexpr (D == 3) {
       // pencil jobs: one per (box, b, chunk of <= PCH scanned points), x NB columns x parts
       const int nparts = (G + PEN_PH - 1) / PEN_PH, PH = (G + nparts - 1) / nparts;
-      const int per = NBP * nparts, PCH = 1024;
+      const int per = NBP * nparts, PCH = 4096;
       for (int64_t jid = 0; jid < njob; ++jid) {
         const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
         if (n <= PCH) {
