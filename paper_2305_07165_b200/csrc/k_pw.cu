@@ -511,13 +511,14 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
 #pragma unroll
   for (int mt = 0; mt < MTP; ++mt) part[mt] = 0.0;
   for (int nt = warp; nt < ntiles; nt += nwarps) {
-    // four independent real accumulators per m-tile (re.re, re.im, im.im, im.re): the 4
-    // DMMAs of a complex MAC never wait on each other
-    double acc[MTP][4][2];
+    // complex MAC in three real products (Gauss): k1 = (a_r + a_i) b_r, k2 = a_r (b_i - b_r),
+    // k3 = a_i (b_r + b_i); re = k1 - k3, im = k1 + k2.  Three independent accumulators per
+    // m-tile: 3 DMMAs per complex MAC instead of 4, none waiting on another
+    double acc[MTP][3][2];
 #pragma unroll
     for (int mt = 0; mt < MTP; ++mt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[mt][e][0] = acc[mt][e][1] = 0.0;
+      for (int e = 0; e < 3; ++e) acc[mt][e][0] = acc[mt][e][1] = 0.0;
     const int rb = nt * 8 + (lane >> 2);
     const bool rv = rb < R;
     const double2* prow = psi + (size_t)(rv ? rb : 0) * n_f;
@@ -528,12 +529,12 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
       double2 A[MTP];
 #pragma unroll
       for (int mt = 0; mt < MTP; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
+      const double bd = B.y - B.x, bs = B.x + B.y;
 #pragma unroll
       for (int mt = 0; mt < MTP; ++mt) {
-        dmma(acc[mt][0][0], acc[mt][0][1], A[mt].x, B.x);
-        dmma(acc[mt][1][0], acc[mt][1][1], A[mt].x, B.y);
-        dmma(acc[mt][2][0], acc[mt][2][1], A[mt].y, B.y);
-        dmma(acc[mt][3][0], acc[mt][3][1], A[mt].y, B.x);
+        dmma(acc[mt][0][0], acc[mt][0][1], A[mt].x + A[mt].y, B.x);
+        dmma(acc[mt][1][0], acc[mt][1][1], A[mt].x, bd);
+        dmma(acc[mt][2][0], acc[mt][2][1], A[mt].y, bs);
       }
     }
     // epilogue: per output row its axis-0/1 mode indices and pair weight from rinfo
@@ -550,7 +551,7 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
         double2 f = make_double2(1.0, 0.0);
         if (D == 2) f = etab[(0 * TB + j) * RS + i0];
         if (D == 3) f = cmul(etab[(0 * TB + j) * RS + i0], etab[(1 * TB + j) * RS + i1]);
-        const double re = acc[mt][0][i2] - acc[mt][2][i2], im = acc[mt][1][i2] + acc[mt][3][i2];
+        const double re = acc[mt][0][i2] - acc[mt][2][i2], im = acc[mt][0][i2] + acc[mt][1][i2];
         part[mt] += wp * (re * f.x - im * f.y);
       }
     }
