@@ -478,14 +478,17 @@ __global__ void __launch_bounds__(128, FGT_TILE_MINB) spread_tile_kernel(PlaneAr
 //   C_p += (q w1[rows] w0[p - a_0]) (x) w2[cols],
 // as a straight-line block of NPL planes chosen by a jump table on the group's first
 // plane; planes past a point's taps read the zero band / zero padding of its staged row,
-// so the plane loop is one shared load, one multiply and one DMMA per plane.
+// so the plane loop is one shared load, one multiply and one DMMA per plane.  Kept rows go
+// to a ring, so groups stay full across chunk boundaries.
 constexpr int PEN_PH = 24;    // planes per pencil part (2 PEN_PH accumulator doubles per lane)
-constexpr int PEN_RS = 40;    // staged row: A 8 | B 8 | zeros 8 | w0 16
-constexpr int PEN_W0 = 24;    // offset of w0 in a staged row
+constexpr int PEN_RS = 38;    // staged row: A 8 | B 8 | zeros 6 | w0 16
+constexpr int PEN_W0 = 22;    // offset of w0 in a staged row (zero band >= NPL - w)
 constexpr int PEN_WARPS = 2;  // warps per CTA (each independent)
-constexpr int PEN_BUF = 32 * PEN_RS;
-// per warp: 2 staged row buffers, 2 x 32 a_0, 32 (j, a_1, a_2) metas
-constexpr size_t PEN_WSMEM = 2 * PEN_BUF * sizeof(double) + 64 * sizeof(int) + 32 * sizeof(int4);
+// staged rows form a ring: <= 3 rows left over + 32 rows of the chunk being processed +
+// 32 rows of the chunk in flight
+constexpr int PEN_RING = 68;
+// per warp: the row ring, its a_0 ring, 32 (j, a_1, a_2) metas
+constexpr size_t PEN_WSMEM = PEN_RING * PEN_RS * sizeof(double) + PEN_RING * sizeof(int) + 32 * sizeof(int4);
 constexpr size_t PEN_SMEM = PEN_WARPS * PEN_WSMEM;
 
 struct PencilArgs {
@@ -498,6 +501,11 @@ struct PencilArgs {
   double* scratch;   // (nscr, PEN_PH * 64) partial pencils
   int w, G, NB, nparts, PH, per;
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 
 __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -544,14 +552,12 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   char* wsm = reinterpret_cast<char*>(psm) + warp * PEN_WSMEM;
   double* stg = reinterpret_cast<double*>(wsm);
-  int* s_a0 = reinterpret_cast<int*>(stg + 2 * PEN_BUF);
-  int4* s_meta = reinterpret_cast<int4*>(s_a0 + 64);
+  int4* s_meta = reinterpret_cast<int4*>(stg + PEN_RING * PEN_RS);
+  int* s_a0 = reinterpret_cast<int*>(s_meta + 32);
   const int NB = a.NB, G = a.G, w = a.w;
   // zero band of every staged row (never written by the staging)
-  for (int e = lane; e < 2 * 32 * 8; e += 32) stg[(e >> 3) * PEN_RS + 16 + (e & 7)] = 0.0;
+  for (int e = lane; e < PEN_RING * 6; e += 32) stg[(e / 6) * PEN_RS + 16 + e % 6] = 0.0;
   const int4* ra4 = reinterpret_cast<const int4*>(a.ra);
-  // staging lane roles: lanes 0-7 row weights, 8-15 column weights, 16-31 axis-0 weights
-  const int st_dst = lane < 16 ? lane : lane + 8;
   while (true) {
     int item = 0;
     if (lane == 0) item = atomicAdd(a.counter, 1);
@@ -564,7 +570,6 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
     const int P0 = h * a.PH, PHc = min(a.PH, G - P0);
     const int c_lo = 8 * t - w + 1, c_hi = 8 * t + 7;
     const int p_lo = P0 - w + 1, p_hi = P0 + PHc - 1;
-    const int st_base = lane < 8 ? 8 * b + lane : 8 * t + lane - 8;
     double acc[PEN_PH][2];
 #pragma unroll
     for (int i = 0; i < PEN_PH; ++i) acc[i][0] = acc[i][1] = 0.0;
@@ -574,54 +579,66 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
       if (32 * c + lane < jb.z) r = ra4[jb.y + 32 * c + lane];
       return r;
     };
-    // keep the chunk's points that touch the pencil; stage their rows into buffer buf
-    auto stage = [&](int c, int4 r, int buf) {
+    // keep the chunk's points that touch the pencil; stage their rows at the ring's tail
+    // (ring positions: monotone counters mod PEN_RING)
+    int head = 0, tail = 0;
+    auto stage = [&](int c, int4 r) {
       const bool ok = r.z >= c_lo && r.z <= c_hi && r.x >= p_lo && r.x <= p_hi;
       const unsigned mask = __ballot_sync(0xffffffffu, ok);
       const int nok = __popc(mask);
-      if (ok) {
-        const int pos = __popc(mask & ((1u << lane) - 1u));
-        s_meta[pos] = make_int4(jb.y + 32 * c + lane, r.y, r.z, 0);
-        s_a0[buf * 32 + pos] = r.x;
-      }
+      if (ok) s_meta[__popc(mask & ((1u << lane) - 1u))] = make_int4(jb.y + 32 * c + lane, r.y, r.z, r.x);
       __syncwarp();
-      double* dst = stg + buf * PEN_BUF + st_dst;
-      for (int i = 0; i < nok; ++i) {
+      // four lanes per kept point (8 points per pass): lane quarter q copies row weights
+      // 2q, 2q + 1, column weights 2q, 2q + 1 (8-byte, zero-filled outside the taps) and
+      // axis-0 weights [4q, 4q + 4) (two 16-byte copies)
+      const int q = lane & 3;
+      for (int i = lane >> 2; i < nok; i += 8) {
         const int4 m = s_meta[i];
-        const int ix = st_base - (lane < 8 ? m.y : m.z);
-        const bool v = lane >= 16 || (unsigned)ix < 16u;
-        const int off = lane < 8 ? ix : (lane < 16 ? 16 + ix : 16 + lane);
-        cp_async8_zfill(dst + i * PEN_RS, a.rw + (int64_t)m.x * 48 + (v ? off : 0), v);
+        const int slot = (tail + i) % PEN_RING;
+        double* dst = stg + slot * PEN_RS;
+        const double* rec = a.rw + (int64_t)m.x * 48;
+        if (q == 0) s_a0[slot] = m.w;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ia = 8 * b + 2 * q + e - m.y, ib = 8 * t + 2 * q + e - m.z;
+          const bool va = (unsigned)ia < 16u, vb = (unsigned)ib < 16u;
+          cp_async8_zfill(dst + 2 * q + e, rec + (va ? ia : 0), va);
+          cp_async8_zfill(dst + 8 + 2 * q + e, rec + 16 + (vb ? ib : 0), vb);
+        }
+        cp_async16(dst + PEN_W0 + 4 * q, rec + 32 + 4 * q);
+        cp_async16(dst + PEN_W0 + 4 * q + 2, rec + 34 + 4 * q);
       }
       cp_async_commit();
       __syncwarp();
-      return nok;
+      tail += nok;
     };
-    int nok_cur = 0;
     int4 r_next = make_int4(0, 0, -1000, 0);
     if (nchunk > 0) {
-      nok_cur = stage(0, load_ra(0), 0);
+      stage(0, load_ra(0));
       if (nchunk > 1) r_next = load_ra(1);
     }
     for (int c = 0; c < nchunk; ++c) {
-      int nok_next = 0;
-      if (c + 1 < nchunk) {
-        nok_next = stage(c + 1, r_next, (c + 1) & 1);
+      const int ready = tail;  // rows of chunks <= c
+      const bool last = c + 1 >= nchunk;
+      if (!last) {
+        stage(c + 1, r_next);
         if (c + 2 < nchunk) r_next = load_ra(c + 2);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      const int buf = c & 1;
-      const double* sb = stg + buf * PEN_BUF;
-      for (int g = 0; 4 * g < nok_cur; ++g) {
-        const int i = 4 * g + (lane & 3);
-        const bool valid = i < nok_cur;
-        const double* row = sb + (valid ? i : 0) * PEN_RS;
+      // full groups of 4 from the ring (a partial group only after the last chunk)
+      const int avail = ready - head;
+      const int ngr = last ? (avail + 3) >> 2 : avail >> 2;
+      for (int g = 0; g < ngr; ++g) {
+        const int k = 4 * g + (lane & 3);
+        const bool valid = k < avail;
+        const int slot = (head + (valid ? k : 0)) % PEN_RING;
+        const double* row = stg + slot * PEN_RS;
         const double A = valid ? row[lane >> 2] : 0.0;
         const double B = valid ? row[8 + (lane >> 2)] : 0.0;
-        const int a0i = valid ? s_a0[buf * 32 + i] : (1 << 20);
+        const int a0i = valid ? s_a0[slot] : (1 << 20);
         bool pend = valid;
         while (true) {
           const int m = __reduce_min_sync(0xffffffffu, pend ? a0i : (1 << 20));
@@ -634,8 +651,8 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
           pend = pend && !sel;
         }
       }
+      head += min(avail, 4 * ngr);
       __syncwarp();
-      nok_cur = nok_next;
     }
     // write the pencil: lane holds rows 8b + lane/4, columns 8t + 2 (lane % 4) + {0, 1}
     const int r = lane >> 2, cc = 2 * (lane & 3);
@@ -1216,6 +1233,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     spread_pencil_kernel<NPL><<<nblk, PEN_WARPS * 32, PEN_SMEM, st>>>(pa);                                   \
   }
       if (!jobs.empty()) {
+        FGT_REQUIRE(w >= 2, FGT_ERANGE, "kernel width < 2");  // zero band >= NPL - w
         if (w <= 5) FGT_PEN(8)
         else if (w <= 9) FGT_PEN(12)
         else FGT_PEN(16)
