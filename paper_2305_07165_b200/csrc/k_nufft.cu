@@ -149,7 +149,8 @@ __host__ __device__ __forceinline__ int row_class(int a, int w) {
   return 2 * (a >> 3) + ((a & 7) >= r ? 1 : 0);
 }
 
-// d = 3 key (box, row class of a_1, a_0, a_2): a pencil's row range is one key range
+// d = 3 key (box, row class of a_1, a_0, a_2) in 16 tap bits (G <= 64): a pencil's row
+// range is one key range
 template <int D>
 __global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __restrict__ ai, int64_t n, int w) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -158,8 +159,8 @@ __global__ void spread_keys_kernel(uint64_t* __restrict__ key, const int* __rest
     if (D == 1) k = (k << 8) | (uint64_t)ai[i];
     if (D == 2) k = (k << 16) | morton2_8((unsigned)ai[i * 2], (unsigned)ai[i * 2 + 1]);
     if (D == 3)
-      k = (k << 24) | ((uint64_t)row_class(ai[i * 3 + 1], w) << 16) | ((uint64_t)ai[i * 3] << 8) |
-          (uint64_t)ai[i * 3 + 2];
+      k = (k << 16) | ((uint64_t)row_class(ai[i * 3 + 1], w) << 12) | ((uint64_t)ai[i * 3] << 6) |
+          (uint64_t)ai[i * 3 + 2];  // G <= 64: taps < 64, classes < 16
     key[i] = k;
   }
 }
@@ -181,8 +182,8 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
       const uint64_t bx = (uint64_t)(t / NB);
       const int b = (int)(t % NB);
       const int clo = row_class(max(0, 8 * b - w + 1), w), chi = row_class(8 * b + 7, w);
-      k0 = (bx << 24) | ((uint64_t)clo << 16);
-      k1 = (bx << 24) | ((uint64_t)(chi + 1) << 16);
+      k0 = (bx << 16) | ((uint64_t)clo << 12);
+      k1 = (bx << 16) + ((uint64_t)(chi + 1) << 12);  // chi + 1 may be 16: the next box
     } else {
       const uint64_t b = (uint64_t)(t / G), p = (uint64_t)(t % G);
       const uint64_t plo = (uint64_t)max(0, (int)p - w + 1);
@@ -1151,8 +1152,9 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     spread_keys_kernel<D><<<grid_for(npts, 256), 256, 0, st>>>(key.get(), ai.get(), npts, w);
     FGT_LAUNCHED();
     iota_i64(iota.get(), npts, st);
-    int bits = 8 * D;
-    while (((int64_t)1 << (bits - 8 * D)) < nbat) ++bits;
+    const int tap_bits = D == 3 ? 16 : 8 * D;  // d = 3 key: 4 class + 6 + 6 tap bits
+    int bits = tap_bits;
+    while (((int64_t)1 << (bits - tap_bits)) < nbat) ++bits;
     sort_pairs_key(tmp, key.get(), skey.get(), iota.get(), perm.get(), npts, bits, st);
     // records first: the GPU builds them while the host waits for the job ranges
     BufView<double> rw{nullptr, 0, st}, rq{nullptr, 0, st}, rw0{nullptr, 0, st};

@@ -53,6 +53,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--subsample", type=int, default=10_000)
     ap.add_argument("--scale", type=float, default=1.0, help="N multiplier (debug)")
     ap.add_argument("--n-s", type=int, default=0, help="override s")
@@ -72,14 +73,14 @@ def main():
     dy, dq, dx = (torch.from_numpy(a).cuda() for a in (y, q, x))
     u = torch.empty(x.shape[0], dtype=torch.float64, device="cuda")
     ms, ph = [], None
-    for i in range(args.steps + 1):
+    for i in range(args.steps + args.warmup):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         _, ph = fgt_points_device(dy, dq, dx, cfg["delta"], cfg["eps"], n_s, cfg["boundary"],
                                   out=u, params=prm, return_times=True)
         b.record()
         torch.cuda.synchronize()
-        if i:
+        if i >= args.warmup:
             ms.append(a.elapsed_time(b))
     # fp64 direct-sum spot check on a target subsample (all N sources)
     r = np.random.default_rng(123)
