@@ -313,7 +313,7 @@ struct GatherArgs {
   const int32_t* p_v;
   const int64_t* dense_ids;
   const int64_t* coords;
-  const double2* phase;   // (3, n_f)
+  const double2* phase;   // (5, n_f): shifts o = -2..2, exp(i m sc o side_lc)
   const double2* phi;
   double2* psi;   // batch-local output
   const int64_t* goff;  // sibling groups: psi index ranges
@@ -408,20 +408,28 @@ __global__ void group_table_kernel(GatherArgs a, int64_t* __restrict__ gt_slot,
 }
 
 // One CTA per (group, chunk of GATHER_CHUNK modes), GATHER_MPT modes per thread.
+// The phase of (member c, source at relative position rel) factors per axis as
+// P_k^(c_k - rel_k) = P_k^(-rel_k) P_k^(c_k): a per-source factor f0_u (rel_k in -1..2,
+// read from the 5-row phase table in shared memory) and a per-member factor Q_c.  So
+//   psi_c = Q_c * sum_{u serving c} (f0_u phi_u),
+// one complex product per source and a complex add per (source, member) pair.
 template <int D>
 __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel(
     GatherArgs a, const int64_t* __restrict__ gt_slot, const unsigned* __restrict__ gt_code,
     const int* __restrict__ gt_nu, const int64_t* __restrict__ gt_out) {
   constexpr int NSIB = 1 << D;
   constexpr int NREL = 1 << (2 * D);
+  constexpr int NFMAX = 64;  // pw_setup requires n_f <= 64
   __shared__ int64_t u_slot[NREL];
   __shared__ unsigned u_code[NREL];
+  __shared__ double2 s_ph[5 * NFMAX];  // rows o = -2..2
   const int64_t g = blockIdx.y;
   const int nu = gt_nu[g];
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
     u_slot[u] = gt_slot[g * NREL + u];
     u_code[u] = gt_code[g * NREL + u];
   }
+  for (int i = threadIdx.x; i < 5 * a.n_f; i += blockDim.x) s_ph[(i / a.n_f) * NFMAX + i % a.n_f] = a.phase[i];
   int64_t outr[NSIB];
 #pragma unroll
   for (int c = 0; c < NSIB; ++c) outr[c] = gt_out[g * NSIB + c];
@@ -432,49 +440,47 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
   for (int j = 0; j < GATHER_MPT; ++j) {
     const unsigned e = (unsigned)blockIdx.x * GATHER_CHUNK + j * GATHER_THREADS + threadIdx.x;
     if (e >= NF) return;
-    double2 P[D];
+    int mk[D];
     {
       unsigned rem = e;
 #pragma unroll
       for (int k = D - 1; k >= 0; --k) {
-        const unsigned mk = k == 0 ? (unsigned)half_plane_mi((int)rem, (int)n_f, a.half) : rem % n_f;
+        mk[k] = k == 0 ? half_plane_mi((int)rem, (int)n_f, a.half) : (int)(rem % n_f);
         rem /= n_f;
-        P[k] = a.phase[2 * n_f + mk];  // shift +1 row
       }
     }
-    double2 acc[NSIB];
+    double2 S[NSIB];
 #pragma unroll
-    for (int c = 0; c < NSIB; ++c) acc[c] = make_double2(0.0, 0.0);
+    for (int c = 0; c < NSIB; ++c) S[c] = make_double2(0.0, 0.0);
 #pragma unroll GATHER_UNROLL
     for (int u = 0; u < nu; ++u) {
       const unsigned code = u_code[u];
       const double2 f = a.phi[(size_t)u_slot[u] * NF + e];
-      // per axis: factor for child bit 0 (o = -rel) and child bit 1 (o = 1 - rel)
-      double2 F[D][2];
+      // f0 = prod_k P_k^(-rel_k): table row -rel_k + 2 = 3 - ((code >> (8 + 2k)) & 3)
+      double2 f0 = s_ph[(3 - (int)((code >> 8) & 3)) * NFMAX + mk[0]];
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const int rel = (int)((code >> (8 + 2 * k)) & 3) - 1;
+      for (int k = 1; k < D; ++k) f0 = cmul(f0, s_ph[(3 - (int)((code >> (8 + 2 * k)) & 3)) * NFMAX + mk[k]]);
+      const double2 gu = cmul(f0, f);
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int o = b - rel;  // -1, 0, 1 where used
-          F[k][b] = o == 0 ? make_double2(1.0, 0.0)
-                           : (o > 0 ? P[k] : make_double2(P[k].x, -P[k].y));
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NSIB; ++c) {
+      for (int c = 0; c < NSIB; ++c)
         if (code & (1u << c)) {
-          double2 ph = F[0][c & 1];
-#pragma unroll
-          for (int k = 1; k < D; ++k) ph = cmul(ph, F[k][(c >> k) & 1]);
-          acc[c].x += ph.x * f.x - ph.y * f.y;
-          acc[c].y += ph.x * f.y + ph.y * f.x;
+          S[c].x += gu.x;
+          S[c].y += gu.y;
         }
-      }
     }
+    // Q_c = prod_{k: c_k = 1} P_k (table row o = +1)
+    double2 P1[D];
 #pragma unroll
-    for (int c = 0; c < NSIB; ++c)
-      if (outr[c] >= 0) a.psi[(size_t)outr[c] * NF + e] = acc[c];
+    for (int k = 0; k < D; ++k) P1[k] = s_ph[3 * NFMAX + mk[k]];
+#pragma unroll
+    for (int c = 0; c < NSIB; ++c) {
+      if (outr[c] < 0) continue;
+      double2 v = S[c];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if ((c >> k) & 1) v = cmul(v, P1[k]);
+      a.psi[(size_t)outr[c] * NF + e] = v;
+    }
   }
 }
 
@@ -726,11 +732,11 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   for (int l = 0; l < T.l_c; ++l) P.side_lc *= 0.5;
   P.w1d.alloc(P.n_f, st);
   P.w1d.from_host(pw.weights_1d, P.n_f);
-  std::vector<double> ph(3 * 2 * P.n_f);
-  for (int o = 0; o < 3; ++o)
+  std::vector<double> ph(5 * 2 * P.n_f);
+  for (int o = 0; o < 5; ++o)
     for (int mi = 0; mi < P.n_f; ++mi) {
       double m = (double)(mi - P.n_f / 2);
-      double arg = m * P.sc * (double)(o - 1) * P.side_lc;
+      double arg = m * P.sc * (double)(o - 2) * P.side_lc;
       ph[(o * P.n_f + mi) * 2] = std::cos(arg);
       ph[(o * P.n_f + mi) * 2 + 1] = std::sin(arg);
     }
