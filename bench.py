@@ -367,7 +367,7 @@ def run_ours(args, world, rank, local):
 
     def e2e_step():
         if world == 1:
-            return fgt_points(ny, nq, nx, CFG["delta"], CFG["eps"], CFG["n_s"], share=share)
+            return fgt_points(ny, nq, nx, CFG["delta"], CFG["eps"], CFG["n_s"], share=share, out=nu)
         ey, eq, ex = (t.to(dev, non_blocking=True) for t in (hy, hq, hx))
         step(ey, eq, ex, u)
         hu.copy_(u, non_blocking=True)
@@ -383,7 +383,8 @@ def run_ours(args, world, rank, local):
         t0 = time.perf_counter()
         res_u = e2e_step()
         e2e_s.append(time.perf_counter() - t0)
-    nu[:] = res_u
+    if res_u is not nu:
+        nu[:] = res_u
     barrier(world)
     e2e_sec = max_over_ranks(float(np.mean(e2e_s)), world)
     h2d = (y.nbytes + q.nbytes + x.nbytes)

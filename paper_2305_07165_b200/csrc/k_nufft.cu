@@ -206,6 +206,7 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
 // kernel has its square-root branch point -- exactly; then each warp writes its 32 x 16
 // weights through shared memory as 128-byte rows.
 constexpr int REC_PTS = 32;
+constexpr int PEN_REC = 48;  // d = 3 record: [q w1 | w2 | w0], 16 zero-padded taps each
 constexpr int HC_MAX = 25;  // max polynomial degree + 1
 template <int D>
 __global__ void __launch_bounds__(D * 32) sort_records_kernel(
@@ -249,15 +250,22 @@ __global__ void __launch_bounds__(D * 32) sort_records_kernel(
     }
   }
   __syncwarp();
-  // d = 3: rw (n, 48) = [q w1 | w2 | w0] (pencil kernel); d = 2: rw (n, 32) = [w0 | w1]
+  // d = 3: rw (n, 48) = [q w1 | w2 | w0], 16 zero-padded taps each (pencil kernel);
+  // d = 2: rw (n, 32) = [w0 (16) | w1 (16)]
   double* dst = rw;
-  int stride, off;
-  if (D == 3) { stride = 48; off = ax == 1 ? 0 : (ax == 2 ? 16 : 32); }
-  else { stride = 32; off = (ax == D - 1) ? 16 : 0; }
   (void)rw0;
-  for (int e = lane; e < REC_PTS * 16; e += 32) {
-    const int pt = e >> 4, t = e & 15;
-    if (j0 + pt < n) dst[(j0 + pt) * stride + off + t] = s_w[ax][pt][t];
+  if (D == 3) {
+    const int off = ax == 1 ? 0 : (ax == 2 ? 16 : 32);
+    for (int e = lane; e < REC_PTS * 16; e += 32) {
+      const int pt = e >> 4, t = e & 15;
+      if (j0 + pt < n) dst[(j0 + pt) * 48 + off + t] = s_w[ax][pt][t];
+    }
+  } else {
+    const int off = (ax == D - 1) ? 16 : 0;
+    for (int e = lane; e < REC_PTS * 16; e += 32) {
+      const int pt = e >> 4, t = e & 15;
+      if (j0 + pt < n) dst[(j0 + pt) * 32 + off + t] = s_w[ax][pt][t];
+    }
   }
 }
 
@@ -496,7 +504,7 @@ struct PencilArgs {
   const int4* jobs;  // row jobs: (box * NB + b, first sorted point, count, scratch base or -1)
   int nitems;        // row jobs x per
   int* counter;      // work-item counter (zeroed before the launch)
-  const double* rw;  // sorted records (n, 48) [q w1 | w2 | w0]
+  const double* rw;  // sorted records (n, PEN_REC) [q w1 | w2 | w0]
   const int* ra;     // (n, 4) first taps (a_0, a_1, a_2, -)
   double* grid;      // (nbat, G^3)
   double* scratch;   // (nscr, PEN_PH * 64) partial pencils
@@ -515,28 +523,46 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bo
 
 // planes [s, s + NPL) of the part, s = S - 15 >= 1 - w, clipped to [0, PEN_PH) at compile
 // time; the lane's axis-0 weight at plane s + q is w0row[q] (zero outside its taps)
+// Planes [NPL_HEAD(NPL), NPL) are issued only when the group spans them (cnt > head): a
+// group whose points share their first tap (up to +1) stops after the head.
+template <int NPL>
+__host__ __device__ constexpr int npl_head() { return NPL == 16 ? 12 : (NPL == 12 ? 9 : 6); }
+
 template <int NPL, int S>
 __device__ __forceinline__ void pencil_planes(double (&acc)[PEN_PH][2], const double* __restrict__ w0row,
-                                              double A, double B) {
+                                              double A, double B, int cnt) {
+  constexpr int H = npl_head<NPL>();
   double wq[NPL];  // all loads first: the DMUL -> DMMA chains then issue back to back
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) {
+  for (int q = 0; q < H; ++q) {
     const int pl = S - 15 + q;
     if (pl >= 0 && pl < PEN_PH) wq[q] = w0row[q];
   }
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) {
+  for (int q = 0; q < H; ++q) {
     const int pl = S - 15 + q;
     if (pl >= 0 && pl < PEN_PH) dmma2(acc[pl][0], acc[pl][1], A * wq[q], B);
+  }
+  if (cnt > H) {
+#pragma unroll
+    for (int q = H; q < NPL; ++q) {
+      const int pl = S - 15 + q;
+      if (pl >= 0 && pl < PEN_PH) wq[q] = w0row[q];
+    }
+#pragma unroll
+    for (int q = H; q < NPL; ++q) {
+      const int pl = S - 15 + q;
+      if (pl >= 0 && pl < PEN_PH) dmma2(acc[pl][0], acc[pl][1], A * wq[q], B);
+    }
   }
 }
 
 template <int NPL>
 __device__ __forceinline__ void pencil_dispatch(int S, double (&acc)[PEN_PH][2], const double* w0row, double A,
-                                                double B) {
+                                                double B, int cnt) {
   switch (S) {
 #define FGT_PL(K) \
-  case K: pencil_planes<NPL, K>(acc, w0row, A, B); break;
+  case K: pencil_planes<NPL, K>(acc, w0row, A, B, cnt); break;
     FGT_PL(0) FGT_PL(1) FGT_PL(2) FGT_PL(3) FGT_PL(4) FGT_PL(5) FGT_PL(6) FGT_PL(7)
     FGT_PL(8) FGT_PL(9) FGT_PL(10) FGT_PL(11) FGT_PL(12) FGT_PL(13) FGT_PL(14) FGT_PL(15)
     FGT_PL(16) FGT_PL(17) FGT_PL(18) FGT_PL(19) FGT_PL(20) FGT_PL(21) FGT_PL(22) FGT_PL(23)
@@ -597,7 +623,7 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
         const int4 m = s_meta[i];
         const int slot = (tail + i) % PEN_RING;
         double* dst = stg + slot * PEN_RS;
-        const double* rec = a.rw + (int64_t)m.x * 48;
+        const double* rec = a.rw + (int64_t)m.x * PEN_REC;
         if (q == 0) s_a0[slot] = m.w;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -605,9 +631,8 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
           const bool va = (unsigned)ia < 16u, vb = (unsigned)ib < 16u;
           cp_async8_zfill(dst + 2 * q + e, rec + (va ? ia : 0), va);
           cp_async8_zfill(dst + 8 + 2 * q + e, rec + 16 + (vb ? ib : 0), vb);
+          cp_async16(dst + PEN_W0 + 4 * q + 2 * e, rec + 32 + 4 * q + 2 * e);  // axis-0 weights
         }
-        cp_async16(dst + PEN_W0 + 4 * q, rec + 32 + 4 * q);
-        cp_async16(dst + PEN_W0 + 4 * q + 2, rec + 34 + 4 * q);
       }
       cp_async_commit();
       __syncwarp();
@@ -645,10 +670,11 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
           const int m = __reduce_min_sync(0xffffffffu, pend ? a0i : (1 << 20));
           if (m == (1 << 20)) break;
           const bool sel = pend && a0i <= m + NPL - w;
+          const int mx = __reduce_max_sync(0xffffffffu, sel ? a0i : -(1 << 20));
           // the lane's axis-0 weights from plane m on: m - a0i in [w - NPL, 0] for a
           // selected lane (the zero band before its taps, zero padding after)
           const double* w0row = row + PEN_W0 + (sel ? m - a0i : 0);
-          pencil_dispatch<NPL>(m - P0 + 15, acc, w0row, sel ? A : 0.0, B);
+          pencil_dispatch<NPL>(m - P0 + 15, acc, w0row, sel ? A : 0.0, B, mx + w - m);
           pend = pend && !sel;
         }
       }
@@ -1160,7 +1186,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     BufView<double> rw{nullptr, 0, st}, rq{nullptr, 0, st}, rw0{nullptr, 0, st};
     BufView<int> ra{nullptr, 0, st};
     if (D >= 2) {
-      rw = g_rw.view(npts * (D == 3 ? 48 : 32), st);
+      rw = g_rw.view(npts * (D == 3 ? PEN_REC : 32), st);
       if (D != 3) rq = g_rq.view(npts, st);
       ra = g_ra.view(npts * 4, st);
       sort_records_kernel<D><<<(unsigned)((npts + REC_PTS - 1) / REC_PTS), D * 32, 0, st>>>(

@@ -98,16 +98,25 @@ def _host_out(n):
 
 
 def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free",
-               return_times=False, share=(0, 1)):
+               return_times=False, share=(0, 1), out=None):
     """Potentials u (M,) at the targets; host arrays in, host array out.
 
     share=(rank, size) evaluates only this rank's cost-balanced range of target leaves
     (other targets get 0); summing the outputs of all ranks gives the full transform.
+    out: optional caller-owned (M,) float64 C-contiguous host array that receives u
+    (overwritten, not accumulated) and is returned; page-locked memory makes the
+    device->host copy run at link speed.
     """
     periodic = _boundary(boundary)
     src, q, tgt, dim = _prep(sources, charges, targets, periodic)
     prm = FgtParams(dim, delta, epsilon, n_s, periodic, share)
-    u = _host_out(tgt.shape[0])
+    if out is None:
+        u = _host_out(tgt.shape[0])
+    else:
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (tgt.shape[0],)
+                and out.flags.c_contiguous and out.flags.writeable):
+            raise ValueError("out must be a writeable C-contiguous float64 array of shape (M,)")
+        u = out
     times = _lib.FgtPhaseTimes()
     P = _lib.ptr
     _lib.check(_lib.load().fgt_points(P(src), src.shape[0], P(q), P(tgt), tgt.shape[0],

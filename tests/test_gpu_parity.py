@@ -215,6 +215,14 @@ def test_device_path_matches_host(cuda):
                            torch.from_numpy(x).cuda(), 1e-4, 1e-9, 200)
     torch.cuda.synchronize()
     assert np.array_equal(ud.cpu().numpy(), u)  # deterministic: no atomics in the sums
+    # caller-owned output buffer: overwritten (not accumulated) and returned
+    out = np.full(x.shape[0], 7.0)
+    uo = fgt_points(y, q, x, 1e-4, 1e-9, 200, out=out)
+    assert uo is out and np.array_equal(out, u)
+    with pytest.raises(ValueError):
+        fgt_points(y, q, x, 1e-4, 1e-9, 200, out=np.zeros(x.shape[0] - 1))
+    with pytest.raises(ValueError):
+        fgt_points(y, q, x, 1e-4, 1e-9, 200, out=np.zeros(x.shape[0], dtype=np.float32))
 
 
 def test_superposition_and_translation(cuda):
