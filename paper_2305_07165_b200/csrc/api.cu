@@ -389,17 +389,40 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
 // finish = translation, evaluation, near field, scatter.
 struct PointsRun {
   cudaStream_t st = nullptr;
+  cudaStream_t sb = nullptr;  // side stream of the overlapped single-GPU path (else null)
+  cudaEvent_t ev_direct = nullptr;
+  KClock k_lists;             // lists on the side stream
   TreeDev T;
   PwDev P;
   const NufftPlan* NP = nullptr;
-  DBuf<double> us;
+  DBuf<double> us, ud;        // ud: near-field sums of the overlapped path
   fgt_tree_params tp;
   fgt_pw_params pw;
   std::vector<double> w1d;
   ExchangePlan X;
   std::unique_ptr<PhaseMarks> pm;
   int64_t l0 = 0, nt = 0;
+  ~PointsRun() {
+    if (ev_direct) cudaEventDestroy(ev_direct);
+  }
 };
+
+// Side stream of the overlapped pipeline: one per (host thread, device), kept.
+static cudaStream_t side_stream() {
+  static thread_local std::map<int, cudaStream_t> per_dev;
+  int dev = 0;
+  FGT_CUDA(cudaGetDevice(&dev));
+  cudaStream_t& s = per_dev[dev];
+  if (!s) FGT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+__global__ void scatter_add_kernel(const double* __restrict__ us, const double* __restrict__ ud,
+                                   const int64_t* __restrict__ perm, int64_t n, double* __restrict__ u) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    u[perm[i]] = us[i] + ud[i];
+}
 
 static void points_begin(PointsRun& R, const double* src, int64_t ns, const double* q, const double* tgt,
                          int64_t nt, const fgt_tree_params& tp, const fgt_pw_params& pw, cudaStream_t st,
@@ -420,11 +443,53 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
   gather_sorted_points(T, src, q, tgt);
   R.pm->mark();
   trace_mark(st, "tree");
+  const double D0 = tp.D0;
+  const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
+  if (tp.part_size <= 1 && !exchange && T.n_dense > 0) {
+    // Single GPU: the form needs only the tree, the lists only the tree, and the near
+    // field only the lists.  The form is enqueued on st first (its one host round trip
+    // waits on st only); then the lists, the psi metadata and the near-field sums run on
+    // a side stream, on the GPU alongside the form's kernels.  Gather / eval (st) wait for
+    // the lists; the final scatter waits for the near field and adds it (u = eval + near,
+    // the same single addition per target as the sequential path).
+    cudaStream_t sb = side_stream();
+    R.sb = sb;
+    Event e_tree, e_lists;
+    FGT_CUDA(cudaEventRecord(e_tree.e, st));
+    FGT_CUDA(cudaStreamWaitEvent(sb, e_tree.e, 0));
+    R.pm->mark();  // (lists: on the side stream, timed by k_lists)
+    T.st = sb;
+    R.k_lists.begin(sb);
+    build_lists_begin(T);  // list enumeration, no host wait
+    T.st = st;
+    R.us.alloc(nt, st);
+    R.us.zero();
+    pw_setup_dense(R.P, T, R.pw);
+    trace_mark(st, "setup");
+    const double X = 0.5 * R.P.side_lc * R.P.sc * (1.0 + 1e-12);
+    R.NP = &nufft_plan_cached(pw.n_f, tol, X, R.w1d.data(), st);
+    pw_form(R.P, T, R.NP);
+    R.pm->mark();
+    trace_mark(st, "form(enqueued)");
+    T.st = sb;
+    build_lists_end(T);
+    pw_setup_psi(R.P, T);
+    R.k_lists.end(sb);
+    FGT_CUDA(cudaEventRecord(e_lists.e, sb));
+    R.ud.alloc(nt, sb);
+    R.ud.zero();
+    direct_lists(T, 1.0 / tp.delta, D0 * D0 * tp.delta, R.ud.get(), &R.P.k_direct);
+    FGT_CUDA(cudaEventCreateWithFlags(&R.ev_direct, cudaEventDisableTiming));
+    FGT_CUDA(cudaEventRecord(R.ev_direct, sb));
+    T.st = st;
+    FGT_CUDA(cudaStreamWaitEvent(st, e_lists.e, 0));
+    trace_mark(st, "form");
+    return;
+  }
   build_lists(T);
   // stored modes (half spectrum for d >= 2) and the NUFFT width the plan will use
   int64_t NH = pw.dim >= 2 ? pw.n_f / 2 + 1 : pw.n_f;
   for (int k = 1; k < pw.dim; ++k) NH *= pw.n_f;
-  const double tol = 0.3 * std::exp(-pw.D0 * pw.D0);
   const int w = std::max(2, std::min((int)std::ceil(std::log10(1.0 / tol) - 1e-9) + 1, 16));
   if (tp.part_size > 1) {
     FGT_REQUIRE(tp.part_rank >= 0 && tp.part_rank < tp.part_size, FGT_EINVAL, "bad part_rank");
@@ -468,11 +533,20 @@ static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, doubl
   }
   R.pm->mark();
   trace_mark(st, "gather+eval");
-  const double D0 = R.tp.D0;
-  direct_lists(T, 1.0 / R.tp.delta, D0 * D0 * R.tp.delta, R.us.get(), &P.k_direct);
-  if (R.nt > 0) {
-    scatter_kernel<<<grid_for(R.nt, 256), 256, 0, st>>>(R.us.get(), T.tgt_perm.get(), R.nt, u);
-    FGT_LAUNCHED();
+  if (R.sb) {
+    // overlapped path: the near field ran on the side stream into ud
+    FGT_CUDA(cudaStreamWaitEvent(st, R.ev_direct, 0));
+    if (R.nt > 0) {
+      scatter_add_kernel<<<grid_for(R.nt, 256), 256, 0, st>>>(R.us.get(), R.ud.get(), T.tgt_perm.get(), R.nt, u);
+      FGT_LAUNCHED();
+    }
+  } else {
+    const double D0 = R.tp.D0;
+    direct_lists(T, 1.0 / R.tp.delta, D0 * D0 * R.tp.delta, R.us.get(), &P.k_direct);
+    if (R.nt > 0) {
+      scatter_kernel<<<grid_for(R.nt, 256), 256, 0, st>>>(R.us.get(), T.tgt_perm.get(), R.nt, u);
+      FGT_LAUNCHED();
+    }
   }
   R.pm->mark();
   trace_mark(st, "direct");
@@ -485,13 +559,14 @@ static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, doubl
   }
   PhaseMarks& pm = *R.pm;
   t.tree_ms = pm.ms(0);
-  t.lists_ms = pm.ms(1);
+  t.lists_ms = R.sb ? R.k_lists.ms() : pm.ms(1);  // overlapped: side-stream time
   t.form_ms = pm.ms(2);
   t.gather_ms = P.k_gather.ms();
   t.eval_ms = pm.ms(3) - t.gather_ms;
   t.direct_ms = pm.ms(4);
   trace_dump();
-  t.total_ms = t.tree_ms + t.lists_ms + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
+  // wall span on the launching stream (the overlapped lists are not on it)
+  t.total_ms = t.tree_ms + pm.ms(1) + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
   t.launches = g_launches - R.l0;
   t.k_form_ms = P.k_form.ms();
   t.k_gather_ms = P.k_gather.ms();

@@ -712,6 +712,13 @@ void launch_eval(const EvalArgs& ea, int64_t n_psi, cudaStream_t st) {
 // ====================================================================== host side
 
 void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
+  pw_setup_dense(P, T, pw);
+  pw_setup_psi(P, T);
+}
+
+// parameters, phase tables and the source count of every P-box slot (the form's inputs;
+// no list is needed)
+void pw_setup_dense(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   FGT_REQUIRE(pw.dim == T.d, FGT_EINVAL, "plane-wave dim != tree dim");
   // n_f even: the quadrature's modes -n_f/2 .. n_f/2-1; odd: the periodic root series
   // -n_p .. n_p (n_f = 2 n_p + 1)
@@ -742,33 +749,37 @@ void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
     }
   P.phase.alloc(ph.size(), st);
   P.phase.from_host(ph.data(), ph.size());
-  // targets per psi box and the parent of each psi box, fetched once (one sync, while the
-  // stream is idle after the lists)
-  // (and the source count of every P-box slot, for the form's path choice)
-  const int64_t n = T.n_psi, nd = T.n_dense;
+  const int64_t nd = T.n_dense;
+  P.h_src.assign(nd, 0);
+  if (nd > 0) {
+    DBuf<int64_t> m(nd, st);
+    gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), m.get());
+    FGT_LAUNCHED();
+    trace_mark(st, "setup:dense");
+    m.to_host(P.h_src.data(), nd);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "setup:dense(sync)");
+  }
+}
+
+// targets per psi box and the sibling groups of the psi boxes (after the lists), fetched
+// with one sync on T.st
+void pw_setup_psi(PwDev& P, const TreeDev& T) {
+  cudaStream_t st = T.st;
+  const int64_t n = T.n_psi;
   P.h_cnt.assign(n, 0);
   P.h_goff.assign(1, 0);
-  P.h_src.assign(nd, 0);
-  std::vector<int64_t> h(2 * n + nd);
-  if (n + nd > 0) {
-    DBuf<int64_t> m(2 * n + nd, st);
-    if (n > 0) {
-      psi_meta_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get(), n, T.tgt_count.get(),
-                                                        T.parent.get(), m.get());
-      FGT_LAUNCHED();
-    }
-    if (nd > 0) {
-      gather_counts_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.src_count.get(), m.get() + 2 * n);
-      FGT_LAUNCHED();
-    }
-    trace_mark(st, "setup:meta");
+  std::vector<int64_t> h(2 * n);
+  if (n > 0) {
+    DBuf<int64_t> m(2 * n, st);
+    psi_meta_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.psi_ids.get(), n, T.tgt_count.get(), T.parent.get(),
+                                                      m.get());
+    FGT_LAUNCHED();
+    trace_mark(st, "setup:psi");
     m.to_host(h.data(), h.size());
     FGT_CUDA(cudaStreamSynchronize(st));
-    trace_mark(st, "setup:meta(sync)");
+    trace_mark(st, "setup:psi(sync)");
     std::copy(h.begin(), h.begin() + n, P.h_cnt.begin());
-    std::copy(h.begin() + 2 * n, h.end(), P.h_src.begin());
-  }
-  if (n > 0) {
     const int64_t nsib = (int64_t)1 << P.d;
     for (int64_t i = 1; i < n; ++i) {
       const int64_t p = h[n + i];

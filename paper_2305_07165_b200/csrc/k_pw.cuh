@@ -55,7 +55,9 @@ struct NufftPlan;
 // NUFFT (spread + separable DFT): FGT_NUFFT_MODE=direct|spread forces one (tests).
 int nufft_mode();
 
-void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
+void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);  // = dense + psi
+void pw_setup_dense(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
+void pw_setup_psi(PwDev& P, const TreeDev& T);
 // Form outgoing expansions of all P-boxes: type-1 exponential sums.
 void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N);
 // Diagonal translation phi -> psi over the P-lists.

@@ -1011,20 +1011,44 @@ __global__ void nonzero_flag_kernel(const int64_t* __restrict__ a, int64_t n, ui
 
 }  // namespace
 
-template <int D>
-static void build_lists_impl(TreeDev& T) {
-  cudaStream_t st = T.st;
+// intermediates kept between build_lists_begin and build_lists_end
+struct ListsPending {
   CubTmp tmp;
+  DBuf<int64_t> cnt, tl, pcnt, dcnt, poff, doff, sel, seloff;
+  DBuf<int64_t> fix_id;
+  DBuf<int32_t> fix_v;
+  int64_t* h = nullptr;  // pinned (4): ntl, n_p, n_d, n_psi (per-thread block, kept)
+  cudaEvent_t ev = nullptr;
+  ~ListsPending() {
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+
+static int64_t* lists_pinned() {
+  static thread_local int64_t* h = nullptr;
+  if (!h) FGT_CUDA(cudaMallocHost((void**)&h, 4 * sizeof(int64_t)));
+  return h;
+}
+
+template <int D>
+static void build_lists_begin_impl(TreeDev& T) {
+  cudaStream_t st = T.st;
+  auto L = std::make_shared<ListsPending>();
+  T.lists_pending = L;
+  CubTmp& tmp = L->tmp;
   const int64_t nb = T.nb;
-  // Sizes stay on the device until one host round trip (target leaves, P/D entry totals,
+  // Sizes stay on the device until one host read-back (target leaves, P/D entry totals,
   // psi boxes); launches before it cover the capacity n_leaves.
   const int64_t cap = T.n_leaves;
-  DBuf<int64_t> cnt(4, st);  // ntl, n_p, n_d, n_psi
+  L->cnt.alloc(4, st);
+  DBuf<int64_t>& cnt = L->cnt;  // ntl, n_p, n_d, n_psi
   // target leaves (leaves with targets), canonical order
   DBuf<uint8_t> flag(nb, st);
   target_leaf_flag_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.is_leaf.get(), T.tgt_count.get(), nb, flag.get());
   FGT_LAUNCHED();
-  DBuf<int64_t> iota(nb, st), tl(nb, st);
+  L->tl.alloc(nb, st);
+  DBuf<int64_t>& tl = L->tl;
+  DBuf<int64_t> iota(nb, st);
   iota_kernel<<<grid_for(nb, 256), 256, 0, st>>>(iota.get(), nb);
   FGT_LAUNCHED();
   size_t bytes = 0;
@@ -1032,14 +1056,20 @@ static void build_lists_impl(TreeDev& T) {
   FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, iota.get(), flag.get(), tl.get(), cnt.get(), (int)nb, st));
   count_launch();
 
-  DBuf<int64_t> pcnt(cap + 1, st), dcnt(cap + 1, st), poff(cap + 1, st), doff(cap + 1, st);
+  L->pcnt.alloc(cap + 1, st);
+  L->dcnt.alloc(cap + 1, st);
+  L->poff.alloc(cap + 1, st);
+  L->doff.alloc(cap + 1, st);
+  DBuf<int64_t>&pcnt = L->pcnt, &dcnt = L->dcnt, &poff = L->poff, &doff = L->doff;
   pcnt.zero();
   dcnt.zero();
   T.pairs_dev.alloc(1, st);
   T.pairs_dev.zero();
   constexpr int CAP = list_cap<D>();
-  DBuf<int64_t> fix_id(cap * CAP, st);
-  DBuf<int32_t> fix_v(cap * CAP * D, st);
+  L->fix_id.alloc(cap * CAP, st);
+  L->fix_v.alloc(cap * CAP * D, st);
+  DBuf<int64_t>& fix_id = L->fix_id;
+  DBuf<int32_t>& fix_v = L->fix_v;
   if (cap > 0) {
     constexpr int NOFF = D == 1 ? 3 : (D == 2 ? 9 : 27);
     DBuf<int32_t> cov_j(cap * NOFF, st), cov_v(cap * NOFF, st);
@@ -1063,17 +1093,31 @@ static void build_lists_impl(TreeDev& T) {
   DBuf<uint8_t> f2(cap + 1, st);
   nonzero_flag_kernel<<<grid_for(cap, 256), 256, 0, st>>>(pcnt.get(), cap, f2.get());
   FGT_LAUNCHED();
-  DBuf<int64_t> sel(cap + 1, st), seloff(cap + 1, st);
+  L->sel.alloc(cap + 1, st);
+  L->seloff.alloc(cap + 1, st);
+  DBuf<int64_t>&sel = L->sel, &seloff = L->seloff;
   bytes = 0;
   FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, tl.get(), f2.get(), sel.get(), cnt.get() + 3, (int)cap, st));
   FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, tl.get(), f2.get(), sel.get(), cnt.get() + 3, (int)cap, st));
   FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, poff.get(), f2.get(), seloff.get(), cnt.get() + 3, (int)cap, st));
   count_launch(2);
-  int64_t h[4];
+  L->h = lists_pinned();
+  FGT_CUDA(cudaMemcpyAsync(L->h, cnt.get(), 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FGT_CUDA(cudaEventCreateWithFlags(&L->ev, cudaEventDisableTiming));
+  FGT_CUDA(cudaEventRecord(L->ev, st));
   trace_mark(st, "lists:enum");
-  cnt.to_host(h, 4);
-  FGT_CUDA(cudaStreamSynchronize(st));
+}
+
+template <int D>
+static void build_lists_end_impl(TreeDev& T) {
+  cudaStream_t st = T.st;
+  auto L = std::static_pointer_cast<ListsPending>(T.lists_pending);
+  FGT_CUDA(cudaEventSynchronize(L->ev));
   trace_mark(st, "lists:enum(sync)");
+  const int64_t* h = L->h;
+  DBuf<int64_t>&cnt = L->cnt, &tl = L->tl, &pcnt = L->pcnt, &dcnt = L->dcnt, &poff = L->poff, &doff = L->doff;
+  DBuf<int64_t>&sel = L->sel, &seloff = L->seloff, &fix_id = L->fix_id;
+  DBuf<int32_t>& fix_v = L->fix_v;
   const int64_t ntl = h[0];
   T.n_dtgt = ntl;
   T.n_p = h[1];
@@ -1102,6 +1146,7 @@ static void build_lists_impl(TreeDev& T) {
   FGT_CUDA(cudaMemcpyAsync(T.p_off.get() + T.n_psi, cnt.get() + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   T.n_direct_pairs = -1;  // read lazily (direct_pairs)
   T.lists_built = true;
+  T.lists_pending.reset();  // the remaining scratch is freed stream-ordered on its stream
 }
 
 int64_t direct_pairs(TreeDev& T) {
@@ -1116,11 +1161,24 @@ int64_t direct_pairs(TreeDev& T) {
   return T.n_direct_pairs;
 }
 
-void build_lists(TreeDev& T) {
+void build_lists_begin(TreeDev& T) {
+  if (T.lists_built || T.lists_pending) return;
+  if (T.d == 1) build_lists_begin_impl<1>(T);
+  else if (T.d == 2) build_lists_begin_impl<2>(T);
+  else build_lists_begin_impl<3>(T);
+}
+
+void build_lists_end(TreeDev& T) {
   if (T.lists_built) return;
-  if (T.d == 1) build_lists_impl<1>(T);
-  else if (T.d == 2) build_lists_impl<2>(T);
-  else build_lists_impl<3>(T);
+  if (!T.lists_pending) build_lists_begin(T);
+  if (T.d == 1) build_lists_end_impl<1>(T);
+  else if (T.d == 2) build_lists_end_impl<2>(T);
+  else build_lists_end_impl<3>(T);
+}
+
+void build_lists(TreeDev& T) {
+  build_lists_begin(T);
+  build_lists_end(T);
 }
 
 }  // namespace fgt

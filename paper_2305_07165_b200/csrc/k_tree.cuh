@@ -1,5 +1,7 @@
 // Device-resident point tree (Alg 1) and P/D interaction lists.
 #pragma once
+#include <memory>
+
 #include "fgt_common.cuh"
 
 namespace fgt {
@@ -46,6 +48,9 @@ struct TreeDev {
   DBuf<int32_t> d_v;     // (n_d * d)
   DBuf<int64_t> d_tgt;   // (n_d) target box id
 
+  // build_lists_begin -> build_lists_end intermediates (k_tree.cu)
+  std::shared_ptr<void> lists_pending;
+
   // multi-GPU share: P-boxes whose expansions this rank needs (empty = all)
   std::vector<uint8_t> dense_need;
 
@@ -58,8 +63,12 @@ void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, in
                 const fgt_tree_params& tp, cudaStream_t st);
 // Gather sorted coordinates (and charges, if given) into T.*_sorted.
 void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt);
-// Target-centric P/D lists.
+// Target-centric P/D lists.  build_lists = begin + end; begin enqueues
+// the enumeration and the read-back of the list sizes on T.st without blocking, end waits
+// for the sizes and enqueues the compaction.
 void build_lists(TreeDev& T);
+void build_lists_begin(TreeDev& T);
+void build_lists_end(TreeDev& T);
 // direct-pair statistic of the lists (one device read, cached)
 int64_t direct_pairs(TreeDev& T);
 
