@@ -493,9 +493,13 @@ constexpr int PEN_PH = 24;    // planes per pencil part (2 PEN_PH accumulator do
 constexpr int PEN_RS = 38;    // staged row: A 8 | B 8 | zeros 6 | w0 16
 constexpr int PEN_W0 = 22;    // offset of w0 in a staged row (zero band >= NPL - w)
 constexpr int PEN_WARPS = 2;  // warps per CTA (each independent)
-// staged rows form a ring: <= 3 rows left over + 32 rows of the chunk being processed +
-// 32 rows of the chunk in flight
-constexpr int PEN_RING = 68;
+// staged rows form a ring: <= 3 rows left over + the kept rows of the chunk being
+// processed + those of the chunk in flight
+#ifndef FGT_PEN_CH
+#define FGT_PEN_CH 32
+#endif
+constexpr int PEN_CH = FGT_PEN_CH;            // points scanned per chunk (<= 32)
+constexpr int PEN_RING = 2 * PEN_CH + 4;      // >= 3 left over + 2 chunks of kept rows
 // per warp: the row ring, its a_0 ring, 32 (j, a_1, a_2) metas
 constexpr size_t PEN_WSMEM = PEN_RING * PEN_RS * sizeof(double) + PEN_RING * sizeof(int) + 32 * sizeof(int4);
 constexpr size_t PEN_SMEM = PEN_WARPS * PEN_WSMEM;
@@ -600,10 +604,10 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
     double acc[PEN_PH][2];
 #pragma unroll
     for (int i = 0; i < PEN_PH; ++i) acc[i][0] = acc[i][1] = 0.0;
-    const int nchunk = (jb.z + 31) >> 5;
+    const int nchunk = (jb.z + PEN_CH - 1) / PEN_CH;
     auto load_ra = [&](int c) {
       int4 r = make_int4(0, 0, -1000, 0);
-      if (32 * c + lane < jb.z) r = ra4[jb.y + 32 * c + lane];
+      if (lane < PEN_CH && PEN_CH * c + lane < jb.z) r = ra4[jb.y + PEN_CH * c + lane];
       return r;
     };
     // keep the chunk's points that touch the pencil; stage their rows at the ring's tail
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
       const bool ok = r.z >= c_lo && r.z <= c_hi && r.x >= p_lo && r.x <= p_hi;
       const unsigned mask = __ballot_sync(0xffffffffu, ok);
       const int nok = __popc(mask);
-      if (ok) s_meta[__popc(mask & ((1u << lane) - 1u))] = make_int4(jb.y + 32 * c + lane, r.y, r.z, r.x);
+      if (ok) s_meta[__popc(mask & ((1u << lane) - 1u))] = make_int4(jb.y + PEN_CH * c + lane, r.y, r.z, r.x);
       __syncwarp();
       // four lanes per kept point (8 points per pass): lane quarter q copies row weights
       // 2q, 2q + 1, column weights 2q, 2q + 1 (8-byte, zero-filled outside the taps) and
