@@ -407,7 +407,8 @@ __global__ void group_table_kernel(GatherArgs a, int64_t* __restrict__ gt_slot,
   }
 }
 
-// One CTA per (group, chunk of GATHER_CHUNK modes), GATHER_MPT modes per thread.
+// One CTA per (group, chunk of GATHER_CHUNK modes), GATHER_MPT modes per thread; the
+// group index runs fastest in the grid.
 // The phase of (member c, source at relative position rel) factors per axis as
 // P_k^(c_k - rel_k) = P_k^(-rel_k) P_k^(c_k): a per-source factor f0_u (rel_k in -1..2,
 // read from the 5-row phase table in shared memory) and a per-member factor Q_c.  So
@@ -423,7 +424,8 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
   __shared__ int64_t u_slot[NREL];
   __shared__ unsigned u_code[NREL];
   __shared__ double2 s_ph[5 * NFMAX];  // rows o = -2..2
-  const int64_t g = blockIdx.y;
+  const int64_t g = blockIdx.x;  // group fastest: CTAs in flight share a mode chunk, so the
+                                 // phi slices of neighbouring groups are reused from L2
   const int nu = gt_nu[g];
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
     u_slot[u] = gt_slot[g * NREL + u];
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
   const unsigned NF = (unsigned)a.NF;
 #pragma unroll 1
   for (int j = 0; j < GATHER_MPT; ++j) {
-    const unsigned e = (unsigned)blockIdx.x * GATHER_CHUNK + j * GATHER_THREADS + threadIdx.x;
+    const unsigned e = (unsigned)blockIdx.y * GATHER_CHUNK + j * GATHER_THREADS + threadIdx.x;
     if (e >= NF) return;
     int mk[D];
     {
@@ -927,7 +929,8 @@ void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   DBuf<int64_t> gt_slot(n_groups * nrel, st), gt_out(n_groups * nsib, st);
   DBuf<unsigned> gt_code(n_groups * nrel, st);
   DBuf<int> gt_nu(n_groups, st);
-  dim3 grid((unsigned)((P.NH + GATHER_CHUNK - 1) / GATHER_CHUNK), (unsigned)n_groups);
+  FGT_REQUIRE((P.NH + GATHER_CHUNK - 1) / GATHER_CHUNK <= 65535, FGT_ERANGE, "too many mode chunks");
+  dim3 grid((unsigned)n_groups, (unsigned)((P.NH + GATHER_CHUNK - 1) / GATHER_CHUNK));
   P.k_gather.begin(st);
 #define FGT_GATHER_D(DD)                                                                      \
   group_table_kernel<DD><<<(unsigned)n_groups, 64, 0, st>>>(ga, gt_slot.get(), gt_code.get(), \
