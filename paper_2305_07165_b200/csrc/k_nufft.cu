@@ -208,10 +208,10 @@ __global__ void job_ranges_kernel(const uint64_t* __restrict__ key, int64_t npts
 constexpr int REC_PTS = 32;
 constexpr int PEN_REC = 48;  // d = 3 record: [q w1 | w2 | w0], 16 zero-padded taps each
 constexpr int HC_MAX = 25;  // max polynomial degree + 1
-template <int D>
+template <int D, int W>  // W: kernel width (taps evaluated; the rest of the 16 are zero)
 __global__ void __launch_bounds__(D * 32) sort_records_kernel(
     const int64_t* __restrict__ perm, int64_t n, const double* __restrict__ tt, const int* __restrict__ ai,
-    const double* __restrict__ qb, int w, double beta, const double* __restrict__ hc, int K,
+    const double* __restrict__ qb, double beta, const double* __restrict__ hc, int K,
     double* __restrict__ rw, double* __restrict__ rq, int* __restrict__ ra, double* __restrict__ rw0) {
   __shared__ double s_c[HC_MAX * 16];
   __shared__ double s_w[D][REC_PTS][17];
@@ -219,25 +219,30 @@ __global__ void __launch_bounds__(D * 32) sort_records_kernel(
   __syncthreads();
   const int ax = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t j0 = (int64_t)blockIdx.x * REC_PTS, j = j0 + lane;
+  constexpr int w = W;
   const double half = 0.5 * w, inv_half = 2.0 / w;
   if (j < n) {
     const int64_t i = perm[j];
     const double x = tt[i * D + ax];
     const double a0 = ceil(x - half);
     const double y = 2.0 * ((a0 - x) + half) - 1.0;
-    double acc[16];
+    double acc[W];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t] = s_c[K * 16 + t];
+    for (int t = 0; t < W; ++t) acc[t] = s_c[K * 16 + t];
     for (int p = K - 1; p >= 0; --p) {
 #pragma unroll
-      for (int t = 0; t < 16; ++t) acc[t] = fma(acc[t], y, s_c[p * 16 + t]);
+      for (int t = 0; t < W; ++t) acc[t] = fma(acc[t], y, s_c[p * 16 + t]);
     }
-#pragma unroll
     const double cq = (D == 3 && ax == 1) ? qb[i] : 1.0;  // d = 3: charge folded into w1
+#pragma unroll
     for (int t = 0; t < 16; ++t) {
-      double v = acc[t];
-      if (t == 0 || t == w - 1) v = es_kernel((a0 + t - x) * inv_half, beta);
-      s_w[ax][lane][t] = t < w ? v * cq : 0.0;
+      double v = 0.0;
+      if (t < W) {
+        v = acc[t < W ? t : 0];
+        if (t == 0 || t == W - 1) v = es_kernel((a0 + t - x) * inv_half, beta);
+        v *= cq;
+      }
+      s_w[ax][lane][t] = v;
     }
     if (ax == 0) {
       if (D != 3) rq[j] = qb[i];
@@ -1193,9 +1198,18 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       rw = g_rw.view(npts * (D == 3 ? PEN_REC : 32), st);
       if (D != 3) rq = g_rq.view(npts, st);
       ra = g_ra.view(npts * 4, st);
-      sort_records_kernel<D><<<(unsigned)((npts + REC_PTS - 1) / REC_PTS), D * 32, 0, st>>>(
-          perm.get(), npts, tt.get(), ai.get(), qb.get(), w, N.beta, N.hc.get(), N.hdeg, rw.get(), rq.get(),
-          ra.get(), rw0.get());
+      switch (w) {
+#define FGT_REC(WV)                                                                                          \
+  case WV:                                                                                                   \
+    sort_records_kernel<D, WV><<<(unsigned)((npts + REC_PTS - 1) / REC_PTS), D * 32, 0, st>>>(              \
+        perm.get(), npts, tt.get(), ai.get(), qb.get(), N.beta, N.hc.get(), N.hdeg, rw.get(), rq.get(), ra.get(), \
+        rw0.get());                                                                                          \
+    break;
+        FGT_REC(2) FGT_REC(3) FGT_REC(4) FGT_REC(5) FGT_REC(6) FGT_REC(7) FGT_REC(8) FGT_REC(9)
+        FGT_REC(10) FGT_REC(11) FGT_REC(12) FGT_REC(13) FGT_REC(14) FGT_REC(15) FGT_REC(16)
+#undef FGT_REC
+        default: throw Error(FGT_ERANGE, "kernel width out of range");
+      }
       FGT_LAUNCHED();
     }
     const int NBP = (G + 7) / 8;  // d = 3: pencil row / column blocks
