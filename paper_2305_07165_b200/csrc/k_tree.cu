@@ -481,16 +481,31 @@ struct BoxSet {
 
 // Split the boxes flagged in `flag` (aligned with keys[lo, lo+n)): append their 2^d
 // children and re-sort.  Returns the number of boxes split.
+// counts (optional): a 2-element device buffer whose slot 1 holds another count computed
+// earlier on the stream; it is read back with the split count in the same round trip
+// (*extra_out).
 int64_t split_flagged(BoxSet& B, int64_t lo, int64_t n, const uint8_t* flag, int d, CubTmp& tmp,
-                      cudaStream_t st, DBuf<uint64_t>* kids_out = nullptr) {
+                      cudaStream_t st, DBuf<uint64_t>* kids_out = nullptr, int64_t* counts = nullptr,
+                      int64_t* extra_out = nullptr) {
   if (n == 0) return 0;
   DBuf<uint64_t> sel(n, st);
-  DBuf<int64_t> nsel(1, st);
+  DBuf<int64_t> nsel_own;
+  if (!counts) nsel_own.alloc(1, st);
+  int64_t* nsel = counts ? counts : nsel_own.get();
   size_t bytes = 0;
-  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, B.keys.get() + lo, flag, sel.get(), nsel.get(), (int)n, st));
-  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, B.keys.get() + lo, flag, sel.get(), nsel.get(), (int)n, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, B.keys.get() + lo, flag, sel.get(), nsel, (int)n, st));
+  FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, B.keys.get() + lo, flag, sel.get(), nsel, (int)n, st));
   count_launch();
-  int64_t k = read_scalar(nsel.get(), st);
+  int64_t k;
+  if (counts) {
+    int64_t h[2];
+    FGT_CUDA(cudaMemcpyAsync(h, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaStreamSynchronize(st));
+    k = h[0];
+    if (extra_out) *extra_out = h[1];
+  } else {
+    k = read_scalar(nsel, st);
+  }
   if (k == 0) return 0;
   const int64_t nc = (int64_t)k << d;
   // the children of the (sorted, stably selected) flagged leaves are sorted and new: merge
@@ -533,15 +548,15 @@ void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st, const
     FGT_LAUNCHED();
     // active candidates, selected before the key array grows
     DBuf<uint64_t> act(ncand, st);
-    DBuf<int64_t> nact(1, st);
+    DBuf<int64_t> counts(2, st);  // split count, active count: one read-back per round
     size_t bytes = 0;
-    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, cand.get(), active.get(), act.get(), nact.get(), (int)ncand, st));
-    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, cand.get(), active.get(), act.get(), nact.get(), (int)ncand, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, cand.get(), active.get(), act.get(), counts.get() + 1, (int)ncand, st));
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(bytes, st), bytes, cand.get(), active.get(), act.get(), counts.get() + 1, (int)ncand, st));
     count_launch();
     DBuf<uint64_t> kids;
-    const int64_t k = split_flagged(B, 0, B.n, split.get(), D, tmp, st, &kids);
+    int64_t na = 0;
+    const int64_t k = split_flagged(B, 0, B.n, split.get(), D, tmp, st, &kids, counts.get(), &na);
     if (k == 0) return;
-    const int64_t na = read_scalar(nact.get(), st);
     const int64_t nk = kids.size();
     DBuf<uint64_t> next(nk + na, st);
     concat_keys_kernel<<<grid_for(nk + na, 256), 256, 0, st>>>(kids.get(), nk, act.get(), na, next.get());
