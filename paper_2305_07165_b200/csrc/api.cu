@@ -920,12 +920,14 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
     Timer tm(os.s);
     DBuf<double> ds(ns * d, os.s), dq(ns, os.s), dt(nt * d, os.s), du(nt, os.s);
     // coordinates first (the tree needs all of them); the charges follow on a side stream
-    // and land while the tree is built (gather_sorted_points waits for them)
+    // and land while the tree is built (gather_sorted_points waits for them).  The copy
+    // is timed by events read after the pipeline: no host wait between the copy and the
+    // tree's first kernels.
     Event q_alloc, q_ready;
     FGT_CUDA(cudaEventRecord(q_alloc.e, os.s));
     ds.from_host(src, ns * d);
     dt.from_host(tgt, nt * d);
-    double h2d = tm.lap();
+    FGT_CUDA(cudaEventRecord(tm.b, os.s));
     FGT_CUDA(cudaStreamWaitEvent(os.side, q_alloc.e, 0));
     if (ns > 0) FGT_CUDA(cudaMemcpyAsync(dq.get(), charges, ns * sizeof(double), cudaMemcpyHostToDevice, os.side));
     FGT_CUDA(cudaEventRecord(q_ready.e, os.side));
@@ -933,6 +935,8 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
     std::memset(&t, 0, sizeof(t));
     points_pipeline(ds.get(), ns, dq.get(), dt.get(), nt, *tp, *pw, du.get(), os.s, &t, q_ready.e, u);
     FGT_CUDA(cudaStreamSynchronize(os.s));  // (points_finish timed the copy: u is on the host)
+    float h2d = 0.f;
+    FGT_CUDA(cudaEventElapsedTime(&h2d, tm.a, tm.b));
     t.h2d_ms = h2d;
     if (times) *times = t;
   });

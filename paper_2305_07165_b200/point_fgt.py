@@ -60,6 +60,22 @@ class FgtParams:
         self.pw = pw
 
 
+_PARAMS_CACHE = {}
+
+
+def _params(dim, delta, epsilon, n_s, periodic, share):
+    """FgtParams memoised on its arguments (the host quadrature and cutoff-level set-up
+    is ~0.05 ms; repeated transforms with the same parameters reuse it read-only)."""
+    key = (int(dim), float(delta), float(epsilon), int(n_s), bool(periodic), tuple(share))
+    p = _PARAMS_CACHE.get(key)
+    if p is None:
+        p = FgtParams(dim, delta, epsilon, n_s, periodic, share)
+        if len(_PARAMS_CACHE) > 64:
+            _PARAMS_CACHE.clear()
+        _PARAMS_CACHE[key] = p
+    return p
+
+
 def _prep(sources, charges, targets, periodic):
     src = np.atleast_2d(np.asarray(sources, dtype=np.float64))
     tgt = np.atleast_2d(np.asarray(targets, dtype=np.float64))
@@ -109,7 +125,7 @@ def fgt_points(sources, charges, targets, delta, epsilon, n_s, boundary="free",
     """
     periodic = _boundary(boundary)
     src, q, tgt, dim = _prep(sources, charges, targets, periodic)
-    prm = FgtParams(dim, delta, epsilon, n_s, periodic, share)
+    prm = _params(dim, delta, epsilon, n_s, periodic, share)
     if out is None:
         u = _host_out(tgt.shape[0])
     else:
@@ -134,7 +150,7 @@ def fgt_points_device(sources, charges, targets, delta, epsilon, n_s, boundary="
         if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
             raise ValueError(f"{name} must be a contiguous CUDA float64 tensor")
     dim = sources.shape[1] if sources.dim() == 2 else targets.shape[1]
-    prm = params or FgtParams(dim, delta, epsilon, n_s, periodic, share)
+    prm = params or _params(dim, delta, epsilon, n_s, periodic, share)
     nt = targets.shape[0]
     if out is None:
         out = torch.empty(nt, dtype=torch.float64, device=targets.device)
