@@ -1271,9 +1271,14 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       // planes per dispatch: the w taps plus room for the group's a_0 spread
 #define FGT_PEN(NPL)                                                                                         \
   {                                                                                                          \
-    FGT_CUDA(cudaFuncSetAttribute(spread_pencil_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PEN_SMEM)); \
-    int per_sm = 0;                                                                                          \
-    FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
+    static int per_sm_dev[64]; /* attribute + occupancy resolved once per device (0: unset) */            \
+    int dev = 0;                                                                                             \
+    FGT_CUDA(cudaGetDevice(&dev));                                                                           \
+    int& per_sm = per_sm_dev[dev & 63];                                                                      \
+    if (per_sm <= 0) {                                                                                       \
+      FGT_CUDA(cudaFuncSetAttribute(spread_pencil_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PEN_SMEM)); \
+      FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
+    }                                                                                                        \
     const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm),       \
                                                         ((int64_t)pa.nitems + PEN_WARPS - 1) / PEN_WARPS));           \
     spread_pencil_kernel<NPL><<<nblk, PEN_WARPS * 32, PEN_SMEM, st>>>(pa);                                   \
