@@ -530,10 +530,17 @@ __device__ __forceinline__ void eval_pass(const double2* __restrict__ etab, cons
     const int rb = nt * 8 + (lane >> 2);
     const bool rv = rb < R;
     const double2* prow = psi + (size_t)(rv ? rb : 0) * n_f;
+    // psi fragments prefetched two k-steps ahead (L2 latency behind the DMMAs)
+    auto ldB = [&](int kk) {
+      const int c = kk * 4 + (lane & 3);
+      return (rv && kk < ksteps && c < n_f) ? prow[c] : make_double2(0.0, 0.0);
+    };
+    double2 Bn0 = ldB(0), Bn1 = ldB(1);
     for (int kk = 0; kk < ksteps; ++kk) {
       const int c = kk * 4 + (lane & 3);
-      double2 B = make_double2(0.0, 0.0);
-      if (rv && c < n_f) B = prow[c];
+      const double2 B = Bn0;
+      Bn0 = Bn1;
+      Bn1 = ldB(kk + 2);
       double2 A[MTP];
 #pragma unroll
       for (int mt = 0; mt < MTP; ++mt) A[mt] = etab[((D - 1) * TB + mt * 8 + (lane >> 2)) * RS + c];
