@@ -759,6 +759,10 @@ void pw_setup_dense(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   P.phase.alloc(ph.size(), st);
   P.phase.from_host(ph.data(), ph.size());
   const int64_t nd = T.n_dense;
+  if ((int64_t)T.h_dense_src.size() == nd) {  // read back with the tree's finalize
+    P.h_src = T.h_dense_src;
+    return;
+  }
   P.h_src.assign(nd, 0);
   if (nd > 0) {
     DBuf<int64_t> m(nd, st);

@@ -567,6 +567,14 @@ void balance_rounds(BoxSet& B, int periodic, CubTmp& tmp, cudaStream_t st, const
   throw Error(FGT_ECUDA, "tree balance did not converge");
 }
 
+__global__ void dense_src_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
+                                 const int64_t* __restrict__ src_count, int64_t cap, int64_t* __restrict__ out) {
+  const int64_t n = *n_dev;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src_count[ids[i]];
+}
+
 template <int D>
 void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tgt, int64_t nt,
                      const fgt_tree_params& tp, cudaStream_t st) {
@@ -810,17 +818,33 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     FGT_LAUNCHED();
     dense_slot_dev_kernel<<<grid_for(nb, 256), 256, 0, st>>>(sel.get(), nsel, nb, T.dense_slot.get());
     FGT_LAUNCHED();
+    // source count of every P-box (the form's per-box path choice), read back with the
+    // finalize round trip below (capacity nb; the first n_dense entries are used)
+    DBuf<int64_t> dsrc(nb, st);
+    dense_src_kernel<<<grid_for(nb, 256), 256, 0, st>>>(sel.get(), nsel, T.src_count.get(), nb, dsrc.get());
+    FGT_LAUNCHED();
     T.dense_ids = std::move(sel);  // capacity nb, first n_dense entries used
     // leaf count
     size_t b2 = 0;
     FGT_CUDA(cub::DeviceReduce::Sum(nullptr, b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     count_launch();
-    std::vector<int64_t> h(l_c + 4);
+    // one pinned block for both read-backs (per thread, grown as needed)
+    static thread_local int64_t* hp = nullptr;
+    static thread_local int64_t hp_cap = 0;
+    const int64_t need = l_c + 4 + nb;
+    if (need > hp_cap) {
+      if (hp) FGT_CUDA(cudaFreeHost(hp));
+      hp_cap = std::max<int64_t>(need, 2 * hp_cap);
+      FGT_CUDA(cudaMallocHost((void**)&hp, hp_cap * sizeof(int64_t)));
+    }
     trace_mark(st, "tree:finalize");
-    fin.to_host(h.data(), h.size());
+    FGT_CUDA(cudaMemcpyAsync(hp, fin.get(), (l_c + 4) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaMemcpyAsync(hp + l_c + 4, dsrc.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     FGT_CUDA(cudaStreamSynchronize(st));
     trace_mark(st, "tree:finalize(sync)");
+    std::vector<int64_t> h(hp, hp + l_c + 4);
+    T.h_dense_src.assign(hp + l_c + 4, hp + l_c + 4 + h[l_c + 2]);
     T.level_off.assign(h.begin(), h.begin() + l_c + 2);
     T.n_dense = h[l_c + 2];
     T.n_leaves = h[l_c + 3];

@@ -31,6 +31,7 @@ struct TreeDev {
   DBuf<double> center;     // (nb * d) box centres (exact builder arithmetic)
   DBuf<int64_t> dense_ids;   // (n_dense) box ids of P-boxes
   DBuf<int64_t> dense_slot;  // (nb) index into dense_ids or -1
+  std::vector<int64_t> h_dense_src;  // host: source count of every P-box (n_dense)
 
   // lists (target-centric), built by build_lists()
   bool lists_built = false;
