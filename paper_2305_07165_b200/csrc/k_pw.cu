@@ -463,12 +463,13 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
 #pragma unroll
       for (int k = 1; k < D; ++k) f0 = cmul(f0, s_ph[(3 - (int)((code >> (8 + 2 * k)) & 3)) * NFMAX + mk[k]]);
       const double2 gu = cmul(f0, f);
+      // S_c += [member c served] gu as a multiply-add by 0 / 1 (branch- and select-free)
 #pragma unroll
-      for (int c = 0; c < NSIB; ++c)
-        if (code & (1u << c)) {
-          S[c].x += gu.x;
-          S[c].y += gu.y;
-        }
+      for (int c = 0; c < NSIB; ++c) {
+        const double bc = __hiloint2double((code >> c) & 1u ? 0x3ff00000 : 0, 0);
+        S[c].x = fma(bc, gu.x, S[c].x);
+        S[c].y = fma(bc, gu.y, S[c].y);
+      }
     }
     // Q_c = prod_{k: c_k = 1} P_k (table row o = +1)
     double2 P1[D];
