@@ -142,12 +142,40 @@ __global__ void __launch_bounds__(256) point_codes_kernel(
   }
 }
 
-// subtree point count of box (l, c): codes in [c << sh, (c+1) << sh)
-__device__ __forceinline__ int64_t prefix_lo(const uint64_t* pkey, int64_t n, uint64_t c, int sh) {
-  return lower_bound_dev(pkey, n, c << sh);
+// Sorted point codes with a coarse index: start[p] = first point whose code lies in the
+// level-L0 cell p (codes >> sh0 == p), ncell + 1 entries.  A lower bound is then one table
+// read when the value is a level-L0 cell boundary, else a binary search inside one cell
+// (a few hundred points) instead of over all points.
+struct PKeyIdx {
+  const uint64_t* key;
+  int64_t n;
+  const int64_t* start;
+  int sh0;
+};
+
+__device__ __forceinline__ int64_t pk_lower(const PKeyIdx& I, uint64_t v) {
+  const uint64_t p = v >> I.sh0;
+  int64_t lo = I.start[p];
+  if ((v & ((uint64_t(1) << I.sh0) - 1)) == 0) return lo;
+  int64_t hi = I.start[p + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (I.key[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
 }
-__device__ __forceinline__ int64_t prefix_hi(const uint64_t* pkey, int64_t n, uint64_t c, int sh) {
-  return lower_bound_dev(pkey, n, (c + 1) << sh);
+
+__global__ void pkey_index_kernel(const uint64_t* __restrict__ key, int64_t n, int sh0, int64_t ncell,
+                                  int64_t* __restrict__ start) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= ncell;
+       p += (int64_t)gridDim.x * blockDim.x)
+    start[p] = lower_bound_dev(key, n, (uint64_t)p << sh0);
+}
+
+// subtree point count of box (l, c): codes in [c << sh, (c+1) << sh)
+__device__ __forceinline__ int64_t prefix_lo(const PKeyIdx& I, uint64_t c, int sh) { return pk_lower(I, c << sh); }
+__device__ __forceinline__ int64_t prefix_hi(const PKeyIdx& I, uint64_t c, int sh) {
+  return pk_lower(I, (c + 1) << sh);
 }
 
 // deepest existing box at level <= l containing cell `code` at level l (tree.py:290-298)
@@ -206,7 +234,7 @@ __global__ void make_children_kernel(const uint64_t* __restrict__ parents, int64
 // Device-count variants for the level loop: the frontier size lives on the device, the
 // launch covers a host-side capacity and entries past the count are flagged 0 / skipped.
 __global__ void count_flag_dev_kernel(const uint64_t* __restrict__ keys, const int64_t* __restrict__ n_dev,
-                                      int64_t cap, const uint64_t* __restrict__ pkey, int64_t npts, int d,
+                                      int64_t cap, PKeyIdx pk, int d,
                                       int l_c, int64_t n_s, uint8_t* __restrict__ flag) {
   const int64_t n = n_dev ? (*n_dev << d) : 1;  // children of the boxes split one level up
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
@@ -216,7 +244,7 @@ __global__ void count_flag_dev_kernel(const uint64_t* __restrict__ keys, const i
       uint64_t k = keys[i];
       int sh = d * (l_c - key_level(k));
       uint64_t c = key_code(k);
-      f = (prefix_hi(pkey, npts, c, sh) - prefix_lo(pkey, npts, c, sh)) > n_s ? 1 : 0;
+      f = (prefix_hi(pk, c, sh) - prefix_lo(pk, c, sh)) > n_s ? 1 : 0;
     }
     flag[i] = f;
   }
@@ -303,7 +331,7 @@ __global__ void concat_keys_kernel(const uint64_t* __restrict__ a, int64_t na, c
 template <int D>
 __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int64_t lo,
                                      int64_t hi, const uint8_t* __restrict__ leaf,
-                                     const uint64_t* __restrict__ pkey, int64_t npts, int l_c,
+                                     PKeyIdx pk, int l_c,
                                      int64_t n_s, int periodic, uint8_t* __restrict__ split,
                                      int* __restrict__ any) {
   // one thread per (box, neighbour offset), as balance_cand_kernel
@@ -322,7 +350,7 @@ __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t 
     for (int k = 0; k < D; ++k) self &= (o[k] == 0);
     if (self) continue;
     uint64_t c = key_code(key);
-    int64_t cnt = prefix_hi(pkey, npts, c, 0) - prefix_lo(pkey, npts, c, 0);
+    int64_t cnt = prefix_hi(pk, c, 0) - prefix_lo(pk, c, 0);
     if (cnt <= n_s) continue;
     int64_t g[D];
     morton_decode(c, D, l_c, g);
@@ -346,7 +374,7 @@ __global__ void level_offsets_kernel(const uint64_t* __restrict__ keys, int64_t 
 // Per-box finalisation: the Tree fields (tree.py:236-254) + subtree counts.
 template <int D>
 __global__ void finalize_boxes_kernel(const uint64_t* __restrict__ keys, int64_t nb,
-                                      const uint64_t* __restrict__ pkey, int64_t npts,
+                                      PKeyIdx pk,
                                       const int64_t* __restrict__ srcpre, int l_c, Root root,
                                       int32_t* __restrict__ level, int64_t* __restrict__ parent,
                                       int64_t* __restrict__ children, int64_t* __restrict__ coords,
@@ -375,7 +403,7 @@ __global__ void finalize_boxes_kernel(const uint64_t* __restrict__ keys, int64_t
     for (int t = 0; t < NC; ++t) children[i * NC + t] = c0 >= 0 ? c0 + t : -1;
     is_leaf[i] = c0 < 0;
     int sh = D * (l_c - l);
-    int64_t lo = prefix_lo(pkey, npts, c, sh), hi = prefix_hi(pkey, npts, c, sh);
+    int64_t lo = prefix_lo(pk, c, sh), hi = prefix_hi(pk, c, sh);
     npoints[i] = hi - lo;
     int64_t sc = srcpre[hi] - srcpre[lo];
     scount[i] = c0 < 0 ? sc : 0;
@@ -396,15 +424,15 @@ __global__ void source_flag_kernel(const int64_t* __restrict__ pidx, int64_t npt
 // first point (two binary searches per leaf instead of one covering search per point);
 // a fill-forward scan then gives every sorted point its leaf.
 __global__ void leaf_first_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ is_leaf,
-                                  int64_t nb, const uint64_t* __restrict__ pkey, int64_t npts, int d, int l_c,
+                                  int64_t nb, PKeyIdx pk, int d, int l_c,
                                   int64_t* __restrict__ mark) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x) {
     if (!is_leaf[b]) continue;
     const uint64_t k = keys[b];
     const int sh = d * (l_c - key_level(k));
-    const int64_t s = prefix_lo(pkey, npts, key_code(k), sh);
-    if (s < npts && s < prefix_hi(pkey, npts, key_code(k), sh)) mark[s] = b;
+    const int64_t s = prefix_lo(pk, key_code(k), sh);
+    if (s < pk.n && s < prefix_hi(pk, key_code(k), sh)) mark[s] = b;
   }
 }
 
@@ -647,6 +675,14 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       T.pidx = std::move(idx);
     }
   }
+  // coarse index of the sorted codes (level L0 = min(l_c, 15 / D) cells)
+  const int L0 = std::min(l_c, 15 / D);
+  const int sh0 = D * (l_c - L0);
+  const int64_t ncell = (int64_t)1 << (D * L0);
+  T.pstart.alloc(ncell + 1, st);
+  pkey_index_kernel<<<grid_for(ncell + 1, 256), 256, 0, st>>>(T.pkey.get(), np, sh0, ncell, T.pstart.get());
+  FGT_LAUNCHED();
+  const PKeyIdx pk{T.pkey.get(), np, T.pstart.get(), sh0};
 
   // ---- level-synchronous refinement (tree.py:493-502).  The frontier of level l is a
   // sorted key array; the children of its split boxes (consecutive codes) form the next
@@ -670,7 +706,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       if (kc == 0) break;
       DBuf<uint8_t> flag(fn, st);
       count_flag_dev_kernel<<<grid_for(fn, 256), 256, 0, st>>>(levels.back().get(), l ? nsel.get() + (l - 1) : nullptr,
-                                                               fn, T.pkey.get(), np, D, l_c, T.n_s, flag.get());
+                                                               fn, pk, D, l_c, T.n_s, flag.get());
       FGT_LAUNCHED();
       DBuf<uint64_t> sel(fn, st);
       size_t bytes = 0;
@@ -716,7 +752,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       leaf_flag_kernel<<<grid_for(B.n, 256), 256, 0, st>>>(B.keys.get(), B.n, D, leaf.get());
       FGT_LAUNCHED();
       densefix_flag_kernel<D><<<grid_for(B.n * 27, 128), 128, 0, st>>>(
-          B.keys.get(), B.n, 0, B.n, leaf.get(), T.pkey.get(), np, l_c, T.n_s, tp.periodic,
+          B.keys.get(), B.n, 0, B.n, leaf.get(), pk, l_c, T.n_s, tp.periodic,
           split.get(), any.get());
       FGT_LAUNCHED();
       DBuf<uint64_t> kids;
@@ -755,7 +791,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   T.tgt_count.alloc(nb, st);
   T.center.alloc(nb * D, st);
   finalize_boxes_kernel<D><<<grid_for(nb, 128), 128, 0, st>>>(
-      T.bkey.get(), nb, T.pkey.get(), np, srcpre.get(), l_c, root, T.level.get(), T.parent.get(),
+      T.bkey.get(), nb, pk, srcpre.get(), l_c, root, T.level.get(), T.parent.get(),
       T.children.get(), T.coords.get(), T.is_leaf.get(), T.n_points.get(), T.src_count.get(),
       T.tgt_count.get(), T.center.get());
   FGT_LAUNCHED();
@@ -767,7 +803,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       DBuf<int64_t> mark(np, st), filled(np, st);
       fill_i64_kernel<<<grid_for(np, 256), 256, 0, st>>>(mark.get(), np, -1);
       FGT_LAUNCHED();
-      leaf_first_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, T.pkey.get(), np, D,
+      leaf_first_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, pk, D,
                                                          l_c, mark.get());
       FGT_LAUNCHED();
       size_t bytes = 0;

@@ -16,6 +16,7 @@ struct TreeDev {
   // points, sorted by Morton code at l_c (stable: ties keep combined index order)
   DBuf<uint64_t> pkey;    // (ntot)
   DBuf<int64_t> pidx;     // (ntot) combined index: <ns source, else ns+target
+  DBuf<int64_t> pstart;   // coarse index of pkey (k_tree.cu PKeyIdx)
 
   // boxes in canonical order: level-major, Morton within level
   int64_t nb = 0, n_leaves = 0, n_dense = 0;
