@@ -517,10 +517,25 @@ class BoxPlan:
         return s
 
 
-def _stack_values(tree, values, k):
+def _host_buffer(shape):
+    """float64 host array in page-locked memory when a GPU is present (torch's caching host
+    allocator): the leaf grids cross PCIe at link speed instead of through the driver's
+    pageable staging."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except ImportError:
+        pass
+    return np.empty(shape, dtype=np.float64)
+
+
+def _stack_values(tree, values, k, pinned=False):
     leaves = np.nonzero(tree.is_leaf)[0]
-    return leaves, np.ascontiguousarray(np.stack([np.asarray(values[b], float).reshape((k,) * tree.dim)
-                                                   for b in leaves]))
+    shape = (len(leaves),) + (k,) * tree.dim
+    V = _host_buffer(shape) if pinned else np.empty(shape, dtype=np.float64)
+    np.stack([np.asarray(values[b], float).reshape((k,) * tree.dim) for b in leaves], out=V)
+    return leaves, V
 
 
 def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, plan=None):
@@ -532,8 +547,8 @@ def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, p
     some = next(iter(values.values()))
     k = np.asarray(some).shape[0]
     plan = plan or BoxPlan(tree, delta, epsilon, k, boundary == "periodic")
-    leaves, V = _stack_values(tree, values, k)
-    U = np.empty_like(V)
+    leaves, V = _stack_values(tree, values, k, pinned=True)
+    U = _host_buffer(V.shape)
     t = _lib.FgtPhaseTimes()
     cs = plan.cstruct()
     _lib.check(_lib.load().fgt_box(ctypes.byref(cs), _lib.ptr(V), _lib.ptr(U), ctypes.byref(t)))
