@@ -504,7 +504,12 @@ constexpr int PEN_WARPS = 2;  // warps per CTA (each independent)
 #define FGT_PEN_CH 32
 #endif
 constexpr int PEN_CH = FGT_PEN_CH;            // points scanned per chunk (<= 32)
-constexpr int PEN_RING = 2 * PEN_CH + 4;      // >= 3 left over + 2 chunks of kept rows
+#ifndef FGT_PEN_RING
+#define FGT_PEN_RING 48
+#endif
+// ring of staged rows: a chunk is staged only when PEN_CH rows are free (else the staged
+// rows are processed first), so any size >= PEN_CH + 3 is correct
+constexpr int PEN_RING = FGT_PEN_RING;
 // per warp: the row ring, its a_0 ring, 32 (j, a_1, a_2) metas
 constexpr size_t PEN_WSMEM = PEN_RING * PEN_RS * sizeof(double) + PEN_RING * sizeof(int) + 32 * sizeof(int4);
 constexpr size_t PEN_SMEM = PEN_WARPS * PEN_WSMEM;
@@ -652,20 +657,10 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
       stage(0, load_ra(0));
       if (nchunk > 1) r_next = load_ra(1);
     }
-    for (int c = 0; c < nchunk; ++c) {
-      const int ready = tail;  // rows of chunks <= c
-      const bool last = c + 1 >= nchunk;
-      if (!last) {
-        stage(c + 1, r_next);
-        if (c + 2 < nchunk) r_next = load_ra(c + 2);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      // full groups of 4 from the ring (a partial group only after the last chunk)
-      const int avail = ready - head;
-      const int ngr = last ? (avail + 3) >> 2 : avail >> 2;
+    // full groups of 4 from [head, end) of the ring (the partial group too when all = true)
+    auto process = [&](int end, bool all) {
+      const int avail = end - head;
+      const int ngr = all ? (avail + 3) >> 2 : avail >> 2;
       for (int g = 0; g < ngr; ++g) {
         const int k = 4 * g + (lane & 3);
         const bool valid = k < avail;
@@ -688,6 +683,26 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
         }
       }
       head += min(avail, 4 * ngr);
+    };
+    for (int c = 0; c < nchunk; ++c) {
+      const int ready = tail;  // rows of chunks <= c
+      const bool last = c + 1 >= nchunk;
+      if (!last) {
+        if (tail - head + PEN_CH > PEN_RING) {
+          // no room for another chunk: finish the staged rows first
+          cp_async_wait<0>();
+          __syncwarp();
+          process(ready, false);
+          __syncwarp();
+        }
+        stage(c + 1, r_next);
+        if (c + 2 < nchunk) r_next = load_ra(c + 2);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      process(ready, last);
       __syncwarp();
     }
     // write the pencil: lane holds rows 8b + lane/4, columns 8t + 2 (lane % 4) + {0, 1}
