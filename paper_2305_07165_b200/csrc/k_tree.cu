@@ -453,6 +453,26 @@ __global__ void iota_kernel(int64_t* a, int64_t n) {
     a[i] = i;
 }
 
+// complete trees: stable partition of the code-sorted points into sources / targets with
+// their leaf (the level-l_c box lc_off + code)
+__global__ void partition_sorted_kernel(const uint64_t* __restrict__ pkey, const int64_t* __restrict__ pidx,
+                                        int64_t np, int64_t ns, const int64_t* __restrict__ srcpre,
+                                        int64_t lc_off, int64_t* __restrict__ src_perm,
+                                        int64_t* __restrict__ leaf_src, int64_t* __restrict__ tgt_perm,
+                                        int64_t* __restrict__ leaf_tgt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pidx[i], leaf = lc_off + (int64_t)pkey[i], k = srcpre[i];
+    if (p < ns) {
+      src_perm[k] = p;
+      leaf_src[k] = leaf;
+    } else {
+      tgt_perm[i - k] = p - ns;
+      leaf_tgt[i - k] = leaf;
+    }
+  }
+}
+
 __global__ void leaf_start_kernel(const int64_t* __restrict__ sorted_leaf, int64_t n,
                                   const uint8_t* __restrict__ is_leaf, int64_t nb,
                                   int64_t* __restrict__ start) {
@@ -691,6 +711,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   // one level are disjoint and hold > n_s points each), so the whole descent costs one
   // host round trip instead of one per level.
   BoxSet B;
+  bool complete = false;
   {
     std::vector<DBuf<uint64_t>> levels;
     std::vector<int64_t> cap;
@@ -730,6 +751,10 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       if (k == 0) break;
       lsize.push_back(k << D);
     }
+    // complete tree: every box of every level < l_c was split (e.g. uniform points), so all
+    // leaves sit at l_c and no balance or dense-fix split can follow
+    complete = (int)lsize.size() == l_c + 1;
+    for (int l = 0; complete && l < l_c; ++l) complete = hsel[l] == lsize[l];
     int64_t tot = 0;
     for (int64_t v : lsize) tot += v;
     B.keys.alloc(tot, st);
@@ -797,7 +822,27 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   FGT_LAUNCHED();
 
   // ---- per-point leaves, stable sorts -> src_perm / tgt_perm (tree.py:533-564)
-  {
+  if (complete && l_c > 0) {
+    // Complete tree: the leaf of sorted point i is the level-l_c box level_off(l_c) + its
+    // code, and the code sort (stable in the combined index) already lists every leaf's
+    // sources and then its targets in ascending original index -- a stable partition of
+    // the sorted points replaces the scatter and the two leaf sorts.
+    int64_t lc_off = 0;
+    for (int l = 0; l < l_c; ++l) lc_off += (int64_t)1 << (D * l);
+    T.src_perm.alloc(ns, st);
+    T.tgt_perm.alloc(nt, st);
+    T.src_start.alloc(nb, st);
+    T.tgt_start.alloc(nb, st);
+    DBuf<int64_t> leaf_src(ns, st), leaf_tgt(nt, st);
+    partition_sorted_kernel<<<grid_for(np, 256), 256, 0, st>>>(T.pkey.get(), T.pidx.get(), np, ns, srcpre.get(), lc_off,
+                                                               T.src_perm.get(), leaf_src.get(), T.tgt_perm.get(),
+                                                               leaf_tgt.get());
+    FGT_LAUNCHED();
+    leaf_start_kernel<<<grid_for(nb, 256), 256, 0, st>>>(leaf_src.get(), ns, T.is_leaf.get(), nb, T.src_start.get());
+    FGT_LAUNCHED();
+    leaf_start_kernel<<<grid_for(nb, 256), 256, 0, st>>>(leaf_tgt.get(), nt, T.is_leaf.get(), nb, T.tgt_start.get());
+    FGT_LAUNCHED();
+  } else {
     DBuf<int64_t> leaf_of(np, st);
     {
       DBuf<int64_t> mark(np, st), filled(np, st);

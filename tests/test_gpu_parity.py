@@ -113,6 +113,9 @@ TREE_CASES = [
     ("shell3d", 3, 20000, 1e-5, 1e-6, 8, False, "shell"),
     ("tiny", 2, 3, 1e-3, 1e-6, 10, False, "uniform"),
     ("onept_dense", 1, 500, 1e-4, 1e-6, 5, False, "clustered"),
+    # complete trees (every cell of every level < l_c split): the stable-partition path
+    ("complete2d_periodic", 2, 20000, 1e-3, 1e-6, 30, True, "uniform"),
+    ("complete3d", 3, 20000, 1e-2, 1e-6, 50, False, "uniform"),
 ]
 
 
