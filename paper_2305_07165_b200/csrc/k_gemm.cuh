@@ -27,13 +27,15 @@ struct GemmArgs {
   int64_t boff;         // batch offset of this launch (grid.z limit)
 };
 
-template <bool AC, bool BC, bool CRE, bool ACC>
+// CTA tile 32 x 48 (2 x 2 warps of 16 x 24); FLAT: 16 x 96 (1 x 4 warps) for M <= 16, so
+// a 16-row problem (e.g. the nh = 16 stored planes of config 5) wastes no DMMA rows
+template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false>
 __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = FLAT ? 0 : warp >> 1, wn = FLAT ? warp : warp & 1;
   const int64_t b = blockIdx.z + g.boff;
-  const int m0 = blockIdx.y * 32 + wm * 16;
-  const int n0 = blockIdx.x * 48 + wn * 24;
+  const int m0 = blockIdx.y * (FLAT ? 16 : 32) + wm * 16;
+  const int n0 = blockIdx.x * (FLAT ? 96 : 48) + wn * 24;
   const double* A = g.A + (g.aidx ? g.aidx[b] : b) * g.sA * (AC ? 2 : 1);
   const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
   const int64_t cb = g.cidx ? g.cidx[b] : b;
@@ -132,8 +134,12 @@ void bgemm(const GemmArgs& g, cudaStream_t st) {
   for (int64_t b0 = 0; b0 < g.batch; b0 += 65535) {
     GemmArgs c = g;
     c.boff = b0;
-    dim3 grid((g.N + 47) / 48, (g.M + 31) / 32, (unsigned)std::min<int64_t>(65535, g.batch - b0));
-    bgemm_kernel<AC, BC, CRE, ACC><<<grid, 128, 0, st>>>(c);
+    const unsigned nz = (unsigned)std::min<int64_t>(65535, g.batch - b0);
+    if (g.M <= 16) {
+      bgemm_kernel<AC, BC, CRE, ACC, true><<<dim3((g.N + 95) / 96, 1, nz), 128, 0, st>>>(c);
+    } else {
+      bgemm_kernel<AC, BC, CRE, ACC><<<dim3((g.N + 47) / 48, (g.M + 31) / 32, nz), 128, 0, st>>>(c);
+    }
     FGT_LAUNCHED();
   }
 }
