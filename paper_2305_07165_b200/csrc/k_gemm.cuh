@@ -29,27 +29,29 @@ struct GemmArgs {
 
 // CTA tile 32 x 48 (2 x 2 warps of 16 x 24); FLAT: 16 x 96 (1 x 4 warps) for M <= 16, so
 // a 16-row problem (e.g. the nh = 16 stored planes of config 5) wastes no DMMA rows
-template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false>
+template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false, bool TALL = false>
 __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = FLAT ? 0 : warp >> 1, wn = FLAT ? warp : warp & 1;
+  // TALL (N <= 32): 64 x 32 (4 x 1 warps of 16 x 32, four 8-column tiles per warp)
+  constexpr int NT = TALL ? 4 : 3;
+  const int wm = FLAT ? 0 : (TALL ? warp : warp >> 1), wn = FLAT ? warp : (TALL ? 0 : warp & 1);
   const int64_t b = blockIdx.z + g.boff;
-  const int m0 = blockIdx.y * (FLAT ? 16 : 32) + wm * 16;
-  const int n0 = blockIdx.x * (FLAT ? 96 : 48) + wn * 24;
+  const int m0 = blockIdx.y * (FLAT ? 16 : (TALL ? 64 : 32)) + wm * 16;
+  const int n0 = blockIdx.x * (FLAT ? 96 : (TALL ? 32 : 48)) + wn * 24;
   const double* A = g.A + (g.aidx ? g.aidx[b] : b) * g.sA * (AC ? 2 : 1);
   const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
   const int64_t cb = g.cidx ? g.cidx[b] : b;
   double* C = g.C + cb * g.sC * (CRE ? 1 : 2);
-  double acc[2][3][4];
+  double acc[2][NT][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
   for (int k0 = 0; k0 < g.K; k0 += 4) {
     const int k = k0 + (lane & 3);
-    double ar[2], ai[2], br[3], bi[3];
+    double ar[2], ai[2], br[NT], bi[NT];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int r = m0 + mt * 8 + (lane >> 2);
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
       }
     }
 #pragma unroll
-    for (int nt = 0; nt < 3; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
       const int c = n0 + nt * 8 + (lane >> 2);
       br[nt] = bi[nt] = 0.0;
       if (c < g.N && k < g.K) {
@@ -82,25 +84,25 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
+      for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
     if (AC && BC) {
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
     }
     if (!CRE) {
       if (BC) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
       }
       if (AC) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
       }
     }
   }
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
     const int r = m0 + mt * 8 + (lane >> 2);
     if (r >= g.M) continue;
 #pragma unroll
-    for (int nt = 0; nt < 3; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int c = n0 + nt * 8 + 2 * (lane & 3) + i;
@@ -137,6 +139,8 @@ void bgemm(const GemmArgs& g, cudaStream_t st) {
     const unsigned nz = (unsigned)std::min<int64_t>(65535, g.batch - b0);
     if (g.M <= 16) {
       bgemm_kernel<AC, BC, CRE, ACC, true><<<dim3((g.N + 95) / 96, 1, nz), 128, 0, st>>>(c);
+    } else if (g.N <= 32) {
+      bgemm_kernel<AC, BC, CRE, ACC, false, true><<<dim3(1, (g.M + 63) / 64, nz), 128, 0, st>>>(c);
     } else {
       bgemm_kernel<AC, BC, CRE, ACC><<<dim3((g.N + 47) / 48, (g.M + 31) / 32, nz), 128, 0, st>>>(c);
     }
