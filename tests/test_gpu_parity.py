@@ -446,3 +446,22 @@ def test_random_tree_sweep_bit_exact(cuda, case):
     b, lb, to = oracle_canonical(y, x, n_s, delta, eps, periodic)
     assert la == lb and tg.root_side == to.root_side
     assert a == b
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-10])
+def test_pencil_spreading_widths_and_splits(cuda, eps, monkeypatch):
+    """d = 3 spreading by pencils for every dispatch width (kernel widths w <= 5, 6-9,
+    >= 10 select 8-, 12- and 16-plane blocks) on a tight cluster whose P-boxes hold more
+    than 4096 points per row range (split row jobs + the ordered partial-pencil reduce),
+    forced through the NUFFT path: <= 10 eps against the exact direct sum."""
+    from paper_2305_07165_b200 import fgt_points
+    monkeypatch.setenv("FGT_NUFFT_MODE", "spread")
+    r = np.random.default_rng(31)
+    n = 60000
+    y = clustered(r, n, 3, k=2, sigma=0.004)
+    x = r.uniform(-0.5, 0.5, (4000, 3))
+    q = r.standard_normal(n)
+    u, t = fgt_points(y, q, x, 1e-4, eps, 2000, return_times=True)
+    assert t["n_spread_boxes"] > 0 and t["n_src_spread"] > 0
+    ex = ofgt.direct_oracle(y, q, x, 1e-4, "free")
+    assert rel(u, ex) <= 10 * eps
