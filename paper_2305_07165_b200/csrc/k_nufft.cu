@@ -574,16 +574,14 @@ __device__ __forceinline__ void pencil_planes(double (&acc)[PEN_PH][2], const do
 template <int NPL>
 __device__ __forceinline__ void pencil_dispatch(int S, double (&acc)[PEN_PH][2], const double* w0row, double A,
                                                 double B, int cnt) {
-  switch (S) {
+  // S in [0, 39); a dense 64-entry switch lowers to one indirect branch
+  switch (S & 63) {
 #define FGT_PL(K) \
   case K: pencil_planes<NPL, K>(acc, w0row, A, B, cnt); break;
-    FGT_PL(0) FGT_PL(1) FGT_PL(2) FGT_PL(3) FGT_PL(4) FGT_PL(5) FGT_PL(6) FGT_PL(7)
-    FGT_PL(8) FGT_PL(9) FGT_PL(10) FGT_PL(11) FGT_PL(12) FGT_PL(13) FGT_PL(14) FGT_PL(15)
-    FGT_PL(16) FGT_PL(17) FGT_PL(18) FGT_PL(19) FGT_PL(20) FGT_PL(21) FGT_PL(22) FGT_PL(23)
-    FGT_PL(24) FGT_PL(25) FGT_PL(26) FGT_PL(27) FGT_PL(28) FGT_PL(29) FGT_PL(30) FGT_PL(31)
-    FGT_PL(32) FGT_PL(33) FGT_PL(34) FGT_PL(35) FGT_PL(36) FGT_PL(37) FGT_PL(38)
+#define FGT_PL8(K) FGT_PL(K) FGT_PL(K + 1) FGT_PL(K + 2) FGT_PL(K + 3) FGT_PL(K + 4) FGT_PL(K + 5) FGT_PL(K + 6) FGT_PL(K + 7)
+    FGT_PL8(0) FGT_PL8(8) FGT_PL8(16) FGT_PL8(24) FGT_PL8(32) FGT_PL8(40) FGT_PL8(48) FGT_PL8(56)
+#undef FGT_PL8
 #undef FGT_PL
-    default: break;
   }
 }
 
