@@ -334,18 +334,15 @@ __device__ __forceinline__ void window_dispatch(int widx, double (&acc)[NB][NB][
                                                 const double* w2, int jr, double cj, int a1, int a2,
                                                 bool valid, int w, int lane) {
   constexpr int NW = NB - 2;
-  switch (widx) {
+  switch (widx & 63) {  // dense: one indirect branch
 #define FGT_WIN(K)                                                                        \
   case K:                                                                                 \
     if constexpr ((K) < NW * NW) tile_window<NB, (K) / NW, (K) % NW>(acc, w1, w2, jr, cj, a1, a2, valid, w, lane); \
     break;
-    FGT_WIN(0) FGT_WIN(1) FGT_WIN(2) FGT_WIN(3) FGT_WIN(4) FGT_WIN(5) FGT_WIN(6) FGT_WIN(7)
-    FGT_WIN(8) FGT_WIN(9) FGT_WIN(10) FGT_WIN(11) FGT_WIN(12) FGT_WIN(13) FGT_WIN(14) FGT_WIN(15)
-    FGT_WIN(16) FGT_WIN(17) FGT_WIN(18) FGT_WIN(19) FGT_WIN(20) FGT_WIN(21) FGT_WIN(22) FGT_WIN(23)
-    FGT_WIN(24) FGT_WIN(25) FGT_WIN(26) FGT_WIN(27) FGT_WIN(28) FGT_WIN(29) FGT_WIN(30) FGT_WIN(31)
-    FGT_WIN(32) FGT_WIN(33) FGT_WIN(34) FGT_WIN(35)
+#define FGT_WIN8(K) FGT_WIN(K) FGT_WIN(K + 1) FGT_WIN(K + 2) FGT_WIN(K + 3) FGT_WIN(K + 4) FGT_WIN(K + 5) FGT_WIN(K + 6) FGT_WIN(K + 7)
+    FGT_WIN8(0) FGT_WIN8(8) FGT_WIN8(16) FGT_WIN8(24) FGT_WIN8(32) FGT_WIN8(40) FGT_WIN8(48) FGT_WIN8(56)
+#undef FGT_WIN8
 #undef FGT_WIN
-    default: break;
   }
 }
 
