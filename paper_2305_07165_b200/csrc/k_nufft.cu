@@ -628,9 +628,10 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
       // 2q, 2q + 1, column weights 2q, 2q + 1 (8-byte, zero-filled outside the taps) and
       // axis-0 weights [4q, 4q + 4) (two 16-byte copies)
       const int q = lane & 3;
+      const int ts = tail % PEN_RING;
       for (int i = lane >> 2; i < nok; i += 8) {
         const int4 m = s_meta[i];
-        const int slot = (tail + i) % PEN_RING;
+        const int slot = ts + i >= PEN_RING ? ts + i - PEN_RING : ts + i;
         double* dst = stg + slot * PEN_RS;
         const double* rec = a.rw + (int64_t)m.x * PEN_REC;
         if (q == 0) s_a0[slot] = m.w;
@@ -656,10 +657,12 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
     auto process = [&](int end, bool all) {
       const int avail = end - head;
       const int ngr = all ? (avail + 3) >> 2 : avail >> 2;
+      const int hs = head % PEN_RING;
       for (int g = 0; g < ngr; ++g) {
         const int k = 4 * g + (lane & 3);
         const bool valid = k < avail;
-        const int slot = (head + (valid ? k : 0)) % PEN_RING;
+        const int kk = hs + (valid ? k : 0);
+        const int slot = kk >= PEN_RING ? kk - PEN_RING : kk;
         const double* row = stg + slot * PEN_RS;
         const double A = valid ? row[lane >> 2] : 0.0;
         const double B = valid ? row[8 + (lane >> 2)] : 0.0;
