@@ -13,7 +13,7 @@
  *
  *  2. Phase/pipeline entry points for the discrete transform (Alg 2,
  *     /root/reference/PAPER.md:840-872; contract SPEC.md:361-444): the GPU tree
- *     (Alg 1, reference tree.py:442-527), the P/D lists, and
+ *     (Alg 1, reference tree.py:259-344), the P/D lists, and
  *     fgt_points.  `*_dev` variants take DEVICE pointers and a
  *     cudaStream_t (passed as void*), so a caller holding inputs already resident
  *     in HBM avoids the host round trip.
@@ -98,7 +98,7 @@ typedef struct fgt_pw_params {
   const double* weights_1d; /* (n_f,) host array: h/(2 sqrt(pi)) exp(-m^2 h^2/4) */
 } fgt_pw_params;
 
-/* Tree construction controls (build_point_tree, tree.py:442-527). */
+/* Tree construction controls (build_point_tree, tree.py:259-344). */
 typedef struct fgt_tree_params {
   int32_t dim;
   int32_t periodic;     /* 0 free space, 1 unit cell [-1/2,1/2)^d with one image layer
@@ -224,7 +224,7 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
 /* ---------------------------------------------------------------------------
  * Layer 3: continuous (box) FGT, Alg 4.
  *
- * The density tree (Alg 3, tree.py:577-644) needs the user's sigma callable, so it is
+ * The density tree (Alg 3, tree.py:394-461) needs the user's sigma callable, so it is
  * built on the host; the host also builds the per-level 1-D tables (J/I moments,
  * poly1d.py:129-210) and the schedules below.  Everything else runs on the GPU:
  * leaf->PW and PW->grid as d separable FP64-DMMA GEMMs per level, the diagonal

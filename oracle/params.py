@@ -66,7 +66,7 @@ def periodic_np(epsilon, delta):
 
 
 def cut_level(delta, epsilon, L0=1.0, kind="density"):
-    """tree.cutoff_level (tree.py:207-233)."""
+    """tree.cutoff_level (tree.py:24-50)."""
     D0 = d0_of(clamp_eps(epsilon))
     cut = D0 * np.sqrt(delta)
     if kind == "point":

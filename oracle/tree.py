@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Follows the reference's
 sequential construction order exactly (creation-order box ids, LIFO balance queue),
 so box ids as well as the box set match the reference:
-  root/l_c (tree.py:458-472), level-synchronous split of boxes with > n_s points
+  root/l_c (tree.py:275-289), level-synchronous split of boxes with > n_s points
   (:493-502), point redistribution by p >= centre (:478-491), 2:1 balance
   (:378-403), dense-cutoff-leaf fix (:506-523), partition (:533-564).
 """
@@ -16,13 +16,13 @@ NO_IDX = np.zeros(0, dtype=np.int64)
 
 
 def offsets(dim):
-    """tree._offsets (tree.py:419-426): axis 0 slowest, values (-1, 0, 1)."""
+    """tree._offsets (tree.py:236-243): axis 0 slowest, values (-1, 0, 1)."""
     g = np.stack(np.meshgrid(*([np.array([-1, 0, 1])] * dim), indexing="ij"), axis=-1)
     return [row.astype(np.int64) for row in g.reshape(-1, dim)]
 
 
 class Boxes:
-    """Mutable struct-of-lists tree (tree._Builder, tree.py:301-416)."""
+    """Mutable struct-of-lists tree (tree._Builder, tree.py:118-233)."""
 
     def __init__(self, dim, rc, rs, periodic):
         self.dim, self.rc, self.rs, self.periodic = dim, np.asarray(rc, dtype=float), float(rs), periodic
@@ -70,7 +70,7 @@ class Boxes:
         raise RuntimeError("no covering box")
 
     def neighbour_cells(self, b):
-        """tree._Builder.neighbor_cells (tree.py:359-376), self excluded."""
+        """tree._Builder.neighbor_cells (tree.py:176-193), self excluded."""
         n_side = 2 ** self.level[b]
         out = []
         for o in self.offs:
@@ -83,7 +83,7 @@ class Boxes:
         return out
 
     def balance(self, on_split):
-        """tree._Builder.balance (tree.py:378-403), LIFO over leaves."""
+        """tree._Builder.balance (tree.py:195-220), LIFO over leaves."""
         stack = [b for b in range(len(self.level)) if self.leaf(b)]
         while stack:
             b = stack.pop()
@@ -118,7 +118,7 @@ class OracleTree:
         self.coords = np.asarray(B.coords, dtype=np.int64).reshape(nb, B.dim)
         self.is_leaf = self.children[:, 0] < 0
         self.l_c, self.R = l_c, R
-        # partition (tree._sort_points, tree.py:533-564)
+        # partition (tree._sort_points, tree.py:350-381)
         self.src_start = np.zeros(nb, np.int64)
         self.src_count = np.zeros(nb, np.int64)
         self.tgt_start = np.zeros(nb, np.int64)
@@ -152,7 +152,7 @@ class OracleTree:
 
 
 def build(sources, targets, n_s, delta, epsilon, periodic=False):
-    """tree.build_point_tree (tree.py:442-527)."""
+    """tree.build_point_tree (tree.py:259-344)."""
     sources = np.atleast_2d(np.asarray(sources, dtype=float))
     targets = np.atleast_2d(np.asarray(targets, dtype=float))
     if sources.size == 0 and targets.size == 0:

@@ -6,7 +6,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
     here by composite Gauss-Legendre on the clipped support (the reference switches to
     the same clipped quadrature outside its recurrence window, poly1d.py:161-172)
   * `fourier_I`: I[P_n](t) = 2 i^n j_n(t) (poly1d.py:198-210)
-  * `density_tree`: tree.build_density_tree (tree.py:577-644), refill="evaluate"
+  * `density_tree`: tree.build_density_tree (tree.py:394-461), refill="evaluate"
   * `fgt_box`: Alg 4 with the conventions SURVEY.md §3(D) verified against quadrature:
     phi_m = w_m (L/2)^d sum_a c_a prod conj(I[P_{a_i}](L m_i h / (2 sqrt(delta)))),
     child->parent exp(-ik.(c_C-c_B)), out->in exp(+ik.(c_T-c_S-v)),
@@ -129,7 +129,7 @@ class DensityTree:
 
 
 def density_tree(density, dim, k, epsilon, periodic=False, l_max=30, root_side=1.0):
-    """tree.build_density_tree (tree.py:577-644) with refill='evaluate'."""
+    """tree.build_density_tree (tree.py:394-461) with refill='evaluate'."""
     eps = clamp_eps(epsilon)
     basis = Basis(k)
     B = Boxes(dim, np.zeros(dim), root_side, periodic)

@@ -254,7 +254,7 @@ inline unsigned grid_for(int64_t n, int block, int64_t cap = 148 * 64) {
 }
 
 // ---------------------------------------------------------------- device math
-// Box centre per axis exactly as tree._Builder.center (tree.py:324-326):
+// Box centre per axis exactly as tree._Builder.center (tree.py:141-143):
 //   (root_center - 0.5*root_side) + (coord + 0.5) * s,  s = root_side / 2**level.
 // Each operation is rounded separately (no FMA contraction), which is what numpy does.
 __device__ __forceinline__ double box_center_1d(double root_low, int64_t coord, double s) {
@@ -265,7 +265,7 @@ __host__ __device__ __forceinline__ int pow2i(int k) { return 1 << k; }
 
 // Morton helpers: a box at level l with integer coords g (each < 2^l) has code
 //   sum_{lv<l} childno(lv) << (d*(l-1-lv)),  childno = sum_k bit_k << k
-// (child c has axis-k bit (c>>k)&1, tree.py:314-315), so code(parent) = code >> d.
+// (child c has axis-k bit (c>>k)&1, tree.py:131-132), so code(parent) = code >> d.
 __host__ __device__ __forceinline__ uint64_t morton_encode(const int64_t* g, int d, int l) {
   uint64_t code = 0;
   for (int b = l - 1; b >= 0; --b) {

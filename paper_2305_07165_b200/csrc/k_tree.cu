@@ -178,7 +178,7 @@ __device__ __forceinline__ int64_t prefix_hi(const PKeyIdx& I, uint64_t c, int s
   return pk_lower(I, (c + 1) << sh);
 }
 
-// deepest existing box at level <= l containing cell `code` at level l (tree.py:290-298)
+// deepest existing box at level <= l containing cell `code` at level l (tree.py:107-115)
 __device__ __forceinline__ int64_t find_covering_dev(const uint64_t* keys, int64_t nb, int d, int l,
                                                      uint64_t code) {
   for (int lv = l; lv >= 0; --lv) {
@@ -190,7 +190,7 @@ __device__ __forceinline__ int64_t find_covering_dev(const uint64_t* keys, int64
 }
 
 // neighbour cell of g at level l by offset o; returns false if outside (free space).
-// Periodic: v = n div 2^l, n -= v 2^l (tree.py:369-371).
+// Periodic: v = n div 2^l, n -= v 2^l (tree.py:186-188).
 template <int D>
 __device__ __forceinline__ bool neighbor_cell(const int64_t* g, const int* o, int l, bool periodic,
                                               int64_t* n, int* v) {
@@ -280,7 +280,7 @@ __global__ void leaf_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, 
   }
 }
 
-// Incremental 2:1 balance round (tree.py:378-403): a leaf b at level l >= 2 forces the
+// Incremental 2:1 balance round (tree.py:195-220): a leaf b at level l >= 2 forces the
 // split of any leaf neighbour covering at level <= l-2.  Checked for a list of
 // candidate boxes (by key), one thread per (candidate, offset); candidates that forced a
 // split are marked active (their neighbourhood changed: re-checked next round).
@@ -326,7 +326,7 @@ __global__ void concat_keys_kernel(const uint64_t* __restrict__ a, int64_t na, c
     out[i] = i < na ? a[i] : b[i - na];
 }
 
-// dense-cutoff-leaf fix (tree.py:506-523): a level-l_c leaf with > n_s points forces
+// dense-cutoff-leaf fix (tree.py:323-340): a level-l_c leaf with > n_s points forces
 // the split of every leaf neighbour at level l_c-1.
 template <int D>
 __global__ void densefix_flag_kernel(const uint64_t* __restrict__ keys, int64_t nb, int64_t lo,
@@ -371,7 +371,7 @@ __global__ void level_offsets_kernel(const uint64_t* __restrict__ keys, int64_t 
   if (l <= nlev) off[l] = lower_bound_dev(keys, nb, box_key(l, 0));
 }
 
-// Per-box finalisation: the Tree fields (tree.py:236-254) + subtree counts.
+// Per-box finalisation: the Tree fields (tree.py:53-71) + subtree counts.
 template <int D>
 __global__ void finalize_boxes_kernel(const uint64_t* __restrict__ keys, int64_t nb,
                                       PKeyIdx pk,
@@ -638,7 +638,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   FGT_REQUIRE(tp.periodic >= 0 && tp.periodic <= 2, FGT_EINVAL, "periodic must be 0, 1 or 2");
   FGT_REQUIRE(T.ntot < ((int64_t)1 << 31), FGT_ERANGE, "more than 2^31 points");
 
-  // ---- root and cutoff level (tree.py:458-472, cutoff_level :207-233)
+  // ---- root and cutoff level (tree.py:275-289, cutoff_level :24-50)
   if (tp.periodic == 2) {
     // root Fourier-series regime: the unit cell is the only box
     for (int k = 0; k < D; ++k) T.root_center[k] = 0.0;
@@ -704,7 +704,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   FGT_LAUNCHED();
   const PKeyIdx pk{T.pkey.get(), np, T.pstart.get(), sh0};
 
-  // ---- level-synchronous refinement (tree.py:493-502).  The frontier of level l is a
+  // ---- level-synchronous refinement (tree.py:310-319).  The frontier of level l is a
   // sorted key array; the children of its split boxes (consecutive codes) form the next
   // sorted frontier, so the level-major box array is their concatenation (no re-sort).
   // Frontier sizes stay on the device (capacities bound the launches: the boxes split at
@@ -766,7 +766,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     }
   }
 
-  // ---- balance + dense-cutoff-leaf fix to the joint fixpoint (tree.py:504-523)
+  // ---- balance + dense-cutoff-leaf fix to the joint fixpoint (tree.py:321-340)
   balance_rounds<D>(B, tp.periodic, tmp, st);
   trace_mark(st, "tree:balance");
   if (l_c >= 1) {
@@ -821,7 +821,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
       T.tgt_count.get(), T.center.get());
   FGT_LAUNCHED();
 
-  // ---- per-point leaves, stable sorts -> src_perm / tgt_perm (tree.py:533-564)
+  // ---- per-point leaves, stable sorts -> src_perm / tgt_perm (tree.py:350-381)
   if (complete && l_c > 0) {
     // Complete tree: the leaf of sorted point i is the level-l_c box level_off(l_c) + its
     // code, and the code sort (stable in the combined index) already lists every leaf's
@@ -971,7 +971,7 @@ void gather_sorted_points(TreeDev& T, const double* src, const double* q, const 
 namespace {
 
 // Enumerate the neighbour leaves of leaf T (tree recipe of SURVEY §8c, matching
-// neighbor_cells tree.py:359-376 + find_covering :290-298): for each offset, the
+// neighbor_cells tree.py:176-193 + find_covering :107-115): for each offset, the
 // covering leaf (colleague or coarse) or, when the colleague is subdivided, its
 // children touching T (fine neighbours; leaves by balance).  Deduplicated on (S, v).
 template <int D>

@@ -3,7 +3,7 @@
 These feed the GPU tree (cutoff level, root side) and the plane-wave kernels (h, n_f,
 weights), so they are evaluated with the same float64 numpy expressions as the
 reference /root/reference/pkg/src/fgt/planewave.py (clamp :23-25, D0 :28-30,
-pw_params :73-98) and tree.cutoff_level (/root/reference/pkg/src/fgt/tree.py:207-233):
+pw_params :73-98) and tree.cutoff_level (/root/reference/pkg/src/fgt/tree.py:24-50):
 identical inputs give bit-identical l_c, root side and box centres.
 """
 

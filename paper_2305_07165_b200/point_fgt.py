@@ -51,7 +51,7 @@ class FgtParams:
             pw.h = float(2.0 * np.pi * np.sqrt(delta))  # k = h n / sqrt(delta) = 2 pi n
         else:
             # NUFFT/plane-wave rule for the cutoff boxes
-            self.pwq = pw_params(float(epsilon), delta, R=self.R, dim=dim)
+            self.pwq = pw_params(float(eps), delta, R=self.R, dim=dim)
             self._w = np.ascontiguousarray(self.pwq.weights_1d, dtype=np.float64)
             pw.n_f = self.pwq.n_f
             pw.D0 = float(self.pwq.D0)

@@ -1,6 +1,6 @@
 """GPU-built level-restricted point tree (Alg 1) with the reference's data layout.
 
-`build_point_tree` mirrors /root/reference/pkg/src/fgt/tree.py:442-527 (same
+`build_point_tree` mirrors /root/reference/pkg/src/fgt/tree.py:259-344 (same
 arguments, same return tuple (tree, partition, l_c, R), same ValueErrors) but the
 construction runs in libfgtcuda.so (Morton codes + radix sort + parallel balance and
 dense-fix rounds).  Box ids are canonical (level-major, Morton order within a level)
@@ -19,7 +19,7 @@ from .planewave import clamp_tolerance, cutoff_factor, cutoff_level
 
 @dataclass
 class Tree:
-    """Adaptive 2^d-tree (fields of reference tree.Tree, tree.py:236-298)."""
+    """Adaptive 2^d-tree (fields of reference tree.Tree, tree.py:53-115)."""
 
     dim: int
     root_center: np.ndarray
@@ -78,7 +78,7 @@ class Tree:
 
 @dataclass
 class PointPartition:
-    """Box-sorted view of the sources and targets (reference tree.py:429-439)."""
+    """Box-sorted view of the sources and targets (reference tree.py:246-256)."""
 
     src_perm: np.ndarray
     tgt_perm: np.ndarray

@@ -3,7 +3,7 @@
 Public entry points mirror the reference / SPEC:
   * `build_density_tree(density, dim, k, epsilon, periodic=False, l_max=30,
     refill="evaluate", root_center=None, root_side=1.0)` -> (tree, values, coeffs),
-    the contract of /root/reference/pkg/src/fgt/tree.py:577-644 (sigma is a user
+    the contract of /root/reference/pkg/src/fgt/tree.py:394-461 (sigma is a user
     callable, so Alg 3 runs on the host; boxes are created in the reference's order);
   * `fgt_box(tree, values, delta, epsilon, boundary="free")` -> {leaf: u (k,)*d}
     (SPEC.md:512-516): the level tables (J/I moments, poly1d.py:129-210) and schedules are
@@ -206,7 +206,7 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
     grid nodes (one call per refinement level and one for the balance refill); the tree
     decisions (tail test, balance) stay on the host."""
     if refill != "evaluate":
-        # the reference's interpolation refill evaluates at local*0.5 (tree.py:665) and is
+        # the reference's interpolation refill evaluates at local*0.5 (tree.py:482) and is
         # wrong by O(1); only re-evaluation is supported
         raise ValueError("only refill='evaluate' is supported")
     rc = np.zeros(dim) if root_center is None else np.asarray(root_center, float)

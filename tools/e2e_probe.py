@@ -2,10 +2,10 @@
 import os, sys, time, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-import bench
+from tools import configs  # noqa: E402
 from paper_2305_07165_b200 import fgt_points, _lib
 from paper_2305_07165_b200 import point_fgt as pf
-y, q, x = bench.gen_config2(10**6, 10**6)
+y, q, x = configs.config2(10**6, 10**6)
 hy, hq, hx = (torch.from_numpy(a).pin_memory().numpy() for a in (y, q, x))
 for i in range(6):
     t0 = time.perf_counter()

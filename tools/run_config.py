@@ -19,34 +19,12 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-CONFIGS = {
-    1: dict(d=2, N=20_000, delta=1e-3, eps=1e-6, n_s=100, boundary="free"),
-    2: dict(d=3, N=1_000_000, delta=1e-4, eps=1e-9, n_s=200, boundary="free"),
-    3: dict(d=2, N=10_000_000, delta=1e-5, eps=1e-8, n_s=100, boundary="periodic"),
-    5: dict(d=3, N=100_000_000, delta=1e-6, eps=1e-6, n_s=256, boundary="free"),
-}
+from tools.configs import CONFIGS  # noqa: E402
+from tools.configs import generate as _generate  # noqa: E402
 
 
 def generate(cfg_id, N):
-    if cfg_id == 1:
-        r = np.random.default_rng(0)
-        y = r.uniform(-0.5, 0.5, (N, 2))
-        return y, r.uniform(-1, 1, N), y.copy()
-    if cfg_id == 2:
-        import bench
-        return bench.gen_config2(N, N)
-    if cfg_id == 3:
-        r = np.random.default_rng(0)
-        y = r.uniform(-0.5, 0.5, (N, 2))
-        q = r.uniform(-1, 1, N)
-        return y, q, np.random.default_rng(1).uniform(-0.5, 0.5, (N, 2))
-    r = np.random.default_rng(0)
-    u = r.standard_normal((N, 3))
-    u /= np.linalg.norm(u, axis=1, keepdims=True)
-    rho = 0.35 + 1e-3 * (r.uniform(size=N) - 0.5)
-    y = rho[:, None] * u
-    q = r.uniform(-1, 1, N)
-    return y, q, np.random.default_rng(1).uniform(-0.5, 0.5, (N, 3))
+    return _generate(cfg_id, N)
 
 
 def main():

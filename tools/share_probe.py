@@ -6,7 +6,7 @@ For each world size P it runs rank r's share (fgt_points_device(..., share=(r, P
 every r on the same GPU, one after another, and reports the per-rank CUDA-event step times.
 The max over ranks is what a P-GPU run of bench.py would measure per step (each rank
 rebuilds the replicated tree and lists, forms the expansions its targets need, and evaluates
-its own targets; there is no data-path collective).  Config-2 input (bench.gen_config2).
+its own targets; there is no data-path collective).  Config-2 input (configs.config2).
 """
 import argparse
 import json
@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-import bench  # noqa: E402
+from tools import configs  # noqa: E402
 from paper_2305_07165_b200 import fgt_points_device  # noqa: E402
 
 
@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--mode", choices=["recompute", "exchange"], default="exchange")
     a = ap.parse_args()
-    y, q, x = bench.gen_config2(a.n, a.n)
+    y, q, x = configs.config2(a.n, a.n)
     dy, dq, dx = (torch.from_numpy(v).cuda() for v in (y, q, x))
     out = {}
     if a.mode == "exchange":
