@@ -514,20 +514,21 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
 
 // u_host (optional): the result's device->host copy is enqueued right behind the scatter,
 // before the phase timings are read (which waits on the stream).
+// FGT_PSI=materialise | fused forces the translate-into-psi-then-evaluate path or the
+// fused translation + evaluation (A/B checks); default: chosen per transform
+static int psi_mode() {
+  const char* e = std::getenv("FGT_PSI");
+  if (e && !std::strcmp(e, "materialise")) return 1;
+  if (e && !std::strcmp(e, "fused")) return 2;
+  return 0;
+}
+
 static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, double* u_host = nullptr) {
   cudaStream_t st = R.st;
   TreeDev& T = R.T;
   PwDev& P = R.P;
   if (T.n_dense > 0) {
-    // psi is produced and consumed in batches of bounded size (<= ~1 GB: one reusable
-    // buffer; larger pool allocations stall the host for tens of ms)
-    const int64_t per = P.NH * 16;
-    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
-    for (int64_t lo = 0; lo < T.n_psi; lo += batch) {
-      const int64_t hi = std::min(T.n_psi, lo + batch);
-      pw_gather(P, T, lo, hi);
-      pw_eval(P, T, R.us.get(), R.NP, lo, hi);
-    }
+    pw_gather_eval(P, T, R.us.get(), R.NP, psi_mode());
     P.phi.release();
     P.psi.release();
   }

@@ -487,6 +487,415 @@ __global__ void __launch_bounds__(GATHER_THREADS, FGT_GATHER_MINB) gather_kernel
   }
 }
 
+// ------------------------------------------------------------------ fused gather + eval
+// psi never reaches HBM: psi_T is consumed only by the evaluation at T's targets
+// (PAPER.md:825-835), so translation and evaluation run in one kernel.
+//
+// Reference point.  The translation phase factors as
+//   e^{i k.(c_T - c_S)} = e^{i k.(c_T - c_ref)} e^{i k.(c_ref - c_S)}
+// for any point c_ref (here the root centre), so with phi'_S = e^{i k.(c_ref - c_S)} phi_S
+// (phi_rephase_kernel, once per P-box) the translation is a plain sum and the target
+// phases are taken from c_ref:
+//   u(x) = Re sum_l e^{i k_l.(x - c_ref)} sum_{S in L_P(T)} phi'_{S,l}.
+// The angles reach |k| |x - c_ref| ~ 1e4 rad, so every phase is formed in double-double
+// (TwoSum / TwoProd) and reduced modulo a two-term 2 pi before the sincos (phase_dd): each
+// factor is exact to ~1 ulp, like the local formulation.  Free space only (periodic image
+// shifts keep the materialising path).
+//
+// One CTA per sibling group (see gather_eval_kernel).  Warp w owns the 8-row x 16-column
+// mode tile (row tile w / CB, column block w % CB) of each chunk of RC = 8 RT stored rows;
+// lane l holds the 4 modes of the DMMA B fragment, row (l >> 2), columns 4 kk + (l & 3).
+// For every member c the lane accumulates S_c = sum_{u serving c} phi'_u in registers
+// (members in halves of 4 for d = 3), each phi'_u read once per group and chunk, and
+// contracts it at once with the member's targets: T1 = E S_c is a complex GEMM tile (3 real
+// DMMAs per complex MAC, Gauss) whose epilogue reduces Re(T1 F) over the warp's 8 rows
+// with F the per-row axis-0/axis-1 factor.  The phase tables come by recurrence from
+// per-target e^{-i (n_f/2) x}, e^{i x}, e^{8 i x}.  Target sums are accumulated per warp in
+// shared memory and combined in a fixed order (no atomics: deterministic).
+constexpr double GE_TWO_PI_HI = 6.283185307179586;
+constexpr int64_t PHI_PAD = 64 * 64 + 64;  // double2 past the expansions (>= RC n_f + 16)
+constexpr double GE_TWO_PI_LO = 2.4492935982947064e-16;
+
+// e^{i m sc (a - b)}, accurate to ~1 ulp for angles up to ~1e8 rad
+__device__ __forceinline__ double2 phase_dd(int m, double sc, double a, double b) {
+  // d = a - b exactly as d_hi + d_lo (TwoSum)
+  const double d_hi = a - b;
+  const double bb = d_hi - a;
+  const double d_lo = (a - (d_hi - bb)) + (-b - bb);
+  // k = m sc exactly as k_hi + k_lo (TwoProd)
+  const double k_hi = (double)m * sc;
+  const double k_lo = fma((double)m, sc, -k_hi);
+  // A = k d in double-double
+  const double p = k_hi * d_hi;
+  const double p_lo = fma(k_hi, d_hi, -p) + (k_hi * d_lo + k_lo * d_hi);
+  const double q = rint(p * (1.0 / GE_TWO_PI_HI));
+  const double r = fma(-q, GE_TWO_PI_HI, p) + (p_lo - q * GE_TWO_PI_LO);
+  double sn, cs;
+  sincos(r, &sn, &cs);
+  return make_double2(cs, sn);
+}
+
+// bp[slot][k][mi] = e^{i (mi - n_f/2) sc (c_ref_k - c_S,k)} for every P-box slot
+template <int D>
+__global__ void box_phase_kernel(const int64_t* __restrict__ dense_ids, int64_t nd,
+                                 const double* __restrict__ center, double3 c_ref, double sc, int n_f,
+                                 double2* __restrict__ bp) {
+  const double cr[3] = {c_ref.x, c_ref.y, c_ref.z};
+  const int64_t n = nd * D * n_f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int mi = (int)(e % n_f);
+    const int k = (int)((e / n_f) % D);
+    const int64_t slot = e / ((int64_t)D * n_f);
+    const int64_t S = dense_ids[slot];
+    bp[e] = phase_dd(mi - n_f / 2, sc, cr[k], center[S * D + k]);
+  }
+}
+
+// phi'_S = e^{i k.(c_ref - c_S)} phi_S in place (stored half spectrum)
+template <int D>
+__global__ void phi_rephase_kernel(double2* __restrict__ phi, int64_t nd, int64_t NH, int n_f, int half,
+                                   const double2* __restrict__ bp) {
+  const int64_t n = nd * NH;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / NH;
+    int64_t rem = e % NH;
+    const double2* b = bp + slot * D * n_f;
+    double2 ph = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      const int idx = (k == 0 && D >= 2) ? half_plane_mi((int)rem, n_f, half) : (int)(rem % n_f);
+      ph = k == D - 1 ? b[k * n_f + idx] : cmul(ph, b[k * n_f + idx]);
+      rem /= n_f;
+    }
+    phi[e] = cmul(ph, phi[e]);
+  }
+}
+
+constexpr int64_t GE_AUTO_MAX_TPG = 128;  // fused path when targets per sibling group <= this
+
+struct GEArgs {
+  const int64_t* psi_ids;
+  const int64_t* tgt_start;
+  const int64_t* tgt_count;
+  const int64_t* pstart;   // (n_psi) first tph slot of the box's targets; -1: not fused
+  const double2* tph;      // (n_ptgt, 3D): per target and axis e^{-i (n_f/2) x}, e^{i x}, e^{8 i x}
+  const double2* phi;      // (n_dense, RH, n_f) rephased expansions phi' (+ PHI_PAD zeros)
+  double* u;               // sorted potentials (accumulated)
+  int64_t NH;
+  int n_f, RH, nh, half, CB, RT, TR;
+};
+
+__host__ __device__ inline int ge_cb(int n_f) { return (n_f + 15) / 16; }
+__host__ __device__ inline int ge_rt(int n_f) { return 8 / ge_cb(n_f) > 0 ? 8 / ge_cb(n_f) : 1; }
+// targets whose phase tables are resident per round (member-aligned 8-target tiles)
+inline int ge_tr(int n_f) { return n_f <= 32 ? 64 : 32; }
+inline size_t ge_smem(int n_f, int D, int RH) {
+  const int CB = ge_cb(n_f), TR = ge_tr(n_f), NREL = 1 << (2 * D);
+  const int ES = CB * 16 + 4, nh = D >= 2 ? n_f / 2 + 1 : 1;
+  return (size_t)TR * ES * sizeof(double2) * 2           // E (last axis), E1 (axis 1)
+         + (size_t)TR * (nh + 1) * sizeof(double2)        // E0 (w x axis-0 factor per plane)
+         + (size_t)8 * TR * sizeof(double)                // s_part: per warp, per target
+         + (size_t)NREL * 8 * sizeof(double)              // u_bc: member masks as 0.0 / 1.0
+         + (size_t)NREL * (sizeof(void*) + sizeof(unsigned) + sizeof(int))  // sources, lists
+         + (size_t)(TR / 8) * 3 * sizeof(int)             // tile list
+         + (size_t)(RH + 64) * sizeof(int);               // row info (padded to whole chunks)
+}
+
+__device__ __forceinline__ double2 cpow(double2 b, int e) {
+  double2 r = make_double2(1.0, 0.0);
+  while (e > 0) {
+    if (e & 1) r = cmul(r, b);
+    b = cmul(b, b);
+    e >>= 1;
+  }
+  return r;
+}
+
+// per fused target and axis: e^{-i (n_f/2) x}, e^{i x}, e^{8 i x}, x = (t - c_ref) sc (phase_dd)
+template <int D>
+__global__ void ge_target_phase_kernel(const int64_t* __restrict__ psi_ids, const int64_t* __restrict__ tgt_start,
+                                       const int64_t* __restrict__ tgt_count, const int64_t* __restrict__ pstart,
+                                       int64_t n_psi, const double* __restrict__ tgt, double3 c_ref, double sc,
+                                       int n_f, double2* __restrict__ tph) {
+  const double cr[3] = {c_ref.x, c_ref.y, c_ref.z};
+  for (int64_t i = blockIdx.x; i < n_psi; i += gridDim.x) {
+    const int64_t p0 = pstart[i];
+    if (p0 < 0) continue;
+    const int64_t T = psi_ids[i];
+    const int64_t t0 = tgt_start[T], n = tgt_count[T];
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double xk = tgt[(t0 + j) * D + k];
+        double2* o = tph + (p0 + j) * 3 * D + 3 * k;
+        o[0] = phase_dd(-(n_f / 2), sc, xk, cr[k]);
+        o[1] = phase_dd(1, sc, xk, cr[k]);
+        o[2] = phase_dd(8, sc, xk, cr[k]);
+      }
+    }
+  }
+}
+
+// One CTA per sibling group.  Per round of <= TR targets (member-aligned 8-target tiles),
+// the targets' phase tables are built once in shared memory (E: last axis; E1: axis 1;
+// E0: pair-weighted axis-0 factor per stored plane), then the CTA sweeps the chunks of
+// RC = 8 RT stored rows: per chunk and member half each warp accumulates S_c for its 8 x 16
+// mode tile (a plain sum of phi' over the sources serving c) and immediately contracts it
+// with the half's target tiles (3-DMMA complex GEMM + row-factor epilogue), adding the
+// target partials into its own s_part row.  No synchronisation inside the sweep; the
+// warps' rows are summed in a fixed order at the end of the round (deterministic).
+template <int D>
+__global__ void __launch_bounds__(256, 2) gather_eval_kernel(
+    GEArgs a, const int64_t* __restrict__ gt_slot, const unsigned* __restrict__ gt_code,
+    const int* __restrict__ gt_nu, const int64_t* __restrict__ gt_out) {
+  constexpr int NSIB = 1 << D;
+  constexpr int NREL = 1 << (2 * D);
+  // Members are processed in halves of MH (d = 3: 4 + 4) so the per-member accumulators
+  // S_c stay in registers at 2 CTAs per SM.
+  constexpr int MH = NSIB < 4 ? NSIB : 4;
+  constexpr int NHALF = NSIB / MH;
+  extern __shared__ double2 sm[];
+  const int CB = a.CB, RT = a.RT, RC = RT * 8, TR = a.TR, NTL = TR / 8;
+  const int n_f = a.n_f, nh = a.nh;
+  const int ES = CB * 16 + 4, FS = nh + 1;
+  double2* sE = sm;                                      // TR x ES: last-axis phases
+  double2* s_e1 = sE + TR * ES;                          // TR x ES: axis-1 phases (d = 3)
+  double2* s_e0 = s_e1 + TR * ES;                        // TR x FS: w x axis-0 phase per plane
+  double* s_part = reinterpret_cast<double*>(s_e0 + TR * FS);     // 8 warps x TR
+  double* u_bc = s_part + 8 * TR;                                   // NREL x 8: member c served
+  const double2** u_ptr = reinterpret_cast<const double2**>(u_bc + NREL * 8);  // NREL
+  unsigned* u_code = reinterpret_cast<unsigned*>(u_ptr + NREL);    // NREL
+  int* u_list = reinterpret_cast<int*>(u_code + NREL);              // NHALF lists, NREL total
+  int* t_mem = u_list + NREL;                                       // NTL: tile member
+  int* t_off = t_mem + NTL;                                         // tile first target
+  int* t_n = t_off + NTL;                                           // tile size
+  int* s_rinfo = t_n + NTL;                                         // n_chunks * RC rows
+  __shared__ int64_t m_cnt[NSIB], m_p0[NSIB], m_t0[NSIB];
+  __shared__ int s_nl[NHALF], s_ntile;
+  const int64_t g = blockIdx.x;
+  const int nu = gt_nu[g];
+  const int n_chunks = (a.RH + RC - 1) / RC;
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    const unsigned code = gt_code[g * NREL + u];
+    u_ptr[u] = a.phi + gt_slot[g * NREL + u] * a.NH;
+    u_code[u] = code;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) u_bc[u * 8 + c] = (c < NSIB && ((code >> c) & 1u)) ? 1.0 : 0.0;
+  }
+  for (int r = threadIdx.x; r < n_chunks * RC; r += blockDim.x) {
+    int info = -1;
+    if (r < a.RH) {
+      const int s = D == 3 ? r / n_f : r;
+      const int i1 = D == 3 ? r % n_f : 0;
+      info = (D >= 2 ? s : 0) | (i1 << 8);
+    }
+    s_rinfo[r] = info;
+  }
+  if (threadIdx.x < NSIB) {
+    const int c = threadIdx.x;
+    const int64_t i = gt_out[g * NSIB + c];
+    const int64_t ps = i >= 0 ? a.pstart[i] : -1;
+    m_cnt[c] = 0;
+    if (ps >= 0) {
+      const int64_t T = a.psi_ids[i];
+      m_cnt[c] = a.tgt_count[T];
+      m_t0[c] = a.tgt_start[T];
+      m_p0[c] = ps;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // compact source list per member half (sources serving no member of a half skipped)
+    int k = 0;
+    for (int h = 0; h < NHALF; ++h) {
+      const int k0 = k;
+      for (int u = 0; u < nu; ++u)
+        if ((u_code[u] >> (h * MH)) & ((1u << MH) - 1u)) u_list[k++] = u;
+      s_nl[h] = k - k0;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nunits = RT * CB;
+  const bool wactive = warp < nunits;
+  const int rt = wactive ? warp / CB : 0, cb = wactive ? warp % CB : 0;
+  const int rloc = rt * 8 + (lane >> 2);
+  const int col0 = cb * 16 + (lane & 3);
+  int pc = 0;
+  int64_t poff = 0;
+  for (;;) {
+    // ---- round: list <= NTL member-aligned tiles, build their phase tables once
+    __syncthreads();  // the previous round is done with tables, tile list and s_part
+    if (threadIdx.x == 0) {
+      int nt = 0;
+      while (nt < NTL && pc < NSIB) {
+        if (poff >= m_cnt[pc]) { ++pc; poff = 0; continue; }
+        t_mem[nt] = pc;
+        t_off[nt] = (int)poff;
+        t_n[nt] = (int)min((int64_t)8, m_cnt[pc] - poff);
+        poff += 8;
+        ++nt;
+      }
+      s_ntile = nt;
+    }
+    __syncthreads();
+    const int ntile = s_ntile;
+    if (ntile == 0) break;
+    {
+      const int nseg = 2 * CB;
+      const int nE = TR * nseg, nE1 = D == 3 ? TR * nseg : 0, nE0 = D >= 2 ? TR : 0;
+      for (int task = threadIdx.x; task < nE + nE1 + nE0; task += blockDim.x) {
+        int tt = task, kind = 0;
+        if (tt >= nE) { tt -= nE; kind = 1; if (tt >= nE1) { tt -= nE1; kind = 2; } }
+        const int slot = kind == 2 ? tt : tt / nseg, seg = kind == 2 ? 0 : tt % nseg;
+        const int j = slot >> 3, k = slot & 7;
+        const bool have = j < ntile && k < t_n[j];
+        const double2* tp = have ? a.tph + (m_p0[t_mem[j]] + t_off[j] + k) * 3 * D : nullptr;
+        if (kind < 2) {
+          double2* out = (kind == 0 ? sE : s_e1) + slot * ES + seg * 8;
+          if (!have) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) out[q] = make_double2(0.0, 0.0);
+            continue;
+          }
+          const int ax = kind == 0 ? D - 1 : 1;
+          double2 v = tp[3 * ax];
+          const double2 st = tp[3 * ax + 1], st8 = tp[3 * ax + 2];
+          for (int q = 0; q < seg; ++q) v = cmul(v, st8);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            out[q] = seg * 8 + q < n_f ? v : make_double2(0.0, 0.0);
+            v = cmul(v, st);
+          }
+        } else {
+          // stored plane s: mode m_0 = s (s < n_f/2, weight 2 unless s = 0) or -n_f/2
+          double2* out = s_e0 + slot * FS;
+          if (!have) {
+            for (int q = 0; q < nh; ++q) out[q] = make_double2(0.0, 0.0);
+            continue;
+          }
+          double2 v = make_double2(1.0, 0.0);
+          const double2 st = tp[1];
+          for (int q = 0; q < nh; ++q) {
+            const int mi = half_plane_mi(q, n_f, a.half);
+            const double w = half_plane_w(q, n_f, a.half);
+            const double2 e = mi - n_f / 2 == q ? v : cmul(tp[0], cpow(st, mi));
+            out[q] = make_double2(w * e.x, w * e.y);
+            v = cmul(v, st);
+          }
+        }
+      }
+      for (int i = threadIdx.x; i < 8 * TR; i += blockDim.x) s_part[i] = 0.0;
+    }
+    __syncthreads();
+    // ---- sweep over the mode chunks (no block synchronisation inside)
+    if (wactive) {
+#pragma unroll 1
+      for (int chunk = 0; chunk < n_chunks; ++chunk) {
+        const int64_t r = (int64_t)chunk * RC + rloc;
+        // columns >= n_f read the next row, rows >= RH the next expansion or the zeroed pad:
+        // finite values that meet zero table entries / zero row factors below
+        const int64_t lane_off = r * n_f + col0;
+        int lbase = 0;
+#pragma unroll 1
+        for (int hf = 0; hf < NHALF; ++hf) {
+          const int cbase = hf * MH;
+          const int nl = s_nl[hf];
+          const int* lst = u_list + lbase;
+          lbase += nl;
+          bool any = false;
+          for (int j = 0; j < ntile; ++j) any |= (t_mem[j] >= cbase && t_mem[j] < cbase + MH);
+          if (!any) continue;
+          double2 S[MH][4];
+#pragma unroll
+          for (int c = 0; c < MH; ++c)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) S[c][kk] = make_double2(0.0, 0.0);
+          // phi' fragments double-buffered one source ahead (ping-pong)
+          auto load = [&](int q, double2 (&f)[4]) {
+            const double2* p = u_ptr[lst[q < nl ? q : nl - 1]] + lane_off;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) f[kk] = p[4 * kk];
+          };
+          auto accumulate = [&](int q, const double2 (&f)[4]) {
+            const double* bcu = u_bc + lst[q] * 8 + cbase;
+#pragma unroll
+            for (int c = 0; c < MH; ++c) {
+              const double bc = bcu[c];
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                S[c][kk].x = fma(bc, f[kk].x, S[c][kk].x);
+                S[c][kk].y = fma(bc, f[kk].y, S[c][kk].y);
+              }
+            }
+          };
+          if (nl > 0) {
+            double2 fa[4], fb[4];
+            load(0, fa);
+#pragma unroll 1
+            for (int q = 0; q < nl; q += 2) {
+              load(q + 1, fb);
+              accumulate(q, fa);
+              if (q + 1 >= nl) break;
+              load(q + 2, fa);
+              accumulate(q + 1, fb);
+            }
+          }
+          // contract with the half's target tiles
+#pragma unroll 1
+          for (int j = 0; j < ntile; ++j) {
+            const int c = t_mem[j] - cbase;
+            if (c < 0 || c >= MH) continue;
+            double2 B[4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) B[kk] = S[0][kk];
+#pragma unroll
+            for (int cc = 1; cc < MH; ++cc)
+              if (cc == c) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) B[kk] = S[cc][kk];
+              }
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            const double2* arow = sE + (j * 8 + (lane >> 2)) * ES + col0;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const double2 A = arow[kk * 4];
+              const double2 Bk = B[kk];
+              dmma(acc[0][0], acc[0][1], A.x + A.y, Bk.x);
+              dmma(acc[1][0], acc[1][1], A.x, Bk.y - Bk.x);
+              dmma(acc[2][0], acc[2][1], A.y, Bk.x + Bk.y);
+            }
+            double part = 0.0;
+            const int tslot = j * 8 + (lane >> 2);
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) {
+              const int inf = s_rinfo[chunk * RC + rt * 8 + 2 * (lane & 3) + i2];
+              double2 F = make_double2(0.0, 0.0);  // rows past RH hold unrelated finite data
+              if (inf >= 0) {
+                F = D >= 2 ? s_e0[tslot * FS + (inf & 255)] : make_double2(1.0, 0.0);
+                if (D == 3) F = cmul(F, s_e1[tslot * ES + (inf >> 8)]);
+              }
+              const double re = acc[0][i2] - acc[2][i2], im = acc[0][i2] + acc[1][i2];
+              part += re * F.x - im * F.y;
+            }
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if ((lane & 3) == 0) s_part[warp * TR + tslot] += part;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- the round's targets: warps' partials summed in a fixed order
+    for (int slot = threadIdx.x; slot < ntile * 8; slot += blockDim.x) {
+      const int j = slot >> 3, k = slot & 7;
+      if (k >= t_n[j]) continue;
+      double sum = 0.0;
+      for (int w = 0; w < nunits; ++w) sum += s_part[w * TR + slot];
+      a.u[m_t0[t_mem[j]] + t_off[j] + k] += sum;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ eval
 struct EvalArgs {
   const double* tgt;      // sorted targets
@@ -807,9 +1216,11 @@ template <int D>
 static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   cudaStream_t st = T.st;
   const int64_t nd = T.n_dense;
-  P.phi.alloc((size_t)nd * P.NH * 2, st);
-  if (nd == 0) return;
+  // + PHI_PAD zeroed double2 past the last expansion: the fused translation kernel reads
+  // whole 8 x 16 mode tiles without bounds checks (columns >= n_f, rows >= RH)
+  P.phi.alloc((size_t)nd * P.NH * 2 + 2 * PHI_PAD, st);
   P.phi.zero();
+  if (nd == 0) return;
   // per-box source counts -> work units of at most KU points (split-K for big boxes)
   const std::vector<int64_t>& cnt = P.h_src;
   const int KU = 2048;
@@ -958,7 +1369,8 @@ void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi) {
   P.k_gather.end(st);
 }
 
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi) {
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi,
+             bool nufft_only) {
   if (hi == lo) return;
   cudaStream_t st = T.st;
   std::vector<int64_t> direct_list, spread_list;
@@ -967,12 +1379,13 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
     const int64_t n = hi - lo;
     const int64_t* h = h_cnt_all;
     for (int64_t i = 0; i < n; ++i) {
-      P.n_tgt_psi += h[i];
       if (prefer_nufft(N, T.d, P.NH, h[i], 2.0)) {
         spread_list.push_back(lo + i);
         P.n_tgt_spread += h[i];
-      } else {
+        P.n_tgt_psi += h[i];
+      } else if (!nufft_only) {
         direct_list.push_back(lo + i);
+        P.n_tgt_psi += h[i];
       }
     }
   }
@@ -1032,6 +1445,129 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
   else { FGT_EVAL_D(3) }
   P.k_eval.end(st);
 #undef FGT_EVAL_D
+}
+
+void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int mode) {
+  const int64_t n = T.n_psi;
+  if (n == 0) return;
+  cudaStream_t st = T.st;
+  // psi boxes evaluated by the NUFFT interpolation path (many targets) need psi itself:
+  // they keep the materialising path (gather into <= 1 GB batches + nufft_eval); every
+  // other box is translated and evaluated by the fused kernel (psi stays on chip)
+  std::vector<int64_t> pstart(n, -1);
+  int64_t np = 0;
+  bool any_nufft = false;
+  for (int64_t i = 0; i < n; ++i) {
+    if (prefer_nufft(N, T.d, P.NH, P.h_cnt[i], 2.0)) {
+      any_nufft = true;
+    } else {
+      pstart[i] = np;
+      np += P.h_cnt[i];
+    }
+  }
+  // The fused kernel rebuilds its targets' phase tables for every mode chunk and pays the
+  // translation once per (group, chunk): it wins when sibling groups hold few targets
+  // (config 5: ~40, where psi would be ~98 GB of HBM traffic).  With hundreds of targets
+  // per group the per-chunk tables dominate and a materialised psi (<= 1 GB batches) is
+  // cheaper to stream: those transforms keep the gather + eval path.
+  const int64_t n_groups_all = (int64_t)P.h_goff.size() - 1;
+  if (mode == 0 && np > GE_AUTO_MAX_TPG * std::max<int64_t>(1, n_groups_all)) mode = 1;
+  if (T.periodic) mode = 1;  // image shifts: the rephased sum needs v = 0
+  if (mode == 1) {
+    const int64_t per = P.NH * 16;
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
+    for (int64_t lo = 0; lo < n; lo += batch) {
+      const int64_t hi = std::min(n, lo + batch);
+      pw_gather(P, T, lo, hi);
+      pw_eval(P, T, u_sorted, N, lo, hi);
+    }
+    P.psi.release();
+    return;
+  }
+  if (any_nufft) {
+    const int64_t per = P.NH * 16;
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
+    for (int64_t lo = 0; lo < n; lo += batch) {
+      const int64_t hi = std::min(n, lo + batch);
+      pw_gather(P, T, lo, hi);
+      pw_eval(P, T, u_sorted, N, lo, hi, /*nufft_only=*/true);
+    }
+    P.psi.release();
+  }
+  if (np == 0) return;
+  P.n_tgt_psi += np;
+  const int n_f = P.n_f;
+  const int CB = ge_cb(n_f), RT = ge_rt(n_f), TR = ge_tr(n_f);
+  const std::vector<int64_t>& goff = P.h_goff;
+  const int64_t n_groups = (int64_t)goff.size() - 1;
+  const int nrel = 1 << (2 * T.d), nsib = 1 << T.d;
+  DBuf<int64_t> pstart_d(n, st), goff_d(goff.size(), st);
+  pstart_d.from_host(pstart.data(), n);
+  goff_d.from_host(goff.data(), goff.size());
+  DBuf<int64_t> gt_slot(n_groups * nrel, st), gt_out(n_groups * nsib, st);
+  DBuf<unsigned> gt_code(n_groups * nrel, st);
+  DBuf<int> gt_nu(n_groups, st);
+  GatherArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  ga.psi_ids = T.psi_ids.get();
+  ga.p_off = T.p_off.get();
+  ga.p_src = T.p_src.get();
+  ga.p_v = T.p_v.get();
+  ga.dense_ids = T.dense_ids.get();
+  ga.coords = T.coords.get();
+  ga.goff = goff_d.get();
+  ga.i0 = 0;
+  ga.n_f = n_f;
+  ga.l_c = T.l_c;
+  DBuf<double> tph((size_t)np * 6 * T.d, st);
+  DBuf<double> bp((size_t)T.n_dense * T.d * n_f * 2, st);
+  GEArgs ea;
+  ea.psi_ids = T.psi_ids.get();
+  ea.tgt_start = T.tgt_start.get();
+  ea.tgt_count = T.tgt_count.get();
+  ea.pstart = pstart_d.get();
+  ea.tph = reinterpret_cast<const double2*>(tph.get());
+  ea.phi = reinterpret_cast<const double2*>(P.phi.get());
+  ea.u = u_sorted;
+  ea.NH = P.NH;
+  ea.n_f = n_f;
+  ea.RH = (int)P.RH;
+  ea.nh = T.d >= 2 ? (int)P.nh : 1;
+  ea.half = P.half;
+  ea.CB = CB;
+  ea.RT = RT;
+  ea.TR = TR;
+  const size_t smem = ge_smem(n_f, T.d, (int)P.RH);
+  FGT_REQUIRE(smem <= 227 * 1024, FGT_ERANGE, "fused translation/evaluation tables exceed shared memory");
+  const double3 cref = make_double3(T.root_center[0], T.root_center[1], T.root_center[2]);
+  P.k_gather.begin(st);
+#define FGT_GE_D(DD)                                                                                   \
+  group_table_kernel<DD><<<(unsigned)n_groups, 64, 0, st>>>(ga, gt_slot.get(), gt_code.get(),          \
+                                                             gt_nu.get(), gt_out.get());               \
+  FGT_LAUNCHED();                                                                                      \
+  box_phase_kernel<DD><<<grid_for(T.n_dense * DD * n_f, 256), 256, 0, st>>>(                          \
+      T.dense_ids.get(), T.n_dense, T.center.get(), cref, P.sc, n_f, reinterpret_cast<double2*>(bp.get())); \
+  FGT_LAUNCHED();                                                                                      \
+  phi_rephase_kernel<DD><<<grid_for(T.n_dense * P.NH, 256), 256, 0, st>>>(                            \
+      reinterpret_cast<double2*>(P.phi.get()), T.n_dense, P.NH, n_f, P.half,                         \
+      reinterpret_cast<const double2*>(bp.get()));                                                    \
+  FGT_LAUNCHED();                                                                                      \
+  P.k_gather.end(st);                                                                                  \
+  P.k_eval.begin(st);                                                                                  \
+  ge_target_phase_kernel<DD><<<grid_for(n, 1, (int64_t)148 * 32), 128, 0, st>>>(                       \
+      T.psi_ids.get(), T.tgt_start.get(), T.tgt_count.get(), pstart_d.get(), n, T.tgt_sorted.get(),    \
+      cref, P.sc, n_f, reinterpret_cast<double2*>(tph.get()));                                         \
+  FGT_LAUNCHED();                                                                                      \
+  FGT_CUDA(cudaFuncSetAttribute(gather_eval_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                (int)smem));                                                           \
+  gather_eval_kernel<DD><<<(unsigned)n_groups, 256, smem, st>>>(ea, gt_slot.get(), gt_code.get(),      \
+                                                               gt_nu.get(), gt_out.get());
+  if (T.d == 1) { FGT_GE_D(1) }
+  else if (T.d == 2) { FGT_GE_D(2) }
+  else { FGT_GE_D(3) }
+#undef FGT_GE_D
+  FGT_LAUNCHED();
+  P.k_eval.end(st);
 }
 
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk) {

@@ -63,7 +63,12 @@ void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N);
 // Diagonal translation phi -> psi over the P-lists.
 void pw_gather(PwDev& P, TreeDev& T, int64_t lo, int64_t hi);
 // Type-2 evaluation of psi at the targets of every psi box; u_sorted += Re(...).
-void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi);
+void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t lo, int64_t hi,
+             bool nufft_only = false);
+// Translation fused with evaluation (psi kept on chip) for every psi box evaluated by the
+// exact sums; boxes routed to the NUFFT interpolation keep the gather + pw_eval path.
+// mode: 0 auto (fused when sibling groups hold few targets), 1 materialise psi, 2 fused.
+void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int mode);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 // Continuous (box) FGT executor (k_volume.cu).

@@ -465,3 +465,30 @@ def test_pencil_spreading_widths_and_splits(cuda, eps, monkeypatch):
     assert t["n_spread_boxes"] > 0 and t["n_src_spread"] > 0
     ex = ofgt.direct_oracle(y, q, x, 1e-4, "free")
     assert rel(u, ex) <= 10 * eps
+
+
+@pytest.mark.parametrize("case", ["clust3d", "periodic2d", "shell", "1d", "periodic3d"])
+def test_fused_translation_eval_matches_materialised_psi(cuda, case, monkeypatch):
+    """Translation fused into evaluation (psi kept on chip, the default) agrees with the
+    translate-into-psi-then-evaluate path to roundoff, free / periodic, d = 1, 2, 3."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(13)
+    if case == "clust3d":
+        y, x, args = clustered(r, 20000, 3), r.uniform(-0.5, 0.5, (20000, 3)), (1e-4, 1e-9, 100, "free")
+    elif case == "periodic2d":
+        y, x, args = r.uniform(-0.5, 0.5, (30000, 2)), r.uniform(-0.5, 0.5, (30000, 2)), (1e-4, 1e-8, 60, "periodic")
+    elif case == "shell":
+        y, x, args = make_points(r, "shell", 30000, 3), r.uniform(-0.5, 0.5, (30000, 3)), (1e-5, 1e-6, 20, "free")
+    elif case == "1d":
+        y, x, args = r.uniform(-0.5, 0.5, (5000, 1)), r.uniform(-0.5, 0.5, (4000, 1)), (1e-4, 1e-9, 30, "free")
+    else:
+        y, x, args = clustered(r, 8000, 3), r.uniform(-0.5, 0.5, (6000, 3)), (1e-3, 1e-6, 40, "periodic")
+    q = r.standard_normal(y.shape[0])
+    monkeypatch.setenv("FGT_NUFFT_MODE", "direct")
+    monkeypatch.setenv("FGT_PSI", "fused")
+    u_fused = fgt_points(y, q, x, *args)
+    monkeypatch.setenv("FGT_PSI", "materialise")
+    u_mat = fgt_points(y, q, x, *args)
+    assert rel(u_fused, u_mat) < 1e-12
+    ex = ofgt.direct_oracle(y, q, x[:1000], args[0], args[3])
+    assert rel(u_fused[:1000], ex) <= 10 * args[1]
