@@ -513,7 +513,7 @@ constexpr size_t PEN_SMEM = PEN_WARPS * PEN_WSMEM;
 
 struct PencilArgs {
   const int4* jobs;  // row jobs: (box * NB + b, first sorted point, count, scratch base or -1)
-  int nitems;        // row jobs x per
+  const int* njobs;  // number of row jobs (device; items = row jobs x per)
   int* counter;      // work-item counter (zeroed before the launch)
   const double* rw;  // sorted records (n, PEN_REC) [q w1 | w2 | w0]
   const int* ra;     // (n, 4) first taps (a_0, a_1, a_2, -)
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
     int item = 0;
     if (lane == 0) item = atomicAdd(a.counter, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= a.nitems) break;
+    if (item >= *a.njobs * a.per) break;
     const int4 jb = a.jobs[item / a.per];
     const int th = item - (item / a.per) * a.per;  // t * nparts + h
     const int t = th / a.nparts, h = th - t * a.nparts;
@@ -730,8 +730,10 @@ __global__ void __launch_bounds__(PEN_WARPS * 32, 5) spread_pencil_kernel(Pencil
 // partial pencils of K-split (box, b) ranges: red = (box * NB + b, first scratch, chunks, -);
 // chunk k's pencil (t, h) is scratch[first + k * NB * nparts + t * nparts + h]; summed in
 // chunk order (deterministic) and scattered into the grid
-__global__ void pencil_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red, int NB,
-                                     int nparts, int PH, int G, double* __restrict__ grid) {
+__global__ void pencil_reduce_kernel(const double* __restrict__ scratch, const int4* __restrict__ red,
+                                     const int* __restrict__ nred, int NB, int nparts, int PH, int G,
+                                     double* __restrict__ grid) {
+  if ((int)blockIdx.y >= *nred) return;  // launched for the host's upper bound
   const int4 rd = red[blockIdx.y];
   const int th = blockIdx.z, t = th / nparts, h = th - t * nparts;
   const int box = rd.x / NB, b = rd.x - box * NB;
@@ -746,6 +748,70 @@ __global__ void pencil_reduce_kernel(const double* __restrict__ scratch, const i
     for (int k = 0; k < rd.z; ++k) s += src[k * stride];
     grid[(int64_t)box * G * G * G + ((int64_t)(P0 + pl) * G + gr) * G + gc] = s;
   }
+}
+
+// Pencil job list on the device (no host round trip): per row job (box, row block) with
+// n points, nc = max(1, ceil(n / PCH)) chunks; row jobs split in more than one chunk keep
+// partial pencils in scratch (per slots each) and get a reduce entry.  One CTA scans the
+// row jobs in tiles of 1024; outputs the unsorted chunk list with sort keys PCH - count
+// (largest chunks first after a stable ascending sort; padding up to the host's bound sorts
+// last) and counts[0] = chunks, counts[1] = reduce entries.
+__global__ void __launch_bounds__(1024) pencil_jobs_kernel(const int* __restrict__ range, int njob, int PCH,
+                                                          int per, int bound, int4* __restrict__ jobs_tmp,
+                                                          uint64_t* __restrict__ key, int64_t* __restrict__ val,
+                                                          int4* __restrict__ reds, int* __restrict__ counts) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int carry[3];
+  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (int base = 0; base < njob; base += 1024) {
+    const int jid = base + (int)threadIdx.x;
+    int n = 0, lo = 0, nc = 0, red = 0;
+    if (jid < njob) {
+      lo = range[2 * jid];
+      n = range[2 * jid + 1] - lo;
+      nc = n <= PCH ? 1 : (n + PCH - 1) / PCH;
+      red = n > PCH;
+    }
+    int o_job, o_red, o_scr, t_job, t_red, t_scr;
+    Scan(ts).ExclusiveSum(nc, o_job, t_job);
+    __syncthreads();
+    Scan(ts).ExclusiveSum(red, o_red, t_red);
+    __syncthreads();
+    Scan(ts).ExclusiveSum(red ? nc * per : 0, o_scr, t_scr);
+    const int cj = carry[0], cr = carry[1], cs = carry[2];
+    if (jid < njob) {
+      for (int c = 0; c < nc; ++c) {
+        const int idx = cj + o_job + c, len = min(PCH, n - c * PCH);
+        jobs_tmp[idx] = make_int4(jid, lo + c * PCH, max(0, len), red ? cs + o_scr + c * per : -1);
+        key[idx] = (uint64_t)(PCH - max(0, len));
+        val[idx] = idx;
+      }
+      if (red) reds[cr + o_red] = make_int4(jid, cs + o_scr, nc, 0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry[0] = cj + t_job;
+      carry[1] = cr + t_red;
+      carry[2] = cs + t_scr;
+    }
+    __syncthreads();
+  }
+  for (int idx = carry[0] + (int)threadIdx.x; idx < bound; idx += blockDim.x) {
+    key[idx] = (uint64_t)(PCH + 1);
+    val[idx] = idx;
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = carry[0];
+    counts[1] = carry[1];
+  }
+}
+
+__global__ void gather_jobs_kernel(const int4* __restrict__ tmp, const int64_t* __restrict__ perm,
+                                   const int* __restrict__ counts, int4* __restrict__ jobs) {
+  const int n = counts[0];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) jobs[i] = tmp[perm[i]];
 }
 
 // d = 1: one warp per (box, cell) job sums c w0[p - a0] over its points
@@ -1142,7 +1208,7 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   const int64_t job_cells = D == 3 ? plane : (D == 2 ? GD : 1);
   CubTmpBuf tmp;
   // per-batch work buffers, allocated once for the largest batch (GrowBuf)
-  GrowBuf<int64_t> g_sl, g_boff, g_iota, g_perm;
+  GrowBuf<int64_t> g_sl, g_boff, g_iota, g_perm, g_perm2;
   GrowBuf<double> g_wts, g_tt, g_qb, g_rw, g_rq, g_rw0, g_grid, g_scratch, g_t1, g_t2;
   GrowBuf<int> g_ai, g_ra, g_range;
   GrowBuf<uint64_t> g_key, g_skey;
@@ -1230,44 +1296,44 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
     auto range = g_range.view(2 * njob, st);
     job_ranges_kernel<D><<<grid_for(njob, 256), 256, 0, st>>>(skey.get(), npts, nbat, G, w, range.get());
     FGT_LAUNCHED();
-    std::vector<int> hr(2 * njob);
     trace_mark(st, "form:taps+sort");
-    range.to_host(hr.data(), hr.size());
-    FGT_CUDA(cudaStreamSynchronize(st));
-    trace_mark(st, "form:ranges(sync)");
-    std::vector<int4> jobs, reds;
-    int nscr = 0;
     if constexpr (D == 3) {
-      // pencil jobs: one per (box, b, chunk of <= PCH scanned points), x NB columns x parts
+      // pencil jobs: one per (box, b, chunk of <= PCH scanned points), x NB columns x parts,
+      // built on the device (pencil_jobs_kernel) -- no host round trip.  Host-side bounds from
+      // the per-box source counts: only boxes with > PCH points can split a row job.
       const int nparts = (G + PEN_PH - 1) / PEN_PH, PH = (G + nparts - 1) / nparts;
       const int per = NBP * nparts, PCH = 4096;
-      for (int64_t jid = 0; jid < njob; ++jid) {
-        const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
-        if (n <= PCH) {
-          jobs.push_back(make_int4((int)jid, lo, n, -1));
-        } else {
-          const int nc = (n + PCH - 1) / PCH;
-          reds.push_back(make_int4((int)jid, nscr, nc, 0));
-          for (int c = 0; c < nc; ++c) {
-            jobs.push_back(make_int4((int)jid, lo + c * PCH, std::min(PCH, n - c * PCH), nscr));
-            nscr += per;
-          }
+      int64_t extra = 0, red_bound = 0;
+      for (int64_t b = 0; b < nbat; ++b) {
+        const int64_t c = scount[slots[b0 + b]];
+        if (c > PCH) {
+          extra += NBP * ((c + PCH - 1) / PCH);
+          red_bound += NBP;
         }
       }
-      // largest row jobs first (the persistent warps take items in order)
-      std::stable_sort(jobs.begin(), jobs.end(), [](const int4& x, const int4& y) { return x.z > y.z; });
-      auto jobs_d = g_jobs.view(jobs.size(), st);
-      auto reds_d = g_reds.view(reds.size(), st);
-      jobs_d.from_host(jobs.data(), jobs.size());
-      if (!reds.empty()) reds_d.from_host(reds.data(), reds.size());
+      const int64_t job_bound = njob + extra;
+      FGT_REQUIRE(job_bound < ((int64_t)1 << 30) / per, FGT_ERANGE, "too many pencil jobs");
+      auto jobs_tmp = g_jobs.view(2 * job_bound, st);
+      int4* jobs_sorted = jobs_tmp.get() + job_bound;
+      auto reds_d = g_reds.view(std::max<int64_t>(1, red_bound), st);
+      auto jkey = g_key.view(std::max<int64_t>(npts, 2 * job_bound), st);  // key/skey reused
+      auto jval = g_iota.view(std::max<int64_t>(npts, job_bound), st);
+      auto jperm = g_perm2.view(job_bound, st);
+      auto counts = g_counter.view(3, st);
+      pencil_jobs_kernel<<<1, 1024, 0, st>>>(range.get(), (int)njob, PCH, per, (int)job_bound, jobs_tmp.get(),
+                                             jkey.get(), jval.get(), reds_d.get(), counts.get());
+      FGT_LAUNCHED();
+      sort_pairs_key(tmp, jkey.get(), jkey.get() + job_bound, jval.get(), jperm.get(), job_bound, 14, st);
+      gather_jobs_kernel<<<grid_for(job_bound, 256), 256, 0, st>>>(jobs_tmp.get(), jperm.get(), counts.get(),
+                                                                   jobs_sorted);
+      FGT_LAUNCHED();
       auto grid = g_grid.view(nbat * GD, st);
-      auto scratch = g_scratch.view((int64_t)nscr * PEN_PH * 64, st);
-      auto counter = g_counter.view(1, st);
-      FGT_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(int), st));
+      auto scratch = g_scratch.view(std::max<int64_t>(1, extra * per) * PEN_PH * 64, st);
+      FGT_CUDA(cudaMemsetAsync(counts.get() + 2, 0, sizeof(int), st));
       PencilArgs pa;
-      pa.jobs = jobs_d.get();
-      pa.nitems = (int)jobs.size() * per;
-      pa.counter = counter.get();
+      pa.jobs = jobs_sorted;
+      pa.njobs = counts.get();
+      pa.counter = counts.get() + 2;
       pa.rw = rw.get();
       pa.ra = ra.get();
       pa.grid = grid.get();
@@ -1293,10 +1359,10 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
     }                                                                                                        \
     const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm),       \
-                                                        ((int64_t)pa.nitems + PEN_WARPS - 1) / PEN_WARPS));           \
+                                                        (job_bound * per + PEN_WARPS - 1) / PEN_WARPS));              \
     spread_pencil_kernel<NPL><<<nblk, PEN_WARPS * 32, PEN_SMEM, st>>>(pa);                                   \
   }
-      if (!jobs.empty()) {
+      {
         FGT_REQUIRE(w >= 2, FGT_ERANGE, "kernel width < 2");  // zero band >= NPL - w
         if (w <= 5) FGT_PEN(8)
         else if (w <= 9) FGT_PEN(12)
@@ -1304,15 +1370,21 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
         FGT_LAUNCHED();
       }
 #undef FGT_PEN
-      if (!reds.empty()) {
-        pencil_reduce_kernel<<<dim3(1, (unsigned)reds.size(), (unsigned)per), 256, 0, st>>>(
-            scratch.get(), reds_d.get(), NBP, nparts, PH, G, grid.get());
+      if (red_bound > 0) {
+        pencil_reduce_kernel<<<dim3(1, (unsigned)red_bound, (unsigned)per), 256, 0, st>>>(
+            scratch.get(), reds_d.get(), counts.get() + 1, NBP, nparts, PH, G, grid.get());
         FGT_LAUNCHED();
       }
       form_modes<D>(N, P, grid.get(), sl_d.get(), nbat, g_t1, g_t2, st);
       b0 += nbat;
       continue;
     }
+    std::vector<int> hr(2 * njob);
+    range.to_host(hr.data(), hr.size());
+    FGT_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "form:ranges(sync)");
+    std::vector<int4> jobs, reds;
+    int nscr = 0;
     for (int64_t jid = 0; jid < njob; ++jid) {
       const int lo = hr[2 * jid], n = hr[2 * jid + 1] - lo;
       if (n <= CH) {
