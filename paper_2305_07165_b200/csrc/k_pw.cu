@@ -1056,6 +1056,7 @@ struct DirectArgs {
   int64_t n;
 };
 
+// CTA-per-target-leaf near field (128 lanes = targets): for leaves holding many targets.
 template <int D>
 __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
   constexpr int TILE = 128;
@@ -1104,6 +1105,75 @@ __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
         }
       }
       if (valid) a.u[t0 + j] += acc;
+    }
+  }
+}
+
+// Warp-per-target-leaf near field: lane = target (chunks of 32 targets), sources of each
+// D-list box staged 32 at a time in the warp's shared-memory slice (coalesced loads, image
+// shift applied) and read back as broadcasts.  Leaves are taken from a global counter, so a
+// leaf with 6 targets occupies one warp instead of a 128-thread CTA; every target is summed
+// by one lane in list order (deterministic).
+template <int D>
+__global__ void __launch_bounds__(256) direct_warp_kernel(DirectArgs a, int* __restrict__ counter) {
+  __shared__ double s_y[8][32 * D];
+  __shared__ double s_q[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sy = s_y[warp];
+  double* sq = s_q[warp];
+  for (;;) {
+    int64_t i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= a.n) break;
+    const int64_t T = a.d_tgt_ids[i];
+    const int64_t e0 = a.d_off[i], e1 = a.d_off[i + 1];
+    if (e0 == e1) continue;
+    const int64_t t0 = a.tgt_start[T];
+    const int ntg = (int)a.tgt_count[T];
+    // leaves with <= 16 targets: NS = 32 / TW lanes share a target, each summing every NS-th
+    // staged source; the lanes' partials meet in a fixed shuffle tree (deterministic)
+    int TW = 32;
+    while (TW > 1 && TW / 2 >= ntg) TW >>= 1;
+    const int NS = 32 / TW, split = lane / TW;
+    for (int tb = 0; tb < ntg; tb += TW) {
+      const int j = tb + lane % TW;
+      const bool valid = j < ntg;
+      double x[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = valid ? a.tgt[(t0 + j) * D + k] : 0.0;
+      double acc = 0.0;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t S = a.d_src[e];
+        const int64_t s0 = a.src_start[S];
+        const int nsrc = (int)a.src_count[S];
+        double shift[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) shift[k] = (double)a.d_v[e * D + k] * a.root_side;
+        for (int sb = 0; sb < nsrc; sb += 32) {
+          const int nj = min(32, nsrc - sb);
+          __syncwarp();
+          if (lane < nj) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) sy[lane * D + k] = a.src[(s0 + sb + lane) * D + k] + shift[k];
+            sq[lane] = a.q[s0 + sb + lane];
+          }
+          __syncwarp();
+          if (valid) {
+            for (int t = split; t < nj; t += NS) {
+              double r2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; ++k) {
+                const double df = x[k] - sy[t * D + k];
+                r2 += df * df;
+              }
+              if (r2 <= a.r2_cut) acc += exp(-r2 * a.inv_delta) * sq[t];
+            }
+          }
+        }
+      }
+      for (int o = TW; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (valid && split == 0) a.u[t0 + j] += acc;
     }
   }
 }
@@ -1590,11 +1660,27 @@ void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted,
   da.r2_cut = r2_cut;
   da.root_side = T.root_side;
   da.n = T.n_dtgt;
-  unsigned g = (unsigned)std::min<int64_t>(T.n_dtgt, 148 * 16);
+  int dev = 0, nsm = 0;
+  FGT_CUDA(cudaGetDevice(&dev));
+  FGT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  // persistent warps (8 per CTA, up to 8 CTAs per SM) taking target leaves from a counter
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((T.n_dtgt + 7) / 8, (int64_t)nsm * 8));
+  DBuf<int> counter(1, st);
+  counter.zero();
   if (clk) clk->begin(st);
-  if (T.d == 1) direct_kernel<1><<<g, 128, 0, st>>>(da);
-  else if (T.d == 2) direct_kernel<2><<<g, 128, 0, st>>>(da);
-  else direct_kernel<3><<<g, 128, 0, st>>>(da);
+  // leaves of a few dozen targets (config 5: ~40 per leaf): a warp each; leaves holding
+  // hundreds (dense clusters): a 128-thread CTA each
+  const bool small = T.n_leaves > 0 && T.nt <= 48 * T.n_leaves;
+  if (small) {
+    if (T.d == 1) direct_warp_kernel<1><<<g, 256, 0, st>>>(da, counter.get());
+    else if (T.d == 2) direct_warp_kernel<2><<<g, 256, 0, st>>>(da, counter.get());
+    else direct_warp_kernel<3><<<g, 256, 0, st>>>(da, counter.get());
+  } else {
+    const unsigned gc = (unsigned)std::min<int64_t>(T.n_dtgt, (int64_t)nsm * 16);
+    if (T.d == 1) direct_kernel<1><<<gc, 128, 0, st>>>(da);
+    else if (T.d == 2) direct_kernel<2><<<gc, 128, 0, st>>>(da);
+    else direct_kernel<3><<<gc, 128, 0, st>>>(da);
+  }
   FGT_LAUNCHED();
   if (clk) clk->end(st);
 }
