@@ -29,26 +29,31 @@ struct GemmArgs {
 
 // CTA tile 32 x 48 (2 x 2 warps of 16 x 24); FLAT: 16 x 96 (1 x 4 warps) for M <= 16, so
 // a 16-row problem (e.g. the nh = 16 stored planes of config 5) wastes no DMMA rows
-template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false, bool TALL = false>
+template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false, bool TALL = false, bool MID = false>
 __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TALL (N <= 32): 64 x 32 (4 x 1 warps of 16 x 32, four 8-column tiles per warp)
-  constexpr int NT = TALL ? 4 : 3;
-  const int wm = FLAT ? 0 : (TALL ? warp : warp >> 1), wn = FLAT ? warp : (TALL ? 0 : warp & 1);
+  // MID (M <= 32, 32 < N <= 40, e.g. the n_f x G axis-1 stage of a G = 33 grid): 32 x 40
+  // (2 x 1 warps of 16 x 40, five 8-column tiles per warp; 64 threads)
+  constexpr int NT = MID ? 5 : (TALL ? 4 : 3);
+  const int wm = FLAT ? 0 : ((TALL || MID) ? warp : warp >> 1), wn = FLAT ? warp : ((TALL || MID) ? 0 : warp & 1);
   const int64_t b = blockIdx.z + g.boff;
   const int m0 = blockIdx.y * (FLAT ? 16 : (TALL ? 64 : 32)) + wm * 16;
-  const int n0 = blockIdx.x * (FLAT ? 96 : (TALL ? 32 : 48)) + wn * 24;
+  const int n0 = blockIdx.x * (FLAT ? 96 : (TALL ? 32 : (MID ? 40 : 48))) + wn * 24;
   const double* A = g.A + (g.aidx ? g.aidx[b] : b) * g.sA * (AC ? 2 : 1);
   const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
   const int64_t cb = g.cidx ? g.cidx[b] : b;
   double* C = g.C + cb * g.sC * (CRE ? 1 : 2);
   double acc[2][NT][4];
+  double gauss[2][NT][2];  // k3 of the 3-product complex MAC (AC && BC && !CRE; not TALL: registers)
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+    for (int j = 0; j < NT; ++j) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+      gauss[i][j][0] = gauss[i][j][1] = 0.0;
+    }
   for (int k0 = 0; k0 < g.K; k0 += 4) {
     const int k = k0 + (lane & 3);
     double ar[2], ai[2], br[NT], bi[NT];
@@ -80,6 +85,28 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
         }
       }
     }
+    if (AC && BC && !CRE && !TALL) {
+      // complex x complex in three real products (Gauss): k1 = (ar + ai) br,
+      // k2 = ar (bi - br), k3 = ai (br + bi); re = k1 - k3, im = k1 + k2, accumulated as
+      // acc[0..1] = k1, acc[2..3] = k2, gauss[..] = k3 and combined in the epilogue
+      double bd[NT], bs[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        bd[nt] = bi[nt] - br[nt];
+        bs[nt] = br[nt] + bi[nt];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double as = ar[mt] + ai[mt];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma2(acc[mt][nt][0], acc[mt][nt][1], as, br[nt]);
+          dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bd[nt]);
+          dmma2(gauss[mt][nt][0], gauss[mt][nt][1], ai[mt], bs[nt]);
+        }
+      }
+      continue;
+    }
     // re += ar br - ai bi ; im += ar bi + ai br   (terms with a real operand vanish)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -105,6 +132,18 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
           for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
       }
     }
+  }
+  if (AC && BC && !CRE && !TALL) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double k1 = acc[mt][nt][i], k2 = acc[mt][nt][2 + i], k3 = gauss[mt][nt][i];
+          acc[mt][nt][i] = k1 - k3;
+          acc[mt][nt][2 + i] = k1 + k2;
+        }
   }
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
@@ -141,6 +180,8 @@ void bgemm(const GemmArgs& g, cudaStream_t st) {
       bgemm_kernel<AC, BC, CRE, ACC, true><<<dim3((g.N + 95) / 96, 1, nz), 128, 0, st>>>(c);
     } else if (g.N <= 32) {
       bgemm_kernel<AC, BC, CRE, ACC, false, true><<<dim3(1, (g.M + 63) / 64, nz), 128, 0, st>>>(c);
+    } else if (g.M <= 32 && g.N <= 40) {
+      bgemm_kernel<AC, BC, CRE, ACC, false, false, true><<<dim3(1, 1, nz), 64, 0, st>>>(c);
     } else {
       bgemm_kernel<AC, BC, CRE, ACC><<<dim3((g.N + 47) / 48, (g.M + 31) / 32, nz), 128, 0, st>>>(c);
     }

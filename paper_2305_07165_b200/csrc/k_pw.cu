@@ -551,23 +551,30 @@ __global__ void box_phase_kernel(const int64_t* __restrict__ dense_ids, int64_t 
   }
 }
 
-// phi'_S = e^{i k.(c_ref - c_S)} phi_S in place (stored half spectrum)
+// phi'_S = e^{i k.(c_ref - c_S)} phi_S in place (stored half spectrum): one CTA per P-box
+// slot; the separable phase is a row factor (axes < d-1, from shared memory) times a
+// column factor (last axis, one per thread), two complex products per mode.
 template <int D>
-__global__ void phi_rephase_kernel(double2* __restrict__ phi, int64_t nd, int64_t NH, int n_f, int half,
-                                   const double2* __restrict__ bp) {
-  const int64_t n = nd * NH;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t slot = e / NH;
-    int64_t rem = e % NH;
+__global__ void __launch_bounds__(256) phi_rephase_kernel(double2* __restrict__ phi, int64_t nd, int64_t NH,
+                                                          int n_f, int RH, int half,
+                                                          const double2* __restrict__ bp) {
+  extern __shared__ double2 s_row[];  // RH
+  const int CW = n_f <= 32 ? 32 : 64;
+  const int c = threadIdx.x % CW, r0 = threadIdx.x / CW, rstep = blockDim.x / CW;
+  for (int64_t slot = blockIdx.x; slot < nd; slot += gridDim.x) {
     const double2* b = bp + slot * D * n_f;
-    double2 ph = make_double2(1.0, 0.0);
-#pragma unroll
-    for (int k = D - 1; k >= 0; --k) {
-      const int idx = (k == 0 && D >= 2) ? half_plane_mi((int)rem, n_f, half) : (int)(rem % n_f);
-      ph = k == D - 1 ? b[k * n_f + idx] : cmul(ph, b[k * n_f + idx]);
-      rem /= n_f;
+    __syncthreads();
+    for (int r = threadIdx.x; r < RH; r += blockDim.x) {
+      double2 v = make_double2(1.0, 0.0);
+      if (D >= 2) v = b[half_plane_mi(D == 3 ? r / n_f : r, n_f, half)];
+      if (D == 3) v = cmul(v, b[n_f + r % n_f]);
+      s_row[r] = v;
     }
-    phi[e] = cmul(ph, phi[e]);
+    __syncthreads();
+    if (c >= n_f) continue;
+    const double2 cf = b[(D - 1) * n_f + c];
+    double2* p = phi + slot * NH + c;
+    for (int r = r0; r < RH; r += rstep) p[(int64_t)r * n_f] = cmul(cmul(s_row[r], cf), p[(int64_t)r * n_f]);
   }
 }
 
@@ -1618,8 +1625,8 @@ void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, 
   box_phase_kernel<DD><<<grid_for(T.n_dense * DD * n_f, 256), 256, 0, st>>>(                          \
       T.dense_ids.get(), T.n_dense, T.center.get(), cref, P.sc, n_f, reinterpret_cast<double2*>(bp.get())); \
   FGT_LAUNCHED();                                                                                      \
-  phi_rephase_kernel<DD><<<grid_for(T.n_dense * P.NH, 256), 256, 0, st>>>(                            \
-      reinterpret_cast<double2*>(P.phi.get()), T.n_dense, P.NH, n_f, P.half,                         \
+  phi_rephase_kernel<DD><<<grid_for(T.n_dense, 1, (int64_t)148 * 16), 256, P.RH * sizeof(double2), st>>>( \
+      reinterpret_cast<double2*>(P.phi.get()), T.n_dense, P.NH, n_f, (int)P.RH, P.half,              \
       reinterpret_cast<const double2*>(bp.get()));                                                    \
   FGT_LAUNCHED();                                                                                      \
   P.k_gather.end(st);                                                                                  \
