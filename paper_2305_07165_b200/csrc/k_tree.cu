@@ -114,10 +114,10 @@ void device_bbox(const double* src, int64_t ns, const double* tgt, int64_t nt, i
 }
 
 // ------------------------------------------------------------------ point codes
-template <int D>
+template <int D, class KT, class IT>
 __global__ void __launch_bounds__(256) point_codes_kernel(
     const double* __restrict__ src, int64_t ns, const double* __restrict__ tgt, int64_t nt,
-    int l_c, Root root, uint64_t* __restrict__ code, int64_t* __restrict__ idx) {
+    int l_c, Root root, KT* __restrict__ code, IT* __restrict__ idx) {
   const int64_t ntot = ns + nt;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -137,8 +137,17 @@ __global__ void __launch_bounds__(256) point_codes_kernel(
       }
       s *= 0.5;
     }
-    code[i] = morton_encode(g, D, l_c);
-    idx[i] = i;
+    code[i] = (KT)morton_encode(g, D, l_c);
+    idx[i] = (IT)i;
+  }
+}
+
+// 32-bit sorted codes / indices -> the tree's 64-bit arrays
+__global__ void widen_kernel(const uint32_t* __restrict__ k32, const int32_t* __restrict__ i32, int64_t n,
+                             uint64_t* __restrict__ k64, int64_t* __restrict__ i64) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    k64[i] = k32[i];
+    i64[i] = i32[i];
   }
 }
 
@@ -423,30 +432,6 @@ __global__ void source_flag_kernel(const int64_t* __restrict__ pidx, int64_t npt
 // Leaves are contiguous ranges of the Morton-sorted points: each non-empty leaf marks its
 // first point (two binary searches per leaf instead of one covering search per point);
 // a fill-forward scan then gives every sorted point its leaf.
-__global__ void leaf_first_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ is_leaf,
-                                  int64_t nb, PKeyIdx pk, int d, int l_c,
-                                  int64_t* __restrict__ mark) {
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
-       b += (int64_t)gridDim.x * blockDim.x) {
-    if (!is_leaf[b]) continue;
-    const uint64_t k = keys[b];
-    const int sh = d * (l_c - key_level(k));
-    const int64_t s = prefix_lo(pk, key_code(k), sh);
-    if (s < pk.n && s < prefix_hi(pk, key_code(k), sh)) mark[s] = b;
-  }
-}
-
-struct FillForward {
-  __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return b >= 0 ? b : a; }
-};
-
-__global__ void leaf_scatter_kernel(const int64_t* __restrict__ filled, const int64_t* __restrict__ pidx,
-                                    int64_t npts, int64_t* __restrict__ leaf_of) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npts;
-       i += (int64_t)gridDim.x * blockDim.x)
-    leaf_of[pidx[i]] = filled[i];
-}
-
 __global__ void iota_kernel(int64_t* a, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -470,6 +455,48 @@ __global__ void partition_sorted_kernel(const uint64_t* __restrict__ pkey, const
       tgt_perm[i - k] = p - ns;
       leaf_tgt[i - k] = leaf;
     }
+  }
+}
+
+// general trees: stable partition of the code-sorted points into sources / targets (the
+// leaves' runs stay contiguous and in Morton order)
+__global__ void partition_points_kernel(const int64_t* __restrict__ pidx, int64_t np, int64_t ns,
+                                        const int64_t* __restrict__ srcpre, int64_t* __restrict__ seq_src,
+                                        int64_t* __restrict__ seq_tgt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pidx[i], k = srcpre[i];
+    if (p < ns) seq_src[k] = p;
+    else seq_tgt[i - k] = p - ns;
+  }
+}
+
+// per leaf: its sorted-point range [lo, hi) (a leaf covers a contiguous code range) mapped
+// to the partitioned source / target sequences; empty ranges for the other boxes
+__global__ void leaf_ranges_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ is_leaf,
+                                   int64_t nb, PKeyIdx pk, int d, int l_c, const int64_t* __restrict__ srcpre,
+                                   int64_t* __restrict__ src_start, int64_t* __restrict__ src_end,
+                                   int64_t* __restrict__ tgt_start, int64_t* __restrict__ tgt_end) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s0 = 0, s1 = 0, t0 = 0, t1 = 0;
+    bool fine = false;
+    if (is_leaf[b]) {
+      const uint64_t k = keys[b];
+      fine = key_level(k) == l_c;
+      const int sh = d * (l_c - key_level(k));
+      const int64_t lo = prefix_lo(pk, key_code(k), sh), hi = prefix_hi(pk, key_code(k), sh);
+      s0 = srcpre[lo];
+      s1 = srcpre[hi];
+      t0 = lo - s0;
+      t1 = hi - s1;
+    }
+    src_start[b] = s0;
+    tgt_start[b] = t0;
+    // sort segments: only coarse leaves (< l_c: at most n_s points) span several codes; a
+    // level-l_c leaf is one code, already in ascending index order
+    src_end[b] = fine ? s0 : s1;
+    tgt_end[b] = fine ? t0 : t1;
   }
 }
 
@@ -514,11 +541,6 @@ __global__ void gather_rows_kernel(const double* __restrict__ a, const int64_t* 
   }
 }
 
-int bits_for(int64_t n) {
-  int b = 1;
-  while (b < 63 && ((int64_t)1 << b) <= n) ++b;
-  return b;
-}
 
 // Box-set state during construction.
 struct BoxSet {
@@ -678,7 +700,21 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   // ---- point codes, stable radix sort
   const int64_t np = T.ntot;
   CubTmp tmp;
-  {
+  if (D * l_c > 0 && D * l_c <= 32) {
+    // codes fit 32 bits (and indices 31): sort 8-byte pairs instead of 16-byte ones
+    DBuf<uint32_t> code(np, st), scode(np, st);
+    DBuf<int32_t> idx(np, st), sidx(np, st);
+    point_codes_kernel<D><<<grid_for(np, 256), 256, 0, st>>>(src, ns, tgt, nt, l_c, root, code.get(), idx.get());
+    FGT_LAUNCHED();
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, code.get(), scode.get(), idx.get(), sidx.get(), (int)np, 0, D * l_c, st));
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes, st), bytes, code.get(), scode.get(), idx.get(), sidx.get(), (int)np, 0, D * l_c, st));
+    count_launch();
+    T.pkey.alloc(np, st);
+    T.pidx.alloc(np, st);
+    widen_kernel<<<grid_for(np, 256), 256, 0, st>>>(scode.get(), sidx.get(), np, T.pkey.get(), T.pidx.get());
+    FGT_LAUNCHED();
+  } else {
     DBuf<uint64_t> code(np, st);
     DBuf<int64_t> idx(np, st);
     point_codes_kernel<D><<<grid_for(np, 256), 256, 0, st>>>(src, ns, tgt, nt, l_c, root, code.get(), idx.get());
@@ -843,41 +879,35 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     leaf_start_kernel<<<grid_for(nb, 256), 256, 0, st>>>(leaf_tgt.get(), nt, T.is_leaf.get(), nb, T.tgt_start.get());
     FGT_LAUNCHED();
   } else {
-    DBuf<int64_t> leaf_of(np, st);
-    {
-      DBuf<int64_t> mark(np, st), filled(np, st);
-      fill_i64_kernel<<<grid_for(np, 256), 256, 0, st>>>(mark.get(), np, -1);
-      FGT_LAUNCHED();
-      leaf_first_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, pk, D,
-                                                         l_c, mark.get());
-      FGT_LAUNCHED();
-      size_t bytes = 0;
-      FGT_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, mark.get(), filled.get(), FillForward(), (int)np, st));
-      FGT_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(bytes, st), bytes, mark.get(), filled.get(), FillForward(), (int)np, st));
-      count_launch();
-      leaf_scatter_kernel<<<grid_for(np, 256), 256, 0, st>>>(filled.get(), T.pidx.get(), np, leaf_of.get());
-      FGT_LAUNCHED();
-    }
-    const int bits = bits_for(nb);
+    // General tree: every leaf covers a contiguous range of the code-sorted points, so a
+    // stable source / target partition keeps each leaf's points contiguous (leaves in Morton
+    // order); a segmented sort by original index then gives the reference's ascending
+    // per-leaf lists (tree.py:350-381) without a scatter or a full re-sort.
+    T.src_perm.alloc(ns, st);
+    T.tgt_perm.alloc(nt, st);
+    T.src_start.alloc(nb, st);
+    T.tgt_start.alloc(nb, st);
+    DBuf<int64_t> seq_src(ns, st), seq_tgt(nt, st), src_end(nb, st), tgt_end(nb, st);
+    partition_points_kernel<<<grid_for(np, 256), 256, 0, st>>>(T.pidx.get(), np, ns, srcpre.get(), seq_src.get(),
+                                                               seq_tgt.get());
+    FGT_LAUNCHED();
+    leaf_ranges_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, pk, D, l_c,
+                                                          srcpre.get(), T.src_start.get(), src_end.get(),
+                                                          T.tgt_start.get(), tgt_end.get());
+    FGT_LAUNCHED();
     for (int which = 0; which < 2; ++which) {
-      int64_t n = which ? nt : ns;
-      DBuf<int64_t>& perm = which ? T.tgt_perm : T.src_perm;
-      DBuf<int64_t>& start = which ? T.tgt_start : T.src_start;
-      perm.alloc(n, st);
-      start.alloc(nb, st);
-      DBuf<int64_t> sorted_leaf(n, st);
-      if (n > 0) {
-        DBuf<int64_t> iota(n, st);
-        iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota.get(), n);
-        FGT_LAUNCHED();
-        const int64_t* keys_in = leaf_of.get() + (which ? ns : 0);
-        size_t bytes = 0;
-        FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sorted_leaf.get(), iota.get(), perm.get(), (int)n, 0, bits, st));
-        FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(bytes, st), bytes, keys_in, sorted_leaf.get(), iota.get(), perm.get(), (int)n, 0, bits, st));
-        count_launch();
-      }
-      leaf_start_kernel<<<grid_for(nb, 256), 256, 0, st>>>(sorted_leaf.get(), n, T.is_leaf.get(), nb, start.get());
-      FGT_LAUNCHED();
+      const int64_t n = which ? nt : ns;
+      if (n == 0) continue;
+      const int64_t* kin = which ? seq_tgt.get() : seq_src.get();
+      int64_t* kout = which ? T.tgt_perm.get() : T.src_perm.get();
+      const int64_t* beg = which ? T.tgt_start.get() : T.src_start.get();
+      const int64_t* end = which ? tgt_end.get() : src_end.get();
+      // level-l_c leaves (empty sort segments) keep the partitioned order
+      FGT_CUDA(cudaMemcpyAsync(kout, kin, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      size_t bytes = 0;
+      FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, kin, kout, (int)n, (int)nb, beg, end, st));
+      FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.get(bytes, st), bytes, kin, kout, (int)n, (int)nb, beg, end, st));
+      count_launch();
     }
   }
 
