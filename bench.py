@@ -27,9 +27,10 @@ A step is one full transform: tree + lists + form + gather + eval + direct.
            bounded samples of the same workload, one sample per host core in parallel
            processes (see `shell_samples`), measured wall time.
 Under torchrun (N>1) every rank runs the same problem and evaluates a cost-balanced
-contiguous share of the target leaves; each rank forms only the P-box expansions it
-owns and the one-box halo of expansions is exchanged with one NCCL all-to-all
-(PointsRun + TorchExchange); time = max over ranks ("scaling": "strong").
+contiguous Morton range of the target leaves; each rank forms only the P-box expansions
+it owns, the one-box halo of expansions is exchanged with one NCCL all-to-all and the
+potentials are assembled on every rank with one NCCL all-reduce (PointsRun +
+TorchExchange); time = max over ranks ("scaling": "strong").
 `--impl reference` times the CPU oracle alone (rank 0; other ranks exit 0) on the same
 samples: every step is one parallel round of full oracle transforms, measured.
 """
@@ -427,7 +428,9 @@ def run_ours(args, world, rank, local):
         # expansions goes over NCCL (one all-to-all), then translation/evaluation/near field
         run = PointsRun(prm, sy, sq, sx)
         run.exchange(xchg)
-        return run.finish(out=out, return_times=True)[1]
+        ph = run.finish(out=out, return_times=True)[1]
+        xchg.assemble(out)  # u of all targets on every rank (NCCL all-reduce of the shares)
+        return ph
 
     for _ in range(args.warmup):
         step()
@@ -441,11 +444,7 @@ def run_ours(args, world, rank, local):
     value = (N + M) / (ms_per_step * 1e-3)
 
     # ---- result check (outside the timed region): this rank's share vs CPU exact sums
-    u_host = u.cpu().numpy()
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)   # shares are disjoint: the sum is u
-        u_host = u.cpu().numpy()
+    u_host = u.cpu().numpy()   # multi-GPU: already assembled on every rank by step()
     check = check_result(u_host, y, q, x, cfg) if rank == 0 else None
     if rank == 0 and not check["pass"]:
         raise SystemExit(f"bench: result check failed: {check}")

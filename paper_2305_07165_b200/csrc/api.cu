@@ -6,6 +6,8 @@
 #include <map>
 #include <memory>
 
+#include <cub/cub.cuh>
+
 #include "k_kernels.cuh"
 #include "k_nufft.cuh"
 
@@ -128,11 +130,12 @@ struct PhaseMarks {
     FGT_CUDA(cudaEventRecord(e, st));
     ev.push_back(e);
   }
-  // elapsed ms between marks i and i + 1
-  double ms(size_t i) const {
-    FGT_CUDA(cudaEventSynchronize(ev[i + 1]));
+  // elapsed ms between marks i and i + 1 (or i and j)
+  double ms(size_t i) const { return ms(i, i + 1); }
+  double ms(size_t i, size_t j) const {
+    FGT_CUDA(cudaEventSynchronize(ev[j]));
     float v = 0;
-    FGT_CUDA(cudaEventElapsedTime(&v, ev[i], ev[i + 1]));
+    FGT_CUDA(cudaEventElapsedTime(&v, ev[i], ev[j]));
     return v;
   }
   ~PhaseMarks() {
@@ -210,6 +213,28 @@ __global__ void leaf_direct_cost_kernel(const int64_t* __restrict__ tl, int64_t 
   }
 }
 
+__global__ void gather_i64_kernel(const uint64_t* __restrict__ a, const int64_t* __restrict__ ids, int64_t n,
+                                  int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)a[ids[i]];
+}
+
+__global__ void iota_pos_kernel(int64_t* a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = i;
+}
+
+// the rank's direct target leaves (positions into the replicated CSR): ids, begin, end
+__global__ void restrict_direct_kernel(const int64_t* __restrict__ pos, int64_t n, const int64_t* __restrict__ tl,
+                                       const int64_t* __restrict__ off, int64_t* __restrict__ ids,
+                                       int64_t* __restrict__ beg, int64_t* __restrict__ end) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos[i];
+    ids[i] = tl[p];
+    beg[i] = off[p];
+    end[i] = off[p + 1];
+  }
+}
+
 std::vector<int64_t> partition_bounds(const std::vector<double>& cost, int parts) {
   const int64_t n = (int64_t)cost.size();
   std::vector<int64_t> b(parts + 1, n);
@@ -262,7 +287,8 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
   // everything the host needs, staged contiguously on the device: one D2H, one sync
   const int64_t np_ = T.n_p, nps = T.n_psi, nd = T.n_dense;
   const int64_t o_nt = 0, o_pr = n, o_fs = 2 * n, o_tl = 3 * n, o_psi = 4 * n, o_poff = o_psi + nps,
-                o_psrc = o_poff + nps + 1, o_dense = o_psrc + np_, tot = o_dense + nd;
+                o_psrc = o_poff + nps + 1, o_dense = o_psrc + np_, o_ktl = o_dense + nd, o_kd = o_ktl + n,
+                tot = o_kd + nd;
   DBuf<int64_t> stage(tot, st);
   if (n > 0) {
     double* sd = reinterpret_cast<double*>(stage.get());
@@ -279,20 +305,38 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
   d2d(o_poff, T.p_off.get(), nps + 1);
   d2d(o_psrc, T.p_src.get(), np_);
   d2d(o_dense, T.dense_ids.get(), nd);
-  std::vector<int64_t> h(tot);
+  // box keys (level << 58 | Morton code) of the target leaves and of the P-boxes
+  if (n > 0) {
+    gather_i64_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.bkey.get(), T.d_tgt_ids.get(), n, stage.get() + o_ktl);
+    FGT_LAUNCHED();
+  }
+  if (nd > 0) {
+    gather_i64_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.bkey.get(), T.dense_ids.get(), nd, stage.get() + o_kd);
+    FGT_LAUNCHED();
+  }
+  // page-locked host staging (per thread, grown as needed): the D2H runs at link speed
+  static thread_local int64_t* hbuf = nullptr;
+  static thread_local int64_t hcap = 0;
+  if (tot > hcap) {
+    if (hbuf) FGT_CUDA(cudaFreeHost(hbuf));
+    hcap = std::max<int64_t>(tot, 2 * hcap);
+    FGT_CUDA(cudaMallocHost((void**)&hbuf, hcap * sizeof(int64_t)));
+  }
+  int64_t* h = hbuf;
   trace_mark(st, "share:stage");
-  stage.to_host(h.data(), tot);
+  if (tot > 0) FGT_CUDA(cudaMemcpyAsync(h, stage.get(), tot * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FGT_CUDA(cudaStreamSynchronize(st));
   trace_mark(st, "share:d2h(sync)");
   auto dv = [&](int64_t off, int64_t cnt) {
     std::vector<double> v(cnt);
-    if (cnt) std::memcpy(v.data(), h.data() + off, cnt * sizeof(double));
+    if (cnt) std::memcpy(v.data(), h + off, cnt * sizeof(double));
     return v;
   };
   const std::vector<double> nt = dv(o_nt, n), pairs = dv(o_pr, n), fsrc = dv(o_fs, n);
-  const std::vector<int64_t> tl(h.begin() + o_tl, h.begin() + o_tl + n), psi(h.begin() + o_psi, h.begin() + o_psi + nps),
-      poff(h.begin() + o_poff, h.begin() + o_poff + nps + 1), psrc(h.begin() + o_psrc, h.begin() + o_psrc + np_),
-      dense(h.begin() + o_dense, h.begin() + o_dense + nd);
+  const int64_t* tl = h + o_tl;
+  const int64_t* psi = h + o_psi;
+  const int64_t* poff = h + o_poff;
+  const int64_t* psrc = h + o_psrc;
   // cost in ns, calibrated on the B200 kernels (profiles/r01f_*): eval 8 N_H flops per
   // target at ~21 TFLOP/s, gather ~2.4 ps per stored mode per P entry, direct ~10 ps per
   // pair; with the exchange, a P-box's form (~2.4 ns per source at w = 11, ~w^3) is
@@ -309,53 +353,98 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
     }
     cost[i] = c;
   }
-  std::vector<int64_t> b = partition_bounds(cost, size);
+  // Leaves in Morton order across levels (key = code at l_c, i.e. code << d (l_c - level)),
+  // so a rank's contiguous range is a compact region of space and its halo is one box deep
+  // (box ids are level-major: a range of them would span all coarse leaves of the domain).
+  const int dd = T.d, lc = T.l_c;
+  auto deep = [&](int64_t key) {
+    const uint64_t k = (uint64_t)key;
+    return key_code(k) << (dd * (lc - key_level(k)));
+  };
+  std::vector<uint64_t> dk(n);
+  for (int64_t i = 0; i < n; ++i) dk[i] = deep(h[o_ktl + i]);
+  // Morton order across levels: radix sort of (deep key, position) on the device
+  std::vector<int64_t> ord(n);
+  if (n > 0) {
+    DBuf<uint64_t> kin(n, st), kout(n, st);
+    DBuf<int64_t> vin(n, st), vout(n, st);
+    kin.from_host(dk.data(), n);
+    iota_pos_kernel<<<grid_for(n, 256), 256, 0, st>>>(vin.get(), n);
+    FGT_LAUNCHED();
+    size_t bytes = 0;
+    const int bits = std::max(1, dd * lc);
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.get(), kout.get(), vin.get(), vout.get(), (int)n, 0, bits, st));
+    DBuf<uint8_t> tmpb(bytes, st);
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmpb.get(), bytes, kin.get(), kout.get(), vin.get(), vout.get(), (int)n, 0, bits, st));
+    count_launch();
+    vout.to_host(ord.data(), n);
+    FGT_CUDA(cudaStreamSynchronize(st));
+  }
+  trace_mark(st, "share:order");
+  std::vector<double> cost_o(n);
+  std::vector<int64_t> psi_o(n);
+  std::vector<uint64_t> dk_o(n);
+  for (int64_t k = 0; k < n; ++k) {
+    cost_o[k] = cost[ord[k]];
+    psi_o[k] = psi_of[ord[k]];
+    dk_o[k] = dk[ord[k]];
+  }
+  std::vector<int64_t> b = partition_bounds(cost_o, size);
+  // psi boxes (level l_c, ascending code = ascending psi index) appear in ascending index
+  // along the Morton order, so every rank's psi boxes are one index range
   auto first_psi = [&](int64_t i) {
     for (; i < n; ++i)
-      if (psi_of[i] >= 0) return psi_of[i];
+      if (psi_o[i] >= 0) return psi_o[i];
     return T.n_psi;
   };
   std::vector<int64_t> pb(size + 1);  // psi index range of every rank
   for (int r = 0; r <= size; ++r) pb[r] = first_psi(b[r]);
   const int64_t lo = b[rank], hi = b[rank + 1];
   const int64_t plo = pb[rank], phi = pb[rank + 1];
-  // slots needed by every rank (from the replicated lists)
-  auto needs = [&](int r) {
-    std::vector<int64_t> v(psrc.begin() + poff[pb[r]], psrc.begin() + poff[pb[r + 1]]);
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
-    return v;
-  };
+  // slots needed by every rank (from the replicated lists): one pass over the P entries,
+  // a rank bit mask per slot (world <= 64)
+  FGT_REQUIRE(size <= 64, FGT_ERANGE, "at most 64 ranks");
+  std::vector<uint64_t> need(T.n_dense, 0);
+  for (int r = 0; r < size; ++r)
+    for (int64_t e = poff[pb[r]]; e < poff[pb[r + 1]]; ++e) need[psrc[e]] |= (uint64_t)1 << r;
+  const uint64_t me = (uint64_t)1 << rank;
   T.dense_need.assign(T.n_dense, 0);
-  const std::vector<int64_t> mine = needs(rank);
   if (!exchange) {
-    for (int64_t s : mine) T.dense_need[s] = 1;
+    for (int64_t s = 0; s < T.n_dense; ++s) T.dense_need[s] = (need[s] & me) != 0;
   } else {
     // owner of a slot: the rank whose target-leaf range holds the box's position
     std::vector<int> owner(T.n_dense);
+    // rank r owns deep keys in [thr[r], thr[r + 1]) (thr[r] = key of its first leaf)
+    std::vector<uint64_t> thr(size + 1, ~(uint64_t)0);
+    for (int r = 0; r < size; ++r) thr[r] = b[r] < n ? dk_o[b[r]] : ~(uint64_t)0;
+    thr[0] = 0;
     for (int64_t s = 0; s < T.n_dense; ++s) {
-      const int64_t pos = std::lower_bound(tl.begin(), tl.end(), dense[s]) - tl.begin();
-      int r = (int)(std::upper_bound(b.begin(), b.end(), pos) - b.begin()) - 1;
+      const uint64_t key = deep(h[o_kd + s]);
+      int r = (int)(std::upper_bound(thr.begin(), thr.begin() + size, key) - thr.begin()) - 1;
       owner[s] = std::max(0, std::min(size - 1, r));
     }
     X->rank = rank;
     X->world = size;
     X->send_off.assign(size + 1, 0);
     X->recv_off.assign(size + 1, 0);
+    // per peer, slots in ascending order on both sides: the owner sends what the peer needs,
+    // the peer receives what it needs from that owner
+    std::vector<std::vector<int64_t>> sendr(size), recvr(size);
+    for (int64_t s = 0; s < T.n_dense; ++s) {
+      const uint64_t m = need[s];
+      if (!m) continue;
+      if (owner[s] == rank) {
+        T.dense_need[s] = 1;
+        for (int r = 0; r < size; ++r)
+          if (r != rank && ((m >> r) & 1)) sendr[r].push_back(s);
+      } else if (m & me) {
+        recvr[owner[s]].push_back(s);
+      }
+    }
     std::vector<int64_t> send, recv;
     for (int r = 0; r < size; ++r) {
-      if (r != rank) {
-        for (int64_t s : needs(r))
-          if (owner[s] == rank) {
-            send.push_back(s);
-            T.dense_need[s] = 1;
-          }
-        for (int64_t s : mine)
-          if (owner[s] == r) recv.push_back(s);
-      } else {
-        for (int64_t s : mine)
-          if (owner[s] == rank) T.dense_need[s] = 1;
-      }
+      send.insert(send.end(), sendr[r].begin(), sendr[r].end());
+      recv.insert(recv.end(), recvr[r].begin(), recvr[r].end());
       X->send_off[r + 1] = (int64_t)send.size();
       X->recv_off[r + 1] = (int64_t)recv.size();
     }
@@ -365,14 +454,22 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
     X->recv_slots.from_host(recv.data(), recv.size());
   }
   trace_mark(st, "share:plans");
-  // restrict direct CSR (absolute offsets stay valid)
+  // restrict the direct lists to the rank's leaves (begin / end per leaf into the
+  // replicated entry arrays)
   {
-    DBuf<int64_t> ids(hi - lo, st), off(hi - lo + 1, st);
-    if (hi > lo) FGT_CUDA(cudaMemcpyAsync(ids.get(), T.d_tgt_ids.get() + lo, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    FGT_CUDA(cudaMemcpyAsync(off.get(), T.d_off.get() + lo, (hi - lo + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    const int64_t m = hi - lo;
+    DBuf<int64_t> pos(std::max<int64_t>(m, 1), st), ids(std::max<int64_t>(m, 1), st), beg(std::max<int64_t>(m, 1), st),
+        end(std::max<int64_t>(m, 1), st);
+    if (m > 0) {
+      pos.from_host(ord.data() + lo, m);
+      restrict_direct_kernel<<<grid_for(m, 256), 256, 0, st>>>(pos.get(), m, T.d_tgt_ids.get(), T.d_off.get(),
+                                                               ids.get(), beg.get(), end.get());
+      FGT_LAUNCHED();
+    }
     T.d_tgt_ids = std::move(ids);
-    T.d_off = std::move(off);
-    T.n_dtgt = hi - lo;
+    T.d_off = std::move(beg);
+    T.d_end = std::move(end);
+    T.n_dtgt = m;
   }
   // restrict psi boxes
   {
@@ -524,6 +621,10 @@ static int psi_mode() {
 }
 
 static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, double* u_host = nullptr) {
+  // phases of finish are timed from its own start: with the exchange path other ranks'
+  // work and the all-to-all sit between begin and finish on a shared GPU
+  const size_t m_fin = R.pm->ev.size();
+  R.pm->mark();
   cudaStream_t st = R.st;
   TreeDev& T = R.T;
   PwDev& P = R.P;
@@ -563,11 +664,12 @@ static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, doubl
   t.lists_ms = R.sb ? R.k_lists.ms() : pm.ms(1);  // overlapped: side-stream time
   t.form_ms = pm.ms(2);
   t.gather_ms = P.k_gather.ms();
-  t.eval_ms = pm.ms(3) - t.gather_ms;
-  t.direct_ms = pm.ms(4);
+  t.eval_ms = pm.ms(m_fin, m_fin + 1) - t.gather_ms;
+  t.direct_ms = pm.ms(m_fin + 1, m_fin + 2);
   trace_dump();
-  // wall span on the launching stream (the overlapped lists are not on it)
-  t.total_ms = t.tree_ms + pm.ms(1) + t.form_ms + t.gather_ms + t.eval_ms + t.direct_ms;
+  // device time on the launching stream: begin (tree, lists, form) + finish (the overlapped
+  // lists are not on it; the exchange between begin and finish is not counted)
+  t.total_ms = t.tree_ms + pm.ms(1) + t.form_ms + pm.ms(m_fin, m_fin + 2);
   t.launches = g_launches - R.l0;
   t.k_form_ms = P.k_form.ms();
   t.k_gather_ms = P.k_gather.ms();

@@ -1048,7 +1048,8 @@ __global__ void __launch_bounds__(256, 2) eval_kernel(EvalArgs a) {
 // ------------------------------------------------------------------ direct
 struct DirectArgs {
   const int64_t* d_tgt_ids;
-  const int64_t* d_off;
+  const int64_t* d_beg;   // entries of leaf i: [d_beg[i], d_end[i])
+  const int64_t* d_end;
   const int64_t* d_src;
   const int32_t* d_v;
   const int64_t* src_start;
@@ -1071,7 +1072,7 @@ __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
   __shared__ double s_q[TILE];
   for (int64_t i = blockIdx.x; i < a.n; i += gridDim.x) {
     const int64_t T = a.d_tgt_ids[i];
-    const int64_t e0 = a.d_off[i], e1 = a.d_off[i + 1];
+    const int64_t e0 = a.d_beg[i], e1 = a.d_end[i];
     if (e0 == e1) continue;
     const int64_t t0 = a.tgt_start[T];
     const int ntg = (int)a.tgt_count[T];
@@ -1134,7 +1135,7 @@ __global__ void __launch_bounds__(256) direct_warp_kernel(DirectArgs a, int* __r
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= a.n) break;
     const int64_t T = a.d_tgt_ids[i];
-    const int64_t e0 = a.d_off[i], e1 = a.d_off[i + 1];
+    const int64_t e0 = a.d_beg[i], e1 = a.d_end[i];
     if (e0 == e1) continue;
     const int64_t t0 = a.tgt_start[T];
     const int ntg = (int)a.tgt_count[T];
@@ -1652,7 +1653,8 @@ void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted,
   cudaStream_t st = T.st;
   DirectArgs da;
   da.d_tgt_ids = T.d_tgt_ids.get();
-  da.d_off = T.d_off.get();
+  da.d_beg = T.d_off.get();
+  da.d_end = T.d_end.size() ? T.d_end.get() : T.d_off.get() + 1;
   da.d_src = T.d_src.get();
   da.d_v = T.d_v.get();
   da.src_start = T.src_start.get();

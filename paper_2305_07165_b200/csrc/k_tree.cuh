@@ -43,7 +43,8 @@ struct TreeDev {
   DBuf<int64_t> p_src;   // (n_p) dense slot of S
   DBuf<int32_t> p_v;     // (n_p * d) image shifts
   DBuf<int64_t> p_tgt;   // (n_p) target box id (for copy-out)
-  DBuf<int64_t> d_off;   // (n_dtgt+1) CSR over direct target leaves
+  DBuf<int64_t> d_off;   // (n_dtgt+1) CSR over direct target leaves (begin of leaf i)
+  DBuf<int64_t> d_end;   // multi-GPU share: (n_dtgt) end of leaf i (else d_off[i + 1])
   DBuf<int64_t> d_tgt_ids; // (n_dtgt)
   int64_t n_dtgt = 0;
   DBuf<int64_t> d_src;   // (n_d) source box id

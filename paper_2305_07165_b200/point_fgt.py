@@ -175,6 +175,14 @@ class TorchExchange:
         dist.all_to_all_single(recv, send, [int(c) * slot for c in recv_counts],
                                [int(c) * slot for c in send_counts], group=self.group)
 
+    def assemble(self, u):
+        """u of the whole transform on every rank (SURVEY.md section 8(e) exchange 3): each
+        target is owned by exactly one rank and the others hold an exact 0.0 there, so a sum
+        over ranks reproduces the single-GPU result bit for bit (one NCCL all-reduce)."""
+        import torch.distributed as dist
+        dist.all_reduce(u, op=dist.ReduceOp.SUM, group=self.group)
+        return u
+
 
 def fgt_points_exchange_begin(sources, charges, targets, delta, epsilon, n_s, boundary="free",
                               share=(0, 1)):

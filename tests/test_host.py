@@ -199,3 +199,42 @@ def test_halo_exchange_all_to_all_gloo():
         p.join(timeout=60)
     for rank, ok in res:
         assert ok, f"rank {rank}: halo blocks out of place"
+
+
+def _assemble_worker(rank, world, port, q):
+    """One gloo rank of the result assembly: the rank holds the potentials of its own
+    targets and exact zeros elsewhere; TorchExchange.assemble leaves the whole transform on
+    every rank, bit for bit."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_07165_b200.point_fgt import TorchExchange
+        full = torch.from_numpy(np.random.default_rng(5).standard_normal(1001))
+        owner = torch.from_numpy(np.random.default_rng(6).integers(0, world, 1001))
+        mine = torch.where(owner == rank, full, torch.zeros_like(full))
+        out = TorchExchange().assemble(mine.clone())
+        q.put((rank, bool(torch.equal(out, full))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_result_assembly_gloo():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    procs = [ctx.Process(target=_assemble_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok in res:
+        assert ok, f"rank {rank}: assembled potentials differ from the whole transform"
