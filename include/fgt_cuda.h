@@ -23,7 +23,11 @@
  *   FGT_ECUDA   (2)  CUDA runtime error  -> RuntimeError (message via fgt_last_error)
  *   FGT_ERANGE  (3)  outside supported range (e.g. tree deeper than 19 levels in 3-D)
  *   FGT_ENOMEM  (4)  device allocation failed
- * Functions are reentrant; all device scratch is stream-ordered (cudaMallocAsync).
+ * Functions are reentrant.  Device scratch comes from two allocators: buffers under
+ * 64 MB are stream-ordered (cudaMallocAsync pool); larger ones from a process-lifetime
+ * cache of cudaMalloc blocks reused in stream order (cudaStreamWaitEvent on reuse) -- when
+ * a new block does not fit, the cache frees its idle blocks after a cudaDeviceSynchronize
+ * and retries once (FGT_ENOMEM if it still fails).
  */
 #ifndef FGT_CUDA_H
 #define FGT_CUDA_H
@@ -110,11 +114,14 @@ typedef struct fgt_tree_params {
   double delta;
   /* periodic trees only: l_c from cutoff_level(kind="density"), root side 1 */
   int32_t l_c_periodic;
-  /* multi-GPU share (fgt_points only): this process evaluates the targets of the
-   * part_rank-th of part_size cost-balanced contiguous ranges (Morton order) of the
-   * target leaves; outgoing expansions are formed for exactly the P-boxes its range
-   * needs (halo recomputed, no exchange).  part_size <= 1 means everything.  Targets
-   * outside the share get u = 0. */
+  /* multi-GPU share: this process evaluates the targets of the part_rank-th of part_size
+   * cost-balanced contiguous ranges of the target leaves in Morton order across levels
+   * (key = Morton code at l_c of the leaf's first cell), so a share is a compact region
+   * of space.  Two modes: fgt_points / fgt_points_dev form every P-box expansion the
+   * range needs (the one-box halo is recomputed, no communication); fgt_points_begin ..
+   * finish forms only the expansions the rank owns and the halo is exchanged between
+   * begin and finish (fgt_points_pack / unpack + one all-to-all).  part_size <= 1 means
+   * everything.  Targets outside the share get u = 0 (summing the shares gives u). */
   int32_t part_rank;
   int32_t part_size;
 } fgt_tree_params;

@@ -7,6 +7,11 @@
 // semantics (used by nufft.nufft_type1/2 and by the kernel-level parity tests).  The
 // FGT pipeline itself uses the list-driven direct kernel (k_direct.cu) and the
 // per-box plane-wave kernels (k_pw.cu).
+#include <algorithm>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include "fgt_common.cuh"
 #include "k_kernels.cuh"
 
@@ -69,68 +74,93 @@ void launch_gauss_direct_allpairs(const double* tgt, int64_t nt, const double* s
 }
 
 // ------------------------------------------------------------------ spreading
-// Per-axis base index and Gaussian weights, _kernels_py._spread_weights (:49-62):
-//   i0 = rint(x / h_r); z_o = x - (i0 + o) h_r; w_o = exp(-z_o^2 / (4 tau)).
+// Deterministic (no atomics): every (point, tap) contribution is keyed by its grid cell,
+// the keys are stable-sorted with their (point, tap) position, and one thread per
+// occupied cell adds the cell's contributions in that order -- ascending point index,
+// then tap order, the accumulation order of the reference's np.add.at.  Per-axis weights
+// as _kernels_py._spread_weights (:49-62):
+//   i0 = rint(x / h_r); z_o = x - (i0 + o - m) h_r; w_o = exp(-z_o^2 / (4 tau)).
 template <int D>
-__global__ void __launch_bounds__(128) nufft_spread_kernel(
-    const double* __restrict__ x, int64_t M, const double* __restrict__ vals, int n_r, int m_sp,
-    double tau, double* __restrict__ grid) {
+__global__ void spread_weights_kernel(const double* __restrict__ x, int64_t j0, int64_t nj, int n_r, int m_sp,
+                                      double tau, double* __restrict__ w, int64_t* __restrict__ base) {
   const int nw = 2 * m_sp + 1;
   const double hr = 2.0 * M_PI / n_r;
   const double inv4tau = 1.0 / (4.0 * tau);
-  extern __shared__ double s_w[];  // per thread: D * nw weights
-  double* w = s_w + threadIdx.x * D * nw;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i0[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      double xk = x[j * D + k];
-      i0[k] = (int64_t)rint(xk / hr);
-      for (int o = 0; o < nw; ++o) {
-        double z = xk - (double)(i0[k] + o - m_sp) * hr;
-        w[k * nw + o] = exp(-z * z * inv4tau);
-      }
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nj * D;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / D;
+    const int k = (int)(t % D);
+    const double xk = x[(j0 + j) * D + k];
+    const int64_t i0 = (int64_t)rint(xk / hr);
+    for (int o = 0; o < nw; ++o) {
+      const double z = xk - (double)(i0 + o - m_sp) * hr;
+      w[(j * D + k) * nw + o] = exp(-z * z * inv4tau);
     }
-    const double vr = vals[2 * j], vi = vals[2 * j + 1];
-    // wrap base indices once; (i0 + o - m) mod n_r, non-negative like Python's %
-    int64_t b[D];
+    // first tap's cell, wrapped non-negative like Python's %
+    base[j * D + k] = ((i0 - m_sp) % n_r + n_r) % n_r;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ int64_t tap_cell(const int64_t* b, int64_t t, int nw, int n_r) {
+  int64_t idx = 0;
+  int64_t rem = t;
+  int o[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) b[k] = ((i0[k] - m_sp) % n_r + n_r) % n_r;
-    if (D == 1) {
-      for (int o0 = 0; o0 < nw; ++o0) {
-        int64_t idx = (b[0] + o0) % n_r;
-        double wt = w[o0];
-        atomicAdd(&grid[2 * idx], wt * vr);
-        atomicAdd(&grid[2 * idx + 1], wt * vi);
+  for (int k = D - 1; k >= 0; --k) {
+    o[k] = (int)(rem % nw);
+    rem /= nw;
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) idx = idx * n_r + (b[k] + o[k]) % n_r;
+  return idx;
+}
+
+template <int D>
+__global__ void spread_keys_kernel(const int64_t* __restrict__ base, int64_t nj, int nw, int n_r,
+                                   uint64_t* __restrict__ key, int64_t* __restrict__ pos) {
+  const int64_t T = [&] { int64_t v = 1; for (int k = 0; k < D; ++k) v *= nw; return v; }();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nj * T;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    key[e] = (uint64_t)tap_cell<D>(base + (e / T) * D, e % T, nw, n_r);
+    pos[e] = e;
+  }
+}
+
+__global__ void run_flag_kernel(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+template <int D>
+__global__ void spread_runs_kernel(const uint64_t* __restrict__ key, const int64_t* __restrict__ pos, int64_t n,
+                                   const int64_t* __restrict__ starts, const int* __restrict__ nruns,
+                                   const double* __restrict__ w, const double* __restrict__ vals, int64_t j0,
+                                   int nw, double* __restrict__ grid) {
+  const int64_t T = [&] { int64_t v = 1; for (int k = 0; k < D; ++k) v *= nw; return v; }();
+  const int64_t nr = *nruns;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = starts[r], b = r + 1 < nr ? starts[r + 1] : n;
+    double sr = 0.0, si = 0.0;
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t e = pos[i], j = e / T;
+      int64_t rem = e % T;
+      int o[D];
+#pragma unroll
+      for (int k = D - 1; k >= 0; --k) {
+        o[k] = (int)(rem % nw);
+        rem /= nw;
       }
-    } else if (D == 2) {
-      for (int o0 = 0; o0 < nw; ++o0) {
-        int64_t r0 = ((b[0] + o0) % n_r) * n_r;
-        double w0 = w[o0];
-        for (int o1 = 0; o1 < nw; ++o1) {
-          int64_t idx = r0 + (b[1] + o1) % n_r;
-          double wt = w0 * w[nw + o1];
-          atomicAdd(&grid[2 * idx], wt * vr);
-          atomicAdd(&grid[2 * idx + 1], wt * vi);
-        }
-      }
-    } else {
-      for (int o0 = 0; o0 < nw; ++o0) {
-        int64_t r0 = ((b[0] + o0) % n_r) * n_r;
-        double w0 = w[o0];
-        for (int o1 = 0; o1 < nw; ++o1) {
-          int64_t r1 = (r0 + (b[1] + o1) % n_r) * n_r;
-          double w01 = w0 * w[nw + o1];
-          for (int o2 = 0; o2 < nw; ++o2) {
-            int64_t idx = r1 + (b[2] + o2) % n_r;
-            double wt = w01 * w[2 * nw + o2];
-            atomicAdd(&grid[2 * idx], wt * vr);
-            atomicAdd(&grid[2 * idx + 1], wt * vi);
-          }
-        }
-      }
+      // weight product in axis order, as the reference's outer products (w0 w1) w2
+      double wt = w[(j * D + 0) * nw + o[0]];
+#pragma unroll
+      for (int k = 1; k < D; ++k) wt *= w[(j * D + k) * nw + o[k]];
+      sr += wt * vals[2 * (j0 + j)];
+      si += wt * vals[2 * (j0 + j) + 1];
     }
+    const int64_t c = (int64_t)key[a];
+    grid[2 * c] += sr;
+    grid[2 * c + 1] += si;
   }
 }
 
@@ -198,21 +228,51 @@ __global__ void __launch_bounds__(128) nufft_interp_kernel(
 void launch_nufft_spread(const double* x, int64_t M, int d, const double* vals, int64_t n_r,
                          int m_sp, double tau, double* grid, cudaStream_t st) {
   if (M == 0) return;
-  const int block = 128;
-  size_t smem = (size_t)block * d * (2 * m_sp + 1) * sizeof(double);
-  FGT_REQUIRE(smem <= 200 * 1024, FGT_ERANGE, "spreading half-width too large");
-  unsigned g = grid_for(M, block);
-  if (d == 1) {
-    FGT_CUDA(cudaFuncSetAttribute(nufft_spread_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    nufft_spread_kernel<1><<<g, block, smem, st>>>(x, M, vals, (int)n_r, m_sp, tau, grid);
-  } else if (d == 2) {
-    FGT_CUDA(cudaFuncSetAttribute(nufft_spread_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    nufft_spread_kernel<2><<<g, block, smem, st>>>(x, M, vals, (int)n_r, m_sp, tau, grid);
-  } else {
-    FGT_CUDA(cudaFuncSetAttribute(nufft_spread_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    nufft_spread_kernel<3><<<g, block, smem, st>>>(x, M, vals, (int)n_r, m_sp, tau, grid);
-  }
+  const int nw = 2 * m_sp + 1;
+  int64_t T = 1;
+  for (int k = 0; k < d; ++k) T *= nw;
+  FGT_REQUIRE(T <= ((int64_t)1 << 26), FGT_ERANGE, "spreading half-width too large");
+  // points in batches of <= 2^25 contributions; batches add to the grid in order
+  const int64_t per = std::max<int64_t>(1, ((int64_t)1 << 25) / T);
+  const int64_t cap = std::min<int64_t>(M, per);
+  DBuf<double> w(cap * d * nw, st);
+  DBuf<int64_t> base(cap * d, st), pos(cap * T, st), spos(cap * T, st), starts(cap * T, st);
+  DBuf<uint64_t> key(cap * T, st), skey(cap * T, st);
+  DBuf<int> flag(cap * T, st), nruns(1, st);
+  DBuf<uint8_t> tmp;
+  int64_t iota_bits = 1;
+  while (((int64_t)1 << iota_bits) <= n_r) ++iota_bits;
+  const int kbits = (int)std::min<int64_t>(64, iota_bits * d);
+  for (int64_t j0 = 0; j0 < M; j0 += cap) {
+    const int64_t nj = std::min(cap, M - j0), ne = nj * T;
+#define FGT_SP(DD)                                                                                        \
+  spread_weights_kernel<DD><<<grid_for(nj * DD, 256), 256, 0, st>>>(x, j0, nj, (int)n_r, m_sp, tau, w.get(), \
+                                                                   base.get());                          \
+  FGT_LAUNCHED();                                                                                         \
+  spread_keys_kernel<DD><<<grid_for(ne, 256), 256, 0, st>>>(base.get(), nj, nw, (int)n_r, key.get(), pos.get()); \
   FGT_LAUNCHED();
+    if (d == 1) { FGT_SP(1) } else if (d == 2) { FGT_SP(2) } else { FGT_SP(3) }
+#undef FGT_SP
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.get(), skey.get(), pos.get(), spos.get(), (int)ne, 0, kbits, st));
+    if (bytes > tmp.size()) tmp.alloc(bytes, st);
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, key.get(), skey.get(), pos.get(), spos.get(), (int)ne, 0, kbits, st));
+    count_launch();
+    run_flag_kernel<<<grid_for(ne, 256), 256, 0, st>>>(skey.get(), ne, flag.get());
+    FGT_LAUNCHED();
+    bytes = 0;
+    thrust::counting_iterator<int64_t> it(0);
+    FGT_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flag.get(), starts.get(), nruns.get(), (int)ne, st));
+    if (bytes > tmp.size()) tmp.alloc(bytes, st);
+    FGT_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flag.get(), starts.get(), nruns.get(), (int)ne, st));
+    count_launch();
+#define FGT_SR(DD)                                                                                         \
+  spread_runs_kernel<DD><<<grid_for(ne, 256), 256, 0, st>>>(skey.get(), spos.get(), ne, starts.get(), nruns.get(), \
+                                                           w.get(), vals, j0, nw, grid);
+    if (d == 1) { FGT_SR(1) } else if (d == 2) { FGT_SR(2) } else { FGT_SR(3) }
+#undef FGT_SR
+    FGT_LAUNCHED();
+  }
 }
 
 void launch_nufft_interp(const double* x, int64_t M, int d, const double* grid, int64_t n_r,

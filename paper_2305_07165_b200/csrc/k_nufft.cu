@@ -1345,18 +1345,25 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
       pa.PH = PH;
       pa.per = per;
       // persistent CTAs: as many as fit on the device at once
-      static int nsm = 0;
-      if (!nsm) FGT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+      int dev_id = 0, nsm = 0;
+      FGT_CUDA(cudaGetDevice(&dev_id));
+      FGT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
       // planes per dispatch: the w taps plus room for the group's a_0 spread
 #define FGT_PEN(NPL)                                                                                         \
   {                                                                                                          \
-    static int per_sm_dev[64]; /* attribute + occupancy resolved once per device (0: unset) */            \
-    int dev = 0;                                                                                             \
-    FGT_CUDA(cudaGetDevice(&dev));                                                                           \
-    int& per_sm = per_sm_dev[dev & 63];                                                                      \
-    if (per_sm <= 0) {                                                                                       \
-      FGT_CUDA(cudaFuncSetAttribute(spread_pencil_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PEN_SMEM)); \
-      FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
+    /* attribute + occupancy resolved once per device (0: unset), under a lock: the C ABI is */ \
+    /* reentrant and a process may drive several GPUs from several threads */                 \
+    static int per_sm_dev[64];                                                                               \
+    static std::mutex per_sm_mu;                                                                             \
+    int per_sm = 0;                                                                                          \
+    {                                                                                                        \
+      std::lock_guard<std::mutex> lock(per_sm_mu);                                                           \
+      int& slot = per_sm_dev[dev_id & 63];                                                                   \
+      if (slot <= 0) {                                                                                       \
+        FGT_CUDA(cudaFuncSetAttribute(spread_pencil_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PEN_SMEM)); \
+        FGT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&slot, spread_pencil_kernel<NPL>, PEN_WARPS * 32, PEN_SMEM)); \
+      }                                                                                                      \
+      per_sm = slot;                                                                                         \
     }                                                                                                        \
     const unsigned nblk = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(1, per_sm),       \
                                                         (job_bound * per + PEN_WARPS - 1) / PEN_WARPS));              \

@@ -17,7 +17,8 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .planewave import PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_factor, periodic_params, pw_params
+from .planewave import (EPS_MAX, EPS_MIN, PERIODIC_IMAGE_DELTA, clamp_tolerance, cutoff_factor,
+                        periodic_params, pw_params)
 from .tree import tree_params
 
 
@@ -27,6 +28,11 @@ class FgtParams:
     def __init__(self, dim, delta, epsilon, n_s, periodic, share=(0, 1)):
         if not delta > 0:
             raise ValueError("delta must be positive")
+        # the supported tolerance window of planewave.pw_params (planewave.py:80-82), enforced
+        # for every boundary; inside it the tree, the near-field cut and the quadrature all use
+        # the same clamped value (clamp_tolerance only moves [0.099, 0.1) to 0.099)
+        if not (EPS_MIN <= float(epsilon) < EPS_MAX):
+            raise ValueError(f"unsupported tolerance {float(epsilon):g}; need 1e-14 <= eps < 0.1")
         eps = clamp_tolerance(epsilon)
         self.tp, self.l_c_periodic, self.R = tree_params(dim, n_s, delta, eps, periodic)
         rank, size = share
