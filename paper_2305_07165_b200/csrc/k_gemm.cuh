@@ -29,17 +29,17 @@ struct GemmArgs {
 
 // CTA tile 32 x 48 (2 x 2 warps of 16 x 24); FLAT: 16 x 96 (1 x 4 warps) for M <= 16, so
 // a 16-row problem (e.g. the nh = 16 stored planes of config 5) wastes no DMMA rows
-template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false, bool TALL = false, bool MID = false>
+template <bool AC, bool BC, bool CRE, bool ACC, bool FLAT = false, bool TALL = false, int MID = 0>
 __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TALL (N <= 32): 64 x 32 (4 x 1 warps of 16 x 32, four 8-column tiles per warp)
-  // MID (M <= 32, 32 < N <= 40, e.g. the n_f x G axis-1 stage of a G = 33 grid): 32 x 40
-  // (2 x 1 warps of 16 x 40, five 8-column tiles per warp; 64 threads)
-  constexpr int NT = MID ? 5 : (TALL ? 4 : 3);
+  // MID = 4 / 5 (M <= 32, N <= 32 / 40, e.g. the n_f x G axis-1 stage per plane): 32 x 8 MID
+  // (2 x 1 warps of 16 x 8 MID, MID 8-column tiles per warp; 64 threads)
+  constexpr int NT = MID ? MID : (TALL ? 4 : 3);
   const int wm = FLAT ? 0 : ((TALL || MID) ? warp : warp >> 1), wn = FLAT ? warp : ((TALL || MID) ? 0 : warp & 1);
   const int64_t b = blockIdx.z + g.boff;
   const int m0 = blockIdx.y * (FLAT ? 16 : (TALL ? 64 : 32)) + wm * 16;
-  const int n0 = blockIdx.x * (FLAT ? 96 : (TALL ? 32 : (MID ? 40 : 48))) + wn * 24;
+  const int n0 = blockIdx.x * (FLAT ? 96 : (TALL ? 32 : (MID ? 8 * MID : 48))) + wn * 24;
   const double* A = g.A + (g.aidx ? g.aidx[b] : b) * g.sA * (AC ? 2 : 1);
   const double* B = g.B + (g.bidx ? g.bidx[b] : b) * g.sB * (BC ? 2 : 1);
   const int64_t cb = g.cidx ? g.cidx[b] : b;
@@ -178,10 +178,13 @@ void bgemm(const GemmArgs& g, cudaStream_t st) {
     const unsigned nz = (unsigned)std::min<int64_t>(65535, g.batch - b0);
     if (g.M <= 16) {
       bgemm_kernel<AC, BC, CRE, ACC, true><<<dim3((g.N + 95) / 96, 1, nz), 128, 0, st>>>(c);
+    } else if (g.M <= 32 && g.N <= 32) {
+      // small square blocks (per-plane axis-1 stages): one 32 x 32 tile, 64 threads
+      bgemm_kernel<AC, BC, CRE, ACC, false, false, 4><<<dim3(1, 1, nz), 64, 0, st>>>(c);
+    } else if (g.M <= 32 && g.N <= 40) {
+      bgemm_kernel<AC, BC, CRE, ACC, false, false, 5><<<dim3(1, 1, nz), 64, 0, st>>>(c);
     } else if (g.N <= 32) {
       bgemm_kernel<AC, BC, CRE, ACC, false, true><<<dim3(1, (g.M + 63) / 64, nz), 128, 0, st>>>(c);
-    } else if (g.M <= 32 && g.N <= 40) {
-      bgemm_kernel<AC, BC, CRE, ACC, false, false, true><<<dim3(1, 1, nz), 64, 0, st>>>(c);
     } else {
       bgemm_kernel<AC, BC, CRE, ACC><<<dim3((g.N + 47) / 48, (g.M + 31) / 32, nz), 128, 0, st>>>(c);
     }
