@@ -611,15 +611,6 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
 
 // u_host (optional): the result's device->host copy is enqueued right behind the scatter,
 // before the phase timings are read (which waits on the stream).
-// FGT_PSI=materialise | fused forces the translate-into-psi-then-evaluate path or the
-// fused translation + evaluation (A/B checks); default: chosen per transform
-static int psi_mode() {
-  const char* e = std::getenv("FGT_PSI");
-  if (e && !std::strcmp(e, "materialise")) return 1;
-  if (e && !std::strcmp(e, "fused")) return 2;
-  return 0;
-}
-
 static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, double* u_host = nullptr) {
   // phases of finish are timed from its own start: with the exchange path other ranks'
   // work and the all-to-all sit between begin and finish on a shared GPU
@@ -629,7 +620,7 @@ static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, doubl
   TreeDev& T = R.T;
   PwDev& P = R.P;
   if (T.n_dense > 0) {
-    pw_gather_eval(P, T, R.us.get(), R.NP, psi_mode());
+    pw_gather_eval(P, T, R.us.get(), R.NP);
     P.phi.release();
     P.psi.release();
   }

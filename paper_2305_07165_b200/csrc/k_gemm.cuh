@@ -25,6 +25,11 @@ struct GemmArgs {
   const int64_t* bidx;  // optional B batch index
   const int64_t* aidx;  // optional A batch index
   int64_t boff;         // batch offset of this launch (grid.z limit)
+  // optional epilogue rephasing of a d = 3 expansion stage (complex C, rows r = s n_f + m1
+  // over the stored half-spectrum planes s, columns m2): C[r][c] *= bp[k][0][hmi(s)]
+  // bp[k][1][m1] bp[k][2][c] with k = cidx[b] (box phases, (slot, 3, n_f) complex)
+  const double2* bp;
+  int bp_nf, bp_half;
 };
 
 // CTA tile 32 x 48 (2 x 2 warps of 16 x 24); FLAT: 16 x 96 (1 x 4 warps) for M <= 16, so
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
         }
       }
     }
-    if (AC && BC && !CRE && !TALL) {
+    if constexpr (AC && BC && !CRE && !TALL) {
       // complex x complex in three real products (Gauss): k1 = (ar + ai) br,
       // k2 = ar (bi - br), k3 = ai (br + bi); re = k1 - k3, im = k1 + k2, accumulated as
       // acc[0..1] = k1, acc[2..3] = k2, gauss[..] = k3 and combined in the epilogue
@@ -105,31 +110,31 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
           dmma2(gauss[mt][nt][0], gauss[mt][nt][1], ai[mt], bs[nt]);
         }
       }
-      continue;
-    }
-    // re += ar br - ai bi ; im += ar bi + ai br   (terms with a real operand vanish)
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
-    if (AC && BC) {
+    } else {
+      // re += ar br - ai bi ; im += ar bi + ai br   (terms with a real operand vanish)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
-    }
-    if (!CRE) {
-      if (BC) {
+        for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], ar[mt], br[nt]);
+      if (AC && BC) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][0], acc[mt][nt][1], -ai[mt], bi[nt]);
       }
-      if (AC) {
+      if (!CRE) {
+        if (BC) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+          for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
+            for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ar[mt], bi[nt]);
+        }
+        if (AC) {
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma2(acc[mt][nt][2], acc[mt][nt][3], ai[mt], br[nt]);
+        }
       }
     }
   }
@@ -161,6 +166,15 @@ __global__ void __launch_bounds__(128) bgemm_kernel(GemmArgs g) {
         } else {
           double2* cp = reinterpret_cast<double2*>(C + 2 * (r * g.ldc + c));
           double2 v = make_double2(acc[mt][nt][i], acc[mt][nt][2 + i]);
+          if (g.bp) {
+            const int nf = g.bp_nf, s = r / nf, m1 = r - s * nf;
+            const int i0 = g.bp_half ? (s + nf / 2) % nf : s;
+            const double2* q = g.bp + cb * 3 * nf;
+            const double2 p0 = q[i0], p1 = q[nf + m1], p2 = q[2 * nf + c];
+            const double2 p01 = make_double2(p0.x * p1.x - p0.y * p1.y, p0.x * p1.y + p0.y * p1.x);
+            const double2 ph = make_double2(p01.x * p2.x - p01.y * p2.y, p01.x * p2.y + p01.y * p2.x);
+            v = make_double2(ph.x * v.x - ph.y * v.y, ph.x * v.y + ph.y * v.x);
+          }
           if (ACC) { v.x += cp->x; v.y += cp->y; }
           *cp = v;
         }
@@ -204,6 +218,9 @@ inline GemmArgs gemm(const double* A, int64_t lda, int64_t sA, const double* B, 
   g.bidx = bidx;
   g.aidx = aidx;
   g.boff = 0;
+  g.bp = nullptr;
+  g.bp_nf = 0;
+  g.bp_half = 0;
   return g;
 }
 

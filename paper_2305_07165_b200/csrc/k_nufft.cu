@@ -1188,8 +1188,15 @@ void form_modes(const NufftPlan& N, PwDev& P, const double* grid, const int64_t*
     bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid, plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
     // Y[s][m2][g3] = sum_g2 Ef[m2][g2] X[s][g2][g3]      (batch = box x s)
     bgemm<true, true, false>(gemm(N.Ef.get(), G, 0, x.get(), G, (int64_t)G * G, y.get(), G, (int64_t)n_f * G, n_f, G, G, nbat * nh), st);
-    // phi[(s m2)][m3] = sum_g3 Y[(s m2)][g3] EfT[g3][m3]
-    bgemm<true, true, false>(gemm(y.get(), G, (int64_t)nh * n_f * G, N.EfT.get(), n_f, 0, phi, n_f, NH, nh * n_f, n_f, G, (int)nbat, sl), st);
+    // phi[(s m2)][m3] = sum_g3 Y[(s m2)][g3] EfT[g3][m3], times the box's rephasing factor
+    // e^{i k.(c_ref - c_S)} on the fused translation path (epilogue; no separate pass)
+    GemmArgs g3 = gemm(y.get(), G, (int64_t)nh * n_f * G, N.EfT.get(), n_f, 0, phi, n_f, NH, nh * n_f, n_f, G, (int)nbat, sl);
+    if (P.fused) {
+      g3.bp = reinterpret_cast<const double2*>(P.bp.get());
+      g3.bp_nf = n_f;
+      g3.bp_half = P.half;
+    }
+    bgemm<true, true, false>(g3, st);
   }
 }
 

@@ -22,6 +22,13 @@
 
 namespace fgt {
 
+int psi_mode() {
+  const char* e = std::getenv("FGT_PSI");
+  if (e && !std::strcmp(e, "materialise")) return 1;
+  if (e && !std::strcmp(e, "fused")) return 2;
+  return 0;
+}
+
 int nufft_mode() {
   const char* e = std::getenv("FGT_NUFFT_MODE");
   if (!e) return 0;
@@ -555,13 +562,15 @@ __global__ void box_phase_kernel(const int64_t* __restrict__ dense_ids, int64_t 
 // slot; the separable phase is a row factor (axes < d-1, from shared memory) times a
 // column factor (last axis, one per thread), two complex products per mode.
 template <int D>
-__global__ void __launch_bounds__(256) phi_rephase_kernel(double2* __restrict__ phi, int64_t nd, int64_t NH,
+__global__ void __launch_bounds__(256) phi_rephase_kernel(double2* __restrict__ phi, int64_t n,
+                                                          const int64_t* __restrict__ slots, int64_t NH,
                                                           int n_f, int RH, int half,
                                                           const double2* __restrict__ bp) {
   extern __shared__ double2 s_row[];  // RH
   const int CW = n_f <= 32 ? 32 : 64;
   const int c = threadIdx.x % CW, r0 = threadIdx.x / CW, rstep = blockDim.x / CW;
-  for (int64_t slot = blockIdx.x; slot < nd; slot += gridDim.x) {
+  for (int64_t it = blockIdx.x; it < n; it += gridDim.x) {
+    const int64_t slot = slots[it];
     const double2* b = bp + slot * D * n_f;
     __syncthreads();
     for (int r = threadIdx.x; r < RH; r += blockDim.x) {
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(256) phi_rephase_kernel(double2* __restrict__ 
   }
 }
 
-constexpr int64_t GE_AUTO_MAX_TPG = 128;  // fused path when targets per sibling group <= this
+constexpr int64_t GE_AUTO_MAX_TPL = 16;  // fused path when targets per level-l_c target leaf <= this
 
 struct GEArgs {
   const int64_t* psi_ids;
@@ -1236,6 +1245,14 @@ void pw_setup_dense(PwDev& P, const TreeDev& T, const fgt_pw_params& pw) {
   for (int l = 0; l < T.l_c; ++l) P.side_lc *= 0.5;
   P.w1d.alloc(P.n_f, st);
   P.w1d.from_host(pw.weights_1d, P.n_f);
+  // translation path: fused (psi on chip) unless the level-l_c target leaves hold more
+  // than GE_AUTO_MAX_TPL targets on average (evaluation then amortises a stored psi);
+  // periodic image shifts keep the materialised path
+  {
+    const int m = psi_mode();
+    const bool few = T.lc_targets <= GE_AUTO_MAX_TPL * std::max<int64_t>(1, T.lc_tleaves);
+    P.fused = !T.periodic && (m == 2 || (m == 0 && few));
+  }
   std::vector<double> ph(5 * 2 * P.n_f);
   for (int o = 0; o < 5; ++o)
     for (int mi = 0; mi < P.n_f; ++mi) {
@@ -1329,8 +1346,33 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
   for (int64_t s = 0; s < nd; ++s) P.n_src_dense += cnt[s];
   P.n_spread_boxes = (int64_t)spread_slots.size();
   P.k_form.begin(st);
+  if (P.fused) {
+    // box phases e^{i m sc (c_ref - c_S)} per slot and axis (phase_dd), used by the d = 3
+    // NUFFT's fused last stages and by the rephasing of every other expansion below
+    P.bp.alloc((size_t)nd * D * P.n_f * 2, st);
+    const double3 cref = make_double3(T.root_center[0], T.root_center[1], T.root_center[2]);
+    box_phase_kernel<D><<<grid_for(nd * D * P.n_f, 256), 256, 0, st>>>(T.dense_ids.get(), nd, T.center.get(), cref,
+                                                                         P.sc, P.n_f,
+                                                                         reinterpret_cast<double2*>(P.bp.get()));
+    FGT_LAUNCHED();
+  }
   if (!spread_slots.empty()) nufft_form(*N, P, T, spread_slots);
   trace_mark(st, "form:nufft");
+  // rephase the expansions not rephased by the d = 3 NUFFT stages (exact-sum boxes; all
+  // boxes for d <= 2) once they are complete
+  auto rephase_rest = [&](const std::vector<int64_t>& slots) {
+    if (!P.fused || slots.empty()) return;
+    DBuf<int64_t> sd(slots.size(), st);
+    sd.from_host(slots.data(), slots.size());
+    phi_rephase_kernel<D><<<grid_for((int64_t)slots.size(), 1, (int64_t)148 * 16), 256, P.RH * sizeof(double2), st>>>(
+        reinterpret_cast<double2*>(P.phi.get()), (int64_t)slots.size(), sd.get(), P.NH, P.n_f, (int)P.RH, P.half,
+        reinterpret_cast<const double2*>(P.bp.get()));
+    FGT_LAUNCHED();
+  };
+  if (D <= 2) rephase_rest(spread_slots);
+  std::vector<int64_t> exact_slots;
+  for (const int4& u : units)
+    if (exact_slots.empty() || exact_slots.back() != u.x) exact_slots.push_back(u.x);
   if (units.empty()) {
     P.k_form.end(st);
     return;
@@ -1382,6 +1424,7 @@ static void pw_form_impl(PwDev& P, TreeDev& T, const NufftPlan* N) {
                                                 P.NH, n_f, (int)P.half, P.w1d.get(), reinterpret_cast<double2*>(P.phi.get()));
     FGT_LAUNCHED();
   }
+  rephase_rest(exact_slots);
 }
 
 void pw_form(PwDev& P, TreeDev& T, const NufftPlan* N) {
@@ -1525,33 +1568,12 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
 #undef FGT_EVAL_D
 }
 
-void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int mode) {
+void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N) {
   const int64_t n = T.n_psi;
   if (n == 0) return;
   cudaStream_t st = T.st;
-  // psi boxes evaluated by the NUFFT interpolation path (many targets) need psi itself:
-  // they keep the materialising path (gather into <= 1 GB batches + nufft_eval); every
-  // other box is translated and evaluated by the fused kernel (psi stays on chip)
-  std::vector<int64_t> pstart(n, -1);
-  int64_t np = 0;
-  bool any_nufft = false;
-  for (int64_t i = 0; i < n; ++i) {
-    if (prefer_nufft(N, T.d, P.NH, P.h_cnt[i], 2.0)) {
-      any_nufft = true;
-    } else {
-      pstart[i] = np;
-      np += P.h_cnt[i];
-    }
-  }
-  // The fused kernel rebuilds its targets' phase tables for every mode chunk and pays the
-  // translation once per (group, chunk): it wins when sibling groups hold few targets
-  // (config 5: ~40, where psi would be ~98 GB of HBM traffic).  With hundreds of targets
-  // per group the per-chunk tables dominate and a materialised psi (<= 1 GB batches) is
-  // cheaper to stream: those transforms keep the gather + eval path.
-  const int64_t n_groups_all = (int64_t)P.h_goff.size() - 1;
-  if (mode == 0 && np > GE_AUTO_MAX_TPG * std::max<int64_t>(1, n_groups_all)) mode = 1;
-  if (T.periodic) mode = 1;  // image shifts: the rephased sum needs v = 0
-  if (mode == 1) {
+  if (!P.fused) {
+    // translate into psi (<= 1 GB batches), then evaluate (exact DMMA sums or NUFFT)
     const int64_t per = P.NH * 16;
     const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
     for (int64_t lo = 0; lo < n; lo += batch) {
@@ -1562,15 +1584,13 @@ void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, 
     P.psi.release();
     return;
   }
-  if (any_nufft) {
-    const int64_t per = P.NH * 16;
-    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(65535, ((int64_t)1 << 30) / per));
-    for (int64_t lo = 0; lo < n; lo += batch) {
-      const int64_t hi = std::min(n, lo + batch);
-      pw_gather(P, T, lo, hi);
-      pw_eval(P, T, u_sorted, N, lo, hi, /*nufft_only=*/true);
-    }
-    P.psi.release();
+  // fused: every psi box, exact evaluation (the expansions are stored rephased)
+  (void)N;
+  std::vector<int64_t> pstart(n, -1);
+  int64_t np = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    pstart[i] = np;
+    np += P.h_cnt[i];
   }
   if (np == 0) return;
   P.n_tgt_psi += np;
@@ -1598,7 +1618,6 @@ void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, 
   ga.n_f = n_f;
   ga.l_c = T.l_c;
   DBuf<double> tph((size_t)np * 6 * T.d, st);
-  DBuf<double> bp((size_t)T.n_dense * T.d * n_f * 2, st);
   GEArgs ea;
   ea.psi_ids = T.psi_ids.get();
   ea.tgt_start = T.tgt_start.get();
@@ -1622,13 +1641,6 @@ void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, 
 #define FGT_GE_D(DD)                                                                                   \
   group_table_kernel<DD><<<(unsigned)n_groups, 64, 0, st>>>(ga, gt_slot.get(), gt_code.get(),          \
                                                              gt_nu.get(), gt_out.get());               \
-  FGT_LAUNCHED();                                                                                      \
-  box_phase_kernel<DD><<<grid_for(T.n_dense * DD * n_f, 256), 256, 0, st>>>(                          \
-      T.dense_ids.get(), T.n_dense, T.center.get(), cref, P.sc, n_f, reinterpret_cast<double2*>(bp.get())); \
-  FGT_LAUNCHED();                                                                                      \
-  phi_rephase_kernel<DD><<<grid_for(T.n_dense, 1, (int64_t)148 * 16), 256, P.RH * sizeof(double2), st>>>( \
-      reinterpret_cast<double2*>(P.phi.get()), T.n_dense, P.NH, n_f, (int)P.RH, P.half,              \
-      reinterpret_cast<const double2*>(bp.get()));                                                    \
   FGT_LAUNCHED();                                                                                      \
   P.k_gather.end(st);                                                                                  \
   P.k_eval.begin(st);                                                                                  \

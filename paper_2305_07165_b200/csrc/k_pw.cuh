@@ -40,6 +40,11 @@ struct PwDev {
   int64_t psi_lo = 0, psi_hi = 0;
   // base pointer such that psi_view() + 2 * i * NH addresses psi box i of the batch
   double* psi_view() const { return psi.get() - 2 * psi_lo * NH; }
+  // fused translation path (pw_gather_eval): chosen before the form from the tree's
+  // level-l_c target statistics; the expansions are then stored rephased to the root
+  // centre, phi' = e^{i k.(c_ref - c_S)} phi (bp: (n_dense, d, n_f) complex box phases)
+  bool fused = false;
+  DBuf<double> bp;
   KClock k_form, k_gather, k_eval, k_direct;
   int64_t n_src_dense = 0, n_tgt_psi = 0, n_spread_boxes = 0, n_spread_psi = 0;
   int64_t n_src_spread = 0, n_tgt_spread = 0;
@@ -54,6 +59,8 @@ struct NufftPlan;
 // Per-box path selection between the exact tensor-factored sums (DMMA) and the box-local
 // NUFFT (spread + separable DFT): FGT_NUFFT_MODE=direct|spread forces one (tests).
 int nufft_mode();
+// FGT_PSI=materialise | fused forces the translation path (A/B checks); 0 = automatic
+int psi_mode();
 
 void pw_setup(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);  // = dense + psi
 void pw_setup_dense(PwDev& P, const TreeDev& T, const fgt_pw_params& pw);
@@ -67,8 +74,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
              bool nufft_only = false);
 // Translation fused with evaluation (psi kept on chip) for every psi box evaluated by the
 // exact sums; boxes routed to the NUFFT interpolation keep the gather + pw_eval path.
-// mode: 0 auto (fused when sibling groups hold few targets), 1 materialise psi, 2 fused.
-void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int mode);
+void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 // Continuous (box) FGT executor (k_volume.cu).

@@ -508,6 +508,21 @@ __global__ void leaf_start_kernel(const int64_t* __restrict__ sorted_leaf, int64
     start[b] = is_leaf[b] ? lower_bound_dev(sorted_leaf, n, b) : 0;
 }
 
+__global__ void lc_target_stats_kernel(const int32_t* __restrict__ level, const uint8_t* __restrict__ leaf,
+                                       const int64_t* __restrict__ tcount, int64_t nb, int l_c,
+                                       int64_t* __restrict__ out) {
+  unsigned long long nl = 0, nt = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    if (leaf[b] && level[b] == l_c && tcount[b] > 0) {
+      ++nl;
+      nt += (unsigned long long)tcount[b];
+    }
+  if (nl) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(out), nl);
+    atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), nt);
+  }
+}
+
 __global__ void dense_flag_kernel(const int32_t* __restrict__ level, const uint8_t* __restrict__ leaf,
                                   const int64_t* __restrict__ npoints, int64_t nb, int l_c,
                                   int64_t n_s, uint8_t* __restrict__ flag) {
@@ -827,7 +842,7 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
   const int64_t nb = B.n;
   T.nb = nb;
   // level offsets (l_c + 2), dense-box count, leaf count: one host round trip at the end
-  DBuf<int64_t> fin(l_c + 4, st);
+  DBuf<int64_t> fin(l_c + 6, st);  // + (level-l_c leaves with targets, their targets)
   level_offsets_kernel<<<1, 64, 0, st>>>(B.keys.get(), B.n, l_c + 1, fin.get());
   FGT_LAUNCHED();
   T.bkey = std::move(B.keys);
@@ -940,22 +955,29 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     FGT_CUDA(cub::DeviceReduce::Sum(nullptr, b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     FGT_CUDA(cub::DeviceReduce::Sum(tmp.get(b2, st), b2, T.is_leaf.get(), fin.get() + l_c + 3, (int)nb, st));
     count_launch();
+    // level-l_c target leaves and their targets (the translation path choice)
+    FGT_CUDA(cudaMemsetAsync(fin.get() + l_c + 4, 0, 2 * sizeof(int64_t), st));
+    lc_target_stats_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.level.get(), T.is_leaf.get(), T.tgt_count.get(), nb,
+                                                              l_c, fin.get() + l_c + 4);
+    FGT_LAUNCHED();
     // one pinned block for both read-backs (per thread, grown as needed)
     static thread_local int64_t* hp = nullptr;
     static thread_local int64_t hp_cap = 0;
-    const int64_t need = l_c + 4 + nb;
+    const int64_t need = l_c + 6 + nb;
     if (need > hp_cap) {
       if (hp) FGT_CUDA(cudaFreeHost(hp));
       hp_cap = std::max<int64_t>(need, 2 * hp_cap);
       FGT_CUDA(cudaMallocHost((void**)&hp, hp_cap * sizeof(int64_t)));
     }
     trace_mark(st, "tree:finalize");
-    FGT_CUDA(cudaMemcpyAsync(hp, fin.get(), (l_c + 4) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    FGT_CUDA(cudaMemcpyAsync(hp + l_c + 4, dsrc.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaMemcpyAsync(hp, fin.get(), (l_c + 6) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaMemcpyAsync(hp + l_c + 6, dsrc.get(), nb * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     FGT_CUDA(cudaStreamSynchronize(st));
     trace_mark(st, "tree:finalize(sync)");
-    std::vector<int64_t> h(hp, hp + l_c + 4);
-    T.h_dense_src.assign(hp + l_c + 4, hp + l_c + 4 + h[l_c + 2]);
+    std::vector<int64_t> h(hp, hp + l_c + 6);
+    T.h_dense_src.assign(hp + l_c + 6, hp + l_c + 6 + h[l_c + 2]);
+    T.lc_tleaves = h[l_c + 4];
+    T.lc_targets = h[l_c + 5];
     T.level_off.assign(h.begin(), h.begin() + l_c + 2);
     T.n_dense = h[l_c + 2];
     T.n_leaves = h[l_c + 3];

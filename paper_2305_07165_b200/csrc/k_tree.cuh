@@ -33,6 +33,7 @@ struct TreeDev {
   DBuf<int64_t> dense_ids;   // (n_dense) box ids of P-boxes
   DBuf<int64_t> dense_slot;  // (nb) index into dense_ids or -1
   std::vector<int64_t> h_dense_src;  // host: source count of every P-box (n_dense)
+  int64_t lc_tleaves = 0, lc_targets = 0;  // host: level-l_c leaves with targets, their targets
 
   // lists (target-centric), built by build_lists()
   bool lists_built = false;
