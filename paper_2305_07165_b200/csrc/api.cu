@@ -196,32 +196,8 @@ __global__ void scatter_kernel(const double* __restrict__ us, const int64_t* __r
     u[perm[i]] = us[i];
 }
 
-__global__ void leaf_direct_cost_kernel(const int64_t* __restrict__ tl, int64_t n,
-                                        const int64_t* __restrict__ d_off, const int64_t* __restrict__ d_src,
-                                        const int64_t* __restrict__ scount, const int64_t* __restrict__ tcount,
-                                        const int64_t* __restrict__ dense_slot, double* __restrict__ nt_out,
-                                        double* __restrict__ pairs_out, double* __restrict__ form_out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0;
-    for (int64_t e = d_off[i]; e < d_off[i + 1]; ++e) s += (double)scount[d_src[e]];
-    const int64_t T = tl[i];
-    double t = (double)tcount[T];
-    nt_out[i] = t;
-    pairs_out[i] = t * s;
-    form_out[i] = dense_slot[T] >= 0 ? (double)scount[T] : 0.0;  // sources of a P-box leaf
-  }
-}
 
-__global__ void gather_i64_kernel(const uint64_t* __restrict__ a, const int64_t* __restrict__ ids, int64_t n,
-                                  int64_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (int64_t)a[ids[i]];
-}
 
-__global__ void iota_pos_kernel(int64_t* a, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) a[i] = i;
-}
 
 // the rank's direct target leaves (positions into the replicated CSR): ids, begin, end
 __global__ void restrict_direct_kernel(const int64_t* __restrict__ pos, int64_t n, const int64_t* __restrict__ tl,
@@ -281,148 +257,183 @@ __global__ void unpack_slots_kernel(double2* __restrict__ phi, const int64_t* __
   }
 }
 
+// ---- share planning on the device: per target leaf its cost, its Morton key across levels
+// (code at l_c of its first cell) and its psi index; the leaves are sorted by that key, the
+// cost prefix sum cut into `size` balanced ranges, every P-box's owner found from its key
+// and every rank's needs marked with a bit per rank (one pass over the P entries).  Only
+// per-rank bounds and per-slot owner / need words (n_dense entries) come back to the host.
+__device__ __forceinline__ uint64_t deep_key(uint64_t key, int d, int l_c) {
+  return key_code(key) << (d * (l_c - key_level(key)));
+}
+
+__global__ void share_leaf_kernel(const int64_t* __restrict__ tl, int64_t n, const int64_t* __restrict__ d_off,
+                                  const int64_t* __restrict__ d_src, const int64_t* __restrict__ scount,
+                                  const int64_t* __restrict__ tcount, const int64_t* __restrict__ dense_slot,
+                                  const int64_t* __restrict__ psi_ids, int64_t nps, const int64_t* __restrict__ p_off,
+                                  const uint64_t* __restrict__ bkey, int d, int l_c, double NH, double form_ns,
+                                  double* __restrict__ cost, uint64_t* __restrict__ dk, int64_t* __restrict__ iota,
+                                  uint8_t* __restrict__ has_psi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t T = tl[i];
+    double src = 0;
+    for (int64_t e = d_off[i]; e < d_off[i + 1]; ++e) src += (double)scount[d_src[e]];
+    const double nt = (double)tcount[T];
+    // cost in ns, calibrated on the B200 kernels: direct ~10 ps per pair, eval 8 N_H flops
+    // per target at ~21 TFLOP/s, gather ~2.4 ps per stored mode per P entry; with the
+    // exchange a P-box's form (~2.4 ns per source at w = 11, ~w^3) is charged to its leaf
+    double c = 0.01 * nt * src + (dense_slot[T] >= 0 ? form_ns * (double)scount[T] : 0.0);
+    const int64_t j = find_dev(psi_ids, nps, T);
+    if (j >= 0) c += 8.0 * NH * nt / 21e3 + 2.4e-3 * NH * (double)(p_off[j + 1] - p_off[j]);
+    cost[i] = c;
+    dk[i] = deep_key(bkey[T], d, l_c);
+    iota[i] = i;
+    has_psi[i] = j >= 0;
+  }
+}
+
+__global__ void share_order_kernel(const int64_t* __restrict__ ord, int64_t n, const double* __restrict__ cost,
+                                   const uint8_t* __restrict__ has_psi, double* __restrict__ cost_o,
+                                   int64_t* __restrict__ psi_flag_o) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    cost_o[k] = cost[ord[k]];
+    psi_flag_o[k] = has_psi[ord[k]];
+  }
+}
+
+// one thread: b[r] (leaf ranges, the host partition_bounds rule on the inclusive prefix),
+// pb[r] (psi index ranges: psi boxes appear in ascending index along the Morton order),
+// thr[r] (first Morton key of rank r); out = [b (P+1) | pb (P+1) | thr (P+1)]
+__global__ void share_bounds_kernel(const double* __restrict__ pre, const int64_t* __restrict__ psi_cnt,
+                                    const uint64_t* __restrict__ dks, int64_t n, int64_t nps, int P,
+                                    int64_t* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  const double total = n > 0 ? pre[n - 1] : 0.0;
+  int64_t* b = out;
+  int64_t* pb = out + P + 1;
+  uint64_t* thr = reinterpret_cast<uint64_t*>(out + 2 * (P + 1));
+  b[0] = 0;
+  b[P] = n;
+  for (int r = 1; r < P; ++r) {
+    const double t = total * r / P;
+    int64_t lo = 0, hi = n;  // first i with pre[i] >= t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (pre[mid] >= t) hi = mid; else lo = mid + 1;
+    }
+    b[r] = lo < n ? lo + 1 : n;
+    if (b[r] < b[r - 1]) b[r] = b[r - 1];
+  }
+  for (int r = 0; r <= P; ++r) {
+    pb[r] = b[r] < n ? psi_cnt[b[r]] : nps;
+    thr[r] = b[r] < n ? dks[b[r]] : ~(uint64_t)0;
+  }
+  thr[0] = 0;
+}
+
+__global__ void share_need_kernel(const int64_t* __restrict__ bounds, int P, int64_t nps,
+                                  const int64_t* __restrict__ p_off, const int64_t* __restrict__ p_src,
+                                  unsigned long long* __restrict__ need) {
+  const int64_t* pb = bounds + P + 1;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nps; j += (int64_t)gridDim.x * blockDim.x) {
+    int r = 0;
+    while (r + 1 < P && pb[r + 1] <= j) ++r;
+    const unsigned long long bit = 1ull << r;
+    for (int64_t e = p_off[j]; e < p_off[j + 1]; ++e) atomicOr(&need[p_src[e]], bit);
+  }
+}
+
+__global__ void share_owner_kernel(const int64_t* __restrict__ bounds, int P, const int64_t* __restrict__ dense_ids,
+                                   int64_t nd, const uint64_t* __restrict__ bkey, int d, int l_c,
+                                   int32_t* __restrict__ owner) {
+  const uint64_t* thr = reinterpret_cast<const uint64_t*>(bounds + 2 * (P + 1));
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nd; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = deep_key(bkey[dense_ids[s]], d, l_c);
+    int r = 0;
+    while (r + 1 < P && thr[r + 1] <= key) ++r;
+    owner[s] = r;
+  }
+}
+
 static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool exchange, ExchangePlan* X) {
   cudaStream_t st = T.st;
-  const int64_t n = T.n_dtgt;
-  // everything the host needs, staged contiguously on the device: one D2H, one sync
-  const int64_t np_ = T.n_p, nps = T.n_psi, nd = T.n_dense;
-  const int64_t o_nt = 0, o_pr = n, o_fs = 2 * n, o_tl = 3 * n, o_psi = 4 * n, o_poff = o_psi + nps,
-                o_psrc = o_poff + nps + 1, o_dense = o_psrc + np_, o_ktl = o_dense + nd, o_kd = o_ktl + n,
-                tot = o_kd + nd;
-  DBuf<int64_t> stage(tot, st);
-  if (n > 0) {
-    double* sd = reinterpret_cast<double*>(stage.get());
-    leaf_direct_cost_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.d_tgt_ids.get(), n, T.d_off.get(), T.d_src.get(),
-                                                              T.src_count.get(), T.tgt_count.get(),
-                                                              T.dense_slot.get(), sd + o_nt, sd + o_pr, sd + o_fs);
-    FGT_LAUNCHED();
-  }
-  auto d2d = [&](int64_t off, const int64_t* srcp, int64_t cnt) {
-    if (cnt > 0) FGT_CUDA(cudaMemcpyAsync(stage.get() + off, srcp, cnt * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-  };
-  d2d(o_tl, T.d_tgt_ids.get(), n);
-  d2d(o_psi, T.psi_ids.get(), nps);
-  d2d(o_poff, T.p_off.get(), nps + 1);
-  d2d(o_psrc, T.p_src.get(), np_);
-  d2d(o_dense, T.dense_ids.get(), nd);
-  // box keys (level << 58 | Morton code) of the target leaves and of the P-boxes
-  if (n > 0) {
-    gather_i64_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.bkey.get(), T.d_tgt_ids.get(), n, stage.get() + o_ktl);
-    FGT_LAUNCHED();
-  }
-  if (nd > 0) {
-    gather_i64_kernel<<<grid_for(nd, 256), 256, 0, st>>>(T.bkey.get(), T.dense_ids.get(), nd, stage.get() + o_kd);
-    FGT_LAUNCHED();
-  }
-  // page-locked host staging (per thread, grown as needed): the D2H runs at link speed
-  static thread_local int64_t* hbuf = nullptr;
-  static thread_local int64_t hcap = 0;
-  if (tot > hcap) {
-    if (hbuf) FGT_CUDA(cudaFreeHost(hbuf));
-    hcap = std::max<int64_t>(tot, 2 * hcap);
-    FGT_CUDA(cudaMallocHost((void**)&hbuf, hcap * sizeof(int64_t)));
-  }
-  int64_t* h = hbuf;
-  trace_mark(st, "share:stage");
-  if (tot > 0) FGT_CUDA(cudaMemcpyAsync(h, stage.get(), tot * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FGT_CUDA(cudaStreamSynchronize(st));
-  trace_mark(st, "share:d2h(sync)");
-  auto dv = [&](int64_t off, int64_t cnt) {
-    std::vector<double> v(cnt);
-    if (cnt) std::memcpy(v.data(), h + off, cnt * sizeof(double));
-    return v;
-  };
-  const std::vector<double> nt = dv(o_nt, n), pairs = dv(o_pr, n), fsrc = dv(o_fs, n);
-  const int64_t* tl = h + o_tl;
-  const int64_t* psi = h + o_psi;
-  const int64_t* poff = h + o_poff;
-  const int64_t* psrc = h + o_psrc;
-  // cost in ns, calibrated on the B200 kernels (profiles/r01f_*): eval 8 N_H flops per
-  // target at ~21 TFLOP/s, gather ~2.4 ps per stored mode per P entry, direct ~10 ps per
-  // pair; with the exchange, a P-box's form (~2.4 ns per source at w = 11, ~w^3) is
-  // charged to the leaf position that owns it
+  FGT_REQUIRE(size <= 64, FGT_ERANGE, "at most 64 ranks");
+  const int64_t n = T.n_dtgt, nps = T.n_psi, nd = T.n_dense;
+  const int P = size;
   const double form_ns = exchange ? 2.4 * std::pow(w / 11.0, 3) : 0.0;
-  std::vector<double> cost(n);
-  std::vector<int64_t> psi_of(n, -1);
-  for (int64_t i = 0, j = 0; i < n; ++i) {
-    while (j < T.n_psi && psi[j] < tl[i]) ++j;
-    double c = 0.01 * pairs[i] + form_ns * fsrc[i];
-    if (j < T.n_psi && psi[j] == tl[i]) {
-      psi_of[i] = j;
-      c += 8.0 * NH * nt[i] / 21e3 + 2.4e-3 * NH * (double)(poff[j + 1] - poff[j]);
-    }
-    cost[i] = c;
-  }
-  // Leaves in Morton order across levels (key = code at l_c, i.e. code << d (l_c - level)),
-  // so a rank's contiguous range is a compact region of space and its halo is one box deep
-  // (box ids are level-major: a range of them would span all coarse leaves of the domain).
-  const int dd = T.d, lc = T.l_c;
-  auto deep = [&](int64_t key) {
-    const uint64_t k = (uint64_t)key;
-    return key_code(k) << (dd * (lc - key_level(k)));
-  };
-  std::vector<uint64_t> dk(n);
-  for (int64_t i = 0; i < n; ++i) dk[i] = deep(h[o_ktl + i]);
-  // Morton order across levels: radix sort of (deep key, position) on the device
-  std::vector<int64_t> ord(n);
+  DBuf<double> cost(std::max<int64_t>(n, 1), st), cost_o(std::max<int64_t>(n, 1), st), pre(std::max<int64_t>(n, 1), st);
+  DBuf<uint64_t> dk(std::max<int64_t>(n, 1), st), dks(std::max<int64_t>(n, 1), st);
+  DBuf<int64_t> iota(std::max<int64_t>(n, 1), st), ord(std::max<int64_t>(n, 1), st),
+      psi_flag(std::max<int64_t>(n, 1), st), psi_cnt(std::max<int64_t>(n, 1), st), bounds(3 * (P + 1), st);
+  DBuf<uint8_t> has_psi(std::max<int64_t>(n, 1), st);
+  DBuf<unsigned long long> need(std::max<int64_t>(nd, 1), st);
+  DBuf<int32_t> owner(std::max<int64_t>(nd, 1), st);
+  DBuf<uint8_t> tmp;
   if (n > 0) {
-    DBuf<uint64_t> kin(n, st), kout(n, st);
-    DBuf<int64_t> vin(n, st), vout(n, st);
-    kin.from_host(dk.data(), n);
-    iota_pos_kernel<<<grid_for(n, 256), 256, 0, st>>>(vin.get(), n);
+    share_leaf_kernel<<<grid_for(n, 256), 256, 0, st>>>(T.d_tgt_ids.get(), n, T.d_off.get(), T.d_src.get(),
+                                                        T.src_count.get(), T.tgt_count.get(), T.dense_slot.get(),
+                                                        T.psi_ids.get(), nps, T.p_off.get(), T.bkey.get(), T.d, T.l_c,
+                                                        (double)NH, form_ns, cost.get(), dk.get(), iota.get(),
+                                                        has_psi.get());
     FGT_LAUNCHED();
     size_t bytes = 0;
-    const int bits = std::max(1, dd * lc);
-    FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.get(), kout.get(), vin.get(), vout.get(), (int)n, 0, bits, st));
-    DBuf<uint8_t> tmpb(bytes, st);
-    FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmpb.get(), bytes, kin.get(), kout.get(), vin.get(), vout.get(), (int)n, 0, bits, st));
+    const int bits = std::max(1, T.d * T.l_c);
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk.get(), dks.get(), iota.get(), ord.get(), (int)n, 0, bits, st));
+    tmp.alloc(bytes, st);
+    FGT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, dk.get(), dks.get(), iota.get(), ord.get(), (int)n, 0, bits, st));
     count_launch();
-    vout.to_host(ord.data(), n);
-    FGT_CUDA(cudaStreamSynchronize(st));
+    share_order_kernel<<<grid_for(n, 256), 256, 0, st>>>(ord.get(), n, cost.get(), has_psi.get(), cost_o.get(),
+                                                         psi_flag.get());
+    FGT_LAUNCHED();
+    bytes = 0;
+    FGT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, cost_o.get(), pre.get(), (int)n, st));
+    if (bytes > tmp.size()) tmp.alloc(bytes, st);
+    FGT_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, cost_o.get(), pre.get(), (int)n, st));
+    bytes = 0;
+    FGT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, psi_flag.get(), psi_cnt.get(), (int)n, st));
+    if (bytes > tmp.size()) tmp.alloc(bytes, st);
+    FGT_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, psi_flag.get(), psi_cnt.get(), (int)n, st));
+    count_launch();
   }
-  trace_mark(st, "share:order");
-  std::vector<double> cost_o(n);
-  std::vector<int64_t> psi_o(n);
-  std::vector<uint64_t> dk_o(n);
-  for (int64_t k = 0; k < n; ++k) {
-    cost_o[k] = cost[ord[k]];
-    psi_o[k] = psi_of[ord[k]];
-    dk_o[k] = dk[ord[k]];
+  share_bounds_kernel<<<1, 1, 0, st>>>(pre.get(), psi_cnt.get(), dks.get(), n, nps, P, bounds.get());
+  FGT_LAUNCHED();
+  if (nd > 0) {
+    need.zero();
+    share_need_kernel<<<grid_for(std::max<int64_t>(nps, 1), 256), 256, 0, st>>>(bounds.get(), P, nps, T.p_off.get(),
+                                                                                 T.p_src.get(), need.get());
+    FGT_LAUNCHED();
+    share_owner_kernel<<<grid_for(nd, 256), 256, 0, st>>>(bounds.get(), P, T.dense_ids.get(), nd, T.bkey.get(), T.d,
+                                                          T.l_c, owner.get());
+    FGT_LAUNCHED();
   }
-  std::vector<int64_t> b = partition_bounds(cost_o, size);
-  // psi boxes (level l_c, ascending code = ascending psi index) appear in ascending index
-  // along the Morton order, so every rank's psi boxes are one index range
-  auto first_psi = [&](int64_t i) {
-    for (; i < n; ++i)
-      if (psi_o[i] >= 0) return psi_o[i];
-    return T.n_psi;
-  };
-  std::vector<int64_t> pb(size + 1);  // psi index range of every rank
-  for (int r = 0; r <= size; ++r) pb[r] = first_psi(b[r]);
-  const int64_t lo = b[rank], hi = b[rank + 1];
-  const int64_t plo = pb[rank], phi = pb[rank + 1];
-  // slots needed by every rank (from the replicated lists): one pass over the P entries,
-  // a rank bit mask per slot (world <= 64)
-  FGT_REQUIRE(size <= 64, FGT_ERANGE, "at most 64 ranks");
-  std::vector<uint64_t> need(T.n_dense, 0);
-  for (int r = 0; r < size; ++r)
-    for (int64_t e = poff[pb[r]]; e < poff[pb[r + 1]]; ++e) need[psrc[e]] |= (uint64_t)1 << r;
+  // read back: bounds (3 (P + 1)), need (nd), owner (nd) into one pinned block
+  static thread_local char* hbuf = nullptr;
+  static thread_local size_t hcap = 0;
+  const size_t o_need = 3 * (P + 1) * sizeof(int64_t), o_own = o_need + nd * sizeof(uint64_t),
+               tot = o_own + nd * sizeof(int32_t);
+  if (tot > hcap) {
+    if (hbuf) FGT_CUDA(cudaFreeHost(hbuf));
+    hcap = std::max(tot, 2 * hcap);
+    FGT_CUDA(cudaMallocHost((void**)&hbuf, hcap));
+  }
+  trace_mark(st, "share:plan(device)");
+  FGT_CUDA(cudaMemcpyAsync(hbuf, bounds.get(), o_need, cudaMemcpyDeviceToHost, st));
+  if (nd > 0) {
+    FGT_CUDA(cudaMemcpyAsync(hbuf + o_need, need.get(), nd * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    FGT_CUDA(cudaMemcpyAsync(hbuf + o_own, owner.get(), nd * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  FGT_CUDA(cudaStreamSynchronize(st));
+  trace_mark(st, "share:d2h(sync)");
+  const int64_t* hb = reinterpret_cast<const int64_t*>(hbuf);
+  const int64_t* hpb = hb + P + 1;
+  const uint64_t* hneed = reinterpret_cast<const uint64_t*>(hbuf + o_need);
+  const int32_t* hown = reinterpret_cast<const int32_t*>(hbuf + o_own);
+  const int64_t lo = hb[rank], hi = hb[rank + 1];
+  const int64_t plo = hpb[rank], phi = hpb[rank + 1];
   const uint64_t me = (uint64_t)1 << rank;
-  T.dense_need.assign(T.n_dense, 0);
+  T.dense_need.assign(nd, 0);
   if (!exchange) {
-    for (int64_t s = 0; s < T.n_dense; ++s) T.dense_need[s] = (need[s] & me) != 0;
+    for (int64_t s = 0; s < nd; ++s) T.dense_need[s] = (hneed[s] & me) != 0;
   } else {
-    // owner of a slot: the rank whose target-leaf range holds the box's position
-    std::vector<int> owner(T.n_dense);
-    // rank r owns deep keys in [thr[r], thr[r + 1]) (thr[r] = key of its first leaf)
-    std::vector<uint64_t> thr(size + 1, ~(uint64_t)0);
-    for (int r = 0; r < size; ++r) thr[r] = b[r] < n ? dk_o[b[r]] : ~(uint64_t)0;
-    thr[0] = 0;
-    for (int64_t s = 0; s < T.n_dense; ++s) {
-      const uint64_t key = deep(h[o_kd + s]);
-      int r = (int)(std::upper_bound(thr.begin(), thr.begin() + size, key) - thr.begin()) - 1;
-      owner[s] = std::max(0, std::min(size - 1, r));
-    }
     X->rank = rank;
     X->world = size;
     X->send_off.assign(size + 1, 0);
@@ -430,15 +441,15 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
     // per peer, slots in ascending order on both sides: the owner sends what the peer needs,
     // the peer receives what it needs from that owner
     std::vector<std::vector<int64_t>> sendr(size), recvr(size);
-    for (int64_t s = 0; s < T.n_dense; ++s) {
-      const uint64_t m = need[s];
+    for (int64_t s = 0; s < nd; ++s) {
+      const uint64_t m = hneed[s];
       if (!m) continue;
-      if (owner[s] == rank) {
+      if (hown[s] == rank) {
         T.dense_need[s] = 1;
         for (int r = 0; r < size; ++r)
           if (r != rank && ((m >> r) & 1)) sendr[r].push_back(s);
       } else if (m & me) {
-        recvr[owner[s]].push_back(s);
+        recvr[hown[s]].push_back(s);
       }
     }
     std::vector<int64_t> send, recv;
@@ -458,11 +469,9 @@ static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool e
   // replicated entry arrays)
   {
     const int64_t m = hi - lo;
-    DBuf<int64_t> pos(std::max<int64_t>(m, 1), st), ids(std::max<int64_t>(m, 1), st), beg(std::max<int64_t>(m, 1), st),
-        end(std::max<int64_t>(m, 1), st);
+    DBuf<int64_t> ids(std::max<int64_t>(m, 1), st), beg(std::max<int64_t>(m, 1), st), end(std::max<int64_t>(m, 1), st);
     if (m > 0) {
-      pos.from_host(ord.data() + lo, m);
-      restrict_direct_kernel<<<grid_for(m, 256), 256, 0, st>>>(pos.get(), m, T.d_tgt_ids.get(), T.d_off.get(),
+      restrict_direct_kernel<<<grid_for(m, 256), 256, 0, st>>>(ord.get() + lo, m, T.d_tgt_ids.get(), T.d_off.get(),
                                                                ids.get(), beg.get(), end.get());
       FGT_LAUNCHED();
     }
