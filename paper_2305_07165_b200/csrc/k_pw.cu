@@ -47,7 +47,11 @@ double box_dft_cost(int D, int G, int n_f) {
   return 0.5 * g * g * g * h + h * g * g * n + h * n * g * n;
 }
 // true if the box-local NUFFT beats the exact sums for a box with npts points
-bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double tap_cost) {
+// tap_cost: relative cost of one kernel tap per point; fixed_mult: weight of the per-box
+// grid <-> mode transform (the evaluation's batched transforms + interpolation measured ~2x
+// the form's per box: with G = 39 at config 2 a factor 1 sent 145-164-target boxes to a
+// slower NUFFT evaluation)
+bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double tap_cost, double fixed_mult = 1.0) {
   // NF: stored modes per expansion
   if (!N) return false;
   if (N->G > 64) return false;  // beyond the spreading kernels' grid (wide root series)
@@ -57,7 +61,7 @@ bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double ta
   double taps = 1;
   for (int k = 0; k < D; ++k) taps *= N->w;
   const double direct = (double)npts * NF;
-  const double spread = tap_cost * npts * taps + box_dft_cost(D, N->G, N->n_f) + 32.0 * NF;
+  const double spread = tap_cost * npts * taps + fixed_mult * (box_dft_cost(D, N->G, N->n_f) + 32.0 * NF);
   return direct > spread;
 }
 }  // namespace
@@ -1500,7 +1504,7 @@ void pw_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N, int64_t
     const int64_t n = hi - lo;
     const int64_t* h = h_cnt_all;
     for (int64_t i = 0; i < n; ++i) {
-      if (prefer_nufft(N, T.d, P.NH, h[i], 2.0)) {
+      if (prefer_nufft(N, T.d, P.NH, h[i], 2.0, 2.0)) {
         spread_list.push_back(lo + i);
         P.n_tgt_spread += h[i];
         P.n_tgt_psi += h[i];

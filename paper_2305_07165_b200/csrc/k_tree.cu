@@ -545,16 +545,6 @@ __global__ void fill_i64_kernel(int64_t* a, int64_t n, int64_t v) {
     a[i] = v;
 }
 
-template <int D>
-__global__ void gather_rows_kernel(const double* __restrict__ a, const int64_t* __restrict__ perm,
-                                   int64_t n, double* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = perm[i];
-#pragma unroll
-    for (int k = 0; k < D; ++k) out[i * D + k] = a[j * D + k];
-  }
-}
 
 
 // Box-set state during construction.
@@ -998,25 +988,53 @@ void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, in
   else build_tree_impl<3>(T, src, ns, tgt, nt, tp, st);
 }
 
+// sources with their charges in one pass (one read of the permutation), UNR independent
+// rows per thread so several random row reads are in flight
+template <int D>
+__global__ void __launch_bounds__(256) gather_src_q_kernel(const double* __restrict__ a, const double* __restrict__ q,
+                                                           const int64_t* __restrict__ perm, int64_t n,
+                                                           double* __restrict__ out, double* __restrict__ qout) {
+  constexpr int UNR = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * UNR) {
+    int64_t j[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) j[u] = i0 + u * stride < n ? perm[i0 + u * stride] : -1;
+    double v[UNR][D + 1];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (j[u] < 0) continue;
+#pragma unroll
+      for (int k = 0; k < D; ++k) v[u][k] = a[j[u] * D + k];
+      if (q) v[u][D] = q[j[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (j[u] < 0) continue;
+      const int64_t i = i0 + u * stride;
+#pragma unroll
+      for (int k = 0; k < D; ++k) out[i * D + k] = v[u][k];
+      if (q) qout[i] = v[u][D];
+    }
+  }
+}
+
 void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt) {
   cudaStream_t st = T.st;
   const int d = T.d;
   T.src_sorted.alloc(T.ns * d, st);
   T.tgt_sorted.alloc(T.nt * d, st);
-  auto gather = [&](const double* a, const int64_t* perm, int64_t n, double* out, int dd) {
+  if (q) T.q_sorted.alloc(T.ns, st);
+  auto gather = [&](const double* a, const double* qq, const int64_t* perm, int64_t n, double* out, double* qo) {
     if (n == 0) return;
-    unsigned g = grid_for(n, 256);
-    if (dd == 1) gather_rows_kernel<1><<<g, 256, 0, st>>>(a, perm, n, out);
-    else if (dd == 2) gather_rows_kernel<2><<<g, 256, 0, st>>>(a, perm, n, out);
-    else gather_rows_kernel<3><<<g, 256, 0, st>>>(a, perm, n, out);
+    unsigned g = grid_for(n, 256 * 4);
+    if (d == 1) gather_src_q_kernel<1><<<g, 256, 0, st>>>(a, qq, perm, n, out, qo);
+    else if (d == 2) gather_src_q_kernel<2><<<g, 256, 0, st>>>(a, qq, perm, n, out, qo);
+    else gather_src_q_kernel<3><<<g, 256, 0, st>>>(a, qq, perm, n, out, qo);
     FGT_LAUNCHED();
   };
-  gather(src, T.src_perm.get(), T.ns, T.src_sorted.get(), d);
-  gather(tgt, T.tgt_perm.get(), T.nt, T.tgt_sorted.get(), d);
-  if (q) {
-    T.q_sorted.alloc(T.ns, st);
-    gather(q, T.src_perm.get(), T.ns, T.q_sorted.get(), 1);
-  }
+  gather(src, q, T.src_perm.get(), T.ns, T.src_sorted.get(), q ? T.q_sorted.get() : nullptr);
+  gather(tgt, nullptr, T.tgt_perm.get(), T.nt, T.tgt_sorted.get(), nullptr);
 }
 
 // ====================================================================== lists
