@@ -565,8 +565,11 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
     FGT_CUDA(cudaStreamWaitEvent(sb, e_tree.e, 0));
     R.pm->mark();  // (lists: on the side stream, timed by k_lists)
     T.st = sb;
+    // side-stream busy time only: two intervals (enumeration; compaction + psi metadata),
+    // not the span in between while the host enqueues the form
     R.k_lists.begin(sb);
     build_lists_begin(T);  // list enumeration, no host wait
+    R.k_lists.end(sb);
     T.st = st;
     R.us.alloc(nt, st);
     R.us.zero();
@@ -578,6 +581,7 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
     R.pm->mark();
     trace_mark(st, "form(enqueued)");
     T.st = sb;
+    R.k_lists.begin(sb);
     build_lists_end(T);
     pw_setup_psi(R.P, T);
     R.k_lists.end(sb);
