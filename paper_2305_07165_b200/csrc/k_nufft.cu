@@ -67,6 +67,7 @@ __host__ __device__ __forceinline__ double es_kernel(double z, double beta) {
 }
 
 constexpr int MAXW = 16;
+constexpr int PROXY_PMAX = 48;  // proxy-point form: Chebyshev nodes per axis
 
 // ------------------------------------------------------------------ spreading
 // Pass 1 (one thread per point): first tap a_k (0-based grid index) and the w kernel
@@ -969,6 +970,127 @@ __global__ void __launch_bounds__(256) interp_kernel(InterpArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ proxy charges
+// grid[b][a_0][a_1 ..] = sum_j q_j prod_k L_{a_k}(x_jk): per box one real GEMM on the DMMA
+// pipe, M = p (axis 0), N = p^(d-1) (last axis padded to 8-column tiles), K = the box's
+// points.  CTA = (box, 8-row m-tile, n-chunk); per chunk of 32 points the d x p Lagrange
+// values of every point go to shared memory once (barycentric form at the Chebyshev
+// nodes; a point on a node takes the Kronecker row), then each warp feeds its n-tiles:
+// A[a_0][j] = q_j L_{a_0}(x_j0), B[j][(a_1 a_2)] = L_{a_1}(x_j1) L_{a_2}(x_j2).
+constexpr int PROXY_NT = 16;  // n-tiles per warp
+struct ProxyArgs {
+  const double* src;
+  const double* q;
+  const double* center;
+  const int64_t* dense_ids;
+  const int64_t* src_start;
+  const int64_t* slots;
+  const int64_t* boff;
+  const double* cheb_x;
+  const double* cheb_lam;
+  double* grid;  // (nbat, p^D)
+  double sc;
+  int p;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) proxy_charges_kernel(ProxyArgs a) {
+  __shared__ double sL[D][32][PROXY_PMAX + 1];
+  __shared__ double sq[32];
+  __shared__ double sx[PROXY_PMAX], slam[PROXY_PMAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = a.p, P8 = (p + 7) / 8;  // 8-column tiles along the last axis
+  const int ntiles = D == 1 ? 1 : (D == 2 ? P8 : p * P8);
+  const int64_t bx = blockIdx.x;
+  const int mt = blockIdx.y;
+  const int nt0 = (blockIdx.z * 8 + warp) * PROXY_NT;
+  const int64_t box = a.dense_ids[a.slots[bx]];
+  const int64_t s0 = a.src_start[box], n = a.boff[bx + 1] - a.boff[bx];
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    sx[i] = a.cheb_x[i];
+    slam[i] = a.cheb_lam[i];
+  }
+  double acc[PROXY_NT][2];
+#pragma unroll
+  for (int t = 0; t < PROXY_NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < n; c0 += 32) {
+    // Lagrange rows of the chunk: thread (point, axis)
+    if (threadIdx.x < 32 * D) {
+      const int pt = threadIdx.x / D, k = threadIdx.x - pt * D;
+      double* L = sL[k][pt];
+      if (c0 + pt < n) {
+        const double x = (a.src[(s0 + c0 + pt) * D + k] - a.center[box * D + k]) * a.sc;
+        double den = 0.0;
+        int hit = -1;
+        for (int i = 0; i < p; ++i) {
+          const double dx = x - sx[i];
+          if (dx == 0.0) hit = i;
+          const double t = slam[i] / dx;
+          L[i] = t;
+          den += t;
+        }
+        const double inv = 1.0 / den;
+        for (int i = 0; i < p; ++i) L[i] = hit < 0 ? L[i] * inv : (i == hit ? 1.0 : 0.0);
+        if (k == 0) sq[pt] = a.q[s0 + c0 + pt];
+      } else {
+        for (int i = 0; i < p; ++i) L[i] = 0.0;
+        if (k == 0) sq[pt] = 0.0;
+      }
+    }
+    __syncthreads();
+    const int row = mt * 8 + (lane >> 2);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int j = ks * 4 + (lane & 3);
+      const double av = row < p ? sq[j] * sL[0][j][row] : 0.0;
+#pragma unroll
+      for (int t = 0; t < PROXY_NT; ++t) {
+        const int nt = nt0 + t;
+        if (nt < ntiles) {  // warp-uniform
+          double bv;
+          if (D == 1) {
+            bv = (lane >> 2) == 0 ? 1.0 : 0.0;
+          } else if (D == 2) {
+            const int a1 = nt * 8 + (lane >> 2);
+            bv = a1 < p ? sL[1][j][a1] : 0.0;
+          } else {
+            const int a1 = nt / P8, a2 = (nt - a1 * P8) * 8 + (lane >> 2);
+            bv = a2 < p ? sL[1][j][a1] * sL[D - 1][j][a2] : 0.0;
+          }
+          dmma2(acc[t][0], acc[t][1], av, bv);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // C fragment: row a_0 = mt 8 + lane / 4, columns 2 (lane % 4) + {0, 1} of the n-tile
+  const int row = mt * 8 + (lane >> 2);
+  int64_t pd = 1;
+  for (int k = 0; k < D; ++k) pd *= p;
+  double* g = a.grid + bx * pd;
+  if (row < p) {
+#pragma unroll
+    for (int t = 0; t < PROXY_NT; ++t) {
+      const int nt = nt0 + t;
+      if (nt >= ntiles) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cidx = 2 * (lane & 3) + e;
+        if (D == 1) {
+          if (cidx == 0) g[row] = acc[t][e];
+        } else if (D == 2) {
+          const int a1 = nt * 8 + cidx;
+          if (a1 < p) g[row * p + a1] = acc[t][e];
+        } else {
+          const int a1 = nt / P8, a2 = (nt - a1 * P8) * 8 + cidx;
+          if (a2 < p) g[((int64_t)row * p + a1) * p + a2] = acc[t][e];
+        }
+      }
+    }
+  }
+}
+
 void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wq) {
   x.resize(n);
   wq.resize(n);
@@ -1076,6 +1198,7 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.n_f = n_f;
   N.tol = tol;
   N.X = X;
+  if (w1d) N.w1d.assign(w1d, w1d + n_f);
   // w = ceil(log10(1/tol)) + 1 taps per axis; the 1e-9 guard keeps tol = 1e-10 at 11
   // taps instead of 12 when log10 lands a hair above an integer
   N.w = (int)std::ceil(std::log10(1.0 / tol) - 1e-9) + 1;
@@ -1153,6 +1276,112 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, 
   N.hc.from_host(hc.data(), hc.size());
   // (pageable host -> device async copies are staged before they return: the host
   // vectors may go out of scope without a stream sync)
+}
+
+// ------------------------------------------------------------------ proxy-point plan
+
+// worst weighted interpolation error of e^{-i m x} on [-X, X] from p Chebyshev nodes
+static double proxy_error(int p, int n_f, double X, const double* w1d) {
+  std::vector<double> xa(p), lam(p);
+  for (int a = 0; a < p; ++a) {
+    const double th = M_PI * (2 * a + 1) / (2.0 * p);
+    xa[a] = X * std::cos(th);
+    lam[a] = ((a & 1) ? -1.0 : 1.0) * std::sin(th);
+  }
+  double wmax = 0.0;
+  for (int mi = 0; mi < n_f; ++mi) wmax = std::max(wmax, w1d ? std::fabs(w1d[mi]) : 1.0);
+  const int ns = 3 * p + 1;
+  double err = 0.0;
+  std::vector<double> L(p);
+  for (int q = 0; q < ns; ++q) {
+    const double x = -X + 2.0 * X * (q + 0.37) / ns;
+    double den = 0.0;
+    for (int a = 0; a < p; ++a) {
+      L[a] = lam[a] / (x - xa[a]);
+      den += L[a];
+    }
+    for (int a = 0; a < p; ++a) L[a] /= den;
+    for (int mi = 0; mi < n_f; ++mi) {
+      const double m = mi - n_f / 2;
+      double re = 0.0, im = 0.0;
+      for (int a = 0; a < p; ++a) {
+        re += L[a] * std::cos(m * xa[a]);
+        im -= L[a] * std::sin(m * xa[a]);
+      }
+      const double dr = re - std::cos(m * x), di = im + std::sin(m * x);
+      const double wgt = (w1d ? std::fabs(w1d[mi]) : 1.0) / wmax;
+      err = std::max(err, wgt * std::sqrt(dr * dr + di * di));
+    }
+  }
+  return err;
+}
+
+static void proxy_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
+  N.n_f = n_f;
+  N.tol = tol;
+  N.X = X;
+  N.w = 0;
+  if (w1d) N.w1d.assign(w1d, w1d + n_f);
+  int p = 4;
+  while (p <= PROXY_PMAX && proxy_error(p, n_f, X, w1d) > tol) ++p;
+  FGT_REQUIRE(p <= PROXY_PMAX, FGT_ERANGE, "proxy-point order beyond 48 nodes per axis");
+  N.G = p;
+  N.gmin = 0;
+  std::vector<double> xa(p), lam(p);
+  for (int a = 0; a < p; ++a) {
+    const double th = M_PI * (2 * a + 1) / (2.0 * p);
+    xa[a] = X * std::cos(th);
+    lam[a] = ((a & 1) ? -1.0 : 1.0) * std::sin(th);
+  }
+  const int G = p, nh = n_f / 2 + 1;
+  std::vector<double> Ef(2 * n_f * G), EfT(2 * n_f * G), EfH(2 * nh * G);
+  for (int mi = 0; mi < n_f; ++mi) {
+    const double m = mi - n_f / 2, wf = w1d ? w1d[mi] : 1.0;
+    for (int g = 0; g < G; ++g) {
+      const double c = wf * std::cos(m * xa[g]), sn = -wf * std::sin(m * xa[g]);
+      Ef[2 * (mi * G + g)] = c;
+      Ef[2 * (mi * G + g) + 1] = sn;
+      EfT[2 * (g * n_f + mi)] = c;
+      EfT[2 * (g * n_f + mi) + 1] = sn;
+    }
+  }
+  for (int s = 0; s < nh; ++s) {
+    const int mi = half_plane_mi(s, n_f, true);
+    for (int g = 0; g < G; ++g) {
+      EfH[2 * (s * G + g)] = Ef[2 * (mi * G + g)];
+      EfH[2 * (s * G + g) + 1] = Ef[2 * (mi * G + g) + 1];
+    }
+  }
+  N.Ef.alloc(Ef.size(), st);
+  N.Ef.from_host(Ef.data(), Ef.size());
+  N.EfT.alloc(EfT.size(), st);
+  N.EfT.from_host(EfT.data(), EfT.size());
+  N.EfH.alloc(EfH.size(), st);
+  N.EfH.from_host(EfH.data(), EfH.size());
+  N.cheb_x.alloc(p, st);
+  N.cheb_x.from_host(xa.data(), p);
+  N.cheb_lam.alloc(p, st);
+  N.cheb_lam.from_host(lam.data(), p);
+}
+
+const NufftPlan& proxy_plan_cached(int n_f, double tol, double X, const double* w1d, cudaStream_t st) {
+  int dev = 0;
+  FGT_CUDA(cudaGetDevice(&dev));
+  std::string key(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  key.append(reinterpret_cast<const char*>(&n_f), sizeof(n_f));
+  key.append(reinterpret_cast<const char*>(&tol), sizeof(tol));
+  key.append(reinterpret_cast<const char*>(&X), sizeof(X));
+  if (w1d) key.append(reinterpret_cast<const char*>(w1d), sizeof(double) * n_f);
+  static std::mutex mu;
+  static auto* cache = new std::map<std::string, NufftPlan*>();  // process lifetime
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache->find(key);
+  if (it != cache->end()) return *it->second;
+  auto* p = new NufftPlan();
+  proxy_plan(*p, n_f, tol, X, w1d, st);
+  FGT_CUDA(cudaStreamSynchronize(st));
+  (*cache)[key] = p;
+  return *p;
 }
 
 namespace {
@@ -1462,6 +1691,51 @@ void nufft_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
   }
 }
 
+// proxy-point form of the listed P-box slots (see k_nufft.cuh)
+template <int D>
+void proxy_form_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots) {
+  if (slots.empty()) return;
+  cudaStream_t st = T.st;
+  const int p = N.G, n_f = N.n_f, nh = P.nh;
+  const int64_t GD = ipow(p, D), plane = GD / p;
+  const std::vector<int64_t>& scount = P.h_src;
+  const int64_t per_box = GD * 8 + (D == 2 ? (int64_t)p * n_f * 16 : 0) +
+                          (D == 3 ? (int64_t)nh * plane * 16 + (int64_t)nh * n_f * p * 16 : 0);
+  const int64_t nb_max = std::max<int64_t>(1, std::min<int64_t>(1 << 16, ((int64_t)4 << 30) / per_box));
+  GrowBuf<int64_t> g_sl, g_boff;
+  GrowBuf<double> g_grid, g_t1, g_t2;
+  const int P8 = (p + 7) / 8;
+  const int ntiles = D == 1 ? 1 : (D == 2 ? P8 : p * P8);
+  const unsigned nz = (unsigned)((ntiles + 8 * PROXY_NT - 1) / (8 * PROXY_NT));
+  for (size_t b0 = 0; b0 < slots.size();) {
+    const int64_t nbat = std::min<int64_t>(nb_max, (int64_t)(slots.size() - b0));
+    std::vector<int64_t> boff(nbat + 1, 0);
+    for (int64_t b = 0; b < nbat; ++b) boff[b + 1] = boff[b] + scount[slots[b0 + b]];
+    auto sl_d = g_sl.view(nbat, st);
+    auto boff_d = g_boff.view(nbat + 1, st);
+    sl_d.from_host(slots.data() + b0, nbat);
+    boff_d.from_host(boff.data(), nbat + 1);
+    auto grid = g_grid.view(nbat * GD, st);
+    ProxyArgs pa;
+    pa.src = T.src_sorted.get();
+    pa.q = T.q_sorted.get();
+    pa.center = T.center.get();
+    pa.dense_ids = T.dense_ids.get();
+    pa.src_start = T.src_start.get();
+    pa.slots = sl_d.get();
+    pa.boff = boff_d.get();
+    pa.cheb_x = N.cheb_x.get();
+    pa.cheb_lam = N.cheb_lam.get();
+    pa.grid = grid.get();
+    pa.sc = P.sc;
+    pa.p = p;
+    proxy_charges_kernel<D><<<dim3((unsigned)nbat, (unsigned)P8, nz), 256, 0, st>>>(pa);
+    FGT_LAUNCHED();
+    form_modes<D>(N, P, grid.get(), sl_d.get(), nbat, g_t1, g_t2, st);
+    b0 += nbat;
+  }
+}
+
 template <int D>
 void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& idx,
                      double* u_sorted) {
@@ -1537,6 +1811,13 @@ void nufft_eval_impl(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector
 }  // namespace
 
 void nufft_form(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots) {
+  if (nufft_mode() == 3) {
+    const NufftPlan& X = proxy_plan_cached(N.n_f, N.tol, N.X, N.w1d.empty() ? nullptr : N.w1d.data(), T.st);
+    if (T.d == 1) proxy_form_impl<1>(X, P, T, slots);
+    else if (T.d == 2) proxy_form_impl<2>(X, P, T, slots);
+    else proxy_form_impl<3>(X, P, T, slots);
+    return;
+  }
   if (T.d == 1) nufft_form_impl<1>(N, P, T, slots);
   else if (T.d == 2) nufft_form_impl<2>(N, P, T, slots);
   else nufft_form_impl<3>(N, P, T, slots);

@@ -23,6 +23,10 @@ struct NufftPlan {
   // coefficient of tap t in y = 2f - 1, f in [0, 1) the first tap's offset (see es_fit)
   int hdeg = 0;
   DBuf<double> hc;
+  std::vector<double> w1d;  // (n_f) plane-wave weights the form matrices carry
+  // proxy-point plans only (proxy_plan_cached): G = p Chebyshev nodes per axis on [-X, X]
+  // and their barycentric weights; Ef / EfT / EfH then hold w1d[m] e^{-i m x_a}
+  DBuf<double> cheb_x, cheb_lam;
 };
 
 void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
@@ -30,7 +34,16 @@ void nufft_plan(NufftPlan& N, int n_f, double tol, double X, const double* w1d_h
 // quadrature and the six small matrix uploads happen once per parameter set.
 const NufftPlan& nufft_plan_cached(int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
 
-// phi[slot] for the listed P-box slots, by spreading + separable DFT (DMMA GEMMs).
+// Proxy-point form: the sources of a box are replaced by equivalent
+// charges on a tensor grid of p Chebyshev proxy points per axis (Lagrange anterpolation as
+// one real DMMA GEMM per box), then the proxy grid goes to the plane-wave basis in tensor
+// product form with the same batched DMMA stages as the NUFFT path -- no spreading kernel,
+// no sort.  p is the smallest order whose interpolation error of e^{-i m x}, weighted by
+// the plane-wave weight of mode m, is below tol on the box.  FGT_NUFFT_MODE=proxy.
+const NufftPlan& proxy_plan_cached(int n_f, double tol, double X, const double* w1d_host, cudaStream_t st);
+
+// phi[slot] for the listed P-box slots, by spreading + separable DFT (DMMA GEMMs)
+// (or, with FGT_NUFFT_MODE=proxy, by proxy points + the same separable stages).
 void nufft_form(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& slots);
 // u_sorted += Re(psi_i evaluated at the targets of psi box i) for the listed psi indices.
 void nufft_eval(const NufftPlan& N, PwDev& P, TreeDev& T, const std::vector<int64_t>& psi_idx,

@@ -34,6 +34,7 @@ int nufft_mode() {
   if (!e) return 0;
   if (!std::strcmp(e, "direct")) return 1;
   if (!std::strcmp(e, "spread")) return 2;
+  if (!std::strcmp(e, "proxy")) return 3;  // form: proxy points (evaluation as "spread")
   return 0;
 }
 
@@ -57,7 +58,7 @@ bool prefer_nufft(const NufftPlan* N, int D, int64_t NF, int64_t npts, double ta
   if (N->G > 64) return false;  // beyond the spreading kernels' grid (wide root series)
   const int mode = nufft_mode();
   if (mode == 1) return false;
-  if (mode == 2) return npts > 0;
+  if (mode >= 2) return npts > 0;
   double taps = 1;
   for (int k = 0; k < D; ++k) taps *= N->w;
   const double direct = (double)npts * NF;

@@ -57,7 +57,8 @@ struct PwDev {
 struct NufftPlan;
 
 // Per-box path selection between the exact tensor-factored sums (DMMA) and the box-local
-// NUFFT (spread + separable DFT): FGT_NUFFT_MODE=direct|spread forces one (tests).
+// NUFFT (spread + separable DFT): FGT_NUFFT_MODE=direct|spread forces one (tests);
+// proxy = 3: form by proxy points + separable stages, evaluation as spread.
 int nufft_mode();
 // FGT_PSI=materialise | fused forces the translation path (A/B checks); 0 = automatic
 int psi_mode();

@@ -512,3 +512,35 @@ def test_fused_translation_eval_matches_materialised_psi(cuda, case, monkeypatch
     assert rel(u_fused, u_mat) < 1e-12
     ex = ofgt.direct_oracle(y, q, x[:1000], args[0], args[3])
     assert rel(u_fused[:1000], ex) <= 10 * args[1]
+
+
+@pytest.mark.parametrize("case", ["clust3d", "shell3d", "uniform2d", "periodic2d", "1d", "periodic3d"])
+def test_proxy_point_form(cuda, case, monkeypatch):
+    """Proxy-point form (FGT_NUFFT_MODE=proxy): every P-box's sources
+    replaced by equivalent charges on a tensor grid of Chebyshev proxy points (one real DMMA
+    GEMM per box), then proxy grid -> plane waves by the separable DMMA stages.  <= 10 eps vs
+    the exact direct sum, and agreement with the ES-kernel spreading form well inside eps."""
+    from paper_2305_07165_b200 import fgt_points
+    r = np.random.default_rng(41)
+    if case == "clust3d":
+        y, x, args = clustered(r, 30000, 3), r.uniform(-0.5, 0.5, (5000, 3)), (1e-4, 1e-6, 100, "free")
+    elif case == "shell3d":
+        y, x, args = make_points(r, "shell", 100000, 3), r.uniform(-0.5, 0.5, (5000, 3)), (1e-4, 1e-5, 20, "free")
+    elif case == "uniform2d":
+        y, x, args = r.uniform(-0.5, 0.5, (30000, 2)), r.uniform(-0.5, 0.5, (5000, 2)), (1e-3, 1e-8, 100, "free")
+    elif case == "periodic2d":
+        y, x, args = r.uniform(-0.5, 0.5, (30000, 2)), r.uniform(-0.5, 0.5, (5000, 2)), (1e-4, 1e-6, 60, "periodic")
+    elif case == "1d":
+        y, x, args = r.uniform(-0.5, 0.5, (5000, 1)), r.uniform(-0.5, 0.5, (4000, 1)), (1e-4, 1e-9, 30, "free")
+    else:
+        y, x, args = clustered(r, 8000, 3), r.uniform(-0.5, 0.5, (3000, 3)), (1e-3, 1e-4, 40, "periodic")
+    q = r.standard_normal(y.shape[0])
+    monkeypatch.setenv("FGT_NUFFT_MODE", "proxy")
+    u_proxy, t = fgt_points(y, q, x, *args, return_times=True)
+    assert t["n_spread_boxes"] > 0 and t["n_src_spread"] > 0
+    assert np.array_equal(u_proxy, fgt_points(y, q, x, *args))  # deterministic
+    monkeypatch.setenv("FGT_NUFFT_MODE", "spread")
+    u_spread = fgt_points(y, q, x, *args)
+    assert rel(u_proxy, u_spread) <= args[1]
+    ex = ofgt.direct_oracle(y, q, x, args[0], args[3])
+    assert rel(u_proxy, ex) <= 10 * args[1]
