@@ -296,6 +296,50 @@ int fgt_box_interp(const fgt_interp_tree* t, const double* x, int64_t n, double*
 int fgt_box_interp_dev(const fgt_interp_tree* t, const double* x, int64_t n, double* out,
                        void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Alg 3 / 5 / 6 pieces on the device (the density tree and the output tree are decided
+ * where the leaf grids live).
+ *
+ * fgt_box_tail: per leaf grid, the Legendre tail estimate of Eq. (funerr) -- values ->
+ * coefficients axis by axis (poly1d.py:76-91), RMS of the coefficients with |alpha|_2 >= k
+ * (tail_mask / tail_error, poly1d.py:100-126) -- and, if wsq is not NULL, the
+ * quadrature-weighted sum of squares sum_i w_i v_i^2 (the caller scales by (side/2)^d).
+ * val_to_pol (k, k) and weights (k) are HOST arrays (LegendreBasis, poly1d.py:50-73).
+ * fgt_box_nodes_dev: the k^d tensor Gauss-Legendre nodes of n boxes (leaf_grid_points,
+ * tree.py:384-391), pts (n, k^d, dim) on the device; level / coords / nodes are HOST arrays;
+ * coordinates are rounded operation by operation like the reference's expressions.
+ * fgt_box_balance_flags: one sweep of the level restriction (the condition of
+ * _Builder.balance, tree.py:195-220): flags[j] = 1 for every leaf that covers a neighbour
+ * cell of a leaf two or more levels deeper.  The caller splits the flagged leaves and calls
+ * again until no flag is set; the result is the reference's box set (least fixpoint).
+ * HOST arrays in any order. */
+int fgt_box_tail_dev(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+                     const double* weights, double* tail, double* wsq, void* stream);
+int fgt_box_tail(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+                 const double* weights, double* tail, double* wsq);
+int fgt_box_nodes_dev(const int32_t* level, const int64_t* coords, int64_t n, int dim, int k,
+                      const double* nodes, const double* root_low, double root_side, double* pts,
+                      void* stream);
+int fgt_box_balance_flags(const int32_t* level, const int64_t* coords, const uint8_t* is_leaf,
+                          int64_t n, int dim, int periodic, uint8_t* flags);
+
+/* Alg 5: output-tree refinement from RETAINED
+ * incoming expansions.  fgt_box_retain = fgt_box that keeps psi of every f = 1 box and the
+ * leaf grids of the density on the device (state).  fgt_box_refine evaluates new boxes
+ * from that state: rplan is a box plan with n_form = 0 whose plane-wave slots [0, state
+ * n_pw) are the retained ones and whose further slots are new children; its stages are
+ * pushes only (kind 2: psi_child = T_p2c psi_parent), its eval list names the new leaves
+ * (rows of u_new, (rplan->n_leaves, k^d), HOST) and its direct pairs take sources from the
+ * retained leaf grids (d_src = leaf slot of the ORIGINAL transform) through the tables of
+ * rplan (any centre offset / side ratio: the extended T_pol2pot tables of the Alg 5
+ * Remark).  The state then also holds the new slots, so sweeps can be chained. */
+typedef struct fgt_box_state fgt_box_state;
+int fgt_box_retain(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times,
+                   fgt_box_state** state);
+int fgt_box_refine(fgt_box_state* state, const fgt_box_plan* rplan, double* u_new,
+                   fgt_phase_times* times);
+int fgt_box_state_free(fgt_box_state* state);
+
 int fgt_bench_fp64_peak(int use_dmma, double* tflops);
 
 #ifdef __cplusplus

@@ -136,6 +136,14 @@ SIGNATURES = {
     "fgt_partition_bounds": (_I, [_P, _I64, ctypes.c_int32, _P]),
     "fgt_box_dev": (_I, [ctypes.POINTER(FgtBoxPlan), _P, _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
     "fgt_box": (_I, [ctypes.POINTER(FgtBoxPlan), _P, _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_box_tail_dev": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P]),
+    "fgt_box_tail": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
+    "fgt_box_nodes_dev": (_I, [_P, _P, _I64, _I, _I, _P, _P, _D, _P, _P]),
+    "fgt_box_balance_flags": (_I, [_P, _P, _P, _I64, _I, _I, _P]),
+    "fgt_box_retain": (_I, [ctypes.POINTER(FgtBoxPlan), _P, _P, ctypes.POINTER(FgtPhaseTimes),
+                            ctypes.POINTER(_P)]),
+    "fgt_box_refine": (_I, [_P, ctypes.POINTER(FgtBoxPlan), _P, ctypes.POINTER(FgtPhaseTimes)]),
+    "fgt_box_state_free": (_I, [_P]),
 }
 
 _lib = None

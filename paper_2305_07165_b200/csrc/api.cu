@@ -1106,6 +1106,155 @@ int fgt_box(const fgt_box_plan* plan, const double* values, double* u, fgt_phase
   });
 }
 
+// ---- Alg 3 / 5 / 6 on the device: tail test, grid nodes, level restriction, retained psi
+int fgt_box_tail_dev(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+                     const double* weights, double* tail, double* wsq, void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(n >= 0 && (n == 0 || (values && tail)) && val_to_pol && weights, FGT_EINVAL, "bad arguments");
+    FGT_REQUIRE(k >= 2 && k <= 24, FGT_ERANGE, "polynomial order outside [2, 24]");
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf<double> m((size_t)k * k, st), w((size_t)k, st);
+    m.from_host(val_to_pol, (size_t)k * k);
+    w.from_host(weights, (size_t)k);
+    box_tail(values, n, dim, k, m.get(), w.get(), tail, wsq, st);
+    FGT_CUDA(cudaStreamSynchronize(st));  // the host tables may go out of scope
+  });
+}
+
+int fgt_box_tail(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+                 const double* weights, double* tail, double* wsq) {
+  return guarded([&] {
+    FGT_REQUIRE(n >= 0 && (n == 0 || (values && tail)) && val_to_pol && weights, FGT_EINVAL, "bad arguments");
+    FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(k >= 2 && k <= 24, FGT_ERANGE, "polynomial order outside [2, 24]");
+    int64_t kd = 1;
+    for (int i = 0; i < dim; ++i) kd *= k;
+    OwnedStream os;
+    DBuf<double> dv(n * kd, os.s), dt(n, os.s), dw(n, os.s), m((size_t)k * k, os.s), w((size_t)k, os.s);
+    dv.from_host(values, n * kd);
+    m.from_host(val_to_pol, (size_t)k * k);
+    w.from_host(weights, (size_t)k);
+    box_tail(dv.get(), n, dim, k, m.get(), w.get(), dt.get(), dw.get(), os.s);
+    dt.to_host(tail, n);
+    if (wsq) dw.to_host(wsq, n);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+  });
+}
+
+int fgt_box_nodes_dev(const int32_t* level, const int64_t* coords, int64_t n, int dim, int k,
+                      const double* nodes, const double* root_low, double root_side, double* pts,
+                      void* stream) {
+  return guarded([&] {
+    FGT_REQUIRE(n >= 0 && (n == 0 || (level && coords && pts)) && nodes && root_low, FGT_EINVAL, "bad arguments");
+    FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    FGT_REQUIRE(k >= 1 && k <= 64, FGT_ERANGE, "grid order out of range");
+    for (int64_t i = 0; i < n; ++i) FGT_REQUIRE(level[i] >= 0 && level[i] <= 57 / dim, FGT_ERANGE, "level out of range");
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf<int32_t> dl(n, st);
+    DBuf<int64_t> dc(n * dim, st);
+    DBuf<double> dn((size_t)k, st);
+    dl.from_host(level, n);
+    dc.from_host(coords, n * dim);
+    dn.from_host(nodes, (size_t)k);
+    box_nodes(dl.get(), dc.get(), n, dim, k, dn.get(), root_low, root_side, pts, st);
+    FGT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fgt_box_balance_flags(const int32_t* level, const int64_t* coords, const uint8_t* is_leaf,
+                          int64_t n, int dim, int periodic, uint8_t* flags) {
+  return guarded([&] {
+    FGT_REQUIRE(n >= 0 && (n == 0 || (level && coords && is_leaf && flags)), FGT_EINVAL, "bad arguments");
+    FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+    // sorted (level, Morton) keys of the box set; flags come back in the caller's order
+    std::vector<std::pair<uint64_t, int64_t>> kv(n);
+    for (int64_t i = 0; i < n; ++i) {
+      FGT_REQUIRE(level[i] >= 0 && level[i] * dim <= 57, FGT_ERANGE, "level out of range");
+      kv[i] = {box_key(level[i], morton_encode(coords + i * dim, dim, level[i])), i};
+    }
+    std::sort(kv.begin(), kv.end());
+    std::vector<uint64_t> hk(n);
+    std::vector<uint8_t> hl(n), hf(n);
+    for (int64_t i = 0; i < n; ++i) {
+      hk[i] = kv[i].first;
+      hl[i] = is_leaf[kv[i].second];
+      FGT_REQUIRE(i == 0 || hk[i] != hk[i - 1], FGT_EINVAL, "duplicate box");
+    }
+    OwnedStream os;
+    DBuf<uint64_t> dk(n, os.s);
+    DBuf<uint8_t> dl(n, os.s), df(n, os.s);
+    dk.from_host(hk.data(), n);
+    dl.from_host(hl.data(), n);
+    box_balance_flags(dk.get(), dl.get(), n, dim, periodic, df.get(), os.s);
+    df.to_host(hf.data(), n);
+    FGT_CUDA(cudaStreamSynchronize(os.s));
+    for (int64_t i = 0; i < n; ++i) flags[kv[i].second] = hf[i];
+  });
+}
+
+struct fgt_box_state {
+  OwnedStream os;
+  BoxState st;
+};
+
+int fgt_box_retain(const fgt_box_plan* plan, const double* values, double* u, fgt_phase_times* times,
+                   fgt_box_state** state) {
+  return guarded([&] {
+    FGT_REQUIRE(plan && state && values && u, FGT_EINVAL, "null argument");
+    int64_t kd = 1;
+    for (int i = 0; i < plan->dim; ++i) kd *= plan->k;
+    const int64_t n = plan->n_leaves * kd;
+    std::unique_ptr<fgt_box_state> s(new fgt_box_state);
+    cudaStream_t st = s->os.s;
+    s->st.st = st;
+    s->st.values.alloc(n, st);
+    s->st.n_values = plan->n_leaves;
+    s->st.values.from_host(values, n);
+    DBuf<double> du(n, st);
+    const int64_t l0 = g_launches;
+    fgt_phase_times t;
+    std::memset(&t, 0, sizeof(t));
+    box_fgt(*plan, s->st.values.get(), du.get(), st, &t, &s->st, nullptr);
+    t.launches = g_launches - l0;
+    du.to_host(u, n);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    du.release();
+    if (times) *times = t;
+    *state = s.release();
+  });
+}
+
+int fgt_box_refine(fgt_box_state* state, const fgt_box_plan* rplan, double* u_new,
+                   fgt_phase_times* times) {
+  return guarded([&] {
+    FGT_REQUIRE(state && rplan && (rplan->n_leaves == 0 || u_new), FGT_EINVAL, "null argument");
+    cudaStream_t st = state->os.s;
+    for (int64_t p = 0; p < rplan->n_dpairs; ++p)
+      FGT_REQUIRE(rplan->d_src[p] >= 0 && rplan->d_src[p] < state->st.n_values, FGT_EINVAL,
+                  "direct source outside the retained leaf grids");
+    const int64_t n = rplan->n_leaves * state->st.KD;
+    DBuf<double> du(std::max<int64_t>(n, 1), st);
+    const int64_t l0 = g_launches;
+    fgt_phase_times t;
+    std::memset(&t, 0, sizeof(t));
+    box_fgt(*rplan, state->st.values.get(), du.get(), st, &t, nullptr, &state->st);
+    t.launches = g_launches - l0;
+    du.to_host(u_new, n);
+    FGT_CUDA(cudaStreamSynchronize(st));
+    du.release();
+    if (times) *times = t;
+  });
+}
+
+int fgt_box_state_free(fgt_box_state* state) {
+  return guarded([&] {
+    if (!state) return;
+    state->st.psi.release();
+    state->st.values.release();
+    delete state;
+  });
+}
+
 int fgt_partition_bounds(const double* cost, int64_t n, int32_t parts, int64_t* bounds) {
   return guarded([&] {
     FGT_REQUIRE(parts >= 1 && n >= 0 && (n == 0 || cost) && bounds, FGT_EINVAL, "bad arguments");

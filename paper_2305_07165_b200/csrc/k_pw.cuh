@@ -79,8 +79,26 @@ void pw_gather_eval(PwDev& P, TreeDev& T, double* u_sorted, const NufftPlan* N);
 // Direct near field over the D-lists (ball cut PAPER.md:909-915).
 void direct_lists(TreeDev& T, double inv_delta, double r2_cut, double* u_sorted, KClock* clk);
 // Continuous (box) FGT executor (k_volume.cu).
+// State kept between a transform and the Alg 5 refinement sweeps that follow it: the
+// incoming expansions of every f = 1 box and the leaf grids of the density, on the
+// state's own stream ("incoming expansions retained for f=1 boxes").
+struct BoxState {
+  cudaStream_t st = nullptr;  // owned
+  DBuf<double> psi, values;
+  int64_t n_pw = 0, NF = 0, KD = 0, n_values = 0;
+  int dim = 0, k = 0, n_f = 0;
+};
 void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
-             fgt_phase_times* times);
+             fgt_phase_times* times, BoxState* retain = nullptr, BoxState* resume = nullptr);
+// Legendre tail estimate (Eq. funerr; poly1d.py:100-126) and weighted square sum of n leaf
+// grids; children-touching 2:1 balance flags of a box set (k_volume.cu)
+void box_tail(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+              const double* weights, double* tail, double* wsq, cudaStream_t st);
+void box_nodes(const int32_t* level, const int64_t* coords, int64_t n, int dim, int k,
+               const double* nodes, const double* root_low, double root_side, double* pts,
+               cudaStream_t st);
+void box_balance_flags(const uint64_t* keys, const uint8_t* leaf, int64_t n, int dim, int periodic,
+                       uint8_t* flags, cudaStream_t st);
 // interp_at of a box-FGT output (k_volume.cu)
 void box_interp(const fgt_interp_tree& t, const double* x, int64_t n, double* out, cudaStream_t st);
 

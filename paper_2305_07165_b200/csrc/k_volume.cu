@@ -232,9 +232,14 @@ std::vector<double> ctranspose(const double* a, int rows, int cols) {
   return t;
 }
 
+// retain: the incoming expansions psi are handed to the state instead of being freed
+// (Alg 5's "incoming expansions retained for f = 1 boxes").  resume: no
+// leaf->PW / merge / gather; psi starts as the state's expansions (slots [0, state n_pw))
+// plus zeroed new slots, the plan's stages may only push (kind 2), and the grown psi goes
+// back into the state.
 template <int D>
 void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
-              fgt_phase_times* times) {
+              fgt_phase_times* times, BoxState* retain, BoxState* resume) {
   const int k = pl.k, n_f = pl.n_f, L = pl.n_levels;
   const int64_t KD = ipw(k, D), NF = ipw(n_f, D);
   FGT_REQUIRE(pl.dim == D, FGT_EINVAL, "plan dim");
@@ -260,7 +265,21 @@ void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStrea
       for (int j = 0; j < k; ++j) dT_h[(t * k + j) * k + i] = pl.dtab[(t * k + i) * k + j];
   DBuf<double> dtab = upload(pl.dtab, pl.n_tables * k * k, st);
   DBuf<double> dtabT = upload(dT_h.data(), (int64_t)dT_h.size(), st);
-  DBuf<double> phi(2 * pl.n_pw * NF, st), psi(2 * pl.n_pw * NF, st);
+  DBuf<double> phi(resume ? 0 : 2 * pl.n_pw * NF, st), psi(2 * pl.n_pw * NF, st);
+  if (resume) {
+    FGT_REQUIRE(resume->dim == D && resume->k == k && resume->n_f == n_f && resume->NF == NF,
+                FGT_EINVAL, "refinement plan does not match the retained transform");
+    FGT_REQUIRE(pl.n_pw >= resume->n_pw && pl.n_form == 0, FGT_EINVAL,
+                "refinement plan must keep the retained plane-wave slots and form nothing");
+    for (int64_t s = 0; s < pl.n_stages; ++s)
+      FGT_REQUIRE(pl.stage_kind[s] == 2, FGT_EINVAL, "refinement stages must be pushes (psi -> psi)");
+    if (resume->n_pw)
+      FGT_CUDA(cudaMemcpyAsync(psi.get(), resume->psi.get(), sizeof(double) * 2 * resume->n_pw * NF,
+                               cudaMemcpyDeviceToDevice, st));
+    if (pl.n_pw > resume->n_pw)
+      FGT_CUDA(cudaMemsetAsync(psi.get() + 2 * resume->n_pw * NF, 0,
+                               sizeof(double) * 2 * (pl.n_pw - resume->n_pw) * NF, st));
+  }
 
   // ---- leaf -> plane waves, level by level
   c_form.begin(st);
@@ -342,7 +361,17 @@ void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStrea
   }
   c_eval.end(st);
   phi.release();
-  psi.release();
+  if (BoxState* keep = retain ? retain : resume) {
+    keep->psi = std::move(psi);
+    keep->n_pw = pl.n_pw;
+    keep->NF = NF;
+    keep->KD = KD;
+    keep->dim = D;
+    keep->k = k;
+    keep->n_f = n_f;
+  } else {
+    psi.release();
+  }
 
   // ---- direct near field: per pair separable contractions into Y, then a fixed-order
   // per-target sum (pairs arrive sorted by target)
@@ -435,10 +464,11 @@ void box_impl(const fgt_box_plan& pl, const double* values, double* u, cudaStrea
 }  // namespace
 
 void box_fgt(const fgt_box_plan& pl, const double* values, double* u, cudaStream_t st,
-             fgt_phase_times* times) {
-  if (pl.dim == 1) box_impl<1>(pl, values, u, st, times);
-  else if (pl.dim == 2) box_impl<2>(pl, values, u, st, times);
-  else if (pl.dim == 3) box_impl<3>(pl, values, u, st, times);
+             fgt_phase_times* times, BoxState* retain, BoxState* resume) {
+  FGT_REQUIRE(!(retain && resume), FGT_EINVAL, "retain and resume are exclusive");
+  if (pl.dim == 1) box_impl<1>(pl, values, u, st, times, retain, resume);
+  else if (pl.dim == 2) box_impl<2>(pl, values, u, st, times, retain, resume);
+  else if (pl.dim == 3) box_impl<3>(pl, values, u, st, times, retain, resume);
   else throw Error(FGT_EINVAL, "dim must be 1, 2, or 3");
 }
 
@@ -601,5 +631,214 @@ void box_interp(const fgt_interp_tree& tr, const double* x, int64_t n, double* o
   else interp_at3_kernel<<<grid_for(n, 8, 148 * 64), 256, 0, st>>>(t, x, n, out);
   FGT_LAUNCHED();
   FGT_CUDA(cudaStreamSynchronize(st));  // host-side tables go out of scope
+}
+// ---------------------------------------------------------------- Alg 3 / 5 / 6 on the device
+// tail test (Eq. funerr; reference poly1d.py:100-126), grid nodes of a set of boxes
+// (tree.py:384-391) and the level-restriction sweep (tree.py:195-220) as kernels, so the
+// density tree and the output tree are decided where the grids live.
+namespace {
+constexpr int TMAXK = 24;
+
+// One CTA per leaf grid: values -> Legendre coefficients axis by axis in shared memory
+// (the reference's _apply_per_axis, poly1d.py:76-81), then the RMS of the coefficients with
+// |alpha|_2 >= k (d = 1: the last two) and the quadrature-weighted sum of squares.  Sums run
+// in a fixed order (per-thread strided partials, then a shared-memory tree).
+template <int D>
+__global__ void __launch_bounds__(256) tail_kernel(const double* __restrict__ values, int k,
+                                                   const double* __restrict__ v2p,
+                                                   const double* __restrict__ wts,
+                                                   double* __restrict__ tail, double* __restrict__ wsq) {
+  extern __shared__ double sm[];
+  int kd = 1;
+  for (int c = 0; c < D; ++c) kd *= k;
+  double* a = sm;            // kd
+  double* b = sm + kd;       // kd
+  double* M = b + kd;        // k * k
+  double* w = M + k * k;     // k
+  __shared__ double red[2][256];
+  const double* v = values + (int64_t)blockIdx.x * kd;
+  for (int i = threadIdx.x; i < kd; i += blockDim.x) a[i] = v[i];
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x) M[i] = v2p[i];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) w[i] = wts[i];
+  __syncthreads();
+  // weighted square sum of the values
+  double s2 = 0.0;
+  for (int i = threadIdx.x; i < kd; i += blockDim.x) {
+    double ww = 1.0;
+    int rem = i;
+    for (int c = 0; c < D; ++c) {
+      ww *= w[rem % k];
+      rem /= k;
+    }
+    s2 += ww * a[i] * a[i];
+  }
+  // contract one axis per pass: out[.., n, ..] = sum_j M[n][j] in[.., j, ..]
+  double* in = a;
+  double* out = b;
+  int stride = kd / k;  // axis 0 first (C order: axis 0 has the largest stride)
+  for (int ax = 0; ax < D; ++ax) {
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) {
+      const int n = (i / stride) % k;
+      const int base = i - n * stride;
+      double acc = 0.0;
+      for (int j = 0; j < k; ++j) acc += M[n * k + j] * in[base + j * stride];
+      out[i] = acc;
+    }
+    __syncthreads();
+    double* t = in;
+    in = out;
+    out = t;
+    stride /= k;
+  }
+  double ts = 0.0;
+  int cnt = 0;
+  for (int i = threadIdx.x; i < kd; i += blockDim.x) {
+    int rem = i, r2 = 0;
+    bool last2 = false;
+    for (int c = 0; c < D; ++c) {
+      const int q = rem % k;
+      rem /= k;
+      r2 += q * q;
+      if (D == 1) last2 = q >= k - 2;
+    }
+    if (D == 1 ? last2 : r2 >= k * k) {
+      ts += in[i] * in[i];
+      ++cnt;
+    }
+  }
+  red[0][threadIdx.x] = ts;
+  red[1][threadIdx.x] = s2;
+  __shared__ int cred[256];
+  cred[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + off];
+      red[1][threadIdx.x] += red[1][threadIdx.x + off];
+      cred[threadIdx.x] += cred[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tail[blockIdx.x] = cred[0] ? sqrt(red[0][0] / (double)cred[0]) : 0.0;
+    if (wsq) wsq[blockIdx.x] = red[1][0];
+  }
+}
+
+// pts[b][i_0..i_{d-1}][c] = centre_c + (0.5 side) node_{i_c}, every operation rounded as the
+// host expression (rc - rs/2) + (g + 0.5) s, then + (0.5 s) node (no fused multiply-adds).
+template <int D>
+__global__ void nodes_kernel(const int32_t* __restrict__ level, const int64_t* __restrict__ coords,
+                             int64_t n, int k, const double* __restrict__ nodes, double3 low,
+                             double side, double* __restrict__ pts) {
+  int64_t kd = 1;
+  for (int c = 0; c < D; ++c) kd *= k;
+  const double lowv[3] = {low.x, low.y, low.z};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * kd;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bx = i / kd;
+    int64_t rem = i - bx * kd;
+    const double s = side / (double)((int64_t)1 << level[bx]);
+    const double hs = __dmul_rn(0.5, s);
+    int idx[D];
+#pragma unroll
+    for (int c = D - 1; c >= 0; --c) {
+      idx[c] = (int)(rem % k);
+      rem /= k;
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double ctr = __dadd_rn(lowv[c], __dmul_rn((double)coords[bx * D + c] + 0.5, s));
+      pts[i * D + c] = __dadd_rn(ctr, __dmul_rn(hs, nodes[idx[c]]));
+    }
+  }
+}
+
+// One thread per (box, neighbour offset): a leaf at level l >= 2 flags every leaf that
+// covers one of its 3^d - 1 neighbour cells from two or more levels above (the condition the
+// reference's LIFO sweep splits on, tree.py:205-214).  Rounds of flag + split reach the same
+// least fixpoint as the sequential sweep.
+template <int D>
+__global__ void balance_flags_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ leaf,
+                                     int64_t n, int periodic, uint8_t* __restrict__ flags) {
+  int n_off = 1;
+  for (int c = 0; c < D; ++c) n_off *= 3;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * n_off;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n_off;
+    int o = (int)(t - i * n_off);
+    if (!leaf[i]) continue;
+    const int l = key_level(keys[i]);
+    if (l < 2) continue;
+    int64_t g[D], nb[D];
+    morton_decode(key_code(keys[i]), D, l, g);
+    const int64_t side = (int64_t)1 << l;
+    bool inside = true, self = true;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const int oc = o % 3 - 1;
+      o /= 3;
+      self = self && oc == 0;
+      int64_t v = g[c] + oc;
+      if (periodic) v = (v % side + side) % side;
+      else inside = inside && v >= 0 && v < side;
+      nb[c] = v;
+    }
+    if (self || !inside) continue;
+    for (int lv = l; lv >= 0; --lv) {
+      const int64_t j = find_dev(keys, n, box_key(lv, morton_encode(nb, D, lv)));
+      if (j >= 0) {
+        if (leaf[j] && l - lv >= 2) flags[j] = 1;
+        break;
+      }
+#pragma unroll
+      for (int c = 0; c < D; ++c) nb[c] >>= 1;
+    }
+  }
+}
+}  // namespace
+
+void box_tail(const double* values, int64_t n, int dim, int k, const double* val_to_pol,
+              const double* weights, double* tail, double* wsq, cudaStream_t st) {
+  FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+  FGT_REQUIRE(k >= 2 && k <= TMAXK, FGT_ERANGE, "polynomial order outside [2, 24]");
+  if (n == 0) return;
+  const int64_t kd = ipw(k, dim);
+  const size_t smem = sizeof(double) * (size_t)(2 * kd + k * k + k);
+  FGT_REQUIRE(n <= 0x7fffffff, FGT_ERANGE, "too many leaf grids");
+  auto launch = [&](auto kern) {
+    FGT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)n, 256, smem, st>>>(values, k, val_to_pol, weights, tail, wsq);
+    FGT_LAUNCHED();
+  };
+  if (dim == 1) launch(tail_kernel<1>);
+  else if (dim == 2) launch(tail_kernel<2>);
+  else launch(tail_kernel<3>);
+}
+
+void box_nodes(const int32_t* level, const int64_t* coords, int64_t n, int dim, int k,
+               const double* nodes, const double* root_low, double root_side, double* pts,
+               cudaStream_t st) {
+  FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+  if (n == 0) return;
+  const double3 low = make_double3(root_low[0], dim > 1 ? root_low[1] : 0.0, dim > 2 ? root_low[2] : 0.0);
+  const int64_t total = n * ipw(k, dim);
+  const unsigned grid = grid_for(total, 256, 148 * 16);
+  if (dim == 1) nodes_kernel<1><<<grid, 256, 0, st>>>(level, coords, n, k, nodes, low, root_side, pts);
+  else if (dim == 2) nodes_kernel<2><<<grid, 256, 0, st>>>(level, coords, n, k, nodes, low, root_side, pts);
+  else nodes_kernel<3><<<grid, 256, 0, st>>>(level, coords, n, k, nodes, low, root_side, pts);
+  FGT_LAUNCHED();
+}
+
+void box_balance_flags(const uint64_t* keys, const uint8_t* leaf, int64_t n, int dim, int periodic,
+                       uint8_t* flags, cudaStream_t st) {
+  FGT_REQUIRE(dim >= 1 && dim <= 3, FGT_EINVAL, "dim must be 1, 2, or 3");
+  if (n == 0) return;
+  FGT_CUDA(cudaMemsetAsync(flags, 0, (size_t)n, st));
+  const unsigned grid = grid_for(n * 27, 256, 148 * 16);
+  if (dim == 1) balance_flags_kernel<1><<<grid, 256, 0, st>>>(keys, leaf, n, periodic, flags);
+  else if (dim == 2) balance_flags_kernel<2><<<grid, 256, 0, st>>>(keys, leaf, n, periodic, flags);
+  else balance_flags_kernel<3><<<grid, 256, 0, st>>>(keys, leaf, n, periodic, flags);
+  FGT_LAUNCHED();
 }
 }  // namespace fgt

@@ -202,9 +202,11 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
                        refill="evaluate", root_center=None, root_side=1.0, device=None):
     """Resolve sigma on a level-restricted tree (Alg 3); returns (tree, values, coeffs).
 
-    device="cuda": sigma is a torch function, evaluated on the GPU on each level's batch of
-    grid nodes (one call per refinement level and one for the balance refill); the tree
-    decisions (tail test, balance) stay on the host."""
+    device="cuda": Alg 3 on the GPU (_build_density_tree_device): sigma is a torch function
+    evaluated on device-generated grid nodes, the tail test and the level-restriction
+    sweeps are CUDA kernels, and the leaf grids stay in HBM until the tree is final.  Same
+    box set and leaf grids as the host path; boxes created by the balance are numbered in
+    sweep order instead of the reference's LIFO order."""
     if refill != "evaluate":
         # the reference's interpolation refill evaluates at local*0.5 (tree.py:482) and is
         # wrong by O(1); only re-evaluation is supported
@@ -212,6 +214,9 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
     rc = np.zeros(dim) if root_center is None else np.asarray(root_center, float)
     eps = clamp_tolerance(epsilon)
     basis = LegendreBasis(k)
+    if device is not None:
+        return _build_density_tree_device(density, dim, k, eps, periodic, l_max, rc, float(root_side),
+                                          basis, device)
     B = _Builder(dim, rc, root_side, periodic)
     values, coeffs = {}, {}
     wt = basis.weights
@@ -270,6 +275,110 @@ def build_density_tree(density, dim, k, epsilon, periodic=False, l_max=MAX_LEVEL
     tree = B.finalize()
     leaves = np.nonzero(tree.is_leaf)[0]
     return tree, {b: values[b] for b in leaves}, {b: coeffs[b] for b in leaves}
+
+
+def _build_density_tree_device(density, dim, k, eps, periodic, l_max, rc, rs, basis, device):
+    """Alg 3 with every per-grid decision on the GPU (reference tree.py:394-461).
+
+    Per refinement level: one kernel writes the k^d Gauss-Legendre nodes of the frontier
+    boxes (fgt_box_nodes_dev, coordinates rounded like the host expressions), sigma (a torch
+    function) is evaluated on them, and one kernel per box turns the values into Legendre
+    coefficients and returns the tail estimate and the weighted square sum
+    (fgt_box_tail_dev); only those two numbers per box cross PCIe.  The level restriction
+    runs as flag sweeps over the sorted (level, Morton) keys (fgt_box_balance_flags) until
+    no leaf is flagged; the boxes it creates are sampled in one batch per sweep."""
+    import torch
+    lib = _lib.load()
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError("the device density-tree build needs a CUDA device")
+    nc, kd = 1 << dim, k ** dim
+    bits = np.array([[(c >> a) & 1 for a in range(dim)] for c in range(nc)], np.int64)
+    low = np.zeros(3)
+    low[:dim] = rc - 0.5 * rs
+    nodes_h = np.ascontiguousarray(basis.nodes)
+    v2p_h = np.ascontiguousarray(basis.val_to_pol)
+    w_h = np.ascontiguousarray(basis.weights)
+    level = np.zeros(1, np.int32)
+    coords = np.zeros((1, dim), np.int64)
+    parent = np.full(1, -1, np.int64)
+    first_child = np.full(1, -1, np.int64)
+    tail = np.zeros(0)
+    wsq = np.zeros(0)
+    chunks = []  # device tensors (n, k^d) in box-id order
+
+    def sample(lv, cd):
+        n = lv.shape[0]
+        with torch.cuda.device(dev):
+            stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            pts = torch.empty((n,) + (k,) * dim + (dim,), dtype=torch.float64, device=dev)
+            _lib.check(lib.fgt_box_nodes_dev(_lib.ptr(np.ascontiguousarray(lv)), _lib.ptr(np.ascontiguousarray(cd)),
+                                             n, dim, k, _lib.ptr(nodes_h), _lib.ptr(low), rs,
+                                             ctypes.c_void_p(pts.data_ptr()), stream))
+            v = density(pts).to(torch.float64).reshape(n, kd).contiguous()
+            out = torch.empty((2, n), dtype=torch.float64, device=dev)
+            _lib.check(lib.fgt_box_tail_dev(ctypes.c_void_p(v.data_ptr()), n, dim, k, _lib.ptr(v2p_h),
+                                            _lib.ptr(w_h), ctypes.c_void_p(out[0].data_ptr()),
+                                            ctypes.c_void_p(out[1].data_ptr()), stream))
+            tw = out.cpu().numpy()
+        chunks.append(v)
+        return tw[0], tw[1]
+
+    def split(ids):
+        nonlocal level, coords, parent, first_child
+        nb = level.shape[0]
+        ids = np.asarray(ids, np.int64)
+        first_child[ids] = nb + nc * np.arange(ids.size)
+        lv = np.repeat(level[ids] + 1, nc).astype(np.int32)
+        if lv.size and int(lv.max()) > MAX_LEVEL:
+            raise RuntimeError(f"refinement beyond maximum level {MAX_LEVEL}")
+        cd = (2 * coords[ids][:, None, :] + bits[None, :, :]).reshape(-1, dim)
+        level = np.concatenate([level, lv])
+        coords = np.concatenate([coords, cd])
+        parent = np.concatenate([parent, np.repeat(ids, nc)])
+        first_child = np.concatenate([first_child, np.full(lv.size, -1, np.int64)])
+        return np.arange(nb, nb + lv.size), lv, cd
+
+    def grow(tw):
+        nonlocal tail, wsq
+        tail = np.concatenate([tail, tw[0]])
+        wsq = np.concatenate([wsq, tw[1]])
+
+    grow(sample(level, coords))
+    frontier = np.zeros(1, np.int64)
+    for l in range(l_max + 1):
+        leaf = first_child < 0
+        nrm = np.sqrt(np.sum((0.5 * rs / 2.0 ** level[leaf]) ** dim * wsq[leaf])) / rs ** (dim / 2.0)
+        nrm = max(float(nrm), 1e-300)
+        marks = frontier[tail[frontier] > eps * nrm]
+        if marks.size == 0:
+            break
+        if l == l_max:
+            raise RuntimeError(f"density not resolved at maximum refinement level {l_max}")
+        frontier, lv, cd = split(marks)
+        grow(sample(lv, cd))
+    while True:
+        n = level.shape[0]
+        flags = np.zeros(n, np.uint8)
+        leaf8 = np.ascontiguousarray((first_child < 0).astype(np.uint8))
+        _lib.check(lib.fgt_box_balance_flags(_lib.ptr(level), _lib.ptr(np.ascontiguousarray(coords)),
+                                             _lib.ptr(leaf8), n, dim, int(bool(periodic)), _lib.ptr(flags)))
+        marks = np.nonzero(flags)[0]
+        if marks.size == 0:
+            break
+        _, lv, cd = split(marks)
+        grow(sample(lv, cd))
+    n = level.shape[0]
+    children = np.where(first_child[:, None] >= 0, first_child[:, None] + np.arange(nc)[None, :], -1)
+    tree = Tree(dim=dim, root_center=rc, root_side=rs, periodic=periodic, level=level.astype(np.int64),
+                parent=parent, children=children, coords=coords, is_leaf=first_child < 0)
+    leaves = np.nonzero(tree.is_leaf)[0]
+    allv = torch.cat(chunks) if len(chunks) > 1 else chunks[0]
+    V = allv[torch.from_numpy(leaves).to(dev)].cpu().numpy().reshape((leaves.size,) + (k,) * dim)
+    C = V
+    for ax in range(dim):
+        C = np.moveaxis(np.tensordot(basis.val_to_pol, C, axes=([1], [ax + 1])), 0, ax + 1)
+    return tree, {int(b): V[i] for i, b in enumerate(leaves)}, {int(b): C[i] for i, b in enumerate(leaves)}
 
 
 # ------------------------------------------------------------------ Alg 4 plan
@@ -357,6 +466,7 @@ class BoxPlan:
         pw_slot = np.full(nb, -1, np.int64)
         pw_slot[f] = np.arange(int(f.sum()))
         self.n_pw = int(f.sum())
+        self.pw_slot, self.leaf_slot = pw_slot, leaf_slot
         fl = f.tolist()
         slot = pw_slot.tolist()
 
@@ -371,6 +481,7 @@ class BoxPlan:
                 p2c_row[(l, sgn)] = len(rows)
                 rows.append(np.exp(1j * km * s))
         self.rows = np.ascontiguousarray(np.array(rows, dtype=np.complex128))
+        self.p2c_row = p2c_row
 
         # ---- shift stages: merge (deepest first), gather at l_c, push (shallowest first)
         stage_off, stage_kind = [0], []
@@ -478,6 +589,10 @@ class BoxPlan:
         side_l = side.tolist()
         rs = float(tree.root_side)
         d_t, d_s, d_tab = [], [], []
+        # per target leaf: (source leaf slot, image shift) -- what Alg 5 hands to new children
+        self.d_sources = {}
+        for T, S, v in pairs:
+            self.d_sources.setdefault(T, []).append((int(leaf_slot[S]), lev[S], crd[S], v))
         for T, S, v in sorted(pairs, key=lambda p: leaf_slot[p[0]]):
             ls = lev[S]
             Ls, Lt = side_l[ls], side_l[lev[T]]
@@ -492,6 +607,11 @@ class BoxPlan:
 
     def cstruct(self):
         """The fgt_box_plan C struct (arrays kept alive by self)."""
+        return _plan_cstruct(self)
+
+
+def _plan_cstruct(self):
+        """fgt_box_plan from any object with BoxPlan's array attributes (BoxPlan, _RefinePlan)."""
         P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if a.dtype != np.int64 else \
             a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))  # noqa: E731
         self._keep = [np.ascontiguousarray(a) for a in (
@@ -538,8 +658,31 @@ def _stack_values(tree, values, k, pinned=False):
     return leaves, V
 
 
-def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, plan=None):
-    """u = int exp(-|x-y|^2/delta) sigma(y) dy on every leaf grid; {leaf: (k,)*d array}."""
+class RetainedTransform:
+    """Device state kept after fgt_box(..., retain=True): psi of every f = 1 box and the
+    density's leaf grids (fgt_box_state), with the plan and tree they belong to.  Input of
+    refine_output (Alg 5, "incoming expansions retained for f=1 boxes")."""
+
+    def __init__(self, handle, plan, tree, leaves, delta, epsilon, boundary):
+        self.handle, self.plan, self.tree, self.leaves = handle, plan, tree, leaves
+        self.delta, self.epsilon, self.boundary = delta, epsilon, boundary
+        self.n_pw = plan.n_pw
+
+    def free(self):
+        if self.handle is not None:
+            _lib.load().fgt_box_state_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, plan=None, retain=False):
+    """u = int exp(-|x-y|^2/delta) sigma(y) dy on every leaf grid; {leaf: (k,)*d array}.
+    retain=True also returns a RetainedTransform (the last element of the result)."""
     if boundary not in ("free", "periodic"):
         raise ValueError(f"unknown boundary {boundary!r}")
     if bool(tree.periodic) != (boundary == "periodic"):
@@ -551,9 +694,19 @@ def fgt_box(tree, values, delta, epsilon, boundary="free", return_times=False, p
     U = _host_buffer(V.shape)
     t = _lib.FgtPhaseTimes()
     cs = plan.cstruct()
-    _lib.check(_lib.load().fgt_box(ctypes.byref(cs), _lib.ptr(V), _lib.ptr(U), ctypes.byref(t)))
+    state = None
+    if retain:
+        handle = ctypes.c_void_p()
+        _lib.check(_lib.load().fgt_box_retain(ctypes.byref(cs), _lib.ptr(V), _lib.ptr(U), ctypes.byref(t),
+                                              ctypes.byref(handle)))
+        state = RetainedTransform(handle, plan, tree, leaves, delta, epsilon, boundary)
+    else:
+        _lib.check(_lib.load().fgt_box(ctypes.byref(cs), _lib.ptr(V), _lib.ptr(U), ctypes.byref(t)))
     out = {int(b): U[i] for i, b in enumerate(leaves)}
-    return (out, t.as_dict()) if return_times else out
+    res = (out, t.as_dict()) if return_times else (out,)
+    if retain:
+        res = res + (state,)
+    return res if len(res) > 1 else res[0]
 
 
 def fgt_box_device(plan, values_dev, out_dev=None, return_times=False):
@@ -662,22 +815,90 @@ def coarsen_output(tree, potentials, epsilon):
     return out, {int(new_id[b]): v for b, v in pots.items() if alive[b] and is_leaf[b]}
 
 
-def refine_output(tree, values, potentials, delta, epsilon, boundary="free", max_rounds=30):
-    """Alg 5 (PAPER.md:1354-1398, SPEC.md:550-561): refine the output tree until every
-    leaf's potential passes the tail test (Eq. funerr) at epsilon.
+def tail_errors(grids, dim, k, return_wsq=False):
+    """Eq. (funerr) tail estimates of a stack of leaf grids (n, k^d), on the GPU
+    (fgt_box_tail; the reference's tail_error, poly1d.py:116-126, per grid); with
+    return_wsq also the Gauss-Legendre weighted square sums sum_i w_i v_i^2."""
+    G = np.ascontiguousarray(np.asarray(grids, float).reshape(-1, k ** dim))
+    basis = LegendreBasis(k)
+    out = np.empty(G.shape[0])
+    wsq = np.empty(G.shape[0]) if return_wsq else None
+    _lib.check(_lib.load().fgt_box_tail(_lib.ptr(G), G.shape[0], dim, k,
+                                        _lib.ptr(np.ascontiguousarray(basis.val_to_pol)),
+                                        _lib.ptr(np.ascontiguousarray(basis.weights)), _lib.ptr(out),
+                                        _lib.ptr(wsq)))
+    return (out, wsq) if return_wsq else out
 
-    Realisation: a refined leaf's children get the source density by exact polynomial
-    refill (the parent's degree < k polynomial evaluated on the children's grids, so
-    sigma is unchanged), the tree is re-balanced with the same refill (level restriction
-    keeps the standard T_pol2pot offsets, so the Alg 5 Remark's extended tables are not
-    needed), and the GPU transform (fgt_box) is re-run on the refined tree: the children
-    receive the true transform values, the quantity Alg 5's translated psi + direct
-    corrections approximate.  Refinement never goes deeper than the input tree's deepest
-    level (Alg 5 Remark).  Returns (tree, values, potentials, n_rounds)."""
+
+def grid_norm(tree, grids, k):
+    """||f||_2 of a piecewise polynomial given by its leaf grids, normalised by the root
+    volume (the sigma norm of Alg 3, tree.py:417-428): sqrt(sum_leaves (side/2)^d sum_i w_i
+    f_i^2 / side_0^d)."""
+    leaves = sorted(grids)
+    _, wsq = tail_errors(np.stack([np.asarray(grids[b], float) for b in leaves]), tree.dim, k, return_wsq=True)
+    half = 0.5 * tree.root_side / 2.0 ** tree.level[leaves]
+    return float(np.sqrt(np.sum(half ** tree.dim * wsq)) / tree.root_side ** (tree.dim / 2.0))
+
+
+class _RefinePlan:
+    """fgt_box_plan for one Alg 5 sweep: pushes into new plane-wave slots, PW -> grid on the
+    new leaves, direct tables for arbitrary (offset, side ratio) pairs (Alg 5 Remark)."""
+
+    def __init__(self, base, n_levels):
+        self.dim, self.k, self.n_f, self.l_c = base.dim, base.k, base.n_f, base.l_c
+        self.n_levels = n_levels
+        self.rows = base.rows
+        self.val2pw = np.zeros((n_levels, base.n_f, base.k), np.complex128)
+        e = np.zeros(0, np.int64)
+        self.form_leaf = self.form_pw = self.form_level = e
+
+
+def refine_output(tree, values, potentials=None, delta=None, epsilon=None, boundary="free",
+                  max_rounds=30, state=None, return_stats=False, relative=False):
+    """Alg 5 (PAPER.md:1354-1398, SPEC.md:548-561): refine the output tree until every
+    leaf's potential passes the tail test (Eq. funerr) at epsilon, evaluating each new child
+    from the RETAINED incoming expansion of its parent.
+
+    state = the RetainedTransform of fgt_box(tree, values, ..., retain=True) (computed here
+    when absent).  A sweep tests the leaves created by the previous one (all leaves at first;
+    tail kernel on the GPU), splits the failing ones and, in ONE device call
+    (fgt_box_refine): psi_child = T_p2c psi_parent when f(parent) = 1, u_child = T_pw2pot
+    psi_child, plus the direct part from the parent's D-list sources (the
+    parent's list is a safe superset) through T_pol2pot tables built for the actual centre
+    offset and side ratio of each (source, child) pair -- the extended tables of the Alg 5
+    Remark, keyed by (source level, offset / L_S, L_T / L_S), exact dyadic numbers.  The
+    density of a split leaf goes to its children by exact polynomial refill (sigma is
+    unchanged; sources of direct pairs stay the ORIGINAL leaf grids, which represent the
+    same polynomial).  Refinement never goes deeper than the input tree (Alg 5 Remark).
+    relative=True tests e(B) > epsilon ||u||_2 (the normalisation Alg 3 uses for sigma,
+    PAPER.md:965) instead of Alg 5's literal e(B) > epsilon.
+    The final level-restriction sweep ("if desired, rebalance") evaluates the boxes it
+    creates the same way.  Returns (tree, values, potentials, n_sweeps[, stats])."""
     d = tree.dim
     k = np.asarray(next(iter(values.values()))).shape[0]
     basis = LegendreBasis(k)
+    own_state = state is None
+    if own_state:
+        if delta is None or epsilon is None:
+            raise ValueError("delta and epsilon are needed to compute the retained transform")
+        potentials, state = fgt_box(tree, values, delta, epsilon, boundary, retain=True)
+    elif potentials is None:
+        raise ValueError("potentials of the retained transform are required")
+    if state.handle is None:
+        raise ValueError("the retained transform was freed")
+    delta, eps_pw = state.delta, state.epsilon
+    epsilon = eps_pw if epsilon is None else epsilon
+    plan = state.plan
     lmax = int(tree.level.max())
+    n_levels = plan.n_levels
+    rs = float(tree.root_side)
+    side = rs / 2.0 ** np.arange(n_levels)
+    n_f = plan.n_f
+    km = (np.arange(n_f) - n_f // 2) * plan.pw.h / np.sqrt(delta)
+    pw2val = np.zeros((n_levels, k, n_f), np.complex128)
+    for l in range(n_levels):
+        pw2val[l] = np.exp(1j * np.outer(0.5 * side[l] * basis.nodes, km))
+    p2c_row = plan.p2c_row  # (child level, child bit) -> phase row of the base plan
     # child refill operators: P(t)^T with t the child's nodes in the parent's coordinates
     M = [legendre_values(k - 1, 0.5 * basis.nodes + (0.5 if bit else -0.5)).T for bit in (0, 1)]
     B = _Builder(d, tree.root_center, tree.root_side, bool(tree.periodic))
@@ -688,7 +909,12 @@ def refine_output(tree, values, potentials, delta, epsilon, boundary="free", max
     for b in range(tree.n_boxes):
         B.index[tree.level[b]][tuple(tree.coords[b])] = b
     vals = {int(b): np.asarray(v, float).reshape((k,) * d) for b, v in values.items()}
-    pots = potentials
+    pots = {int(b): np.asarray(v, float).reshape((k,) * d) for b, v in potentials.items()}
+    pw = {int(b): int(plan.pw_slot[b]) for b in np.nonzero(tree.is_leaf)[0]}
+    dsrc = {int(b): plan.d_sources.get(int(b), []) for b in pw}
+    n_pw = state.n_pw
+    stats = {"added": 0, "balance_added": 0, "pushes": 0, "direct_pairs": 0, "tables": 0}
+    tab_cache = {}
 
     def refill(b, kids):
         coef = apply_per_axis(basis.val_to_pol, vals.pop(b), d)
@@ -698,18 +924,122 @@ def refine_output(tree, values, potentials, delta, epsilon, boundary="free", max
                 out = np.moveaxis(np.tensordot(M[(c >> ax) & 1], out, axes=([1], [ax])), 0, ax)
             vals[kid] = np.ascontiguousarray(out)
 
-    rounds = 0
-    cur = tree
-    for rounds in range(max_rounds + 1):
-        marks = [b for b, u in pots.items()
-                 if cur.level[b] < lmax and tail_error(apply_per_axis(basis.val_to_pol,
-                                                                      np.asarray(u).reshape((k,) * d), d)) > epsilon]
-        if not marks or rounds == max_rounds:
-            break
-        for b in marks:
-            if B.leaf(b):
-                refill(b, B.split(b))
-        B.balance(refill)
-        cur = B.finalize()
-        pots = fgt_box(cur, vals, delta, epsilon, boundary)
-    return cur, vals, pots, rounds
+    class Sweep:
+        """Children to evaluate in one fgt_box_refine call."""
+
+        def __init__(self):
+            self.kids, self.push, self.pairs = [], [], []  # (kid), (level, dst, src, rows), (row, S, tabs)
+            self.tabs, self.tab_id = [], {}
+
+        def table(self, ls, o, r):
+            key = (ls, o, r)
+            t = self.tab_id.get(key)
+            if t is None:
+                mat = tab_cache.get(key)
+                if mat is None:
+                    Ls = side[ls]
+                    Jm = gauss_moment_J(2 * np.sqrt(delta) / Ls, k - 1, 2 * o + r * basis.nodes)
+                    mat = tab_cache[key] = ((Ls / 2.0) * Jm.T) @ basis.val_to_pol
+                    stats["tables"] += 1
+                t = self.tab_id[key] = len(self.tabs)
+                self.tabs.append(mat)
+            return t
+
+        def add(self, b, kids):
+            nonlocal n_pw
+            refill(b, kids)
+            pots.pop(b, None)
+            for kid in kids:
+                lk = B.level[kid]
+                g = B.coords[kid]
+                row = len(self.kids)
+                self.kids.append(kid)
+                if pw[b] >= 0:
+                    pw[kid] = n_pw
+                    n_pw += 1
+                    self.push.append((lk, pw[kid], pw[b],
+                                      [p2c_row[(lk, int(gc - 2 * gb))] for gc, gb in zip(g, B.coords[b])]))
+                else:
+                    pw[kid] = -1
+                dsrc[kid] = dsrc[b]
+                for S, ls, gs, v in dsrc[b]:
+                    # (c_T - c_S - v rs) / L_S and L_T / L_S: dyadic, exact in floating point
+                    r = 2.0 ** (ls - lk)
+                    tabs = [self.table(ls, (2 * int(g[ax]) + 1) * 0.5 * r - (2 * gs[ax] + 1) * 0.5
+                                       - v[ax] * float(1 << ls), r) for ax in range(d)]
+                    self.pairs.append((row, S, tabs))
+
+        def run(self):
+            if not self.kids:
+                return
+            rp = _RefinePlan(plan, n_levels)
+            rp.leaves = np.arange(len(self.kids))
+            rp.n_pw = n_pw
+            rp.pw2val = pw2val
+            rp.dtab = (np.ascontiguousarray(np.array(self.tabs, np.float64).reshape(-1, k, k))
+                       if self.tabs else np.zeros((0, k, k)))
+            push = sorted(self.push, key=lambda e: e[0])  # parents before children
+            stage_off, stage_kind, last = [0], [], None
+            for i, e in enumerate(push):
+                if last is not None and (e[0] != last or i - stage_off[-1] >= 65535):
+                    stage_off.append(i)
+                    stage_kind.append(2)
+                last = e[0]
+            if push:
+                stage_off.append(len(push))
+                stage_kind.append(2)
+            rp.stage_off = np.array(stage_off, np.int64)
+            rp.stage_kind = np.array(stage_kind, np.int64)
+            rp.dst = np.array([e[1] for e in push], np.int64)
+            rp.dst_acc = np.zeros(len(push), np.int64)
+            rp.dst_off = np.arange(len(push) + 1, dtype=np.int64)
+            rp.ent_src = np.array([e[2] for e in push], np.int64)
+            rp.ent_rows = np.array([e[3] for e in push], np.int64).reshape(-1, d)
+            ev = [(i, pw[kid], B.level[kid]) for i, kid in enumerate(self.kids) if pw[kid] >= 0]
+            rp.eval_leaf = np.array([e[0] for e in ev], np.int64)
+            rp.eval_pw = np.array([e[1] for e in ev], np.int64)
+            rp.eval_level = np.array([e[2] for e in ev], np.int64)
+            rp.d_tgt = np.array([p[0] for p in self.pairs], np.int64)
+            rp.d_src = np.array([p[1] for p in self.pairs], np.int64)
+            rp.d_tab = np.array([p[2] for p in self.pairs], np.int64).reshape(-1, d)
+            U = np.empty((len(self.kids),) + (k,) * d)
+            cs = _plan_cstruct(rp)
+            _lib.check(_lib.load().fgt_box_refine(state.handle, ctypes.byref(cs), _lib.ptr(U), None))
+            state.n_pw = n_pw
+            for i, kid in enumerate(self.kids):
+                pots[kid] = U[i]
+            stats["pushes"] += len(push)
+            stats["direct_pairs"] += len(self.pairs)
+
+    sweeps = 0
+    fresh = sorted(pots)
+    if relative:
+        epsilon = epsilon * max(grid_norm(tree, pots, k), 1e-300)
+    stats["threshold"] = epsilon
+    try:
+        while fresh and sweeps < max_rounds:
+            cand = [b for b in fresh if B.level[b] < lmax]
+            if not cand:
+                break
+            te = tail_errors(np.stack([pots[b] for b in cand]), d, k)
+            marks = [b for b, e in zip(cand, te) if e > epsilon]
+            if not marks:
+                break
+            sw = Sweep()
+            for b in marks:
+                sw.add(b, B.split(b))
+            sw.run()
+            stats["added"] += len(sw.kids)
+            fresh = sw.kids
+            sweeps += 1
+        sw = Sweep()
+        B.balance(sw.add)
+        sw.run()
+        stats["balance_added"] = len(sw.kids)
+    finally:
+        if own_state:
+            state.free()
+    cur = B.finalize()
+    leaf_ids = np.nonzero(cur.is_leaf)[0].tolist()
+    out = (cur, {b: vals[b] for b in leaf_ids}, {b: pots[b] for b in leaf_ids}, sweeps)
+    return out + (stats,) if return_stats else out
