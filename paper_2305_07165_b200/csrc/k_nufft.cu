@@ -1392,6 +1392,181 @@ int64_t ipow(int64_t b, int e) {
 }
 
 // grid -> modes for a batch of spread grids (see nufft_form_impl)
+// ---------------------------------------------------------------- fused d = 3 stages 2 + 3
+// After the axis-0 stage (bgemm: X[s][g2 g3] = sum_g1 EfH[s][g1] grid[g1][g2 g3], the one
+// stage that needs the whole grid of a box), the two remaining stages of a stored plane s
+// run in ONE warp with the intermediate on chip:
+//   stage 2  Y[m2][g3]      = sum_g2 Ef[m2][g2] X_s[g2][g3]     16 rows of m2 at a time
+//   stage 3  phi[s][m2][m3] = sum_g3 Y[m2][g3] Ef[m3][g3]        Y through the warp's own
+//            shared-memory rows; epilogue = the box's rephasing factor (fused translation)
+// so Y (222 KB per box written and read back by the three-launch path) never reaches HBM.
+// One CTA per box, 8 independent warps (no barrier after the prologue), warp w takes planes
+// w, w + 8, ...: X_s (13 KB, contiguous) comes in by cp.async into padded rows, and the next
+// plane's copy is issued as soon as stage 2 has consumed the current one, under stage 3.
+// Complex x complex MACs as three real DMMAs (Gauss), like bgemm.  Row pitches make every
+// fragment load bank-conflict free (16-byte lanes, quarter-warp phases).  Needs G <= 32 and
+// n_f <= 32 (220 KB of shared memory at G = 29: config 5); larger grids keep three launches.
+constexpr int DF_XP = 34;  // X row pitch in complex: 4 DF_XP = 8 (mod 32) words
+constexpr int DF_EP = 36;  // Ef / Y row pitch: 4 DF_EP = 16 (mod 32) words
+constexpr int DF_W = 8;    // warps per CTA
+
+struct Dft3Args {
+  const double2* x;     // (nbat, nh, G, G) complex: axis 0 already contracted
+  const double2* Ef;    // (n_f, G)
+  const int64_t* sl;    // expansion slot of each batch item
+  double2* phi;         // (slot, nh n_f, n_f), slot stride NH
+  int64_t NH;
+  int G, n_f, nh;
+  const double2* bp;    // optional box phases (slot, 3, n_f)
+  int bp_half;
+};
+
+inline size_t dft3_smem(int G) {
+  return sizeof(double2) * ((size_t)DF_W * (G * DF_XP + 16 * DF_EP) + (size_t)32 * DF_EP + 3 * 32);
+}
+
+__device__ __forceinline__ double2 df_cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+inline bool dft3_fused_ok(int G, int n_f) {
+  const char* e = std::getenv("FGT_DFT_FUSED");
+  return G <= 32 && n_f <= 32 && dft3_smem(G) <= 227 * 1024 && !(e && e[0] == '0');
+}
+
+__global__ void __launch_bounds__(DF_W * 32, 1) dft3_fused_kernel(Dft3Args a) {
+  extern __shared__ double2 dsm[];
+  const int G = a.G, n_f = a.n_f, nh = a.nh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  double2* Xs = dsm + (size_t)warp * (G * DF_XP + 16 * DF_EP);  // G x DF_XP
+  double2* Yw = Xs + G * DF_XP;                                  // 16 x DF_EP
+  double2* sE = dsm + (size_t)DF_W * (G * DF_XP + 16 * DF_EP);   // 32 x DF_EP (zero padded)
+  double2* sQ = sE + 32 * DF_EP;                                 // 3 x 32 rephasing factors
+  const int64_t b = blockIdx.x;
+  const int plane = G * G;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  const int64_t slot = a.sl ? a.sl[b] : b;
+  // X_s of plane sp -> the warp's padded rows (16-byte cp.async per element)
+  auto load_x = [&](int sp) {
+    const double2* src = a.x + ((int64_t)b * nh + sp) * plane;
+    for (int e = lane; e < plane; e += 32) {
+      const int g2 = e / G, g3 = e - g2 * G;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(Xs + g2 * DF_XP + g3);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + e));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (warp < nh) load_x(warp);
+  for (int e = threadIdx.x; e < 32 * DF_EP; e += blockDim.x) {
+    const int m = e / DF_EP, g = e - m * DF_EP;
+    sE[e] = (m < n_f && g < G) ? a.Ef[m * G + g] : zero2;
+  }
+  if (a.bp && threadIdx.x < 96) {
+    const int ax = threadIdx.x >> 5, m = threadIdx.x & 31;
+    sQ[threadIdx.x] = m < n_f ? a.bp[slot * 3 * n_f + ax * n_f + m] : zero2;
+  }
+  // pad columns of X (stage-2 B fragments read g3 up to 31; the copies never touch them)
+  for (int e = lane; e < G * (DF_XP - G); e += 32) Xs[(e / (DF_XP - G)) * DF_XP + G + e % (DF_XP - G)] = zero2;
+  __syncthreads();
+  const bool q = a.bp != nullptr;
+  const int nhalf = (n_f + 15) / 16;
+  for (int sp = warp; sp < nh; sp += DF_W) {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();
+    double2* out = a.phi + slot * a.NH + (int64_t)sp * n_f * n_f;
+    const double2 p0 = q ? sQ[a.bp_half ? (sp + n_f / 2) % n_f : sp] : make_double2(1.0, 0.0);
+    for (int h = 0; h < nhalf; ++h) {
+      double acc[2][4][4], gs[2][4][2];
+      auto clear = [&]() {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+            gs[mt][nt][0] = gs[mt][nt][1] = 0.0;
+          }
+      };
+      auto mac = [&](const double2 (&av)[2], const double2 (&bw)[4]) {
+        double bd[4], bs[4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          bd[nt] = bw[nt].y - bw[nt].x;
+          bs[nt] = bw[nt].x + bw[nt].y;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const double as = av[mt].x + av[mt].y;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            dmma2(acc[mt][nt][0], acc[mt][nt][1], as, bw[nt].x);
+            dmma2(acc[mt][nt][2], acc[mt][nt][3], av[mt].x, bd[nt]);
+            dmma2(gs[mt][nt][0], gs[mt][nt][1], av[mt].y, bs[nt]);
+          }
+        }
+      };
+      // stage 2: Y[16 h + ..][g3] = sum_g2 E[m2][g2] X_s[g2][g3]
+      clear();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = 4 * j + lk;
+        double2 av[2], bw[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) av[mt] = sE[(16 * h + 8 * mt + lr) * DF_EP + k];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bw[nt] = k < G ? Xs[k * DF_XP + 8 * nt + lr] : zero2;
+        mac(av, bw);
+      }
+      if (h == nhalf - 1 && sp + DF_W < nh) {
+        __syncwarp();  // every lane has read X_s: the next plane may land
+        load_x(sp + DF_W);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double k1 = acc[mt][nt][i], k2 = acc[mt][nt][2 + i], k3 = gs[mt][nt][i];
+            Yw[(8 * mt + lr) * DF_EP + 8 * nt + 2 * lk + i] = make_double2(k1 - k3, k1 + k2);
+          }
+      __syncwarp();
+      // stage 3: phi[s][16 h + ..][m3] = sum_g3 Y[m2][g3] E[m3][g3]
+      clear();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = 4 * j + lk;
+        double2 av[2], bw[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) av[mt] = Yw[(8 * mt + lr) * DF_EP + k];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bw[nt] = sE[(8 * nt + lr) * DF_EP + k];
+        mac(av, bw);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int m2 = 16 * h + 8 * mt + lr;
+        if (m2 >= n_f) continue;
+        double2 p01 = p0;
+        if (q) p01 = df_cmul(p0, sQ[32 + m2]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int m3 = 8 * nt + 2 * lk + i;
+            if (m3 >= n_f) continue;
+            const double k1 = acc[mt][nt][i], k2 = acc[mt][nt][2 + i], k3 = gs[mt][nt][i];
+            double2 v = make_double2(k1 - k3, k1 + k2);
+            if (q) v = df_cmul(df_cmul(p01, sQ[64 + m3]), v);
+            out[(int64_t)m2 * n_f + m3] = v;
+          }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int D>
 void form_modes(const NufftPlan& N, PwDev& P, const double* grid, const int64_t* sl, int64_t nbat,
                 GrowBuf<double>& g_t1, GrowBuf<double>& g_t2, cudaStream_t st) {
@@ -1410,6 +1585,25 @@ void form_modes(const NufftPlan& N, PwDev& P, const double* grid, const int64_t*
     bgemm<false, true, false>(gemm(grid, G, GD, N.EfT.get(), n_f, 0, t1.get(), n_f, (int64_t)G * n_f, G, n_f, G, (int)nbat), st);
     // phi[s][m2] = sum_g1 EfH[s][g1] T1[g1][m2]
     bgemm<true, true, false>(gemm(N.EfH.get(), G, 0, t1.get(), n_f, (int64_t)G * n_f, phi, n_f, NH, nh, n_f, G, (int)nbat, sl), st);
+  } else if (dft3_fused_ok(G, n_f)) {
+    auto x = g_t1.view(2 * nbat * nh * plane, st);
+    // X[s][(g2 g3)] = sum_g1 EfH[s][g1] grid[g1][(g2 g3)]
+    bgemm<true, false, false>(gemm(N.EfH.get(), G, 0, grid, plane, GD, x.get(), plane, nh * plane, nh, (int)plane, G, (int)nbat), st);
+    Dft3Args da;
+    da.x = reinterpret_cast<const double2*>(x.get());
+    da.Ef = reinterpret_cast<const double2*>(N.Ef.get());
+    da.sl = sl;
+    da.phi = reinterpret_cast<double2*>(phi);
+    da.NH = NH;
+    da.G = G;
+    da.n_f = n_f;
+    da.nh = nh;
+    da.bp = P.fused ? reinterpret_cast<const double2*>(P.bp.get()) : nullptr;
+    da.bp_half = P.half;
+    const size_t smem = dft3_smem(G);
+    FGT_CUDA(cudaFuncSetAttribute(dft3_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dft3_fused_kernel<<<(unsigned)nbat, DF_W * 32, smem, st>>>(da);
+    FGT_LAUNCHED();
   } else {
     auto x = g_t1.view(2 * nbat * nh * plane, st);
     auto y = g_t2.view(2 * nbat * nh * n_f * G, st);
