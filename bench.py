@@ -263,7 +263,8 @@ def kernel_rooflines(phases, fp64_peak_tf, hbm_gbs, d):
 PHASE_KERNELS = {
     "form": ("spread_pencil_kernel", "pencil_reduce_kernel", "pencil_jobs_kernel", "gather_jobs_kernel",
              "spread_tile_kernel", "sort_records_kernel", "spread_taps_kernel", "spread_keys_kernel",
-             "form_kernel", "form_reduce_kernel", "plane_reduce_kernel", "bgemm_kernel", "job_ranges_kernel"),
+             "form_kernel", "form_reduce_kernel", "plane_reduce_kernel", "bgemm_kernel", "dft3_fused_kernel",
+             "job_ranges_kernel"),
     "eval": ("eval_kernel", "interp_kernel", "gather_eval_kernel"),
     "direct": ("direct_warp_kernel", "direct_kernel"),
     "gather": ("gather_kernel", "group_table_kernel"),

@@ -231,9 +231,11 @@ int fgt_points(const double* src, int64_t ns, const double* charges, const doubl
 /* ---------------------------------------------------------------------------
  * Layer 3: continuous (box) FGT, Alg 4.
  *
- * The density tree (Alg 3, tree.py:394-461) needs the user's sigma callable, so it is
- * built on the host; the host also builds the per-level 1-D tables (J/I moments,
- * poly1d.py:129-210) and the schedules below.  Everything else runs on the GPU:
+ * The density tree (Alg 3, tree.py:394-461) needs the user's sigma callable: the host
+ * drives it (optionally with the per-grid tests on the device, fgt_box_tail_dev /
+ * fgt_box_nodes_dev / fgt_box_balance_flags below); the host also builds the per-level 1-D
+ * tables (J/I moments, poly1d.py:129-210) and the schedules below.  Everything else runs on
+ * the GPU:
  * leaf->PW and PW->grid as d separable FP64-DMMA GEMMs per level, the diagonal
  * merge / gather / push shifts, and the direct near field as separable k x k
  * contractions.  All index arrays are HOST int64 arrays; complex = interleaved.

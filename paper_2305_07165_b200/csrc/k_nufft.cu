@@ -1450,10 +1450,18 @@ __global__ void __launch_bounds__(DF_W * 32, 1) dft3_fused_kernel(Dft3Args a) {
   // X_s of plane sp -> the warp's padded rows (16-byte cp.async per element)
   auto load_x = [&](int sp) {
     const double2* src = a.x + ((int64_t)b * nh + sp) * plane;
+    // (g2, g3) of element e = lane + 32 i by increments: no division in the copy loop
+    int g2 = lane / G, g3 = lane - g2 * G;
+    const int d2 = 32 / G, d3 = 32 - d2 * G;
     for (int e = lane; e < plane; e += 32) {
-      const int g2 = e / G, g3 = e - g2 * G;
       const unsigned dst = (unsigned)__cvta_generic_to_shared(Xs + g2 * DF_XP + g3);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + e));
+      g2 += d2;
+      g3 += d3;
+      if (g3 >= G) {
+        g3 -= G;
+        ++g2;
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };

@@ -1,10 +1,13 @@
-"""Continuous (box) FGT on the GPU: Alg 3 density tree on the host, Alg 4 in CUDA.
+"""Continuous (box) FGT on the GPU: Alg 3 density tree (host, or decided on the device),
+Alg 4 in CUDA, Alg 5 from retained incoming expansions, Alg 6, interp_at.
 
 Public entry points mirror the reference / SPEC:
   * `build_density_tree(density, dim, k, epsilon, periodic=False, l_max=30,
     refill="evaluate", root_center=None, root_side=1.0)` -> (tree, values, coeffs),
     the contract of /root/reference/pkg/src/fgt/tree.py:394-461 (sigma is a user
-    callable, so Alg 3 runs on the host; boxes are created in the reference's order);
+    callable, so Alg 3 is driven from the host; boxes are created in the reference's order;
+    device="cuda" moves the node generation, sigma, the tail tests and the balance sweeps
+    to the GPU);
   * `fgt_box(tree, values, delta, epsilon, boundary="free")` -> {leaf: u (k,)*d}
     (SPEC.md:512-516): the level tables (J/I moments, poly1d.py:129-210) and schedules are
     built here, then one C call (`fgt_box`, include/fgt_cuda.h) runs leaf->PW, merge,
