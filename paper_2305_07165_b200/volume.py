@@ -759,12 +759,49 @@ def interp_at(tree, potentials, targets):
 
 
 
-def coarsen_output(tree, potentials, epsilon):
+def _coarsen_output_device(tree, potentials, epsilon):
+    """Alg 6 with the per-grid work on the GPU: per level, the k^d nodes of every candidate
+    parent (all children leaves) are evaluated through the current tree's leaf interpolants
+    (`fgt_box_interp`: the deepest leaf holding a node is the child the host sweep picks,
+    Gauss-Legendre nodes being interior) and tested by the tail kernel (`fgt_box_tail`); the
+    host only edits the tree.  Same merges as the host sweep."""
+    d = tree.dim
+    k = np.asarray(next(iter(potentials.values()))).shape[0]
+    basis = LegendreBasis(k)
+    pots = {int(b): np.asarray(v, float).reshape((k,) * d) for b, v in potentials.items()}
+    is_leaf = tree.is_leaf.copy()
+    alive = np.ones(tree.n_boxes, bool)
+    for lev in range(int(tree.level.max()) - 1, -1, -1):
+        cand = [int(b) for b in np.nonzero((tree.level == lev) & ~is_leaf & alive)[0]
+                if all(is_leaf[c] for c in tree.children[b])]
+        if not cand:
+            continue
+        cur = Tree(dim=d, root_center=tree.root_center, root_side=tree.root_side, periodic=tree.periodic,
+                   level=tree.level, parent=tree.parent, children=tree.children, coords=tree.coords,
+                   is_leaf=is_leaf & alive)
+        nodes = np.concatenate([leaf_grid(tree, b, basis).reshape(-1, d) for b in cand])
+        V = interp_at(cur, pots, nodes).reshape((len(cand),) + (k,) * d)
+        te = tail_errors(V, d, k)
+        for i, b in enumerate(cand):
+            if te[i] <= epsilon:
+                pots[b] = V[i]
+                is_leaf[b] = True
+                for c in tree.children[b]:
+                    alive[c] = False
+                    pots.pop(int(c), None)
+    return _renumber_alive(tree, is_leaf, alive, pots)
+
+
+def coarsen_output(tree, potentials, epsilon, device=None):
     """Alg 6: bottom-up, a non-leaf box whose
     children are all leaves gets the potential at its own k^d grid by evaluating whichever
     child holds each node; if that grid's Legendre tail error (Eq. funerr, tail_error) is
     <= epsilon the children are deleted and the box becomes a leaf.  Returns (tree,
-    potentials) with boxes renumbered (level-restriction is not re-imposed)."""
+    potentials) with boxes renumbered (level-restriction is not re-imposed).
+    device="cuda": the interpolation and the tail tests run on the GPU, one batch per level
+    (_coarsen_output_device); None: host numpy."""
+    if device is not None:
+        return _coarsen_output_device(tree, potentials, epsilon)
     d = tree.dim
     k = np.asarray(next(iter(potentials.values()))).shape[0]
     basis = LegendreBasis(k)
@@ -804,7 +841,12 @@ def coarsen_output(tree, potentials, epsilon):
                 for c in ch:
                     alive[c] = False
                     pots.pop(int(c), None)
+    return _renumber_alive(tree, is_leaf, alive, pots)
+
+
+def _renumber_alive(tree, is_leaf, alive, pots):
     # renumber the surviving boxes (creation order kept)
+    d = tree.dim
     keep = np.nonzero(alive)[0]
     new_id = np.full(tree.n_boxes, -1, np.int64)
     new_id[keep] = np.arange(keep.size)

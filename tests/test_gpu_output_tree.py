@@ -144,6 +144,7 @@ REFINE_CASES = [
     ("direct", 2, 6, 1e-3, 1e-4, 1e-9, 1e-9, False),
     ("periodic", 2, 6, 1e-6, 2e-3, 1e-8, 3e-9, True),
     ("d3", 3, 5, 1e-3, 4e-3, 1e-7, 1e-8, False),
+    ("d3direct", 3, 6, 1e-2, 1e-3, 1e-6, 1e-8, False),
     ("rootseries", 2, 6, 1e-6, 5e-2, 1e-10, 1e-9, True),
     ("d1", 1, 8, 1e-4, 1e-3, 1e-10, 1e-10, False),
 ]
@@ -165,7 +166,7 @@ def test_refine_from_retained_expansions(cuda, case):
     tree, vals, _ = pv.build_density_tree(dens, d, k, eps_tree, periodic=periodic)
     u, state = pv.fgt_box(tree, vals, delta, eps, bnd, retain=True)
     lmax = int(tree.level.max())
-    if name == "direct":
+    if name in ("direct", "d3direct"):
         assert lmax <= state.plan.l_c  # every leaf is at or above the cutoff level: direct only
     assert any(_tail(pv, v, k, d) > eps_ref and tree.level[b] < lmax for b, v in u.items())
     t2, v2, u2, sweeps, stats = pv.refine_output(tree, vals, u, epsilon=eps_ref, boundary=bnd, state=state,
@@ -173,7 +174,7 @@ def test_refine_from_retained_expansions(cuda, case):
     state.free()
     assert sweeps >= 1 and stats["added"] > 0 and t2.n_boxes == tree.n_boxes + stats["added"] + stats["balance_added"]
     assert int(t2.level.max()) <= lmax
-    if name == "direct":
+    if name in ("direct", "d3direct"):
         assert stats["pushes"] == 0 and stats["direct_pairs"] > 0 and stats["tables"] > 0
     if name in ("pw", "rootseries"):
         assert stats["pushes"] > 0
@@ -227,7 +228,11 @@ def test_output_resolution_section_4_2(cuda):
     assert err_in >= 1e-8
     assert err_out <= 1e-11
     assert stats["added"] > 0.25 * tree.n_boxes
-    t3, u3 = pv.coarsen_output(t2, u2, stats["threshold"])
+    t3, u3 = pv.coarsen_output(t2, u2, stats["threshold"], device="cuda")
+    # the device sweep (interp_at + tail kernel per level) makes the host sweep's merges
+    t3h, u3h = pv.coarsen_output(t2, u2, stats["threshold"])
+    assert t3.n_boxes == t3h.n_boxes and np.array_equal(t3.coords, t3h.coords)
+    assert max(np.max(np.abs(u3[b] - u3h[b])) for b in u3h) <= 1e-13 * max(np.max(np.abs(v)) for v in u3h.values())
     err_c = np.linalg.norm(pv.interp_at(t3, u3, x) - ex) / np.linalg.norm(ex)
     print(f"section 4.2: coarsening deleted {t2.n_boxes - t3.n_boxes} boxes -> {t3.n_boxes}, error {err_c:.2e}")
     assert t3.n_boxes < t2.n_boxes and err_c <= 1e-10
