@@ -13,7 +13,8 @@ CLASSES = ["DMMA", "DFMA", "DMUL", "DADD", "LDG", "STG", "LDS", "STS", "LDGSTS",
            "BAR", "SHFL", "MUFU", "ATOM", "RED"]
 HOT = ["gather_eval_kernel", "spread_pencil_kernel", "bgemm_kernel", "eval_kernel", "gather_kernel",
        "sort_records_kernel", "direct_warp_kernel", "direct_kernel", "form_kernel", "spread_tile_kernel",
-       "phi_rephase_kernel", "point_codes_kernel", "spread_runs_kernel", "nufft_spread"]
+       "phi_rephase_kernel", "point_codes_kernel", "spread_runs_kernel", "nufft_spread",
+       "dft3_fused_kernel", "tail_kernel", "balance_flags_kernel", "nodes_kernel", "shift_kernel", "direct3_kernel"]
 
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
 cur, counts = None, collections.OrderedDict()
