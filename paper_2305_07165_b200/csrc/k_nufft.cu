@@ -1401,8 +1401,9 @@ int64_t ipow(int64_t b, int e) {
 //            shared-memory rows; epilogue = the box's rephasing factor (fused translation)
 // so Y (222 KB per box written and read back by the three-launch path) never reaches HBM.
 // One CTA per box, 8 independent warps (no barrier after the prologue), warp w takes planes
-// w, w + 8, ...: X_s (13 KB, contiguous) comes in by cp.async into padded rows, and the next
-// plane's copy is issued as soon as stage 2 has consumed the current one, under stage 3.
+// w, w + 8, ...: X_s (13 KB, contiguous) comes in by TMA bulk copies (one per row, into padded
+// rows, completion on the warp's mbarrier), and the next plane's copy is issued as soon as
+// stage 2 has consumed the current one, under stage 3.
 // Complex x complex MACs as three real DMMAs (Gauss), like bgemm.  Row pitches make every
 // fragment load bank-conflict free (16-byte lanes, quarter-warp phases).  Needs G <= 32 and
 // n_f <= 32 (220 KB of shared memory at G = 29: config 5); larger grids keep three launches.
@@ -1447,23 +1448,39 @@ __global__ void __launch_bounds__(DF_W * 32, 1) dft3_fused_kernel(Dft3Args a) {
   const int plane = G * G;
   const double2 zero2 = make_double2(0.0, 0.0);
   const int64_t slot = a.sl ? a.sl[b] : b;
-  // X_s of plane sp -> the warp's padded rows (16-byte cp.async per element)
+  // X_s of plane sp -> the warp's padded rows: one TMA bulk copy per row of G complex
+  // (cp.async.bulk, SASS UBLKCP; lane g2 issues row g2), all completing on the warp's
+  // mbarrier, whose phase flips once per plane
+  __shared__ uint64_t s_bar[DF_W];
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar[warp]);
+  const unsigned row_bytes = (unsigned)(G * sizeof(double2));
+  if (lane == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  __syncwarp();
   auto load_x = [&](int sp) {
     const double2* src = a.x + ((int64_t)b * nh + sp) * plane;
-    // (g2, g3) of element e = lane + 32 i by increments: no division in the copy loop
-    int g2 = lane / G, g3 = lane - g2 * G;
-    const int d2 = 32 / G, d3 = 32 - d2 * G;
-    for (int e = lane; e < plane; e += 32) {
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(Xs + g2 * DF_XP + g3);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + e));
-      g2 += d2;
-      g3 += d3;
-      if (g3 >= G) {
-        g3 -= G;
-        ++g2;
-      }
+    // earlier generic-proxy reads of X_s are ordered before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(row_bytes * G));
+    __syncwarp();
+    for (int g2 = lane; g2 < G; g2 += 32) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(Xs + g2 * DF_XP);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+          "l"(src + (int64_t)g2 * G), "r"(row_bytes), "r"(bar)
+          : "memory");
     }
-    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto wait_x = [&](unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar), "r"(parity)
+          : "memory");
+    }
   };
   if (warp < nh) load_x(warp);
   for (int e = threadIdx.x; e < 32 * DF_EP; e += blockDim.x) {
@@ -1479,9 +1496,10 @@ __global__ void __launch_bounds__(DF_W * 32, 1) dft3_fused_kernel(Dft3Args a) {
   __syncthreads();
   const bool q = a.bp != nullptr;
   const int nhalf = (n_f + 15) / 16;
+  unsigned parity = 0;
   for (int sp = warp; sp < nh; sp += DF_W) {
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncwarp();
+    wait_x(parity);
+    parity ^= 1u;
     double2* out = a.phi + slot * a.NH + (int64_t)sp * n_f * n_f;
     const double2 p0 = q ? sQ[a.bp_half ? (sp + n_f / 2) % n_f : sp] : make_double2(1.0, 0.0);
     for (int h = 0; h < nhalf; ++h) {
