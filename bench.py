@@ -236,10 +236,20 @@ def kernel_rooflines(phases, fp64_peak_tf, hbm_gbs, d):
     f_direct = (3.0 * d + 3.0 + 20.0) * ph["n_direct_pairs"]
     mean = lambda k: float(np.mean([p[k] for p in phases]))  # noqa: E731
     out = []
+    # fused translation + evaluation (psi never stored): the gather phase holds only the group
+    # table (its time could not move the compulsory phi + psi bytes at the HBM peak), so the
+    # translation's 8 N_F flops per P-list entry count with the
+    # evaluation kernel that performs them and there is no separate gather line
+    fused = mean("k_gather_ms") > 0 and b_gather / (mean("k_gather_ms") * 1e-3) / 1e9 > hbm_gbs
+    eval_name = "eval (exact DMMA sums + ES-kernel NUFFT)"
+    if fused:
+        f_eval += 8.0 * NF * ph["n_p_entries"]
+        b_gather = 0.0
+        eval_name = "translation + eval (fused: psi never stored; exact DMMA sums)"
     for name, alg, ms, bound in (
             ("form (exact DMMA sums + ES-kernel NUFFT: taps, records, pencils, DFT stages)", f_form,
              mean("k_form_ms"), "tensor"),
-            ("eval (exact DMMA sums + ES-kernel NUFFT)", f_eval, mean("k_eval_ms"), "tensor"),
+            (eval_name, f_eval, mean("k_eval_ms"), "tensor"),
             ("gather (diagonal translation)", b_gather, mean("k_gather_ms"), "hbm"),
             ("direct (near field, ball cut)", f_direct, mean("k_direct_ms"), "fp64")):
         if ms <= 0 or alg <= 0:
@@ -266,6 +276,7 @@ PHASE_KERNELS = {
              "form_kernel", "form_reduce_kernel", "plane_reduce_kernel", "bgemm_kernel", "dft3_fused_kernel",
              "job_ranges_kernel"),
     "eval": ("eval_kernel", "interp_kernel", "gather_eval_kernel"),
+    "translation": ("eval_kernel", "interp_kernel", "gather_eval_kernel"),
     "direct": ("direct_warp_kernel", "direct_kernel"),
     "gather": ("gather_kernel", "group_table_kernel"),
 }

@@ -1,6 +1,6 @@
 """Per-kernel SASS instruction-class counts of libfgtcuda.so (cuobjdump -sass), for the hot
 kernels: DMMA (FP64 tensor core), DFMA/DMUL/DADD (FP64 pipe), LDG/STG, LDS/STS, LDGSTS
-(cp.async), UTMALDG (TMA), BAR, SHFL.  Static counts (instructions in the binary), not
+(cp.async), UTMALDG / UBLKCP (TMA tensor / bulk copies), SYNCS (mbarrier), BAR, SHFL.  Static counts (instructions in the binary), not
 executed counts.  Prints JSON."""
 import collections
 import json
@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_2305_07165_b200/libfgtcuda.so"
-CLASSES = ["DMMA", "DFMA", "DMUL", "DADD", "LDG", "STG", "LDS", "STS", "LDGSTS", "UTMALDG", "UTMASTG",
+CLASSES = ["DMMA", "DFMA", "DMUL", "DADD", "LDG", "STG", "LDS", "STS", "LDGSTS", "UTMALDG", "UTMASTG", "UBLKCP", "SYNCS",
            "BAR", "SHFL", "MUFU", "ATOM", "RED"]
 HOT = ["gather_eval_kernel", "spread_pencil_kernel", "bgemm_kernel", "eval_kernel", "gather_kernel",
        "sort_records_kernel", "direct_warp_kernel", "direct_kernel", "form_kernel", "spread_tile_kernel",
