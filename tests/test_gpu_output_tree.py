@@ -145,6 +145,7 @@ REFINE_CASES = [
     ("periodic", 2, 6, 1e-6, 2e-3, 1e-8, 3e-9, True),
     ("d3", 3, 5, 1e-3, 4e-3, 1e-7, 1e-8, False),
     ("d3direct", 3, 6, 1e-2, 1e-3, 1e-6, 1e-8, False),
+    ("perdirect", 2, 6, 1e-2, 1e-4, 1e-8, 1e-8, True),  # direct pairs with image shifts, levels 1-2
     ("rootseries", 2, 6, 1e-6, 5e-2, 1e-10, 1e-9, True),
     ("d1", 1, 8, 1e-4, 1e-3, 1e-10, 1e-10, False),
 ]
@@ -166,7 +167,7 @@ def test_refine_from_retained_expansions(cuda, case):
     tree, vals, _ = pv.build_density_tree(dens, d, k, eps_tree, periodic=periodic)
     u, state = pv.fgt_box(tree, vals, delta, eps, bnd, retain=True)
     lmax = int(tree.level.max())
-    if name in ("direct", "d3direct"):
+    if name in ("direct", "d3direct", "perdirect"):
         assert lmax <= state.plan.l_c  # every leaf is at or above the cutoff level: direct only
     assert any(_tail(pv, v, k, d) > eps_ref and tree.level[b] < lmax for b, v in u.items())
     t2, v2, u2, sweeps, stats = pv.refine_output(tree, vals, u, epsilon=eps_ref, boundary=bnd, state=state,
@@ -174,7 +175,7 @@ def test_refine_from_retained_expansions(cuda, case):
     state.free()
     assert sweeps >= 1 and stats["added"] > 0 and t2.n_boxes == tree.n_boxes + stats["added"] + stats["balance_added"]
     assert int(t2.level.max()) <= lmax
-    if name in ("direct", "d3direct"):
+    if name in ("direct", "d3direct", "perdirect"):
         assert stats["pushes"] == 0 and stats["direct_pairs"] > 0 and stats["tables"] > 0
     if name in ("pw", "rootseries"):
         assert stats["pushes"] > 0
@@ -190,7 +191,10 @@ def test_refine_from_retained_expansions(cuda, case):
     old = np.concatenate([np.asarray(u[b]).reshape(-1) for b in u])
     # (to the resolution reached: leaves at the input tree's deepest level cannot be refined)
     reached = max([eps_ref] + [_tail(pv, v, k, d) for b, v in u2.items() if t2.level[b] == lmax])
-    assert np.max(np.abs(pv.interp_at(t2, u2, nodes) - old)) <= 10 * max(reached, eps * scale)
+    # (the tail RMS sits up to ~15x below a leaf's largest interpolation error on trees this
+    # coarse, hence 30x when the depth cap leaves unresolved leaves)
+    factor = 10 if reached <= eps_ref else 30
+    assert np.max(np.abs(pv.interp_at(t2, u2, nodes) - old)) <= factor * max(reached, eps * scale)
     x = np.random.default_rng(51).uniform(-0.5, 0.5, (3000, d))
     assert np.max(np.abs(pv.interp_at(t2, v2, x) - pv.interp_at(tree, vals, x))) < 1e-12
     # idempotence: a resolved output is left alone
