@@ -885,6 +885,17 @@ def grid_norm(tree, grids, k):
     return float(np.sqrt(np.sum(half ** tree.dim * wsq)) / tree.root_side ** (tree.dim / 2.0))
 
 
+def direct_table_key(lt, gt, ls, gs, v):
+    """Per-axis centre offset (c_T - c_S - v L_0) / L_S and side ratio L_T / L_S of a target box
+    (level lt, integer coords gt) and a source box (ls, gs) under image shift v: the key of
+    the T_pol2pot table of the pair (J_lam[P_n](2 o + r xi); any level
+    difference, Alg 5 Remark).  Dyadic numbers from integer box coordinates: exact in floating
+    point, so equal pairs share a table."""
+    r = 2.0 ** (ls - lt)
+    return [(2 * int(gt[ax]) + 1) * 0.5 * r - (2 * int(gs[ax]) + 1) * 0.5 - int(v[ax]) * float(1 << ls)
+            for ax in range(len(gs))], r
+
+
 class _RefinePlan:
     """fgt_box_plan for one Alg 5 sweep: pushes into new plane-wave slots, PW -> grid on the
     new leaves, direct tables for arbitrary (offset, side ratio) pairs (Alg 5 Remark)."""
@@ -1008,10 +1019,8 @@ def refine_output(tree, values, potentials=None, delta=None, epsilon=None, bound
                     pw[kid] = -1
                 dsrc[kid] = dsrc[b]
                 for S, ls, gs, v in dsrc[b]:
-                    # (c_T - c_S - v rs) / L_S and L_T / L_S: dyadic, exact in floating point
-                    r = 2.0 ** (ls - lk)
-                    tabs = [self.table(ls, (2 * int(g[ax]) + 1) * 0.5 * r - (2 * gs[ax] + 1) * 0.5
-                                       - v[ax] * float(1 << ls), r) for ax in range(d)]
+                    offs, r = direct_table_key(lk, g, ls, gs, v)
+                    tabs = [self.table(ls, o, r) for o in offs]
                     self.pairs.append((row, S, tabs))
 
         def run(self):

@@ -88,3 +88,31 @@ def test_coarsen_output_alg6():
     const = {int(b): np.full((k,) * d, 3.0) for b in np.nonzero(tree.is_leaf)[0]}
     t3, p3 = pv.coarsen_output(tree, const, 1e-12)
     assert t3.n_boxes == 1 and np.allclose(p3[0], 3.0)
+
+
+@pytest.mark.parametrize("d,periodic", [(2, True), (2, False), (3, False)])
+def test_direct_table_key_matches_plan_offsets(d, periodic):
+    """The integer-coordinate key Alg 5 uses for its extended T_pol2pot tables
+    (direct_table_key) reproduces, on every leaf pair of the plan's D-lists, the (offset,
+    ratio) the Alg 4 plan reads from box centres -- one of the 11 standard offsets -- so the
+    standard tables are the level-restricted special case of the extended ones."""
+    from paper_2305_07165_b200 import volume as pv
+    k, delta, eps = 6, 1e-4, 1e-8
+    dens = lambda p: 0.3 + sigma_f(d)(p)  # noqa: E731
+    t, vals, _ = pv.build_density_tree(dens, d, k, 1e-4 if d == 2 else 1e-2, periodic=periodic)
+    plan = pv.BoxPlan(t, delta, eps, k, periodic)
+    assert plan.d_sources
+    ctr = t.centers()
+    n = 0
+    for T, lst in plan.d_sources.items():
+        for S_slot, ls, gs, v in lst:
+            S = int(plan.leaves[S_slot])
+            offs, r = pv.direct_table_key(int(t.level[T]), t.coords[T], ls, gs, v)
+            Ls = t.root_side / 2.0 ** ls
+            want = (ctr[T] - ctr[S] - np.asarray(v) * t.root_side) / Ls
+            assert np.allclose(offs, want, rtol=0, atol=1e-12) and r == 2.0 ** (ls - int(t.level[T]))
+            assert all((o, r) in pv.OFFSETS for o in offs)
+            n += 1
+    assert n == plan.d_tgt.size
+    if periodic:
+        assert any(any(v) for lst in plan.d_sources.values() for _, _, _, v in lst)
