@@ -66,16 +66,26 @@ __global__ void __launch_bounds__(256) shift_kernel(ShiftArgs a) {
       rem /= n_f;
     }
     double2 acc = acc_in ? out[e] : make_double2(0.0, 0.0);
-    for (int i = 0; i < ne; ++i) {
-      double2 p = a.rows[(int64_t)s_row[i][0] * n_f + m[0]];
+    // entries four at a time: the four expansion loads are issued before any phase product
+    // (same summation order as one at a time)
+    for (int i0 = 0; i0 < ne; i0 += 4) {
+      double2 f[4];
 #pragma unroll
-      for (int k = 1; k < D; ++k) {
-        const double2 q = a.rows[(int64_t)s_row[i][k] * n_f + m[k]];
-        p = make_double2(p.x * q.x - p.y * q.y, p.x * q.y + p.y * q.x);
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u < ne) f[u] = __ldg(a.src + s_src[i0 + u] * a.NF + e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        if (i >= ne) break;
+        double2 p = __ldg(a.rows + (int64_t)s_row[i][0] * n_f + m[0]);
+#pragma unroll
+        for (int k = 1; k < D; ++k) {
+          const double2 q = __ldg(a.rows + (int64_t)s_row[i][k] * n_f + m[k]);
+          p = make_double2(p.x * q.x - p.y * q.y, p.x * q.y + p.y * q.x);
+        }
+        acc.x += p.x * f[u].x - p.y * f[u].y;
+        acc.y += p.x * f[u].y + p.y * f[u].x;
       }
-      const double2 f = a.src[s_src[i] * a.NF + e];
-      acc.x += p.x * f.x - p.y * f.y;
-      acc.y += p.x * f.y + p.y * f.x;
     }
     out[e] = acc;
   }
