@@ -354,6 +354,47 @@ __global__ void share_owner_kernel(const int64_t* __restrict__ bounds, int P, co
   }
 }
 
+// boxes whose points a rank touches: its target leaves and their D-list sources, its psi
+// boxes, and the P-boxes whose expansions it forms
+__global__ void need_leaf_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ off,
+                                 const int64_t* __restrict__ end, int64_t n, const int64_t* __restrict__ d_src,
+                                 uint8_t* __restrict__ need_src, uint8_t* __restrict__ need_tgt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    need_tgt[ids[i]] = 1;
+    for (int64_t e = off[i]; e < end[i]; ++e) need_src[d_src[e]] = 1;
+  }
+}
+__global__ void need_ids_kernel(const int64_t* __restrict__ ids, const uint8_t* __restrict__ sel, int64_t n,
+                                uint8_t* __restrict__ need) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!sel || sel[i]) need[ids[i]] = 1;
+}
+
+// leaf-ordered points of the rank's share only (after plan_share)
+static void gather_share_points(TreeDev& T, const double* src, const double* q, const double* tgt) {
+  cudaStream_t st = T.st;
+  DBuf<uint8_t> ns(std::max<int64_t>(T.nb, 1), st), nt(std::max<int64_t>(T.nb, 1), st);
+  ns.zero();
+  nt.zero();
+  if (T.n_dtgt > 0) {
+    need_leaf_kernel<<<grid_for(T.n_dtgt, 256), 256, 0, st>>>(T.d_tgt_ids.get(), T.d_off.get(), T.d_end.get(), T.n_dtgt,
+                                                             T.d_src.get(), ns.get(), nt.get());
+    FGT_LAUNCHED();
+  }
+  if (T.n_psi > 0) {
+    need_ids_kernel<<<grid_for(T.n_psi, 256), 256, 0, st>>>(T.psi_ids.get(), nullptr, T.n_psi, nt.get());
+    FGT_LAUNCHED();
+  }
+  if (T.n_dense > 0) {
+    DBuf<uint8_t> sel(T.n_dense, st);
+    sel.from_host(T.dense_need.data(), T.n_dense);
+    need_ids_kernel<<<grid_for(T.n_dense, 256), 256, 0, st>>>(T.dense_ids.get(), sel.get(), T.n_dense, ns.get());
+    FGT_LAUNCHED();
+    // (dense_need is pageable host memory: the copy above has left it when it returned)
+  }
+  gather_needed_points(T, src, q, tgt, ns.get(), nt.get());
+}
+
 static void plan_share(TreeDev& T, int rank, int size, int64_t NH, int w, bool exchange, ExchangePlan* X) {
   cudaStream_t st = T.st;
   FGT_REQUIRE(size <= 64, FGT_ERANGE, "at most 64 ranks");
@@ -546,7 +587,14 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
   TreeDev& T = R.T;
   build_tree(T, src, ns, tgt, nt, tp, st);
   if (q_ready) FGT_CUDA(cudaStreamWaitEvent(st, q_ready, 0));  // charges copied on a side stream
-  gather_sorted_points(T, src, q, tgt);
+  // multi-GPU shares gather the leaf-ordered points after the share is planned, and only
+  // the rank's own (plan_share needs counts, not coordinates)
+  // (below ~8M points the full gather is cheaper than planning the restricted one;
+  // FGT_SHARE_GATHER_MIN overrides the threshold for tests)
+  const char* env_min = std::getenv("FGT_SHARE_GATHER_MIN");
+  const int64_t gather_min = env_min ? atoll(env_min) : ((int64_t)1 << 23);
+  const bool shared = tp.part_size > 1 && ns + nt >= gather_min;
+  if (!shared) gather_sorted_points(T, src, q, tgt);
   R.pm->mark();
   trace_mark(st, "tree");
   const double D0 = tp.D0;
@@ -604,6 +652,7 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
   if (tp.part_size > 1) {
     FGT_REQUIRE(tp.part_rank >= 0 && tp.part_rank < tp.part_size, FGT_EINVAL, "bad part_rank");
     plan_share(T, tp.part_rank, tp.part_size, NH, w, exchange, &R.X);
+    if (shared) gather_share_points(T, src, q, tgt);
   }
   R.pm->mark();
   trace_mark(st, "lists");

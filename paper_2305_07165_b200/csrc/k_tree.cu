@@ -1037,6 +1037,69 @@ void gather_sorted_points(TreeDev& T, const double* src, const double* q, const 
   gather(tgt, nullptr, T.tgt_perm.get(), T.nt, T.tgt_sorted.get(), nullptr);
 }
 
+// Multi-GPU shares: only the leaves a rank works on get their points gathered (warp per box:
+// sources + charges of the boxes flagged in need_src, targets of those in need_tgt); the
+// rest of src_sorted / tgt_sorted stays unwritten and is never read by that rank.
+namespace {
+// BIG = false: a warp per box of the tree, except P-boxes above GN_BIG points; BIG = true: a
+// CTA per listed P-box above GN_BIG points (all 256 threads stride over its points) -- so a
+// 50k-point leaf of a clustered input does not serialise on one warp.  Leaves that are not
+// P-boxes hold <= n_s points.
+constexpr int64_t GN_BIG = 1024;
+template <int D, bool BIG>
+__global__ void __launch_bounds__(256) gather_needed_kernel(
+    const double* __restrict__ a, const double* __restrict__ q, const int64_t* __restrict__ perm,
+    const int64_t* __restrict__ start, const int64_t* __restrict__ count, const uint8_t* __restrict__ is_leaf,
+    const uint8_t* __restrict__ need, const int64_t* __restrict__ dense_slot, const int64_t* __restrict__ dense_ids,
+    int64_t nb, double* __restrict__ out, double* __restrict__ qout) {
+  const int lane = BIG ? threadIdx.x : (threadIdx.x & 31);
+  const int width = BIG ? 256 : 32;
+  const int64_t nunit = BIG ? (int64_t)gridDim.x : (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t unit = BIG ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int64_t it = unit; it < nb; it += nunit) {
+    const int64_t b = BIG ? dense_ids[it] : it;
+    if (!need[b] || !is_leaf[b]) continue;
+    const int64_t s0 = start[b], n = count[b];
+    if (BIG ? n <= GN_BIG : (n > GN_BIG && dense_slot[b] >= 0)) continue;
+    for (int64_t i = lane; i < n; i += width) {
+      const int64_t j = perm[s0 + i];
+#pragma unroll
+      for (int k = 0; k < D; ++k) out[(s0 + i) * D + k] = a[j * D + k];
+      if (q) qout[s0 + i] = q[j];
+    }
+  }
+}
+}  // namespace
+
+void gather_needed_points(TreeDev& T, const double* src, const double* q, const double* tgt,
+                          const uint8_t* need_src, const uint8_t* need_tgt) {
+  cudaStream_t st = T.st;
+  const int d = T.d;
+  T.src_sorted.alloc(T.ns * d, st);
+  T.tgt_sorted.alloc(T.nt * d, st);
+  if (q) T.q_sorted.alloc(T.ns, st);
+  const unsigned g = grid_for(T.nb, 8), gb = (unsigned)std::min<int64_t>(std::max<int64_t>(T.n_dense, 1), 148 * 8);
+  auto run = [&](const double* a, const double* qq, const int64_t* perm, const int64_t* start, const int64_t* count,
+                 const uint8_t* need, double* out, double* qo) {
+    const uint8_t* lf = T.is_leaf.get();
+    const int64_t* dsl = T.dense_slot.get();
+    const int64_t* dids = T.dense_ids.get();
+#define FGT_GN(DD)                                                                                           \
+  gather_needed_kernel<DD, false><<<g, 256, 0, st>>>(a, qq, perm, start, count, lf, need, dsl, dids, T.nb, out, qo); \
+  FGT_LAUNCHED();                                                                                            \
+  if (T.n_dense > 0) {                                                                                       \
+    gather_needed_kernel<DD, true><<<gb, 256, 0, st>>>(a, qq, perm, start, count, lf, need, dsl, dids, T.n_dense, out, qo); \
+    FGT_LAUNCHED();                                                                                          \
+  }
+    if (d == 1) { FGT_GN(1) } else if (d == 2) { FGT_GN(2) } else { FGT_GN(3) }
+#undef FGT_GN
+  };
+  if (T.ns > 0) run(src, q, T.src_perm.get(), T.src_start.get(), T.src_count.get(), need_src, T.src_sorted.get(),
+                    q ? T.q_sorted.get() : nullptr);
+  if (T.nt > 0) run(tgt, nullptr, T.tgt_perm.get(), T.tgt_start.get(), T.tgt_count.get(), need_tgt, T.tgt_sorted.get(),
+                    nullptr);
+}
+
 // ====================================================================== lists
 namespace {
 

@@ -67,6 +67,9 @@ void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, in
                 const fgt_tree_params& tp, cudaStream_t st);
 // Gather sorted coordinates (and charges, if given) into T.*_sorted.
 void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt);
+// same for the boxes flagged in need_src / need_tgt only ((nb) device flags; multi-GPU shares)
+void gather_needed_points(TreeDev& T, const double* src, const double* q, const double* tgt,
+                          const uint8_t* need_src, const uint8_t* need_tgt);
 // Target-centric P/D lists.  build_lists = begin + end; begin enqueues
 // the enumeration and the read-back of the list sizes on T.st without blocking, end waits
 // for the sizes and enqueues the compaction.

@@ -285,11 +285,16 @@ def test_single_point_and_flat_kernel(cuda):
     assert rel(u, np.full(2000, q.sum())) < 1e-6
 
 
+@pytest.mark.parametrize("gather_min", [None, "0"], ids=["fullgather", "sharegather"])
 @pytest.mark.parametrize("size", [2, 3])
-def test_shares_sum_to_full(cuda, size):
+def test_shares_sum_to_full(cuda, size, gather_min, monkeypatch):
     """Multi-GPU shares run one after another on one GPU: disjoint, and their sum is
-    bitwise the full transform (each target is owned by exactly one share)."""
+    bitwise the full transform (each target is owned by exactly one share).  sharegather:
+    each rank gathers only the leaf-ordered points of its own share (the path taken above
+    2^23 points), forced here by FGT_SHARE_GATHER_MIN=0."""
     from paper_2305_07165_b200 import fgt_points
+    if gather_min is not None:
+        monkeypatch.setenv("FGT_SHARE_GATHER_MIN", gather_min)
     r = np.random.default_rng(8)
     y = clustered(r, 20000, 3)
     x = r.uniform(-0.5, 0.5, (20000, 3))
@@ -380,15 +385,18 @@ def _emulated_exchange(runs):
         run.unpack(recv)
 
 
+@pytest.mark.parametrize("gather_min", [None, "0"], ids=["fullgather", "sharegather"])
 @pytest.mark.parametrize("size", [2, 3, 5])
 @pytest.mark.parametrize("case", ["clust3d", "periodic2d"])
-def test_exchange_shares_sum_to_full(cuda, size, case):
+def test_exchange_shares_sum_to_full(cuda, size, case, gather_min, monkeypatch):
     """Owner-formed expansions + halo exchange (the multi-GPU path), ranks run one after
     another on one GPU with the all-to-all emulated by device copies: the shares are
     disjoint and sum bitwise to the single-GPU transform; each expansion is formed once."""
     import torch
     from paper_2305_07165_b200 import fgt_points_device
     from paper_2305_07165_b200.point_fgt import fgt_points_exchange_begin
+    if gather_min is not None:
+        monkeypatch.setenv("FGT_SHARE_GATHER_MIN", gather_min)  # restricted per-rank gather
     r = np.random.default_rng(12)
     if case == "clust3d":
         y, x, args = clustered(r, 20000, 3), r.uniform(-0.5, 0.5, (20000, 3)), (1e-4, 1e-9, 100, "free")
