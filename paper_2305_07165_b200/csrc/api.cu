@@ -392,6 +392,7 @@ static void gather_share_points(TreeDev& T, const double* src, const double* q, 
     FGT_LAUNCHED();
     // (dense_need is pageable host memory: the copy above has left it when it returned)
   }
+  order_leaf_points(T, ns.get(), nt.get());
   gather_needed_points(T, src, q, tgt, ns.get(), nt.get());
 }
 
@@ -585,15 +586,17 @@ static void points_begin(PointsRun& R, const double* src, int64_t ns, const doub
   R.pm.reset(new PhaseMarks(st));  // marks: 0 start, 1 tree, 2 lists, 3 form, 4 gather+eval, 5 direct
   trace_mark(st, "start");
   TreeDev& T = R.T;
+  {
+    const char* env_min = std::getenv("FGT_SHARE_GATHER_MIN");
+    T.defer_order = tp.part_size > 1 && ns + nt >= (env_min ? atoll(env_min) : ((int64_t)1 << 23));
+  }
   build_tree(T, src, ns, tgt, nt, tp, st);
   if (q_ready) FGT_CUDA(cudaStreamWaitEvent(st, q_ready, 0));  // charges copied on a side stream
   // multi-GPU shares gather the leaf-ordered points after the share is planned, and only
   // the rank's own (plan_share needs counts, not coordinates)
   // (below ~8M points the full gather is cheaper than planning the restricted one;
   // FGT_SHARE_GATHER_MIN overrides the threshold for tests)
-  const char* env_min = std::getenv("FGT_SHARE_GATHER_MIN");
-  const int64_t gather_min = env_min ? atoll(env_min) : ((int64_t)1 << 23);
-  const bool shared = tp.part_size > 1 && ns + nt >= gather_min;
+  const bool shared = T.defer_order;
   if (!shared) gather_sorted_points(T, src, q, tgt);
   R.pm->mark();
   trace_mark(st, "tree");

@@ -650,6 +650,49 @@ __global__ void dense_src_kernel(const int64_t* __restrict__ ids, const int64_t*
     out[i] = src_count[ids[i]];
 }
 
+// Per-leaf ascending lists of a general tree (see build_tree_impl): src_perm / tgt_perm = the
+// leaf-partitioned indices, with the coarse leaves' runs sorted by original index (CUB
+// segmented sort; level-l_c leaves are empty segments and keep the partitioned order).
+// need_src / need_tgt ((nb) flags, multi-GPU shares): only the flagged leaves are sorted;
+// the others keep the partitioned order (still a permutation, never read in leaf order).
+__global__ void restrict_segments_kernel(const int64_t* __restrict__ start, int64_t* __restrict__ end,
+                                         const uint8_t* __restrict__ need, int64_t nb) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    if (!need[b]) end[b] = start[b];
+}
+
+}  // namespace
+
+void order_leaf_points(TreeDev& T, const uint8_t* need_src, const uint8_t* need_tgt) {
+  if (!T.order_pending) return;
+  cudaStream_t st = T.st;
+  CubTmp tmp;
+  for (int which = 0; which < 2; ++which) {
+    const int64_t n = which ? T.nt : T.ns;
+    if (n == 0) continue;
+    const int64_t* kin = which ? T.seq_tgt.get() : T.seq_src.get();
+    int64_t* kout = which ? T.tgt_perm.get() : T.src_perm.get();
+    const int64_t* beg = which ? T.tgt_start.get() : T.src_start.get();
+    int64_t* end = which ? T.tgt_end.get() : T.src_end.get();
+    const uint8_t* need = which ? need_tgt : need_src;
+    if (need) {
+      restrict_segments_kernel<<<grid_for(T.nb, 256), 256, 0, st>>>(beg, end, need, T.nb);
+      FGT_LAUNCHED();
+    }
+    FGT_CUDA(cudaMemcpyAsync(kout, kin, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    size_t bytes = 0;
+    FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, kin, kout, (int)n, (int)T.nb, beg, end, st));
+    FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.get(bytes, st), bytes, kin, kout, (int)n, (int)T.nb, beg, end, st));
+    count_launch();
+  }
+  T.seq_src.release();
+  T.seq_tgt.release();
+  T.src_end.release();
+  T.tgt_end.release();
+  T.order_pending = false;
+}
+
+namespace {
 template <int D>
 void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tgt, int64_t nt,
                      const fgt_tree_params& tp, cudaStream_t st) {
@@ -892,28 +935,21 @@ void build_tree_impl(TreeDev& T, const double* src, int64_t ns, const double* tg
     T.tgt_perm.alloc(nt, st);
     T.src_start.alloc(nb, st);
     T.tgt_start.alloc(nb, st);
-    DBuf<int64_t> seq_src(ns, st), seq_tgt(nt, st), src_end(nb, st), tgt_end(nb, st);
-    partition_points_kernel<<<grid_for(np, 256), 256, 0, st>>>(T.pidx.get(), np, ns, srcpre.get(), seq_src.get(),
-                                                               seq_tgt.get());
+    T.seq_src.alloc(ns, st);
+    T.seq_tgt.alloc(nt, st);
+    T.src_end.alloc(nb, st);
+    T.tgt_end.alloc(nb, st);
+    partition_points_kernel<<<grid_for(np, 256), 256, 0, st>>>(T.pidx.get(), np, ns, srcpre.get(), T.seq_src.get(),
+                                                               T.seq_tgt.get());
     FGT_LAUNCHED();
     leaf_ranges_kernel<<<grid_for(nb, 256), 256, 0, st>>>(T.bkey.get(), T.is_leaf.get(), nb, pk, D, l_c,
-                                                          srcpre.get(), T.src_start.get(), src_end.get(),
-                                                          T.tgt_start.get(), tgt_end.get());
+                                                          srcpre.get(), T.src_start.get(), T.src_end.get(),
+                                                          T.tgt_start.get(), T.tgt_end.get());
     FGT_LAUNCHED();
-    for (int which = 0; which < 2; ++which) {
-      const int64_t n = which ? nt : ns;
-      if (n == 0) continue;
-      const int64_t* kin = which ? seq_tgt.get() : seq_src.get();
-      int64_t* kout = which ? T.tgt_perm.get() : T.src_perm.get();
-      const int64_t* beg = which ? T.tgt_start.get() : T.src_start.get();
-      const int64_t* end = which ? tgt_end.get() : src_end.get();
-      // level-l_c leaves (empty sort segments) keep the partitioned order
-      FGT_CUDA(cudaMemcpyAsync(kout, kin, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-      size_t bytes = 0;
-      FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, kin, kout, (int)n, (int)nb, beg, end, st));
-      FGT_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.get(bytes, st), bytes, kin, kout, (int)n, (int)nb, beg, end, st));
-      count_launch();
-    }
+    // the ascending per-leaf order: now, or (multi-GPU shares) after the share is planned and
+    // for the rank's own leaves only
+    T.order_pending = true;
+    if (!T.defer_order) order_leaf_points(T, nullptr, nullptr);
   }
 
   // ---- P-boxes: leaves at l_c with > n_s points

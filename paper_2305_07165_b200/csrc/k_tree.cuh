@@ -29,6 +29,9 @@ struct TreeDev {
   DBuf<uint8_t> is_leaf;   // (nb)
   DBuf<int64_t> n_points, src_start, src_count, tgt_start, tgt_count;  // (nb)
   DBuf<int64_t> src_perm, tgt_perm;  // original index of each sorted point
+  // general trees: the per-leaf ascending order may be deferred (order_leaf_points)
+  bool defer_order = false, order_pending = false;
+  DBuf<int64_t> seq_src, seq_tgt, src_end, tgt_end;
   DBuf<double> center;     // (nb * d) box centres (exact builder arithmetic)
   DBuf<int64_t> dense_ids;   // (n_dense) box ids of P-boxes
   DBuf<int64_t> dense_slot;  // (nb) index into dense_ids or -1
@@ -67,6 +70,8 @@ void build_tree(TreeDev& T, const double* src, int64_t ns, const double* tgt, in
                 const fgt_tree_params& tp, cudaStream_t st);
 // Gather sorted coordinates (and charges, if given) into T.*_sorted.
 void gather_sorted_points(TreeDev& T, const double* src, const double* q, const double* tgt);
+// deferred per-leaf order of a general tree (all leaves, or the flagged ones)
+void order_leaf_points(TreeDev& T, const uint8_t* need_src, const uint8_t* need_tgt);
 // same for the boxes flagged in need_src / need_tgt only ((nb) device flags; multi-GPU shares)
 void gather_needed_points(TreeDev& T, const double* src, const double* q, const double* tgt,
                           const uint8_t* need_src, const uint8_t* need_tgt);
