@@ -121,7 +121,10 @@ typedef struct fgt_tree_params {
    * range needs (the one-box halo is recomputed, no communication); fgt_points_begin ..
    * finish forms only the expansions the rank owns and the halo is exchanged between
    * begin and finish (fgt_points_pack / unpack + one all-to-all).  part_size <= 1 means
-   * everything.  Targets outside the share get u = 0 (summing the shares gives u). */
+   * everything.  Targets outside the share get u = 0 (summing the shares gives u).
+   * Every rank builds the same tree structure and lists from all the points; above 2^23
+   * points the per-point tail of the build (per-leaf ascending order, leaf-ordered
+   * coordinates) is done after the share is planned, for the rank's own leaves only. */
   int32_t part_rank;
   int32_t part_size;
 } fgt_tree_params;
