@@ -196,6 +196,19 @@ __global__ void scatter_kernel(const double* __restrict__ us, const int64_t* __r
     u[perm[i]] = us[i];
 }
 
+// multi-GPU shares: the potentials of the listed boxes' targets only (a warp per box; u was
+// zeroed, and a share's targets all sit in its direct target leaves or its psi boxes)
+__global__ void scatter_boxes_kernel(const int64_t* __restrict__ ids, int64_t n, const int64_t* __restrict__ start,
+                                     const int64_t* __restrict__ count, const double* __restrict__ us,
+                                     const int64_t* __restrict__ perm, double* __restrict__ u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n; k += nwarp) {
+    const int64_t b = ids[k], s0 = start[b], m = count[b];
+    for (int64_t i = lane; i < m; i += 32) u[perm[s0 + i]] = us[s0 + i];
+  }
+}
+
 
 
 
@@ -701,7 +714,20 @@ static void points_finish(PointsRun& R, double* u, fgt_phase_times* times, doubl
   } else {
     const double D0 = R.tp.D0;
     direct_lists(T, 1.0 / R.tp.delta, D0 * D0 * R.tp.delta, R.us.get(), &P.k_direct);
-    if (R.nt > 0) {
+    if (R.nt > 0 && T.defer_order) {
+      // a share of a large transform: zero u, then write the share's own targets only
+      FGT_CUDA(cudaMemsetAsync(u, 0, R.nt * sizeof(double), st));
+      if (T.n_dtgt > 0) {
+        scatter_boxes_kernel<<<grid_for(T.n_dtgt, 8), 256, 0, st>>>(T.d_tgt_ids.get(), T.n_dtgt, T.tgt_start.get(),
+                                                                    T.tgt_count.get(), R.us.get(), T.tgt_perm.get(), u);
+        FGT_LAUNCHED();
+      }
+      if (T.n_psi > 0) {
+        scatter_boxes_kernel<<<grid_for(T.n_psi, 8), 256, 0, st>>>(T.psi_ids.get(), T.n_psi, T.tgt_start.get(),
+                                                                   T.tgt_count.get(), R.us.get(), T.tgt_perm.get(), u);
+        FGT_LAUNCHED();
+      }
+    } else if (R.nt > 0) {
       scatter_kernel<<<grid_for(R.nt, 256), 256, 0, st>>>(R.us.get(), T.tgt_perm.get(), R.nt, u);
       FGT_LAUNCHED();
     }
