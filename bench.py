@@ -396,6 +396,18 @@ def timed_device_steps(step, steps, flush, stream, lib, local, world):
     torch.cuda.synchronize()
     l0 = lib.fgt_launch_count()
     with ClockSampler(local) as clk:
+        # more untimed steps for ~1 s while nvidia-smi starts (its NVML initialisation stalls
+        # kernel launches for tens of ms once: it showed as a single 270-285 ms step among
+        # 243 ms ones when the sampler started with the first timed step)
+        t_start = time.perf_counter()
+        while True:
+            step()
+            torch.cuda.synchronize()
+            if time.perf_counter() - t_start > 1.0:
+                break
+        barrier(world)
+        torch.cuda.synchronize()
+        l0 = lib.fgt_launch_count()
         for i in range(steps):
             flush.fill_(float(i))          # L2 flush, outside the events
             ev[i][0].record(stream)
