@@ -403,7 +403,8 @@ def timed_device_steps(step, steps, flush, stream, lib, local, world):
         while True:
             step()
             torch.cuda.synchronize()
-            if time.perf_counter() - t_start > 1.0:
+            # (every rank must run the same number of steps: the decision is all-reduced)
+            if max_over_ranks(1.0 if time.perf_counter() - t_start > 1.0 else 0.0, world) > 0.5:
                 break
         barrier(world)
         torch.cuda.synchronize()
